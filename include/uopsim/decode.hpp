@@ -1,0 +1,63 @@
+#pragma once
+// Decode-layer graph builder (ext): a Llama/Qwen-style decoder expressed as
+// an OperatorGraph of decode kinds, ready for generator::generate().
+//
+// Per layer l (B = 1, all vectors (M,1)):
+//   L.qkv  rms_gemv  [L.wqkv, x.all, L.attn_norm] -> [L.q, L.kc.seg, L.vc.seg]
+//          (RMSNorm fused, interleaved-pair RoPE on q/k rows, k/v rows appended
+//           to the caches at the step position: the KV append)
+//   L.attn attn_decode [L.q.grp, L.kc.page, L.vc.page] -> [L.part]  (split-KV, GQA)
+//   L.comb attn_combine [L.part] -> [L.attn]
+//   L.o    gemv_add  [L.wo, L.attn.all, x.blk] -> [L.x1]      (residual fused)
+//   L.gu   rms_gemv  [L.wgu, L.x1.all, L.mlp_norm] -> [L.a]   (SwiGLU fused)
+//   L.down gemv_add  [L.wd, L.a.all, L.x1.blk] -> [L.x2]
+// plus `embed` (embed_row, token from the step block) and `head`
+// (rms_gemv: final norm + lm_head -> fp32 logits).
+// Weight layout conventions (part of the model definition, mirrored by the
+// oracle): wqkv rows = [q heads | k heads | v heads]; wgu rows come in blocks
+// of `gu_block` = [gate x gu_block/2 | up x gu_block/2].
+
+#include <cstdint>
+#include <string>
+
+#include "uopsim/workload.hpp"
+
+namespace uopsim::decode {
+
+struct ModelConfig {
+    std::string name = "tiny";
+    int layers = 2;
+    int hidden = 256;
+    int heads = 4;
+    int kv_heads = 4;
+    int head_dim = 64;
+    int ffn = 512;
+    int vocab = 512;
+    float eps = 1e-5f;
+    float theta = 10000.0f;
+    workload::ElemType dtype = workload::ElemType::f32;
+    bool scaled_init = false;  // (u-1)/2/sqrt(fan_in) weights instead of raw unit_float
+};
+
+struct LayoutConfig {
+    int ctx_pages = 1;       // KV pages covered by the program (ctx <= ctx_pages * page_rows)
+    int max_ctx = 64;        // cache capacity T (>= ctx_pages * page_rows)
+    int page_rows = 64;
+    int pages_per_job = 1;   // split-KV granularity
+    int job_rows = 16;       // output rows per GEMV job (divides head_dim)
+    int head_job_rows = 64;  // output rows per lm_head job
+    int gu_block = 16;       // swiglu interleave block (== job_rows for the gu node)
+    int wtile_bytes = 16384; // target weight tile bytes
+};
+
+ModelConfig llama3_8b();
+ModelConfig qwen3_8b();
+ModelConfig llama3_70b();
+ModelConfig tiny_llama();
+
+workload::OperatorGraph build_decode_graph(const ModelConfig& m, const LayoutConfig& l);
+
+// weight tile shape (rows, cols) used for a (M,K) matrix under `l`
+std::pair<int64_t, int64_t> weight_tile(int64_t rows, int64_t cols, workload::ElemType e, const LayoutConfig& l);
+
+}  // namespace uopsim::decode

@@ -1,0 +1,136 @@
+/*
+ * vdc.h — C-ABI of the B200 µop decode engine (drop-in boundary).
+ *
+ * The reference (arxiv 2605.03190 "VDCores", /root/reference/proj) exposes its
+ * executor only as C++ (`uopsim::machine::Machine` / `simulate`,
+ * include/uopsim/machine.hpp:94-126, bodies absent from the tree) and its
+ * builder as `uopsim::generator::generate` (include/uopsim/generator.hpp:132).
+ * This header is the C-level replacement: plain pointers and sizes, no C++ or
+ * torch types, `int` status codes, no exceptions across the boundary.
+ *
+ *   reference                                  replaced by
+ *   ---------------------------------------    -----------------------------------------
+ *   Machine(p, hw, inputs, opt)  machine.hpp:96 vdc_create + vdc_load_program + vdc_bind_tensor
+ *   Machine::run(watchdog)       machine.hpp:112 vdc_launch + vdc_wait (report.status, deadlock)
+ *   ExecutionReport              machine.hpp:65  vdc_report
+ *   MachineError / Termination   machine.hpp:19,58 VDC_ERR_* / vdc_report.status
+ *   simulate(p, hw, opt, wd)     machine.hpp:124 vdc_program_build + vdc_program_load + launch/wait
+ *   generator::generate(g,hw,o)  generator.hpp:132 vdc_program_build (request JSON)
+ *   serialize_stream/_sidecar    generator.hpp:154 vdc_program_text
+ *   isa::encode_stream           isa.hpp:134      vdc_program_words
+ *
+ * Status codes mirror the reference CLI's exit codes:
+ * 0 ok, 1 internal, 2 input, 3 deadlock. The last error message of the
+ * calling thread is available from vdc_last_error().
+ */
+#ifndef VDC_H
+#define VDC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VDC_OK 0
+#define VDC_ERR_INTERNAL 1
+#define VDC_ERR_INPUT 2
+#define VDC_ERR_DEADLOCK 3
+
+#define VDC_DTYPE_F32 0
+#define VDC_DTYPE_BF16 1
+#define VDC_DTYPE_I64 2
+
+/* Virtual-core declaration of the device (costmodel::HardwareProfile subset). */
+typedef struct vdc_profile {
+    uint32_t sm_count;    /* persistent CTAs (<= multiprocessor count) */
+    uint32_t vcc_per_sm;  /* compute virtual cores per SM (1 or 2)     */
+    uint32_t slot_size;   /* bytes per shared-memory slot              */
+    uint32_t slot_budget; /* slots per SM                              */
+    uint32_t ldu_count;   /* load units per VMC (1 or 2)               */
+    uint32_t stu_count;   /* store units per VMC (1 or 2)              */
+} vdc_profile;
+
+/* One tile descriptor (generator::TileDescriptor). Tensors are row-major in
+ * device memory; tiles are the 2-d boxes over the trailing two dims. */
+typedef struct vdc_desc {
+    int64_t base;       /* first global tile index                       */
+    int64_t shape[4];
+    int64_t grid[4];
+    int64_t tile_rows;
+    int64_t tile_cols;
+    uint32_t rank;      /* rank of shape == rank of grid                  */
+    uint32_t dtype;     /* VDC_DTYPE_*                                    */
+    int32_t view_of;    /* storage owner descriptor, -1 = owns storage    */
+    uint32_t pad;
+} vdc_desc;
+
+/* Dependency queue wiring (generator::QueueInfo). */
+typedef struct vdc_queue {
+    uint16_t dep_id;
+    uint16_t depth;
+    uint16_t producer_sm;
+    uint16_t consumer_sm;
+    uint32_t local; /* slot handoff (STORE_LOCAL -> LOAD_LOCAL) */
+} vdc_queue;
+
+typedef struct vdc_report {
+    int32_t status;            /* VDC_OK or VDC_ERR_DEADLOCK / VDC_ERR_INTERNAL */
+    uint32_t n_stalled;        /* cores still blocked when the watchdog fired    */
+    uint64_t uops_executed;
+    uint64_t bytes_loaded;     /* global -> shared (DRAM/L2) bytes               */
+    uint64_t bytes_stored;     /* shared -> global bytes                         */
+    double elapsed_ms;         /* device time of the last launch                 */
+    uint32_t stalled_core[16]; /* core index (CoreId order) of blocked cores     */
+    uint32_t stalled_pc[16];
+    char message[256];
+} vdc_report;
+
+typedef struct vdc_ctx vdc_ctx;
+typedef struct vdc_program vdc_program;
+
+const char* vdc_last_error(void);
+const char* vdc_version(void);
+
+/* ---- device executor ------------------------------------------------- */
+int vdc_create(const vdc_profile* profile, int device, vdc_ctx** out);
+int vdc_destroy(vdc_ctx* ctx);
+
+/* words: concatenated isa::encode_stream bytes of every core in CoreId order
+ * (sm0.vmc, sm0.vcc0, sm0.vcc1, sm1.vmc, ...), words_per_core[i] 16-byte words. */
+int vdc_load_program(vdc_ctx* ctx, const uint8_t* words, const uint32_t* words_per_core, uint32_t n_cores,
+                     const vdc_queue* queues, uint32_t n_queues, const vdc_desc* descs, uint32_t n_desc,
+                     uint16_t slot_budget, uint16_t local_depth);
+/* extension handler parameter table (LoweredProgram::params) */
+int vdc_set_params(vdc_ctx* ctx, const float* params, uint32_t n);
+/* device memory (row-major) backing descriptor `tensor`; the caller owns it */
+int vdc_bind_tensor(vdc_ctx* ctx, uint16_t tensor, void* dptr, size_t bytes, int dtype);
+/* step block: device-resident int64 scalars read by SET_ACC_MEM */
+int vdc_bind_step(vdc_ctx* ctx, int64_t* dptr, uint32_t n);
+/* one execution of the loaded program on `stream` (a cudaStream_t, NULL =
+ * default stream); readiness counters and queues are reset on the stream. */
+int vdc_launch(vdc_ctx* ctx, void* stream);
+/* synchronise with the last launch and fill the report */
+int vdc_wait(vdc_ctx* ctx, vdc_report* report);
+/* watchdog: abort a launch whose cores make no progress for `ms` (0 = off) */
+int vdc_set_watchdog(vdc_ctx* ctx, uint32_t ms);
+
+/* ---- host program builder (uopsim C++ library) ------------------------ */
+/* request_json: {"workload": {...} | "model": {...}, "profile": {...},
+ *                "options": {...}, "tilings": {...}, "passes": [...]}      */
+int vdc_program_build(const char* request_json, vdc_program** out);
+int vdc_program_parse(const char* streams_json, const char* sidecar, vdc_program** out);
+void vdc_program_free(vdc_program* prog);
+/* JSON: {"streams":{core:text}, "sidecar":..., "words":{core:hex}?, "tilings":..., ...} */
+int vdc_program_text(const vdc_program* prog, int with_words, char** out_json);
+int vdc_program_cores(const vdc_program* prog, uint32_t* n_cores, uint32_t* sm_count, uint32_t* vcc_per_sm);
+/* encoded stream of core i (CoreId order over sm_count x (1 + vcc_per_sm)) */
+int vdc_program_words(const vdc_program* prog, uint32_t core, const uint8_t** words, uint32_t* n_words);
+int vdc_program_load(vdc_ctx* ctx, const vdc_program* prog);
+void vdc_free_string(char* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VDC_H */

@@ -1,0 +1,177 @@
+"""ctypes binding of the C-ABI in include/vdc.h (libvdc.so, built in-tree).
+
+The product path is native: every entry point below is a C function of
+paper_2605_03190_b200/lib/libvdc.so. There is no Python fallback — if the
+library is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "lib" / "libvdc.so"
+
+VDC_OK, VDC_ERR_INTERNAL, VDC_ERR_INPUT, VDC_ERR_DEADLOCK = 0, 1, 2, 3
+DTYPE = {"f32": 0, "bf16": 1, "i64": 2}
+
+
+class VdcError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[vdc status {code}] {msg}")
+        self.code = code
+
+
+class vdc_profile(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint32) for n in ("sm_count", "vcc_per_sm", "slot_size", "slot_budget", "ldu_count", "stu_count")]
+
+
+class vdc_desc(ctypes.Structure):
+    _fields_ = [
+        ("base", ctypes.c_int64),
+        ("shape", ctypes.c_int64 * 4),
+        ("grid", ctypes.c_int64 * 4),
+        ("tile_rows", ctypes.c_int64),
+        ("tile_cols", ctypes.c_int64),
+        ("rank", ctypes.c_uint32),
+        ("dtype", ctypes.c_uint32),
+        ("view_of", ctypes.c_int32),
+        ("pad", ctypes.c_uint32),
+    ]
+
+
+class vdc_queue(ctypes.Structure):
+    _fields_ = [
+        ("dep_id", ctypes.c_uint16),
+        ("depth", ctypes.c_uint16),
+        ("producer_sm", ctypes.c_uint16),
+        ("consumer_sm", ctypes.c_uint16),
+        ("local", ctypes.c_uint32),
+    ]
+
+
+class vdc_report(ctypes.Structure):
+    _fields_ = [
+        ("status", ctypes.c_int32),
+        ("n_stalled", ctypes.c_uint32),
+        ("uops_executed", ctypes.c_uint64),
+        ("bytes_loaded", ctypes.c_uint64),
+        ("bytes_stored", ctypes.c_uint64),
+        ("elapsed_ms", ctypes.c_double),
+        ("stalled_core", ctypes.c_uint32 * 16),
+        ("stalled_pc", ctypes.c_uint32 * 16),
+        ("message", ctypes.c_char * 256),
+    ]
+
+
+# every symbol include/vdc.h declares (the CPU suite checks they are exported)
+EXPORTS = [
+    "vdc_last_error", "vdc_version", "vdc_create", "vdc_destroy", "vdc_load_program", "vdc_set_params",
+    "vdc_bind_tensor", "vdc_bind_step", "vdc_launch", "vdc_wait", "vdc_set_watchdog", "vdc_program_build",
+    "vdc_program_parse", "vdc_program_free", "vdc_program_text", "vdc_program_cores", "vdc_program_words",
+    "vdc_program_load", "vdc_free_string",
+]
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+    L = ctypes.CDLL(str(LIB_PATH))
+    c = ctypes
+    vp = c.c_void_p
+    sig = {
+        "vdc_last_error": ([], c.c_char_p),
+        "vdc_version": ([], c.c_char_p),
+        "vdc_create": ([c.POINTER(vdc_profile), c.c_int, c.POINTER(vp)], c.c_int),
+        "vdc_destroy": ([vp], c.c_int),
+        "vdc_load_program": ([vp, c.c_void_p, c.POINTER(c.c_uint32), c.c_uint32, c.POINTER(vdc_queue), c.c_uint32,
+                              c.POINTER(vdc_desc), c.c_uint32, c.c_uint16, c.c_uint16], c.c_int),
+        "vdc_set_params": ([vp, c.POINTER(c.c_float), c.c_uint32], c.c_int),
+        "vdc_bind_tensor": ([vp, c.c_uint16, vp, c.c_size_t, c.c_int], c.c_int),
+        "vdc_bind_step": ([vp, vp, c.c_uint32], c.c_int),
+        "vdc_launch": ([vp, vp], c.c_int),
+        "vdc_wait": ([vp, c.POINTER(vdc_report)], c.c_int),
+        "vdc_set_watchdog": ([vp, c.c_uint32], c.c_int),
+        "vdc_program_build": ([c.c_char_p, c.POINTER(vp)], c.c_int),
+        "vdc_program_parse": ([c.c_char_p, c.c_char_p, c.POINTER(vp)], c.c_int),
+        "vdc_program_free": ([vp], None),
+        "vdc_program_text": ([vp, c.c_int, c.POINTER(c.c_void_p)], c.c_int),
+        "vdc_program_cores": ([vp, c.POINTER(c.c_uint32), c.POINTER(c.c_uint32), c.POINTER(c.c_uint32)], c.c_int),
+        "vdc_program_words": ([vp, c.c_uint32, c.POINTER(c.c_void_p), c.POINTER(c.c_uint32)], c.c_int),
+        "vdc_program_load": ([vp, vp], c.c_int),
+        "vdc_free_string": ([c.c_void_p], None),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L
+
+
+def check(code: int) -> None:
+    if code != VDC_OK:
+        raise VdcError(code, lib().vdc_last_error().decode())
+
+
+def take_string(ptr: ctypes.c_void_p) -> str:
+    try:
+        return ctypes.string_at(ptr).decode()
+    finally:
+        lib().vdc_free_string(ptr)
+
+
+class Program:
+    """Owns a vdc_program handle (generator::LoweredProgram + encoded words)."""
+
+    def __init__(self, handle: ctypes.c_void_p):
+        self._h = handle
+        self._info = None
+
+    @classmethod
+    def build(cls, request: dict) -> "Program":
+        h = ctypes.c_void_p()
+        check(lib().vdc_program_build(json.dumps(request).encode(), ctypes.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def parse(cls, streams: dict, sidecar: str) -> "Program":
+        h = ctypes.c_void_p()
+        check(lib().vdc_program_parse(json.dumps(streams).encode(), sidecar.encode(), ctypes.byref(h)))
+        return cls(h)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def text(self, with_words: bool = False) -> dict:
+        out = ctypes.c_void_p()
+        check(lib().vdc_program_text(self._h, 1 if with_words else 0, ctypes.byref(out)))
+        return json.loads(take_string(out))
+
+    def info(self) -> dict:
+        if self._info is None:
+            self._info = self.text(False)
+        return self._info
+
+    def cores(self):
+        n, sms, vcc = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
+        check(lib().vdc_program_cores(self._h, ctypes.byref(n), ctypes.byref(sms), ctypes.byref(vcc)))
+        return n.value, sms.value, vcc.value
+
+    def words(self, core: int) -> bytes:
+        p, n = ctypes.c_void_p(), ctypes.c_uint32()
+        check(lib().vdc_program_words(self._h, core, ctypes.byref(p), ctypes.byref(n)))
+        return ctypes.string_at(p, n.value * 16) if n.value else b""
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.vdc_program_free(self._h)
+            self._h = None

@@ -1,0 +1,196 @@
+// Decode-layer graph builder (ext). See include/uopsim/decode.hpp for the
+// operator sequence and weight-layout conventions.
+#include <cmath>
+
+#include "uopsim/decode.hpp"
+#include "uopsim/util.hpp"
+
+namespace uopsim::decode {
+
+using workload::ElemType;
+using workload::InitKind;
+using workload::OperatorGraph;
+using workload::OperatorNode;
+using workload::OpKind;
+using workload::TensorRef;
+
+ModelConfig llama3_8b() {
+    ModelConfig m;
+    m.name = "llama3-8b";
+    m.layers = 32;
+    m.hidden = 4096;
+    m.heads = 32;
+    m.kv_heads = 8;
+    m.head_dim = 128;
+    m.ffn = 14336;
+    m.vocab = 128256;
+    m.eps = 1e-5f;
+    m.theta = 500000.0f;
+    m.dtype = ElemType::bf16;
+    m.scaled_init = true;
+    return m;
+}
+ModelConfig qwen3_8b() {
+    ModelConfig m = llama3_8b();
+    m.name = "qwen3-8b";
+    m.layers = 36;
+    m.ffn = 12288;
+    m.vocab = 151936;
+    m.eps = 1e-6f;
+    m.theta = 1000000.0f;
+    return m;
+}
+ModelConfig llama3_70b() {
+    ModelConfig m = llama3_8b();
+    m.name = "llama3-70b";
+    m.layers = 80;
+    m.hidden = 8192;
+    m.heads = 64;
+    m.kv_heads = 8;
+    m.ffn = 28672;
+    return m;
+}
+ModelConfig tiny_llama() {
+    ModelConfig m;  // C1: 2 layers, hidden 256, 4 heads x 64, fp32
+    m.scaled_init = true;
+    return m;
+}
+
+std::pair<int64_t, int64_t> weight_tile(int64_t rows, int64_t cols, ElemType e, const LayoutConfig& l) {
+    (void)rows;
+    const int64_t eb = workload::elem_bytes(e);
+    const int64_t tc = std::min<int64_t>(cols, std::max<int64_t>(1, l.wtile_bytes / (eb * 4)));
+    int64_t tr = std::max<int64_t>(1, l.wtile_bytes / (tc * eb));
+    return {tr, tc};
+}
+
+namespace {
+
+struct Builder {
+    OperatorGraph g;
+    const ModelConfig& m;
+    const LayoutConfig& l;
+
+    TensorRef& add(const std::string& name, std::vector<int64_t> shape, int64_t tr, int64_t tc, InitKind init,
+                   ElemType e, float scale = 1.0f) {
+        TensorRef t;
+        t.name = name;
+        t.shape = std::move(shape);
+        t.tile_rows = tr;
+        t.tile_cols = tc;
+        t.init = init;
+        t.elem = e;
+        t.init_scale = scale;
+        g.tensors.push_back(t);
+        return g.tensors.back();
+    }
+    // vector (rows, 1) produced in tiles of `tile` rows
+    std::string vec(const std::string& name, int64_t rows, int64_t tile, ElemType e) {
+        add(name, {rows, 1}, tile, 1, InitKind::zeros, e);
+        return name;
+    }
+    // a view of `base` with a different row tiling (same row-major storage)
+    std::string view(const std::string& base, const std::string& suffix, int64_t tile_rows, int64_t tile_cols = 0) {
+        const TensorRef& b = g.tensor(base);
+        if (tile_rows == b.tile_rows && (tile_cols == 0 || tile_cols == b.tile_cols)) return base;
+        const std::string name = base + suffix;
+        if (g.find_tensor(name)) return name;
+        TensorRef v = b;
+        v.name = name;
+        v.tile_rows = tile_rows;
+        if (tile_cols) v.tile_cols = tile_cols;
+        v.init = InitKind::zeros;
+        v.state = false;
+        v.view_of = base;
+        g.tensors.push_back(v);
+        return name;
+    }
+    // weight matrix (rows x cols) with the layout's tile shape; job_rows must
+    // be a multiple of the tile rows so tiles never straddle two jobs
+    std::string weight(const std::string& name, int64_t rows, int64_t cols, int64_t job_rows, float fan_in) {
+        auto [tr, tc] = weight_tile(rows, cols, m.dtype, l);
+        while (job_rows % tr) --tr;
+        const InitKind init = m.scaled_init ? InitKind::centered : InitKind::random;
+        add(name, {rows, cols}, tr, tc, init, m.dtype, m.scaled_init ? float(1.0 / std::sqrt(double(fan_in))) : 1.0f);
+        return name;
+    }
+    std::string norm(const std::string& name, int64_t rows) {
+        add(name, {rows, 1}, rows, 1, InitKind::ones, m.dtype);
+        return name;
+    }
+    void node(const std::string& id, OpKind k, std::vector<std::string> in, std::vector<std::string> out,
+              std::map<std::string, std::string> attrs = {}) {
+        g.nodes.push_back(OperatorNode{id, k, std::move(in), std::move(out), std::move(attrs)});
+    }
+};
+
+std::string num(double v) {
+    char buf[32];
+    std::snprintf(buf, sizeof buf, "%.9g", v);
+    return buf;
+}
+
+}  // namespace
+
+OperatorGraph build_decode_graph(const ModelConfig& m, const LayoutConfig& l) {
+    if (m.head_dim % l.job_rows || l.job_rows % 2) throw workload::WorkloadError("job_rows must divide head_dim and be even");
+    if (m.heads % m.kv_heads) throw workload::WorkloadError("heads must be a multiple of kv_heads");
+    if (l.max_ctx < l.ctx_pages * l.page_rows) throw workload::WorkloadError("max_ctx below ctx_pages*page_rows");
+    Builder b{{}, m, l};
+    const ElemType e = m.dtype;
+    const int64_t d = m.hidden, hd = m.head_dim, hq = m.heads, hkv = m.kv_heads, grp = hq / hkv;
+    const int64_t qrows = hq * hd, kvrows = hkv * hd, R = l.job_rows;
+    const int64_t splits = (l.ctx_pages + l.pages_per_job - 1) / l.pages_per_job;
+    const std::string eps = num(m.eps), theta = num(m.theta);
+
+    b.add("embed.table", {m.vocab, d}, 1, d, m.scaled_init ? InitKind::centered : InitKind::random, e);
+    b.vec("embed.x", d, d, e);
+    b.node("embed", OpKind::EMBED_ROW, {"embed.table"}, {"embed.x"});
+    std::string x = "embed.x";
+
+    for (int li = 0; li < m.layers; ++li) {
+        const std::string L = "L" + std::to_string(li) + ".";
+        // attention block
+        b.norm(L + "attn_norm", d);
+        b.weight(L + "wqkv", qrows + 2 * kvrows, d, R, float(d));
+        b.vec(L + "q", qrows, R, e);
+        for (const char* c : {"kc", "vc"}) {
+            TensorRef& t = b.add(L + c, {hkv, l.max_ctx, hd}, l.page_rows, hd,
+                                 m.scaled_init ? InitKind::centered : InitKind::random, e);
+            t.state = true;
+            b.view(L + c, ".seg", 1, R);
+        }
+        b.node(L + "qkv", OpKind::RMS_GEMV, {L + "wqkv", b.view(x, ".all", d), L + "attn_norm"},
+               {L + "q", L + "kc.seg", L + "vc.seg"},
+               {{"eps", eps}, {"theta", theta}, {"rope", "1"}, {"job_rows", std::to_string(R)}});
+        b.add(L + "part", {hkv * splits * grp, hd + 2}, grp, hd + 2, InitKind::zeros, ElemType::f32);
+        b.node(L + "attn", OpKind::ATTN_DECODE, {b.view(L + "q", ".grp", grp * hd), L + "kc", L + "vc"}, {L + "part"},
+               {{"ctx_pages", std::to_string(l.ctx_pages)}, {"pages_per_job", std::to_string(l.pages_per_job)}});
+        b.vec(L + "attn", qrows, grp * hd, e);
+        b.node(L + "comb", OpKind::ATTN_COMBINE, {L + "part"}, {L + "attn"});
+        b.weight(L + "wo", d, qrows, R, float(qrows));
+        b.vec(L + "x1", d, R, e);
+        b.node(L + "o", OpKind::GEMV_ADD, {L + "wo", b.view(L + "attn", ".all", qrows), b.view(x, ".blk", R)}, {L + "x1"},
+               {{"job_rows", std::to_string(R)}});
+        // MLP block
+        b.norm(L + "mlp_norm", d);
+        b.weight(L + "wgu", 2 * int64_t(m.ffn), d, l.gu_block, float(d));
+        b.vec(L + "a", m.ffn, l.gu_block / 2, e);
+        b.node(L + "gu", OpKind::RMS_GEMV, {L + "wgu", b.view(L + "x1", ".all", d), L + "mlp_norm"}, {L + "a"},
+               {{"eps", eps}, {"swiglu", std::to_string(l.gu_block)}, {"job_rows", std::to_string(l.gu_block)}});
+        b.weight(L + "wd", d, m.ffn, R, float(m.ffn));
+        b.vec(L + "x2", d, R, e);
+        b.node(L + "down", OpKind::GEMV_ADD, {L + "wd", b.view(L + "a", ".all", m.ffn), L + "x1"}, {L + "x2"},
+               {{"job_rows", std::to_string(R)}});
+        x = L + "x2";
+    }
+    b.norm("final_norm", d);
+    b.weight("lm_head", m.vocab, d, l.head_job_rows, float(d));
+    b.add("logits", {m.vocab, 1}, l.head_job_rows, 1, InitKind::zeros, ElemType::f32);
+    b.node("head", OpKind::RMS_GEMV, {"lm_head", b.view(x, ".all", d), "final_norm"}, {"logits"},
+           {{"eps", eps}, {"job_rows", std::to_string(l.head_job_rows)}});
+    b.g.validate();
+    return std::move(b.g);
+}
+
+}  // namespace uopsim::decode
