@@ -1,0 +1,1714 @@
+// Persistent sm_100a µop engine: one CTA per SM executing that SM's VMC and
+// VCC streams (see engine.cuh for the warp roles). Semantics of every µop
+// follow the reference's executable restatement (reference
+// src/elaborate.cpp:108-344) and handler arithmetic
+// (reference src/handlers.cpp:37-168); decode extensions follow
+// include/uopsim/decode_abi.h.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+
+#include "engine.cuh"
+#include "uopsim/decode_abi.h"
+#include "vdc.h"
+
+namespace vdc_dev {
+
+// ---------------------------------------------------------------------------
+// opcodes (uopsim::isa::Opcode values)
+enum : uint32_t {
+    OP_LOAD = 0x01, OP_STORE = 0x02, OP_LOAD_DEP = 0x03, OP_STORE_DEP = 0x04, OP_LOAD_LOCAL = 0x05,
+    OP_STORE_LOCAL = 0x06, OP_ALLOC = 0x07, OP_FREE = 0x08, OP_LOAD_WAIT = 0x09,
+    OP_MATVEC = 0x20, OP_GEMM_TILE = 0x21, OP_ATTN = 0x22, OP_ROPE = 0x23, OP_RMSNORM = 0x24, OP_ELEMWISE = 0x25,
+    OP_EMBED = 0x26, OP_GEMV = 0x27, OP_RMS_GEMV = 0x28, OP_GEMV_ADD = 0x29, OP_ATTN_DECODE = 0x2A,
+    OP_ATTN_COMBINE = 0x2B,
+    OP_LOOP = 0x40, OP_REPEAT = 0x41, OP_CONTINUE_IF = 0x42, OP_SET_ACC = 0x43, OP_ADD_ACC = 0x44, OP_HALT = 0x45,
+    OP_SET_ACC_MEM = 0x46,
+};
+constexpr uint32_t F_SEND = 1, F_RECV = 2, F_DYN = 4;
+
+struct Word {
+    uint32_t op, flags, kind, rank, dep, flow, size, reg0, reg1;
+    int32_t imm;
+    uint32_t tensor;
+    uint64_t payload;  // 48-bit literal offset / packed coords
+};
+
+__device__ __forceinline__ Word decode(uint4 w) {
+    Word d;
+    d.op = w.x & 0xff;
+    const uint32_t b1 = (w.x >> 8) & 0xff;
+    d.flags = b1 & 0xf;
+    d.kind = (b1 >> 4) & 3;
+    d.rank = (b1 >> 6) + 1;
+    d.dep = w.x >> 16;
+    d.flow = w.y & 0xff;
+    d.size = (w.y >> 8) & 0xffff;
+    d.reg0 = (w.y >> 28) & 0xf;
+    d.reg1 = (w.y >> 24) & 0xf;
+    d.imm = int32_t(w.z);
+    d.tensor = w.z & 0xffff;
+    d.payload = uint64_t(w.z >> 16) | (uint64_t(w.w) << 16);
+    return d;
+}
+
+__device__ __forceinline__ bool is_control(uint32_t op) { return op >= OP_LOOP; }
+__device__ __forceinline__ bool is_memory(uint32_t op) { return op < OP_MATVEC; }
+
+// ---------------------------------------------------------------------------
+// PTX helpers
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_addr(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long now_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void named_bar(int id, int threads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory"); }
+
+__device__ __forceinline__ float bf16_to_f(uint16_t b) { return __uint_as_float(uint32_t(b) << 16); }
+__device__ __forceinline__ float load_elem(const char* p, int dtype, int64_t i) {
+    return dtype == VDC_DTYPE_BF16 ? bf16_to_f(reinterpret_cast<const uint16_t*>(p)[i]) : reinterpret_cast<const float*>(p)[i];
+}
+__device__ __forceinline__ void store_elem(char* p, int dtype, int64_t i, float v) {
+    if (dtype == VDC_DTYPE_BF16)
+        reinterpret_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(v);
+    else
+        reinterpret_cast<float*>(p)[i] = v;
+}
+
+// ---------------------------------------------------------------------------
+// engine-wide state visible to all roles of one CTA
+struct Cta {
+    const EngineParams* P;
+    Control* C;
+    char* slots;
+    uint32_t sm;
+    uint32_t core_base;  // CoreId-order index of this SM's VMC
+
+    __device__ char* slot_ptr(uint32_t first) const { return slots + size_t(first) * P->slot_size; }
+    __device__ bool aborted() const { return *reinterpret_cast<volatile int32_t*>(&P->status->abort) != 0; }
+};
+
+// Spin until `cond()` (evaluated by the calling thread) holds; watchdog aware.
+// Returns false when the engine aborts.
+template <typename F>
+__device__ __forceinline__ bool spin_until(const Cta& c, F cond, uint32_t core, uint32_t pc) {
+    if (cond()) return true;
+    const unsigned long long t0 = now_ns();
+    for (uint32_t n = 0;; ++n) {
+        if (cond()) return true;
+        if ((n & 63) == 63) {
+            if (c.aborted()) return false;
+            if (c.P->watchdog_ns && now_ns() - t0 > c.P->watchdog_ns) {
+                Status* st = c.P->status;
+                const int k = atomicAdd(&st->n_stalled, 1);
+                if (k < 16) {
+                    st->stalled_core[k] = core;
+                    st->stalled_pc[k] = pc;
+                }
+                atomicExch(&st->abort, 1);
+                return false;
+            }
+        }
+        if (n > 32) __nanosleep(n > 4096 ? 256 : 32);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// address resolution (reference fold.cpp:278-293 + descriptor geometry)
+
+struct TileRef {
+    int32_t desc;
+    char* gptr;
+    int64_t gpitch;   // bytes
+    int32_t rows_at, cols_at;
+    int32_t row0, col0;
+    int32_t tile_cols;
+    int32_t elem, dtype;
+    uint32_t bytes;   // payload bytes (rows_at x cols_at)
+    int32_t storage;
+};
+
+__device__ int find_desc(const EngineParams& P, int64_t glin) {
+    int lo = 0, hi = P.n_desc - 1;
+    while (lo < hi) {  // last descriptor with base <= glin
+        const int mid = (lo + hi + 1) >> 1;
+        if (P.descs[mid].base <= glin) lo = mid; else hi = mid - 1;
+    }
+    const DevDesc& d = P.descs[lo];
+    return (glin >= d.base && glin < d.base + d.tile_count) ? lo : -1;
+}
+
+__device__ TileRef tile_of(const EngineParams& P, int di, int64_t lin) {
+    const DevDesc& d = P.descs[di];
+    int64_t c[4] = {0, 0, 0, 0};
+    for (int i = d.grid_rank - 1; i >= 0; --i) {
+        c[i] = lin % d.grid[i];
+        lin /= d.grid[i];
+    }
+    const int64_t rt = c[d.grid_rank - 2], ct = c[d.grid_rank - 1];
+    int64_t off = rt * d.tile_rows * d.cols + ct * d.tile_cols;
+    for (int i = 0; i + 2 < d.grid_rank; ++i) off += c[i] * d.lead_stride[i];
+    TileRef t;
+    t.desc = di;
+    t.elem = d.elem;
+    t.dtype = d.dtype;
+    t.gptr = d.ptr + off * d.elem;
+    t.gpitch = d.cols * d.elem;
+    t.rows_at = int32_t(min(d.tile_rows, d.rows - rt * d.tile_rows));
+    t.cols_at = int32_t(min(d.tile_cols, d.cols - ct * d.tile_cols));
+    t.row0 = int32_t(rt * d.tile_rows);
+    t.col0 = int32_t(ct * d.tile_cols);
+    t.tile_cols = int32_t(d.tile_cols);
+    t.bytes = uint32_t(t.rows_at) * uint32_t(t.cols_at) * uint32_t(d.elem);
+    t.storage = d.storage;
+    return t;
+}
+
+// resolve a memory word's address; false on an out-of-range dynamic address
+__device__ bool resolve(const EngineParams& P, const Word& w, const long long* acc, TileRef& out) {
+    if (w.kind == 2) {  // coord
+        const DevDesc& d = P.descs[w.tensor];
+        int64_t lin = 0;
+        for (int i = 0; i < d.grid_rank; ++i) {
+            const int64_t ci = i < int(w.rank) ? int64_t((w.payload >> (12 * i)) & 0xfff) : 0;
+            lin = lin * d.grid[i] + ci;
+        }
+        int di = int(w.tensor);
+        if (w.flags & F_DYN) {
+            const int64_t glin = d.base + lin + acc[w.reg0];
+            di = find_desc(P, glin);
+            if (di < 0) return false;
+            lin = glin - P.descs[di].base;
+        }
+        out = tile_of(P, di, lin);
+        return true;
+    }
+    if (w.kind == 1) {  // literal element offset: a contiguous run of up to size slots
+        const DevDesc& d = P.descs[w.tensor];
+        int64_t off = int64_t(w.payload);
+        if (w.flags & F_DYN) off += acc[w.reg0];
+        if (off < 0 || off > d.elem_count) return false;
+        const int64_t max_elems = (int64_t(max(1u, w.size)) * P.slot_size) / d.elem;
+        const int64_t n = min(max_elems, d.elem_count - off);
+        out.desc = int32_t(w.tensor);
+        out.elem = d.elem;
+        out.dtype = d.dtype;
+        out.gptr = d.ptr + off * d.elem;
+        out.gpitch = n * d.elem;
+        out.rows_at = int32_t(n);
+        out.cols_at = 1;
+        out.row0 = int32_t(off);
+        out.col0 = 0;
+        out.tile_cols = 1;
+        out.bytes = uint32_t(n * d.elem);
+        out.storage = d.storage;
+        return true;
+    }
+    out = TileRef{-1, nullptr, 0, 0, 0, 0, 0, 0, 4, 0, 0, -1};
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// VMC control-flow unit
+
+struct LoopFrame {
+    uint32_t start, remaining;
+};
+
+__device__ void cfu_role(Cta& c) {
+    const EngineParams& P = *c.P;
+    Control& C = *c.C;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t core = c.core_base;
+    const uint32_t w0 = P.core_off[core], n = P.core_off[core + 1] - w0;
+    long long acc[16];
+    for (int i = 0; i < 16; ++i) acc[i] = 0;
+    LoopFrame loops[8];
+    int depth = 0;
+    uint32_t chunk = 0xffffffffu;
+    const uint32_t budget_mask = P.slot_budget >= 32 ? 0xffffffffu : ((1u << P.slot_budget) - 1u);
+    unsigned long long uops = 0;
+    uint32_t m2c_head[kMaxVcc] = {0, 0};
+    uint32_t unit_head_ldu[kMaxLdu] = {0, 0}, unit_head_stu[kMaxStu] = {0, 0};
+
+    // the next chunk is held in registers (two words per lane) while the
+    // current one is decoded from shared memory, hiding the stream fetch
+    uint4 pre0 = make_uint4(0, 0, 0, 0), pre1 = make_uint4(0, 0, 0, 0);
+    uint32_t pre_chunk = 0xffffffffu;
+    auto prefetch = [&](uint32_t ch) {
+        const uint32_t a0 = ch * kCfuChunk + lane, a1 = a0 + 32;
+        pre0 = a0 < n ? __ldg(&P.words[w0 + a0]) : make_uint4(0, 0, 0, 0);
+        pre1 = a1 < n ? __ldg(&P.words[w0 + a1]) : make_uint4(0, 0, 0, 0);
+        pre_chunk = ch;
+    };
+    for (uint32_t pc = 0; pc < n;) {
+        if (c.aborted()) break;
+        const uint32_t want = pc / kCfuChunk;
+        if (want != chunk) {  // warp-cooperative refill of the stream buffer
+            if (pre_chunk != want) prefetch(want);
+            __syncwarp();
+            C.cfu_buf[lane] = pre0;
+            C.cfu_buf[lane + 32] = pre1;
+            __syncwarp();
+            chunk = want;
+            prefetch(want + 1);
+        }
+        const Word w = decode(C.cfu_buf[pc % kCfuChunk]);
+        ++uops;
+        if (is_control(w.op)) {
+            switch (w.op) {
+                case OP_LOOP:
+                    if (w.size == 0) {
+                        pc += uint32_t(w.imm) + 2;
+                    } else {
+                        if (depth < 8) loops[depth++] = {pc + 1, w.size};
+                        ++pc;
+                    }
+                    break;
+                case OP_REPEAT:
+                    if (depth > 0 && --loops[depth - 1].remaining > 0) {
+                        pc = loops[depth - 1].start;
+                    } else {
+                        if (depth > 0) --depth;
+                        ++pc;
+                    }
+                    break;
+                case OP_SET_ACC: acc[w.reg0] = w.imm; ++pc; break;
+                case OP_ADD_ACC: acc[w.reg0] += w.imm; ++pc; break;
+                case OP_SET_ACC_MEM: {
+                    const int idx = w.imm & 0xff;
+                    const long long mult = (w.imm >> 8) ? (w.imm >> 8) : 1;
+                    acc[w.reg0] = (idx < P.n_step ? P.step[idx] : 0) * mult;
+                    ++pc;
+                    break;
+                }
+                case OP_CONTINUE_IF:
+                    if (depth > 0 && acc[w.reg0] == w.imm) {
+                        // skip to the innermost REPEAT (scan in global memory)
+                        uint32_t q = pc + 1;
+                        for (int nest = 0; q < n; ++q) {
+                            const uint32_t op = __ldg(&P.words[w0 + q]).x & 0xff;
+                            if (op == OP_LOOP) ++nest;
+                            if (op == OP_REPEAT && nest-- == 0) break;
+                        }
+                        pc = q;
+                    } else {
+                        ++pc;
+                    }
+                    break;
+                default:  // HALT
+                    pc = n;
+                    break;
+            }
+            continue;
+        }
+        if (!is_memory(w.op)) {  // compute word in a VMC stream: program error
+            if (lane == 0) {
+                P.status->fault_code = 1;
+                P.status->fault_info = pc;
+                atomicExch(&P.status->abort, 2);
+            }
+            break;
+        }
+        TileRef t;
+        if (!resolve(P, w, acc, t)) {
+            if (lane == 0) {
+                P.status->fault_code = 2;
+                P.status->fault_info = pc;
+                atomicExch(&P.status->abort, 2);
+            }
+            break;
+        }
+        const bool allocates = (w.op == OP_LOAD || w.op == OP_LOAD_DEP || w.op == OP_ALLOC || w.op == OP_LOAD_WAIT) && w.size > 0;
+        uint32_t first = 0, count = allocates ? w.size : 0;
+        bool ok = true;
+        if (allocates) {  // in-order, first-fit contiguous allocation
+            uint32_t got = 0xffffffffu;
+            if (lane == 0) {
+                const unsigned long long t0 = clock64();
+                ok = spin_until(c, [&] {
+                    const uint32_t freebits = ~C.alloc_mask & budget_mask;
+                    uint32_t runs = freebits;
+                    for (uint32_t k = 1; k < count && runs; ++k) runs &= freebits >> k;
+                    if (!runs) return false;
+                    got = __ffs(runs) - 1;
+                    return true;
+                }, core, pc);
+                if (ok) {
+                    const uint32_t bits = (count >= 32 ? 0xffffffffu : ((1u << count) - 1u)) << got;
+                    atomicOr(const_cast<uint32_t*>(&C.alloc_mask), bits);
+                }
+                c.P->stats[c.sm].cfu_stall_cycles += clock64() - t0;
+            }
+            ok = __shfl_sync(0xffffffffu, ok, 0);
+            first = __shfl_sync(0xffffffffu, got, 0);
+            if (!ok) break;
+        }
+        // m2c reservation (stream order per VCC)
+        uint32_t m2c_idx = 0;
+        if (w.flags & F_SEND) {
+            const uint32_t v = w.reg1;
+            m2c_idx = m2c_head[v];
+            if (lane == 0) {
+                ok = spin_until(c, [&] { return m2c_idx - C.m2c_ring[v].tail < uint32_t(kM2cDepth); }, core, pc);
+                if (ok) {
+                    M2C& e = C.m2c[v][m2c_idx % kM2cDepth];
+                    const bool data = w.op != OP_ALLOC && w.op != OP_LOAD_LOCAL && t.bytes > 0;
+                    uint32_t parity = 0;
+                    if (data) {
+                        parity = C.bar_uses[first] & 1;
+                        C.bar_uses[first] += 1;
+                    }
+                    e.slots = first | (count << 8);
+                    e.rows = t.rows_at;
+                    e.cols = t.cols_at;
+                    e.stride = t.tile_cols;
+                    e.row0 = t.row0;
+                    e.col0 = t.col0;
+                    e.meta = uint32_t(t.dtype) | (parity << 8) | ((data ? 1u : 0u) << 9) | (first << 16);
+                    if (w.op == OP_ALLOC) {
+                        __threadfence_block();
+                        e.ready = m2c_idx + 1;
+                    }
+                }
+            }
+            ok = __shfl_sync(0xffffffffu, ok, 0);
+            if (!ok) break;
+            m2c_head[w.reg1] = m2c_idx + 1;
+            if (lane == 0) C.m2c_ring[w.reg1].head = m2c_idx + 1;
+        }
+        if (w.op == OP_ALLOC) {
+            ++pc;
+            continue;
+        }
+        // dispatch to the flow's unit
+        const bool load_unit = w.op == OP_LOAD || w.op == OP_LOAD_DEP || w.op == OP_LOAD_LOCAL || w.op == OP_LOAD_WAIT;
+        const uint32_t u = load_unit ? w.flow % P.ldu_count : w.flow % P.stu_count;
+        Ring& ring = load_unit ? C.ldu_ring[u] : C.stu_ring[u];
+        uint32_t& head = load_unit ? unit_head_ldu[u] : unit_head_stu[u];
+        if (lane == 0) {
+            ok = spin_until(c, [&] { return head - ring.tail < uint32_t(kUnitDepth); }, core, pc);
+            if (ok) {
+                UnitOp& q = load_unit ? C.ldu_q[u][head % kUnitDepth] : C.stu_q[u][head % kUnitDepth];
+                q.op = uint8_t(w.op);
+                q.flags = uint8_t(w.flags);
+                q.reg1 = uint8_t(w.reg1);
+                q.dtype = uint8_t(t.dtype);
+                q.dep_id = uint16_t(w.dep);
+                q.size = uint16_t(w.size);
+                q.slots = first | (count << 8);
+                q.m2c = m2c_idx;
+                q.storage = t.storage;
+                q.bytes = (w.size == 0 && w.op != OP_LOAD_LOCAL) ? 0 : t.bytes;
+                q.rows_at = t.rows_at;
+                q.cols_at = t.cols_at;
+                q.elem = t.elem;
+                q.tile_cols = t.tile_cols;
+                q.gptr = t.gptr;
+                q.gpitch = t.gpitch;
+                q.core_pc = pc;
+                __threadfence_block();
+                ring.head = head + 1;
+            }
+        }
+        ok = __shfl_sync(0xffffffffu, ok, 0);
+        if (!ok) break;
+        ++head;
+        ++pc;
+    }
+    if (lane == 0) {
+        c.P->stats[c.sm].uops += uops;
+        __threadfence_block();
+        atomicAdd(const_cast<int32_t*>(&C.done_roles), 1);  // CFU finished dispatching
+    }
+    __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// load unit
+
+// copy one tile region global -> shared; completes the slot barrier
+__device__ void copy_in(Cta& c, const UnitOp& q, uint32_t lane) {
+    Control& C = *c.C;
+    const uint32_t first = q.slots & 0xff;
+    char* dst = c.slot_ptr(first);
+    uint64_t* bar = &C.full_bar[first];
+    const uint32_t row_bytes = uint32_t(q.cols_at) * q.elem;
+    const uint32_t spitch = uint32_t(q.tile_cols) * q.elem;
+    const bool contiguous = q.rows_at == 1 || (int64_t(row_bytes) == q.gpitch && row_bytes == spitch);
+    const bool aligned = (reinterpret_cast<uintptr_t>(q.gptr) & 15) == 0;
+    if (contiguous && aligned && (q.bytes & 15) == 0) {
+        if (lane == 0) {
+            mbar_expect_tx(bar, q.bytes);
+            bulk_g2s(dst, q.gptr, q.bytes, bar);
+        }
+    } else if (aligned && (row_bytes & 15) == 0 && (q.gpitch & 15) == 0 && (spitch & 15) == 0) {
+        if (lane == 0) mbar_expect_tx(bar, q.bytes);
+        __syncwarp();
+        for (int r = int(lane); r < q.rows_at; r += 32) bulk_g2s(dst + size_t(r) * spitch, q.gptr + r * q.gpitch, row_bytes, bar);
+    } else {  // odd geometry: cooperative element copy, then a plain arrive
+        const int elems = q.rows_at * q.cols_at;
+        for (int i = int(lane); i < elems; i += 32) {
+            const int r = i / q.cols_at, col = i % q.cols_at;
+            const char* s = q.gptr + r * q.gpitch + int64_t(col) * q.elem;
+            char* d = dst + size_t(r) * spitch + size_t(col) * q.elem;
+            if (q.elem == 4) *reinterpret_cast<uint32_t*>(d) = *reinterpret_cast<const volatile uint32_t*>(s);
+            else if (q.elem == 2) *reinterpret_cast<uint16_t*>(d) = *reinterpret_cast<const volatile uint16_t*>(s);
+            else *reinterpret_cast<uint64_t*>(d) = *reinterpret_cast<const volatile uint64_t*>(s);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar);
+    }
+}
+
+__device__ void ldu_role(Cta& c, uint32_t u) {
+    const EngineParams& P = *c.P;
+    Control& C = *c.C;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t core = c.core_base;
+    unsigned long long bytes = 0;
+    for (uint32_t tail = 0;; ++tail) {
+        bool ok = true, have = false;
+        if (lane == 0) {
+            ok = spin_until(c, [&] {
+                if (C.ldu_ring[u].head != tail) {
+                    have = true;
+                    return true;
+                }
+                return C.done_roles > 0 && C.ldu_ring[u].head == tail;  // CFU done and drained
+            }, core, 0xffff0000u | tail);
+        }
+        ok = __shfl_sync(0xffffffffu, ok, 0);
+        have = __shfl_sync(0xffffffffu, have, 0);
+        if (!ok || !have) break;
+        __threadfence_block();
+        const UnitOp q = C.ldu_q[u][tail % kUnitDepth];
+        M2C* e = (q.flags & F_SEND) ? &C.m2c[q.reg1][q.m2c % kM2cDepth] : nullptr;
+        // dependency side
+        if (q.op == OP_LOAD_DEP || q.op == OP_LOAD_LOCAL) {
+            DepQueue* dq = &P.deps[q.dep_id];
+            uint32_t payload[4] = {0, 0, 0, 0};
+            if (lane == 0) {
+                const uint32_t mine = dq->consumed;
+                ok = spin_until(c, [&] { return ld_acquire(&dq->produced) > mine; }, core, q.core_pc);
+                if (ok) {
+                    for (int i = 0; i < 4; ++i) payload[i] = reinterpret_cast<volatile uint32_t*>(dq->payload)[i];
+                    st_release(&dq->consumed, mine + 1);
+                }
+            }
+            ok = __shfl_sync(0xffffffffu, ok, 0);
+            if (!ok) break;
+            if (q.op == OP_LOAD_LOCAL) {  // slot ownership arrives with the token
+                if (lane == 0 && e) {
+                    e->slots = payload[0];
+                    e->rows = int32_t(payload[1]);
+                    e->cols = int32_t(payload[2]);
+                    e->stride = int32_t(payload[3]);
+                    e->meta &= ~(1u << 9);  // no data movement to wait for
+                    __threadfence_block();
+                    e->ready = q.m2c + 1;
+                }
+                __syncwarp();
+                if (lane == 0) C.ldu_ring[u].tail = tail + 1;
+                continue;
+            }
+            if (lane == 0) fence_proxy_async();
+        }
+        if (q.op == OP_LOAD_WAIT && q.dep_id) {
+            if (lane == 0) {
+                const uint32_t* ctr = &P.counters[q.storage];
+                ok = spin_until(c, [&] { return ld_acquire(ctr) >= q.dep_id; }, core, q.core_pc);
+                fence_proxy_async();
+            }
+            ok = __shfl_sync(0xffffffffu, ok, 0);
+            if (!ok) break;
+        }
+        if (q.bytes > 0 && (q.slots >> 8) > 0) {
+            copy_in(c, q, lane);
+            bytes += q.bytes;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            if (e) {
+                __threadfence_block();
+                e->ready = q.m2c + 1;
+            }
+            C.ldu_ring[u].tail = tail + 1;
+        }
+    }
+    if (lane == 0) atomicAdd(&c.P->stats[c.sm].bytes_loaded, bytes);
+}
+
+// ---------------------------------------------------------------------------
+// store unit
+
+__device__ __forceinline__ void free_slots(Control& C, uint32_t slots) {
+    const uint32_t first = slots & 0xff, count = slots >> 8;
+    if (!count) return;
+    const uint32_t bits = (count >= 32 ? 0xffffffffu : ((1u << count) - 1u)) << first;
+    atomicAnd(const_cast<uint32_t*>(&C.alloc_mask), ~bits);
+}
+
+// slot -> global copy of the target tile (generic stores, warp-cooperative)
+__device__ void copy_out(Cta& c, const UnitOp& q, const C2M& m, uint32_t lane) {
+    const char* src = c.slot_ptr(m.slots & 0xff);
+    const int rows = q.rows_at, cols = q.cols_at;
+    const uint32_t spitch = uint32_t(q.tile_cols) * q.elem;
+    const uint32_t row_bytes = uint32_t(cols) * q.elem;
+    const bool contiguous = rows == 1 || (int64_t(row_bytes) == q.gpitch && row_bytes == spitch);
+    if (contiguous && (reinterpret_cast<uintptr_t>(q.gptr) & 15) == 0 && (q.bytes & 15) == 0) {
+        const int n16 = int(q.bytes >> 4);
+        for (int i = int(lane); i < n16; i += 32)
+            reinterpret_cast<uint4*>(q.gptr)[i] = reinterpret_cast<const uint4*>(src)[i];
+    } else {
+        const int elems = rows * cols;
+        for (int i = int(lane); i < elems; i += 32) {
+            const int r = i / cols, col = i % cols;
+            char* d = q.gptr + r * q.gpitch + int64_t(col) * q.elem;
+            const char* s = src + size_t(r) * spitch + size_t(col) * q.elem;
+            if (q.elem == 4) *reinterpret_cast<uint32_t*>(d) = *reinterpret_cast<const uint32_t*>(s);
+            else if (q.elem == 2) *reinterpret_cast<uint16_t*>(d) = *reinterpret_cast<const uint16_t*>(s);
+            else *reinterpret_cast<uint64_t*>(d) = *reinterpret_cast<const uint64_t*>(s);
+        }
+    }
+}
+
+__device__ void stu_role(Cta& c, uint32_t u) {
+    const EngineParams& P = *c.P;
+    Control& C = *c.C;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t core = c.core_base;
+    // each VCC's c2m ring is popped by exactly one STU (checked at load time)
+    uint32_t c2m_tail[kMaxVcc] = {0, 0};
+    unsigned long long bytes = 0;
+    for (uint32_t tail = 0;; ++tail) {
+        bool ok = true, have = false;
+        if (lane == 0) {
+            ok = spin_until(c, [&] {
+                if (C.stu_ring[u].head != tail) {
+                    have = true;
+                    return true;
+                }
+                return C.done_roles > 0 && C.stu_ring[u].head == tail;
+            }, core, 0xfffe0000u | tail);
+        }
+        ok = __shfl_sync(0xffffffffu, ok, 0);
+        have = __shfl_sync(0xffffffffu, have, 0);
+        if (!ok || !have) break;
+        __threadfence_block();
+        const UnitOp q = C.stu_q[u][tail % kUnitDepth];
+        const uint32_t v = q.reg1;
+        const bool recv = (q.flags & F_RECV) != 0;
+        const uint32_t need = q.op == OP_FREE ? q.size : (recv ? 1u : 0u);
+        if (need) {
+            if (lane == 0) {
+                const uint32_t t0 = c2m_tail[v];
+                ok = spin_until(c, [&] { return C.c2m_ring[v].head - t0 >= need; }, core, q.core_pc);
+            }
+            ok = __shfl_sync(0xffffffffu, ok, 0);
+            if (!ok) break;
+            __threadfence_block();
+        }
+        C2M first_msg = need ? C.c2m[v][c2m_tail[v] % kC2mDepth] : C2M{0, 0, 0, 0};
+        if (q.op == OP_FREE) {
+            if (lane == 0)
+                for (uint32_t i = 0; i < need; ++i) free_slots(C, C.c2m[v][(c2m_tail[v] + i) % kC2mDepth].slots);
+        } else if (q.op == OP_STORE || q.op == OP_STORE_DEP || q.op == OP_STORE_LOCAL) {
+            const bool data = q.op != OP_STORE_LOCAL && recv && q.size > 0 && q.bytes > 0;
+            if (data) {
+                copy_out(c, q, first_msg, lane);
+                bytes += q.bytes;
+                __syncwarp();
+            }
+            if (lane == 0) {
+                if (data) {
+                    __threadfence();
+                    if (q.storage >= 0) red_release_add(&P.counters[q.storage], 1u);
+                }
+                if (q.op == OP_STORE_DEP || q.op == OP_STORE_LOCAL) {
+                    DepQueue* dq = &P.deps[q.dep_id];
+                    const uint32_t made = dq->produced;
+                    ok = spin_until(c, [&] { return made - ld_acquire(&dq->consumed) < dq->depth; }, core, q.core_pc);
+                    if (ok) {
+                        if (q.op == OP_STORE_LOCAL) {
+                            volatile uint32_t* pl = dq->payload;
+                            pl[0] = first_msg.slots;
+                            pl[1] = uint32_t(first_msg.rows);
+                            pl[2] = uint32_t(first_msg.cols);
+                            pl[3] = uint32_t(first_msg.stride);
+                        }
+                        __threadfence();
+                        st_release(&dq->produced, made + 1);
+                    }
+                }
+                if ((q.op == OP_STORE || q.op == OP_STORE_DEP) && recv) free_slots(C, first_msg.slots);
+            }
+            ok = __shfl_sync(0xffffffffu, ok, 0);
+            if (!ok) break;
+        }
+        if (need) {
+            c2m_tail[v] += need;
+            if (lane == 0) C.c2m_ring[v].tail = c2m_tail[v];
+        }
+        if (lane == 0) C.stu_ring[u].tail = tail + 1;
+    }
+    if (lane == 0) atomicAdd(&c.P->stats[c.sm].bytes_stored, bytes);
+}
+
+// ---------------------------------------------------------------------------
+// compute virtual core
+
+struct Msg {
+    char* data;
+    int32_t rows, cols, stride, row0, col0, dtype;
+    uint32_t slots;
+};
+
+struct Vcc {
+    Cta* c;
+    uint32_t v;        // vcc index on the SM
+    uint32_t t;        // thread in the VCC (0..127)
+    uint32_t core;     // CoreId-order index
+    int bar;           // named barrier id
+    uint32_t m2c_tail = 0, c2m_head = 0;
+    long long acc[16];
+    bool ok = true;
+
+    __device__ void sync() const { named_bar(bar, 32 * kVccWarps); }
+
+    __device__ bool pop(Msg& m, uint32_t pc) {
+        Control& C = *c->C;
+        M2C& e = C.m2c[v][m2c_tail % kM2cDepth];
+        const uint32_t want = m2c_tail + 1;
+        bool good = true;
+        if (t == 0) good = spin_until(*c, [&] { return e.ready == want; }, core, pc);
+        sync();
+        if (t == 0) C.red[v][0] = good ? 1.f : 0.f;
+        sync();
+        if (C.red[v][0] == 0.f) {
+            ok = false;
+            return false;
+        }
+        __threadfence_block();
+        const uint32_t meta = e.meta;
+        m.slots = e.slots;
+        m.rows = e.rows;
+        m.cols = e.cols;
+        m.stride = e.stride;
+        m.row0 = e.row0;
+        m.col0 = e.col0;
+        m.dtype = int32_t(meta & 0xff);
+        m.data = c->slot_ptr(m.slots & 0xff);
+        if (meta & (1u << 9)) {
+            uint64_t* b = &C.full_bar[meta >> 16];
+            const uint32_t parity = (meta >> 8) & 1;
+            while (!mbar_try(b, parity)) {
+            }
+        }
+        ++m2c_tail;
+        sync();
+        if (t == 0) C.m2c_ring[v].tail = m2c_tail;
+        return true;
+    }
+
+    // wait for entry m2c_tail + i and read it without consuming it
+    __device__ bool peek(int i, Msg& m, uint32_t pc) {
+        Control& C = *c->C;
+        M2C& e = C.m2c[v][(m2c_tail + i) % kM2cDepth];
+        const uint32_t want = m2c_tail + i + 1;
+        bool good = true;
+        if (t == 0) good = spin_until(*c, [&] { return e.ready == want; }, core, pc);
+        sync();
+        if (t == 0) C.red[v][0] = good ? 1.f : 0.f;
+        sync();
+        if (C.red[v][0] == 0.f) {
+            ok = false;
+            return false;
+        }
+        __threadfence_block();
+        const uint32_t meta = e.meta;
+        m.slots = e.slots;
+        m.rows = e.rows;
+        m.cols = e.cols;
+        m.stride = e.stride;
+        m.row0 = e.row0;
+        m.col0 = e.col0;
+        m.dtype = int32_t(meta & 0xff);
+        m.data = c->slot_ptr(m.slots & 0xff);
+        if (meta & (1u << 9)) {
+            uint64_t* b = &C.full_bar[meta >> 16];
+            const uint32_t parity = (meta >> 8) & 1;
+            while (!mbar_try(b, parity)) {
+            }
+        }
+        return true;
+    }
+    __device__ void advance(int n) {
+        m2c_tail += uint32_t(n);
+        sync();
+        if (t == 0) c->C->m2c_ring[v].tail = m2c_tail;
+    }
+
+    // release a region (all threads must be done with it: call after sync())
+    __device__ bool push(const Msg& m, uint32_t pc) {
+        Control& C = *c->C;
+        bool good = true;
+        if (t == 0) {
+            const uint32_t h = c2m_head;
+            good = spin_until(*c, [&] { return h - C.c2m_ring[v].tail < uint32_t(kC2mDepth); }, core, pc);
+            if (good) {
+                C2M& e = C.c2m[v][h % kC2mDepth];
+                e.slots = m.slots;
+                e.rows = m.rows;
+                e.cols = m.cols;
+                e.stride = m.stride;
+                __threadfence_block();
+                C.c2m_ring[v].head = h + 1;
+            }
+        }
+        ++c2m_head;
+        if (!good) ok = false;
+        return good;
+    }
+};
+
+__device__ __forceinline__ float warp_sum(float x) {
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+__device__ __forceinline__ float warp_max(float x) {
+    for (int o = 16; o; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
+    return x;
+}
+
+// block (VCC) reduction of one float; all threads get the result
+__device__ float vcc_sum(Vcc& k, float x) {
+    Control& C = *k.c->C;
+    x = warp_sum(x);
+    if ((k.t & 31) == 0) C.red[k.v][1 + (k.t >> 5)] = x;
+    k.sync();
+    float s = 0.f;
+    for (int i = 0; i < kVccWarps; ++i) s += C.red[k.v][1 + i];
+    k.sync();
+    return s;
+}
+
+// ---- reference handlers (non-streaming: every pop first, result slot is the accumulator)
+
+__device__ void h_reference(Vcc& k, const Word& w, uint32_t pc) {
+    // pops: prologue, groups, result (reference isa.cpp:511-526 HandlerIo)
+    int pro = 0, per = 2;
+    switch (w.op) {
+        case OP_ATTN: pro = 1; per = 2; break;
+        case OP_ELEMWISE: pro = 0; per = 1; break;
+        case OP_EMBED: pro = 1; per = 1; break;
+        default: pro = 0; per = 2; break;
+    }
+    const int groups = int(w.size);
+    const int total = pro + per * groups + 1;
+    if (total > kM2cDepth) {
+        if (k.t == 0) {
+            k.c->P->status->fault_code = 3;
+            atomicExch(&k.c->P->status->abort, 2);
+        }
+        k.ok = false;
+        return;
+    }
+    // every message stays in the m2c ring until the job retires (ring depth >= pops)
+    auto msg = [&](int i, Msg& m) { return k.peek(i, m, pc); };
+    Msg res;
+    if (!msg(total - 1, res)) return;
+
+    const int orows = res.rows, ocols = res.cols, ostride = res.stride;
+    float* acc = reinterpret_cast<float*>(res.data);  // reference outputs are fp32
+    float* ml = k.c->C->acc[k.v];                      // ATTN running max / sum per row
+    for (int i = int(k.t); i < orows * ostride; i += 32 * kVccWarps) acc[i] = 0.f;
+    if (w.op == OP_ATTN)
+        for (int r = int(k.t); r < orows; r += 32 * kVccWarps) {
+            ml[r] = -INFINITY;
+            ml[kAccRows / 2 + r] = 0.f;
+        }
+    k.sync();
+    auto at = [](const Msg& g, int r, int col) { return load_elem(g.data, g.dtype, int64_t(r) * g.stride + col); };
+    Msg pro_msg{};
+    if (pro && !msg(0, pro_msg)) return;
+    for (int gi = 0; gi < groups; ++gi) {
+        Msg in[2];
+        for (int i = 0; i < per; ++i)
+            if (!msg(pro + gi * per + i, in[i])) return;
+        switch (w.op) {
+            case OP_MATVEC:
+            case OP_GEMM_TILE: {  // in[0] = B (k x n), in[1] = A (m x k)
+                const Msg &b = in[0], &a = in[1];
+                for (int o = int(k.t); o < a.rows * b.cols; o += 32 * kVccWarps) {
+                    const int r = o / b.cols, col = o % b.cols;
+                    float s = 0.f;
+                    for (int kk = 0; kk < a.cols; ++kk) s += at(a, r, kk) * at(b, kk, col);
+                    acc[r * ostride + col] += s;
+                }
+                break;
+            }
+            case OP_ATTN: {  // online softmax (reference handlers.cpp:54-87), warp per q row
+                const Msg &kt = in[0], &vt = in[1], &q = pro_msg;
+                const float scale = 1.0f / sqrtf(float(q.cols));
+                const int lane = int(k.t & 31), wp = int(k.t >> 5);
+                for (int r = wp; r < q.rows; r += kVccWarps) {
+                    float rmax = ml[r];
+                    for (int j = lane; j < kt.rows; j += 32) {
+                        float s = 0.f;
+                        for (int d = 0; d < q.cols; ++d) s += at(q, r, d) * at(kt, j, d);
+                        rmax = fmaxf(rmax, s * scale);
+                    }
+                    rmax = warp_max(rmax);
+                    const float mold = ml[r];
+                    const float sc = mold == -INFINITY ? 0.f : expf(mold - rmax);
+                    float sum = 0.f;
+                    for (int j = lane; j < kt.rows; j += 32) {
+                        float s = 0.f;
+                        for (int d = 0; d < q.cols; ++d) s += at(q, r, d) * at(kt, j, d);
+                        sum += expf(s * scale - rmax);
+                    }
+                    sum = warp_sum(sum);
+                    for (int col = lane; col < ocols; col += 32) {
+                        float o = acc[r * ostride + col] * sc;
+                        for (int j = 0; j < kt.rows; ++j) {
+                            float s = 0.f;
+                            for (int d = 0; d < q.cols; ++d) s += at(q, r, d) * at(kt, j, d);
+                            o += expf(s * scale - rmax) * at(vt, j, col);
+                        }
+                        acc[r * ostride + col] = o;
+                    }
+                    __syncwarp();
+                    if (lane == 0) {
+                        ml[kAccRows / 2 + r] = ml[kAccRows / 2 + r] * sc + sum;
+                        ml[r] = rmax;
+                    }
+                }
+                break;
+            }
+            case OP_ROPE: {  // in[0] = x, in[1] = angles; consecutive row pairs
+                const Msg &x = in[0], &th = in[1];
+                for (int r = 2 * int(k.t); r + 1 < x.rows; r += 2 * 32 * kVccWarps) {
+                    const float ang = at(th, r, 0), cs = cosf(ang), sn = sinf(ang);
+                    const float a = at(x, r, 0), b = at(x, r + 1, 0);
+                    acc[r * ostride] = a * cs - b * sn;
+                    acc[(r + 1) * ostride] = a * sn + b * cs;
+                }
+                break;
+            }
+            case OP_RMSNORM: {
+                const Msg &x = in[0], &g = in[1];
+                float ss = 0.f;
+                for (int r = int(k.t); r < x.rows; r += 32 * kVccWarps) {
+                    const float v = at(x, r, 0);
+                    ss += v * v;
+                }
+                ss = vcc_sum(k, ss);
+                const float inv = 1.0f / sqrtf(ss / float(x.rows) + 1e-5f);
+                for (int r = int(k.t); r < x.rows; r += 32 * kVccWarps) acc[r * ostride] = at(x, r, 0) * inv * at(g, r, 0);
+                break;
+            }
+            case OP_ELEMWISE: {
+                const Msg& x = in[0];
+                const bool unary = groups == 1 && gi == 0 && w.imm <= 1;
+                for (int o = int(k.t); o < x.rows * x.cols; o += 32 * kVccWarps) {
+                    const int r = o / x.cols, col = o % x.cols;
+                    const float v = at(x, r, col);
+                    float& a = acc[r * ocols + col];  // reference indexes acc with out.cols
+                    if (unary) a = w.imm == 0 ? (v > 0.f ? v : 0.f) : v / (1.0f + expf(-v));
+                    else if (gi == 0) a = v;
+                    else a = w.imm == 3 ? a * v : a + v;
+                }
+                break;
+            }
+            case OP_EMBED: {  // prologue = id column; groups sweep table row tiles
+                const Msg &table = in[0], &ids = pro_msg;
+                for (int o = int(k.t); o < orows * ocols; o += 32 * kVccWarps) {
+                    const int r = o / ocols, col = o % ocols;
+                    const long id = lroundf(at(ids, r, 0));
+                    const long local = id - table.row0;
+                    if (local < 0 || local >= table.rows) continue;
+                    acc[r * ocols + col] = at(table, int(local), col);
+                }
+                break;
+            }
+            default:
+                break;
+        }
+        k.sync();
+    }
+    if (w.op == OP_ATTN)  // finalize: normalise by the running sum
+        for (int o = int(k.t); o < orows * ocols; o += 32 * kVccWarps) {
+            const int r = o / ocols, col = o % ocols;
+            const float l = ml[kAccRows / 2 + r];
+            acc[r * ostride + col] = l > 0.f ? acc[r * ostride + col] / l : 0.f;
+        }
+    // ELEMWISE / EMBED index the scratch with out.cols (reference handlers.cpp:118-149);
+    // with a padded stride the payload must be re-laid out before the store.
+    if ((w.op == OP_ELEMWISE || w.op == OP_EMBED) && ostride != ocols) {
+        k.sync();
+        for (int r = orows - 1; r >= 0; --r) {
+            for (int col = ocols - 1 - int(k.t); col >= 0; col -= 32 * kVccWarps) acc[r * ostride + col] = acc[r * ocols + col];
+            k.sync();
+        }
+    }
+    k.sync();
+    // releases: iteration inputs, epilogue (prologue), result — in m2c order
+    for (int gi = 0; gi < groups; ++gi)
+        for (int i = 0; i < per; ++i) {
+            Msg m;
+            if (!msg(pro + gi * per + i, m) || !k.push(m, pc)) return;
+        }
+    if (pro && !k.push(pro_msg, pc)) return;
+    k.push(res, pc);
+    k.advance(total);
+}
+
+// ---- decode handlers (streaming)
+
+__device__ __forceinline__ float dot_bf16x8(uint4 a, uint4 b) {
+    float s = 0.f;
+    const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        s = fmaf(__uint_as_float(av[i] << 16), __uint_as_float(bv[i] << 16), s);
+        s = fmaf(__uint_as_float(av[i] & 0xffff0000u), __uint_as_float(bv[i] & 0xffff0000u), s);
+    }
+    return s;
+}
+
+__device__ void h_gemv(Vcc& k, const Word& w, uint32_t pc) {
+    Control& C = *k.c->C;
+    const EngineParams& P = *k.c->P;
+    const int pbase = w.imm >> 8, variant = w.imm & 0xff;
+    const float* hp = P.hparams + pbase;
+    const int lane = int(k.t & 31), wp = int(k.t >> 5);
+    Msg x, third{}, g, res;
+    if (!k.pop(x, pc)) return;
+    const bool has_third = w.op != OP_GEMV;
+    if (has_third && !k.pop(third, pc)) return;
+    const int K = x.rows * x.cols;
+    float* acc = C.acc[k.v];
+    for (int i = int(k.t); i < kAccRows; i += 32 * kVccWarps) acc[i] = 0.f;
+    if (w.op == OP_RMS_GEMV) {  // x <- round(x * rsqrt(mean(x^2) + eps) * w), in place
+        float ss = 0.f;
+        for (int i = int(k.t); i < K; i += 32 * kVccWarps) {
+            const float v = load_elem(x.data, x.dtype, i);
+            ss += v * v;
+        }
+        ss = vcc_sum(k, ss);
+        const float inv = 1.0f / sqrtf(ss / float(K) + hp[VDC_GEMV_P_EPS]);
+        for (int i = int(k.t); i < K; i += 32 * kVccWarps)
+            store_elem(x.data, x.dtype, i, load_elem(x.data, x.dtype, i) * inv * load_elem(third.data, third.dtype, i));
+    }
+    k.sync();
+    int job_row0 = -1, raw_rows = 0;
+    for (int gi = 0; gi < int(w.size); ++gi) {
+        if (!k.pop(g, pc)) return;
+        if (job_row0 < 0) job_row0 = g.row0;
+        const int rbase = g.row0 - job_row0;
+        raw_rows = max(raw_rows, rbase + g.rows);
+        const bool fast = g.dtype == VDC_DTYPE_BF16 && x.dtype == VDC_DTYPE_BF16 && (g.cols & 7) == 0 &&
+                          (g.stride & 7) == 0 && (g.col0 & 7) == 0;
+        for (int r = wp; r < g.rows; r += kVccWarps) {
+            float s = 0.f;
+            if (fast) {
+                const uint4* wr = reinterpret_cast<const uint4*>(g.data + size_t(r) * g.stride * 2);
+                const uint4* xv = reinterpret_cast<const uint4*>(x.data + size_t(g.col0) * 2);
+                const int n8 = g.cols >> 3;
+                for (int ch = lane; ch < n8; ch += 32) s += dot_bf16x8(wr[ch], xv[ch]);
+            } else {
+                for (int col = lane; col < g.cols; col += 32)
+                    s += load_elem(g.data, g.dtype, int64_t(r) * g.stride + col) * load_elem(x.data, x.dtype, g.col0 + col);
+            }
+            s = warp_sum(s);
+            if (lane == 0 && rbase + r < kAccRows) acc[rbase + r] += s;
+        }
+        k.sync();
+        if (!k.push(g, pc)) return;
+    }
+    if (!k.pop(res, pc)) return;
+    k.sync();
+    // epilogue
+    const int nout = res.rows * res.cols;
+    if (variant & VDC_GEMV_SWIGLU) {
+        const int B = int(hp[VDC_GEMV_P_SWIGLU_BLOCK]);
+        for (int o = int(k.t); o < nout; o += 32 * kVccWarps) {
+            const int blk = o / (B / 2), j = o % (B / 2);
+            const float gt = acc[blk * B + j], up = acc[blk * B + B / 2 + j];
+            store_elem(res.data, res.dtype, o, gt / (1.0f + expf(-gt)) * up);
+        }
+    } else if (variant & VDC_GEMV_ROPE) {
+        const double theta = hp[VDC_GEMV_P_THETA];
+        const int hd = int(hp[VDC_GEMV_P_HEAD_DIM]);
+        const int rope_rows = int(hp[VDC_GEMV_P_ROPE_ROWS]);
+        const double pos = double(k.acc[w.reg0]);
+        for (int o = 2 * int(k.t); o + 1 < nout; o += 2 * 32 * kVccWarps) {
+            const int row = job_row0 + o;
+            float a = acc[o], b = acc[o + 1];
+            if (row < rope_rows) {
+                const int d = row % hd;
+                const double ang = pos * pow(theta, -double(d) / double(hd));
+                const float cs = float(cos(ang)), sn = float(sin(ang));
+                const float na = a * cs - b * sn, nb = a * sn + b * cs;
+                a = na;
+                b = nb;
+            }
+            store_elem(res.data, res.dtype, o, a);
+            store_elem(res.data, res.dtype, o + 1, b);
+        }
+    } else if (w.op == OP_GEMV_ADD) {
+        for (int o = int(k.t); o < nout; o += 32 * kVccWarps)
+            store_elem(res.data, res.dtype, o, load_elem(third.data, third.dtype, o) + acc[o]);
+    } else {
+        for (int o = int(k.t); o < nout; o += 32 * kVccWarps) store_elem(res.data, res.dtype, o, acc[o]);
+    }
+    k.sync();
+    if (!k.push(x, pc)) return;
+    if (has_third && !k.push(third, pc)) return;
+    k.push(res, pc);
+}
+
+__device__ void h_attn_decode(Vcc& k, const Word& w, uint32_t pc) {
+    const EngineParams& P = *k.c->P;
+    const float* hp = P.hparams + (w.imm >> 8);
+    const float scale = hp[VDC_ATTN_P_SCALE];
+    const int hd = int(hp[VDC_ATTN_P_HEAD_DIM]), G = int(hp[VDC_ATTN_P_GROUP]);
+    const long long ctx = k.acc[w.reg0];
+    const int lane = int(k.t & 31), wp = int(k.t >> 5);
+    constexpr int kMaxHeads = 2, kMaxDims = 4;  // per warp: heads wp, wp+4 ; dims per lane (hd <= 128)
+    const int dpl = hd / 32;
+    Msg q, kt, vt, res;
+    if (!k.pop(q, pc)) return;
+    float m[kMaxHeads], l[kMaxHeads], o[kMaxHeads][kMaxDims];
+    for (int h = 0; h < kMaxHeads; ++h) {
+        m[h] = -INFINITY;
+        l[h] = 0.f;
+        for (int d = 0; d < kMaxDims; ++d) o[h][d] = 0.f;
+    }
+    for (int gi = 0; gi < int(w.size); ++gi) {
+        if (!k.pop(kt, pc)) return;
+        if (!k.pop(vt, pc)) return;
+        for (int hi = 0; hi < kMaxHeads; ++hi) {
+            const int h = wp + hi * kVccWarps;
+            if (h >= G) break;
+            // scores: lane owns rows lane, lane+32
+            float s[2];
+            for (int rr = 0; rr < 2; ++rr) {
+                const int r = lane + 32 * rr;
+                s[rr] = -INFINITY;
+                if (r >= kt.rows || kt.row0 + r >= ctx) continue;
+                float acc = 0.f;
+                if (kt.dtype == VDC_DTYPE_BF16 && q.dtype == VDC_DTYPE_BF16 && (hd & 7) == 0) {
+                    const int nch = hd >> 3;
+                    const uint4* kr = reinterpret_cast<const uint4*>(kt.data + size_t(r) * kt.stride * 2);
+                    const uint4* qv = reinterpret_cast<const uint4*>(q.data + size_t(h) * hd * 2);
+                    for (int cc = 0; cc < nch; ++cc) {
+                        const int ch = (cc + lane) % nch;  // rotate to spread smem banks
+                        acc += dot_bf16x8(kr[ch], qv[ch]);
+                    }
+                } else {
+                    for (int d = 0; d < hd; ++d)
+                        acc += load_elem(q.data, q.dtype, int64_t(h) * hd + d) * load_elem(kt.data, kt.dtype, int64_t(r) * kt.stride + d);
+                }
+                s[rr] = acc * scale;
+            }
+            const float pmax = warp_max(fmaxf(s[0], s[1]));
+            if (pmax == -INFINITY) continue;  // no valid row in this page
+            const float mnew = fmaxf(m[hi], pmax);
+            const float corr = m[hi] == -INFINITY ? 0.f : expf(m[hi] - mnew);
+            float p[2];
+            for (int rr = 0; rr < 2; ++rr) p[rr] = s[rr] == -INFINITY ? 0.f : expf(s[rr] - mnew);
+            const float psum = warp_sum(p[0] + p[1]);
+            l[hi] = l[hi] * corr + psum;
+            for (int d = 0; d < dpl; ++d) o[hi][d] *= corr;
+            for (int r = 0; r < vt.rows && r < 64; ++r) {
+                const float pr = __shfl_sync(0xffffffffu, p[r >> 5], r & 31);
+                if (pr == 0.f) continue;
+                for (int d = 0; d < dpl; ++d)
+                    o[hi][d] += pr * load_elem(vt.data, vt.dtype, int64_t(r) * vt.stride + lane * dpl + d);
+            }
+            m[hi] = mnew;
+        }
+        k.sync();
+        if (!k.push(kt, pc) || !k.push(vt, pc)) return;
+    }
+    if (!k.pop(res, pc)) return;
+    float* out = reinterpret_cast<float*>(res.data);  // G x (hd + 2) fp32
+    for (int hi = 0; hi < kMaxHeads; ++hi) {
+        const int h = wp + hi * kVccWarps;
+        if (h >= G) break;
+        for (int d = 0; d < dpl; ++d) out[h * (hd + 2) + lane * dpl + d] = o[hi][d];
+        if (lane == 0) {
+            out[h * (hd + 2) + hd] = m[hi];
+            out[h * (hd + 2) + hd + 1] = l[hi];
+        }
+    }
+    k.sync();
+    if (!k.push(q, pc)) return;
+    k.push(res, pc);
+}
+
+__device__ void h_attn_combine(Vcc& k, const Word& w, uint32_t pc) {
+    const EngineParams& P = *k.c->P;
+    const float* hp = P.hparams + (w.imm >> 8);
+    const int hd = int(hp[VDC_COMB_P_HEAD_DIM]), G = int(hp[VDC_COMB_P_GROUP]);
+    const int lane = int(k.t & 31), wp = int(k.t >> 5), dpl = hd / 32;
+    constexpr int kMaxHeads = 2, kMaxDims = 4;
+    float M[kMaxHeads], L[kMaxHeads], O[kMaxHeads][kMaxDims];
+    for (int h = 0; h < kMaxHeads; ++h) {
+        M[h] = -INFINITY;
+        L[h] = 0.f;
+        for (int d = 0; d < kMaxDims; ++d) O[h][d] = 0.f;
+    }
+    Msg part, res;
+    for (int gi = 0; gi < int(w.size); ++gi) {
+        if (!k.pop(part, pc)) return;
+        const float* pp = reinterpret_cast<const float*>(part.data);
+        for (int hi = 0; hi < kMaxHeads; ++hi) {
+            const int h = wp + hi * kVccWarps;
+            if (h >= G) break;
+            const float ms = pp[h * (hd + 2) + hd], ls = pp[h * (hd + 2) + hd + 1];
+            if (ms == -INFINITY || !(ls > 0.f)) continue;
+            const float mn = fmaxf(M[hi], ms);
+            const float a = M[hi] == -INFINITY ? 0.f : expf(M[hi] - mn), b = expf(ms - mn);
+            for (int d = 0; d < dpl; ++d) O[hi][d] = O[hi][d] * a + pp[h * (hd + 2) + lane * dpl + d] * b;
+            L[hi] = L[hi] * a + ls * b;
+            M[hi] = mn;
+        }
+        k.sync();
+        if (!k.push(part, pc)) return;
+    }
+    if (!k.pop(res, pc)) return;
+    for (int hi = 0; hi < kMaxHeads; ++hi) {
+        const int h = wp + hi * kVccWarps;
+        if (h >= G) break;
+        for (int d = 0; d < dpl; ++d)
+            store_elem(res.data, res.dtype, int64_t(h) * hd + lane * dpl + d, L[hi] > 0.f ? O[hi][d] / L[hi] : 0.f);
+    }
+    k.sync();
+    k.push(res, pc);
+}
+
+__device__ void vcc_role(Cta& c, uint32_t v, uint32_t tid) {
+    const EngineParams& P = *c.P;
+    Vcc k;
+    k.c = &c;
+    k.v = v;
+    k.t = tid;
+    k.core = c.core_base + 1 + v;
+    k.bar = 1 + int(v);
+    for (int i = 0; i < 16; ++i) k.acc[i] = 0;
+    const uint32_t w0 = P.core_off[k.core], n = P.core_off[k.core + 1] - w0;
+    LoopFrame loops[8];
+    int depth = 0;
+    unsigned long long uops = 0;
+    uint4 cur = n ? __ldg(&P.words[w0]) : make_uint4(0, 0, 0, 0);
+    uint32_t cur_pc = 0;
+    for (uint32_t pc = 0; pc < n && k.ok;) {
+        if (c.aborted()) break;
+        if (pc != cur_pc) {  // a jump: refetch
+            cur = __ldg(&P.words[w0 + pc]);
+            cur_pc = pc;
+        }
+        const uint4 nxt = pc + 1 < n ? __ldg(&P.words[w0 + pc + 1]) : make_uint4(0, 0, 0, 0);
+        const Word w = decode(cur);
+        cur = nxt;
+        cur_pc = pc + 1;
+        ++uops;
+        if (is_control(w.op)) {
+            switch (w.op) {
+                case OP_LOOP:
+                    if (w.size == 0) pc += uint32_t(w.imm) + 2;
+                    else {
+                        if (depth < 8) loops[depth++] = {pc + 1, w.size};
+                        ++pc;
+                    }
+                    break;
+                case OP_REPEAT:
+                    if (depth > 0 && --loops[depth - 1].remaining > 0) pc = loops[depth - 1].start;
+                    else {
+                        if (depth > 0) --depth;
+                        ++pc;
+                    }
+                    break;
+                case OP_SET_ACC: k.acc[w.reg0] = w.imm; ++pc; break;
+                case OP_ADD_ACC: k.acc[w.reg0] += w.imm; ++pc; break;
+                case OP_SET_ACC_MEM: {
+                    const int idx = w.imm & 0xff;
+                    const long long mult = (w.imm >> 8) ? (w.imm >> 8) : 1;
+                    k.acc[w.reg0] = (idx < P.n_step ? P.step[idx] : 0) * mult;
+                    ++pc;
+                    break;
+                }
+                case OP_CONTINUE_IF:
+                    if (depth > 0 && k.acc[w.reg0] == w.imm) {
+                        uint32_t q = pc + 1;
+                        for (int nest = 0; q < n; ++q) {
+                            const uint32_t op = __ldg(&P.words[w0 + q]).x & 0xff;
+                            if (op == OP_LOOP) ++nest;
+                            if (op == OP_REPEAT && nest-- == 0) break;
+                        }
+                        pc = q;
+                    } else ++pc;
+                    break;
+                default:
+                    pc = n;
+                    break;
+            }
+            continue;
+        }
+        switch (w.op) {
+            case OP_GEMV:
+            case OP_RMS_GEMV:
+            case OP_GEMV_ADD: h_gemv(k, w, pc); break;
+            case OP_ATTN_DECODE: h_attn_decode(k, w, pc); break;
+            case OP_ATTN_COMBINE: h_attn_combine(k, w, pc); break;
+            case OP_MATVEC:
+            case OP_GEMM_TILE:
+            case OP_ATTN:
+            case OP_ROPE:
+            case OP_RMSNORM:
+            case OP_ELEMWISE:
+            case OP_EMBED: h_reference(k, w, pc); break;
+            default:
+                if (tid == 0) {
+                    P.status->fault_code = 4;
+                    P.status->fault_info = (k.core << 16) | pc;
+                    atomicExch(&P.status->abort, 2);
+                }
+                k.ok = false;
+                break;
+        }
+        ++pc;
+    }
+    if (tid == 0) atomicAdd(&c.P->stats[c.sm].uops, uops);
+}
+
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(32 * (1 + kMaxLdu + kMaxStu + kMaxVcc * kVccWarps), 1)
+    engine_kernel(const __grid_constant__ EngineParams P) {
+    extern __shared__ __align__(1024) char smem[];
+    Cta c;
+    c.P = &P;
+    c.slots = smem;
+    c.C = reinterpret_cast<Control*>(smem + size_t(P.slot_budget) * P.slot_size);
+    c.sm = blockIdx.x;
+    c.core_base = blockIdx.x * (1 + P.vcc_per_sm);
+    Control& C = *c.C;
+    // zero the control block, init slot barriers
+    for (uint32_t i = threadIdx.x; i < sizeof(Control) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(&C)[i] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kMaxSlots; ++i) mbar_init(&C.full_bar[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t ldu0 = 1, stu0 = 1 + P.ldu_count, vcc0 = stu0 + P.stu_count;
+    if (warp == 0) cfu_role(c);
+    else if (warp < stu0) ldu_role(c, warp - ldu0);
+    else if (warp < vcc0) stu_role(c, warp - stu0);
+    else {
+        const uint32_t v = (warp - vcc0) / kVccWarps;
+        if (v < P.vcc_per_sm) vcc_role(c, v, threadIdx.x - (vcc0 + v * kVccWarps) * 32);
+    }
+}
+
+}  // namespace vdc_dev
+
+// ===========================================================================
+// host side of the device C-ABI
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "capi_common.hpp"
+
+using namespace vdc_dev;
+using vdc_impl::fail;
+
+struct vdc_ctx {
+    vdc_profile prof{};
+    int device = 0;
+    int num_sms = 0;
+    size_t smem_bytes = 0;
+    // program
+    std::vector<vdc_desc> descs;
+    std::vector<DevDesc> dev_descs;
+    std::vector<void*> bound;  // per descriptor (owner pointer)
+    std::vector<size_t> bound_bytes;
+    uint32_t n_cores = 0;
+    uint16_t slot_budget = 0, local_depth = 0;
+    uint32_t max_dep = 0;
+    std::vector<DepQueue> dep_init;
+    // device buffers
+    uint4* d_words = nullptr;
+    uint32_t* d_core_off = nullptr;
+    DevDesc* d_descs = nullptr;
+    DepQueue* d_deps = nullptr;
+    uint32_t* d_counters = nullptr;
+    float* d_params = nullptr;
+    int64_t* d_step = nullptr;
+    uint32_t n_step = 0;
+    SmStats* d_stats = nullptr;
+    Status* d_status = nullptr;
+    bool descs_dirty = true;
+    bool loaded = false;
+    uint32_t watchdog_ms = 2000;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaStream_t last_stream = nullptr;
+};
+
+namespace {
+
+#define CU(x)                                                                         \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess) return fail(VDC_ERR_INTERNAL, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <typename T>
+void dfree(T*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+size_t control_bytes() { return (sizeof(Control) + 127) & ~size_t(127); }
+
+}  // namespace
+
+extern "C" {
+
+int vdc_create(const vdc_profile* p, int device, vdc_ctx** out) {
+    if (!p || !out) return fail(VDC_ERR_INPUT, "null argument");
+    if (p->vcc_per_sm < 1 || p->vcc_per_sm > uint32_t(kMaxVcc)) return fail(VDC_ERR_INPUT, "vcc_per_sm must be 1..2");
+    if (p->ldu_count < 1 || p->ldu_count > uint32_t(kMaxLdu)) return fail(VDC_ERR_INPUT, "ldu_count must be 1..2");
+    if (p->stu_count < 1 || p->stu_count > uint32_t(kMaxStu)) return fail(VDC_ERR_INPUT, "stu_count must be 1..2");
+    if (p->slot_budget < 1 || p->slot_budget > uint32_t(kMaxSlots)) return fail(VDC_ERR_INPUT, "slot_budget must be 1..32");
+    if (p->slot_size % 1024) return fail(VDC_ERR_INPUT, "slot_size must be a multiple of 1024");
+    CU(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) return fail(VDC_ERR_INPUT, "device is not sm_100 class (B200 required)");
+    auto ctx = new vdc_ctx;
+    ctx->prof = *p;
+    ctx->device = device;
+    ctx->num_sms = prop.multiProcessorCount;
+    if (p->sm_count < 1 || int(p->sm_count) > prop.multiProcessorCount) {
+        delete ctx;
+        return fail(VDC_ERR_INPUT, "sm_count exceeds the device's multiprocessors");
+    }
+    ctx->smem_bytes = size_t(p->slot_budget) * p->slot_size + control_bytes();
+    if (ctx->smem_bytes > prop.sharedMemPerBlockOptin) {
+        const size_t need = ctx->smem_bytes;
+        delete ctx;
+        return fail(VDC_ERR_INPUT, "slots + control block need " + std::to_string(need) + " B of shared memory, device allows " +
+                                       std::to_string(prop.sharedMemPerBlockOptin));
+    }
+    CU(cudaFuncSetAttribute(engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ctx->smem_bytes)));
+    CU(cudaMalloc(&ctx->d_stats, sizeof(SmStats) * p->sm_count));
+    CU(cudaMalloc(&ctx->d_status, sizeof(Status)));
+    CU(cudaEventCreate(&ctx->ev0));
+    CU(cudaEventCreate(&ctx->ev1));
+    *out = ctx;
+    return VDC_OK;
+}
+
+int vdc_destroy(vdc_ctx* ctx) {
+    if (!ctx) return VDC_OK;
+    dfree(ctx->d_words);
+    dfree(ctx->d_core_off);
+    dfree(ctx->d_descs);
+    dfree(ctx->d_deps);
+    dfree(ctx->d_counters);
+    dfree(ctx->d_params);
+    dfree(ctx->d_stats);
+    dfree(ctx->d_status);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    delete ctx;
+    return VDC_OK;
+}
+
+int vdc_load_program(vdc_ctx* ctx, const uint8_t* words, const uint32_t* words_per_core, uint32_t n_cores,
+                     const vdc_queue* queues, uint32_t n_queues, const vdc_desc* descs, uint32_t n_desc,
+                     uint16_t slot_budget, uint16_t local_depth) {
+    if (!ctx || !words_per_core || (!descs && n_desc)) return fail(VDC_ERR_INPUT, "null argument");
+    const uint32_t expect = ctx->prof.sm_count * (1 + ctx->prof.vcc_per_sm);
+    if (n_cores != expect)
+        return fail(VDC_ERR_INPUT, "program has " + std::to_string(n_cores) + " cores, device declares " + std::to_string(expect));
+    if (slot_budget != ctx->prof.slot_budget)
+        return fail(VDC_ERR_INPUT, "program slot budget " + std::to_string(slot_budget) + " != device slot budget " +
+                                       std::to_string(ctx->prof.slot_budget));
+    if (local_depth > kM2cDepth) return fail(VDC_ERR_INPUT, "local queue depth exceeds the device rings (64)");
+    std::vector<uint32_t> off(n_cores + 1, 0);
+    for (uint32_t i = 0; i < n_cores; ++i) off[i + 1] = off[i] + words_per_core[i];
+    // every µop that pops a VCC's c2m ring must map to the same store unit
+    // (flow mod stu_count), so each ring has a single in-order consumer
+    const uint32_t per_sm = 1 + ctx->prof.vcc_per_sm;
+    for (uint32_t core = 0; core < n_cores; core += per_sm) {
+        int owner[kMaxVcc] = {-1, -1};
+        for (uint32_t i = off[core]; i < off[core + 1]; ++i) {
+            const uint8_t* b = words + size_t(i) * 16;
+            const uint32_t op = b[0], flags = b[1] & 0xf, flow = b[4], reg1 = b[7] & 0xf;
+            if (op >= 0x20) continue;
+            if (!(flags & 2)) continue;  // recv
+            if (reg1 >= ctx->prof.vcc_per_sm) return fail(VDC_ERR_INPUT, "recv µop targets a VCC the device does not declare");
+            const int unit = int(flow % ctx->prof.stu_count);
+            if (owner[reg1] >= 0 && owner[reg1] != unit)
+                return fail(VDC_ERR_INPUT, "program routes one VCC's releases to two store units (use stu_count=1)");
+            owner[reg1] = unit;
+        }
+    }
+    dfree(ctx->d_words);
+    dfree(ctx->d_core_off);
+    dfree(ctx->d_descs);
+    dfree(ctx->d_deps);
+    dfree(ctx->d_counters);
+    CU(cudaMalloc(&ctx->d_words, std::max<size_t>(16, size_t(off[n_cores]) * 16)));
+    if (off[n_cores]) CU(cudaMemcpy(ctx->d_words, words, size_t(off[n_cores]) * 16, cudaMemcpyHostToDevice));
+    CU(cudaMalloc(&ctx->d_core_off, off.size() * 4));
+    CU(cudaMemcpy(ctx->d_core_off, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
+    ctx->n_cores = n_cores;
+    ctx->slot_budget = slot_budget;
+    ctx->local_depth = local_depth;
+    ctx->descs.assign(descs, descs + n_desc);
+    ctx->bound.assign(n_desc, nullptr);
+    ctx->bound_bytes.assign(n_desc, 0);
+    ctx->dev_descs.assign(n_desc, DevDesc{});
+    for (uint32_t i = 0; i < n_desc; ++i) {
+        const vdc_desc& s = descs[i];
+        DevDesc& d = ctx->dev_descs[i];
+        if (s.rank < 1 || s.rank > 4) return fail(VDC_ERR_INPUT, "descriptor rank must be 1..4");
+        if (s.view_of >= int32_t(n_desc)) return fail(VDC_ERR_INPUT, "view_of out of range");
+        d.base = s.base;
+        d.grid_rank = int32_t(s.rank < 2 ? 2 : s.rank);
+        for (int k = 0; k < 4; ++k) d.grid[k] = s.grid[k];
+        d.rows = s.rank >= 2 ? s.shape[s.rank - 2] : 1;
+        d.cols = s.shape[s.rank - 1];
+        d.tile_rows = s.tile_rows;
+        d.tile_cols = s.tile_cols;
+        d.tile_count = 1;
+        for (int k = 0; k < d.grid_rank; ++k) d.tile_count *= d.grid[k];
+        d.elem_count = 1;
+        for (uint32_t k = 0; k < s.rank; ++k) d.elem_count *= s.shape[k];
+        d.lead_stride[0] = d.lead_stride[1] = 0;
+        if (s.rank == 3) d.lead_stride[0] = d.rows * d.cols;
+        if (s.rank == 4) {
+            d.lead_stride[0] = s.shape[1] * d.rows * d.cols;
+            d.lead_stride[1] = d.rows * d.cols;
+        }
+        d.dtype = int32_t(s.dtype);
+        d.elem = s.dtype == VDC_DTYPE_BF16 ? 2 : s.dtype == VDC_DTYPE_I64 ? 8 : 4;
+        d.storage = s.view_of >= 0 ? s.view_of : int32_t(i);
+        d.ptr = nullptr;
+    }
+    ctx->max_dep = 0;
+    for (uint32_t i = 0; i < n_queues; ++i) ctx->max_dep = std::max<uint32_t>(ctx->max_dep, queues[i].dep_id);
+    ctx->dep_init.assign(ctx->max_dep + 1, DepQueue{0, 0, 4, 0, {0, 0, 0, 0}});
+    for (uint32_t i = 0; i < n_queues; ++i) {
+        ctx->dep_init[queues[i].dep_id].depth = std::max<uint16_t>(1, queues[i].depth);
+        ctx->dep_init[queues[i].dep_id].local = queues[i].local;
+    }
+    CU(cudaMalloc(&ctx->d_deps, sizeof(DepQueue) * ctx->dep_init.size()));
+    CU(cudaMalloc(&ctx->d_counters, sizeof(uint32_t) * std::max<uint32_t>(1, n_desc)));
+    CU(cudaMalloc(&ctx->d_descs, sizeof(DevDesc) * std::max<uint32_t>(1, n_desc)));
+    ctx->descs_dirty = true;
+    ctx->loaded = true;
+    return VDC_OK;
+}
+
+int vdc_set_params(vdc_ctx* ctx, const float* params, uint32_t n) {
+    if (!ctx) return fail(VDC_ERR_INPUT, "null ctx");
+    dfree(ctx->d_params);
+    CU(cudaMalloc(&ctx->d_params, sizeof(float) * std::max<uint32_t>(1, n)));
+    if (n) CU(cudaMemcpy(ctx->d_params, params, sizeof(float) * n, cudaMemcpyHostToDevice));
+    return VDC_OK;
+}
+
+int vdc_bind_tensor(vdc_ctx* ctx, uint16_t tensor, void* dptr, size_t bytes, int dtype) {
+    if (!ctx || !ctx->loaded) return fail(VDC_ERR_INPUT, "no program loaded");
+    if (tensor >= ctx->descs.size()) return fail(VDC_ERR_INPUT, "tensor index out of range");
+    const vdc_desc& s = ctx->descs[tensor];
+    if (s.view_of >= 0) return fail(VDC_ERR_INPUT, "bind the storage owner, not a view");
+    if (int(s.dtype) != dtype) return fail(VDC_ERR_INPUT, "dtype mismatch for tensor " + std::to_string(tensor));
+    const DevDesc& d = ctx->dev_descs[tensor];
+    const size_t need = size_t(d.elem_count) * size_t(d.elem);
+    if (bytes < need) return fail(VDC_ERR_INPUT, "tensor " + std::to_string(tensor) + " needs " + std::to_string(need) + " bytes");
+    ctx->bound[tensor] = dptr;
+    ctx->bound_bytes[tensor] = bytes;
+    for (size_t i = 0; i < ctx->dev_descs.size(); ++i)
+        if (ctx->dev_descs[i].storage == int32_t(tensor)) ctx->dev_descs[i].ptr = static_cast<char*>(dptr);
+    ctx->descs_dirty = true;
+    return VDC_OK;
+}
+
+int vdc_bind_step(vdc_ctx* ctx, int64_t* dptr, uint32_t n) {
+    if (!ctx) return fail(VDC_ERR_INPUT, "null ctx");
+    ctx->d_step = dptr;
+    ctx->n_step = n;
+    return VDC_OK;
+}
+
+int vdc_set_watchdog(vdc_ctx* ctx, uint32_t ms) {
+    if (!ctx) return fail(VDC_ERR_INPUT, "null ctx");
+    ctx->watchdog_ms = ms;
+    return VDC_OK;
+}
+
+int vdc_launch(vdc_ctx* ctx, void* stream) {
+    if (!ctx || !ctx->loaded) return fail(VDC_ERR_INPUT, "no program loaded");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    for (size_t i = 0; i < ctx->dev_descs.size(); ++i)
+        if (!ctx->dev_descs[i].ptr) return fail(VDC_ERR_INPUT, "tensor " + std::to_string(i) + " (" + std::to_string(ctx->dev_descs[i].storage) + ") is not bound");
+    if (ctx->descs_dirty) {
+        CU(cudaMemcpyAsync(ctx->d_descs, ctx->dev_descs.data(), sizeof(DevDesc) * ctx->dev_descs.size(), cudaMemcpyHostToDevice, s));
+        ctx->descs_dirty = false;
+    }
+    CU(cudaMemcpyAsync(ctx->d_deps, ctx->dep_init.data(), sizeof(DepQueue) * ctx->dep_init.size(), cudaMemcpyHostToDevice, s));
+    CU(cudaMemsetAsync(ctx->d_counters, 0, sizeof(uint32_t) * std::max<size_t>(1, ctx->dev_descs.size()), s));
+    CU(cudaMemsetAsync(ctx->d_status, 0, sizeof(Status), s));
+    CU(cudaMemsetAsync(ctx->d_stats, 0, sizeof(SmStats) * ctx->prof.sm_count, s));
+    EngineParams P{};
+    P.words = ctx->d_words;
+    P.core_off = ctx->d_core_off;
+    P.descs = ctx->d_descs;
+    P.n_desc = int32_t(ctx->dev_descs.size());
+    P.deps = ctx->d_deps;
+    P.counters = ctx->d_counters;
+    P.hparams = ctx->d_params;
+    P.step = ctx->d_step;
+    P.n_step = int32_t(ctx->d_step ? ctx->n_step : 0);
+    P.sm_count = ctx->prof.sm_count;
+    P.vcc_per_sm = ctx->prof.vcc_per_sm;
+    P.ldu_count = ctx->prof.ldu_count;
+    P.stu_count = ctx->prof.stu_count;
+    P.slot_size = ctx->prof.slot_size;
+    P.slot_budget = ctx->prof.slot_budget;
+    P.local_depth = ctx->local_depth;
+    P.stats = ctx->d_stats;
+    P.status = ctx->d_status;
+    P.watchdog_ns = (unsigned long long)ctx->watchdog_ms * 1000000ull;
+    const uint32_t warps = 1 + ctx->prof.ldu_count + ctx->prof.stu_count + ctx->prof.vcc_per_sm * kVccWarps;
+    void* args[] = {&P};
+    CU(cudaEventRecord(ctx->ev0, s));
+    CU(cudaLaunchCooperativeKernel((const void*)engine_kernel, dim3(ctx->prof.sm_count), dim3(32 * warps), args,
+                                   ctx->smem_bytes, s));
+    CU(cudaEventRecord(ctx->ev1, s));
+    ctx->last_stream = s;
+    return VDC_OK;
+}
+
+int vdc_wait(vdc_ctx* ctx, vdc_report* r) {
+    if (!ctx) return fail(VDC_ERR_INPUT, "null ctx");
+    CU(cudaEventSynchronize(ctx->ev1));
+    Status st{};
+    CU(cudaMemcpy(&st, ctx->d_status, sizeof(Status), cudaMemcpyDeviceToHost));
+    std::vector<SmStats> stats(ctx->prof.sm_count);
+    CU(cudaMemcpy(stats.data(), ctx->d_stats, sizeof(SmStats) * stats.size(), cudaMemcpyDeviceToHost));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    if (r) {
+        std::memset(r, 0, sizeof(*r));
+        for (const auto& s : stats) {
+            r->uops_executed += s.uops;
+            r->bytes_loaded += s.bytes_loaded;
+            r->bytes_stored += s.bytes_stored;
+        }
+        r->elapsed_ms = ms;
+        r->n_stalled = uint32_t(st.n_stalled);
+        for (int i = 0; i < 16; ++i) {
+            r->stalled_core[i] = st.stalled_core[i];
+            r->stalled_pc[i] = st.stalled_pc[i];
+        }
+        r->status = st.abort == 0 ? VDC_OK : st.abort == 1 ? VDC_ERR_DEADLOCK : VDC_ERR_INTERNAL;
+        if (st.abort == 1)
+            std::snprintf(r->message, sizeof r->message, "deadlock: %d core(s) made no progress for %u ms", st.n_stalled, ctx->watchdog_ms);
+        else if (st.abort == 2)
+            std::snprintf(r->message, sizeof r->message, "fault code %u info %u", st.fault_code, st.fault_info);
+    }
+    if (st.abort == 1) return fail(VDC_ERR_DEADLOCK, "device watchdog: deadlock");
+    if (st.abort == 2) return fail(VDC_ERR_INTERNAL, "device fault code " + std::to_string(st.fault_code));
+    return VDC_OK;
+}
+
+int vdc_program_load(vdc_ctx* ctx, const vdc_program* prog) {
+    if (!ctx || !prog) return fail(VDC_ERR_INPUT, "null argument");
+    const auto* b = reinterpret_cast<const vdc_impl::ProgramBox*>(prog);
+    try {
+        std::vector<uint8_t> words;
+        std::vector<uint32_t> per_core;
+        for (const auto& w : b->words) {
+            words.insert(words.end(), w.begin(), w.end());
+            per_core.push_back(uint32_t(w.size() / 16));
+        }
+        std::vector<vdc_queue> qs;
+        for (const auto& q : b->program.queues)
+            qs.push_back(vdc_queue{q.dep_id, q.depth, q.producer.sm, q.consumer.sm, q.local ? 1u : 0u});
+        std::vector<vdc_desc> ds;
+        for (const auto& d : b->program.descriptors) {
+            vdc_desc x{};
+            x.base = d.base;
+            x.rank = uint32_t(d.shape.size());
+            for (size_t k = 0; k < d.shape.size() && k < 4; ++k) x.shape[k] = d.shape[k];
+            for (size_t k = 0; k < d.grid.size() && k < 4; ++k) x.grid[k] = d.grid[k];
+            x.tile_rows = d.tile_rows;
+            x.tile_cols = d.tile_cols;
+            x.dtype = uint32_t(d.elem);
+            x.view_of = d.view_of;
+            ds.push_back(x);
+        }
+        int rc = vdc_load_program(ctx, words.data(), per_core.data(), uint32_t(per_core.size()), qs.data(), uint32_t(qs.size()),
+                                  ds.data(), uint32_t(ds.size()), b->program.slot_budget, b->program.local_queue_depth);
+        if (rc != VDC_OK) return rc;
+        return vdc_set_params(ctx, b->program.params.data(), uint32_t(b->program.params.size()));
+    } catch (const std::exception& e) {
+        return fail(VDC_ERR_INTERNAL, e.what());
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,147 @@
+// Device-side data structures of the persistent µop engine.
+//
+// One CTA per SM, warp-specialised into the paper's virtual cores:
+//   warp 0                 VMC control-flow unit (CFU): fetches the VMC
+//                          stream, runs control µops, resolves addresses,
+//                          allocates slots in stream order (the in-order
+//                          allocation that the generator's certificate
+//                          proves deadlock-free), dispatches to units
+//   warps 1..ldu           load units (LDU): dependency waits + bulk copies
+//                          global -> shared slot (cp.async.bulk / mbarrier)
+//   next stu warps         store units (STU): FREE / STORE / dep tokens
+//   4 warps per VCC        compute virtual cores executing the handlers
+// Shared memory: `slot_budget` slots of `slot_size` bytes, then the control
+// block below (rings between the cores, slot barriers, allocator mask).
+#pragma once
+#include <cstdint>
+
+namespace vdc_dev {
+
+constexpr int kMaxVcc = 2;
+constexpr int kMaxLdu = 2;
+constexpr int kMaxStu = 2;
+constexpr int kVccWarps = 4;
+constexpr int kM2cDepth = 64;   // >= any program's local_queue_depth (checked at load)
+constexpr int kC2mDepth = 64;
+constexpr int kUnitDepth = 32;
+constexpr int kCfuChunk = 64;   // words per stream prefetch chunk (1 KB)
+constexpr int kAccRows = 256;   // per-VCC fp32 accumulator scratch (streaming GEMV rows)
+constexpr int kMaxSlots = 32;
+
+// Resolved-tile view of a descriptor, prepared on the host at load/bind.
+struct DevDesc {
+    int64_t base;         // first global tile index
+    int64_t grid[4];
+    int64_t lead_stride[2];  // element stride of the leading (plane) grid dims
+    int64_t rows, cols;   // trailing two extents
+    int64_t tile_rows, tile_cols;
+    int64_t tile_count;
+    int64_t elem_count;
+    char* ptr;            // storage base (view -> owner's pointer)
+    int32_t grid_rank;
+    int32_t elem;         // bytes per element
+    int32_t dtype;        // VDC_DTYPE_*
+    int32_t storage;      // counter index (owner descriptor)
+};
+
+struct DepQueue {          // global FIFO per dep id (single producer / consumer site)
+    uint32_t produced;
+    uint32_t consumed;
+    uint32_t depth;
+    uint32_t local;
+    uint32_t payload[4];   // STORE_LOCAL slot handoff: first | count<<8 ; rows ; cols ; stride
+};
+
+struct SmStats {
+    unsigned long long uops;
+    unsigned long long bytes_loaded;
+    unsigned long long bytes_stored;
+    unsigned long long cfu_stall_cycles;
+    unsigned long long pad[4];
+};
+
+struct Status {
+    int32_t abort;          // 1 = deadlock watchdog fired, 2 = fault
+    int32_t n_stalled;
+    uint32_t stalled_core[16];
+    uint32_t stalled_pc[16];
+    uint32_t fault_code;
+    uint32_t fault_info;
+};
+
+struct EngineParams {
+    const uint4* words;
+    const uint32_t* core_off;  // n_cores + 1 word offsets (CoreId order)
+    DevDesc* descs;
+    int32_t n_desc;
+    DepQueue* deps;
+    uint32_t* counters;        // per descriptor (storage) store counts
+    const float* hparams;
+    const int64_t* step;
+    int32_t n_step;
+    uint32_t sm_count, vcc_per_sm, ldu_count, stu_count;
+    uint32_t slot_size, slot_budget, local_depth;
+    SmStats* stats;
+    Status* status;
+    unsigned long long watchdog_ns;
+};
+
+// m2c message: one slot region handed from the VMC to a VCC.
+struct M2C {
+    uint32_t slots;     // first | count << 8
+    int32_t rows, cols; // payload extents (edge-trimmed)
+    int32_t stride;     // padded row stride in elements (tile_cols)
+    int32_t row0, col0; // global first row / col of the tile (trailing dims)
+    uint32_t meta;      // dtype | (parity << 8) | (wait << 9) | (first_slot_bar << 16)
+    volatile uint32_t ready;  // entry index + 1 once the LDU has issued the data movement
+};
+
+// c2m message: a region released (or produced) by a VCC.
+struct C2M {
+    uint32_t slots;
+    int32_t rows, cols, stride;
+};
+
+// CFU -> unit work item.
+struct UnitOp {
+    uint8_t op, flags, reg1, dtype;
+    uint16_t dep_id, size;
+    uint32_t slots;       // allocated / carried region
+    uint32_t m2c;         // m2c entry index (send)
+    int32_t storage;      // counter index of the resolved tensor (-1 none)
+    uint32_t bytes;       // tile payload bytes (0 = no data movement)
+    int32_t rows_at, cols_at;
+    int32_t elem;         // bytes per element
+    int32_t tile_cols;    // slot row stride in elements
+    char* gptr;           // first element of the tile in global memory
+    int64_t gpitch;       // global row pitch in bytes
+    uint32_t core_pc;
+    uint32_t pad;
+};
+
+struct Ring {
+    volatile uint32_t head;
+    volatile uint32_t tail;
+};
+
+struct alignas(16) Control {
+    uint64_t full_bar[kMaxSlots];
+    uint32_t bar_uses[kMaxSlots];
+    volatile uint32_t alloc_mask;
+    uint32_t pad0[3];
+    Ring m2c_ring[kMaxVcc];
+    Ring c2m_ring[kMaxVcc];
+    Ring ldu_ring[kMaxLdu];
+    Ring stu_ring[kMaxStu];
+    M2C m2c[kMaxVcc][kM2cDepth];
+    C2M c2m[kMaxVcc][kC2mDepth];
+    UnitOp ldu_q[kMaxLdu][kUnitDepth];
+    UnitOp stu_q[kMaxStu][kUnitDepth];
+    uint4 cfu_buf[kCfuChunk];
+    uint4 vcc_word[kMaxVcc];
+    float acc[kMaxVcc][kAccRows];
+    float red[kMaxVcc][32];
+    volatile int32_t done_roles;
+};
+
+}  // namespace vdc_dev

@@ -234,6 +234,15 @@ std::string ProgramBox::text(bool with_words) const {
                          {"init", int(d.init)}, {"init_scale", d.init_scale}});
     out["descriptors"] = descs;
     out["params"] = program.params;
+    json queues = json::array();
+    for (const auto& q : program.queues)
+        queues.push_back({{"dep", q.dep_id}, {"depth", q.depth}, {"local", q.local}, {"producer_sm", q.producer.sm},
+                          {"consumer_sm", q.consumer.sm}});
+    out["queues"] = queues;
+    out["slot_size"] = hw.slot_size;
+    out["ldu_count"] = hw.ldu_count;
+    out["stu_count"] = hw.stu_count;
+    out["step_scalars"] = program.step_scalars;
     out["slot_budget"] = program.slot_budget;
     out["local_queue_depth"] = program.local_queue_depth;
     out["sm_count"] = sm_count;

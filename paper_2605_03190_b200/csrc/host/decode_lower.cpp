@@ -399,11 +399,25 @@ class DecodeLowering {
                     cm.push_back({j.ordinal, task_of[ji], -1});
                 }
             }
+            // A dependency-gated load of operator o may not precede any µop of an
+            // earlier operator on this VMC: in the sequential (certificate) model
+            // the VMC would block on a counter whose producer store sits later in
+            // its own stream.
+            auto next_op = [&](uint32_t v) {
+                return cursor[v] < parts[v].size() ? parts[v][cursor[v]].second.op : UINT32_MAX;
+            };
             for (;;) {
                 int pick = -1;
                 for (uint32_t v = 0; v < vccs; ++v)
                     if (cursor[v] < parts[v].size() && (pick < 0 || fed[v] < fed[size_t(pick)])) pick = int(v);
                 if (pick < 0) break;
+                const auto& cand = parts[size_t(pick)][cursor[size_t(pick)]];
+                if (cand.first.opcode == Opcode::LOAD_WAIT)
+                    for (uint32_t v = 0; v < vccs; ++v)
+                        if (int(v) != pick && next_op(v) < cand.second.op) {
+                            pick = int(v);
+                            break;
+                        }
                 const auto& [u, m] = parts[size_t(pick)][cursor[size_t(pick)]++];
                 if (isa::is_load_class(u.opcode) && u.opcode != Opcode::ALLOC) fed[size_t(pick)] += desc_[u.addr.tensor].tile_bytes();
                 vs.push_back(u);

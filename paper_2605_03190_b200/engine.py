@@ -1,0 +1,137 @@
+"""Device executor: the reference's `machine::Machine` shape over the C-ABI.
+
+reference include/uopsim/machine.hpp:94-126      this module
+  Machine(p, hw, inputs, opt)                     Engine(program, device) + bind()/bind_inputs()
+  Machine::run(watchdog) -> ExecutionReport       Engine.run() -> Report (status, uops, bytes, ms)
+  simulate(p, hw, opt, watchdog)                  simulate(program, inputs)
+Deadlock is a report status (VDC_ERR_DEADLOCK), not an exception, exactly
+like the reference's Termination::deadlock. Device memory is owned by the
+caller (torch tensors); there is no CPU execution path.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._native import (DTYPE, VDC_ERR_DEADLOCK, VDC_OK, Program, VdcError, check, lib, vdc_profile, vdc_report)
+
+
+@dataclass
+class Report:
+    status: int
+    uops_executed: int
+    bytes_loaded: int
+    bytes_stored: int
+    elapsed_ms: float
+    message: str
+    stalled: list = field(default_factory=list)
+
+    @property
+    def completed(self) -> bool:
+        return self.status == VDC_OK
+
+
+def _torch():
+    import torch  # PyTorch is the device-memory/stream plumbing, not the compute path
+
+    return torch
+
+
+TORCH_DTYPE = {"f32": "float32", "bf16": "bfloat16", "i64": "int64"}
+
+
+class Engine:
+    """One vdc_ctx (one persistent-kernel configuration) with a loaded program."""
+
+    def __init__(self, program: Program, device: int = 0, watchdog_ms: int = 2000):
+        info = program.info()
+        prof = vdc_profile(sm_count=info["sm_count"], vcc_per_sm=info["vcc_per_sm"], slot_size=info["slot_size"],
+                           slot_budget=info["slot_budget"], ldu_count=info["ldu_count"], stu_count=info["stu_count"])
+        self.program = program
+        self.info = info
+        self.device = device
+        h = ctypes.c_void_p()
+        check(lib().vdc_create(ctypes.byref(prof), device, ctypes.byref(h)))
+        self._h = h
+        check(lib().vdc_program_load(self._h, program.handle))
+        check(lib().vdc_set_watchdog(self._h, watchdog_ms))
+        self.tensors: dict[str, object] = {}
+        self._step = None
+        self.descs = {d["name"]: d for d in info["descriptors"]}
+
+    # -- memory -------------------------------------------------------------
+    def storage_names(self):
+        return [d["name"] for d in self.info["descriptors"] if d["view_of"] < 0]
+
+    def bind(self, name: str, tensor) -> None:
+        d = self.descs[name]
+        torch = _torch()
+        if not tensor.is_cuda or not tensor.is_contiguous():
+            raise VdcError(2, f"{name}: expected a contiguous CUDA tensor")
+        if str(tensor.dtype) != "torch." + TORCH_DTYPE[d["dtype"]]:
+            raise VdcError(2, f"{name}: dtype {tensor.dtype} != {d['dtype']}")
+        check(lib().vdc_bind_tensor(self._h, d["index"], ctypes.c_void_p(tensor.data_ptr()),
+                                    tensor.numel() * tensor.element_size(), DTYPE[d["dtype"]]))
+        self.tensors[name] = tensor
+        del torch
+
+    def bind_inputs(self, arrays: dict) -> dict:
+        """Allocate every storage tensor on the device from host arrays (float32
+        values; bf16 tensors are cast); missing names are zero-filled."""
+        torch = _torch()
+        out = {}
+        for d in self.info["descriptors"]:
+            if d["view_of"] >= 0:
+                continue
+            n = int(np.prod(d["shape"]))
+            dt = getattr(torch, TORCH_DTYPE[d["dtype"]])
+            if d["name"] in arrays:
+                t = torch.from_numpy(np.ascontiguousarray(arrays[d["name"]], dtype=np.float32).reshape(-1)).to(
+                    f"cuda:{self.device}").to(dt)
+            else:
+                t = torch.zeros(n, dtype=dt, device=f"cuda:{self.device}")
+            self.bind(d["name"], t)
+            out[d["name"]] = t
+        return out
+
+    def bind_step(self, tensor) -> None:
+        """Device-resident int64 step block (token, pos, ctx, ...)."""
+        check(lib().vdc_bind_step(self._h, ctypes.c_void_p(tensor.data_ptr()), tensor.numel()))
+        self._step = tensor
+
+    # -- execution ----------------------------------------------------------
+    def launch(self, stream=None) -> None:
+        s = ctypes.c_void_p(stream.cuda_stream if stream is not None else _torch().cuda.current_stream(self.device).cuda_stream)
+        check(lib().vdc_launch(self._h, s))
+
+    def wait(self) -> Report:
+        r = vdc_report()
+        rc = lib().vdc_wait(self._h, ctypes.byref(r))
+        if rc not in (VDC_OK, VDC_ERR_DEADLOCK) and r.status == 0:
+            check(rc)
+        return Report(r.status, r.uops_executed, r.bytes_loaded, r.bytes_stored, r.elapsed_ms, r.message.decode(),
+                      [(r.stalled_core[i], r.stalled_pc[i]) for i in range(min(16, r.n_stalled))])
+
+    def run(self, stream=None) -> Report:
+        self.launch(stream)
+        return self.wait()
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().vdc_destroy(self._h)
+            self._h = None
+
+
+def simulate(program: Program, inputs: dict, step=None, device: int = 0):
+    """Build + bind + run once; returns (report, {name: host float32 array})."""
+    torch = _torch()
+    eng = Engine(program, device)
+    tens = eng.bind_inputs(inputs)
+    if step is not None:
+        st = torch.tensor(list(step) + [0] * (8 - len(step)), dtype=torch.int64, device=f"cuda:{device}")
+        eng.bind_step(st)
+    rep = eng.run()
+    host = {k: v.float().cpu().numpy() for k, v in tens.items()}
+    return rep, host
