@@ -4,6 +4,8 @@
 //   out_dir      : receives index.json, inputs.bin (initial storage tensors) and
 //                  outputs.bin (storage tensors after execution), float32 LE
 //   inputs.bin   : optional override of the initial contents (same layout)
+#include <chrono>
+#include <cstdlib>
 #include <fstream>
 #include <iostream>
 #include <sstream>
@@ -81,19 +83,22 @@ int main(int argc, char** argv) {
         for (auto& [i, v] : mem) in.read(reinterpret_cast<char*>(v.data()), std::streamsize(v.size() * 4));
     }
     const std::string out = argv[2];
-    {
+    const bool dump = !std::getenv("ORACLE_NO_DUMP");
+    if (dump) {
         std::ofstream o(out + "/inputs.bin", std::ios::binary);
         for (auto& [i, v] : mem) o.write(reinterpret_cast<const char*>(v.data()), std::streamsize(v.size() * 4));
     }
     oracle::Interp interp(p, mem);
+    const auto t0 = std::chrono::steady_clock::now();
     const auto r = interp.run();
-    {
+    const double exec_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (dump) {
         std::ofstream o(out + "/outputs.bin", std::ios::binary);
         for (auto& [i, v] : mem) o.write(reinterpret_cast<const char*>(v.data()), std::streamsize(v.size() * 4));
     }
     std::ofstream(out + "/index.json") << json{{"tensors", index}, {"completed", r.completed}, {"uops", r.uops},
                                                {"stall", r.stall}, {"queues_drained", r.queues_drained},
-                                               {"slots_all_free", r.slots_all_free}}.dump(1);
-    std::cout << (r.completed ? "completed" : "DEADLOCK " + r.stall) << " uops=" << r.uops << "\n";
+                                               {"slots_all_free", r.slots_all_free}, {"exec_seconds", exec_s}}.dump(1);
+    std::cout << (r.completed ? "completed" : "DEADLOCK " + r.stall) << " uops=" << r.uops << " exec_s=" << exec_s << "\n";
     return r.completed ? 0 : 3;
 }

@@ -126,6 +126,15 @@ struct Cta {
     uint32_t core_base;  // CoreId-order index of this SM's VMC
 
     __device__ char* slot_ptr(uint32_t first) const { return slots + size_t(first) * P->slot_size; }
+    // byte `off` of a (possibly scattered) slot region
+    __device__ char* region_ptr(const SlotList& l, uint32_t off) const {
+        return slot_ptr(l.at(off >> P->slot_shift)) + (off & (P->slot_size - 1));
+    }
+    __device__ static bool contiguous(const SlotList& l) {
+        for (uint32_t i = 1; i < l.count; ++i)
+            if (l.at(i) != l.at(0) + i) return false;
+        return true;
+    }
     __device__ bool aborted() const { return *reinterpret_cast<volatile int32_t*>(&P->status->abort) != 0; }
 };
 
@@ -361,29 +370,52 @@ __device__ void cfu_role(Cta& c) {
             break;
         }
         const bool allocates = (w.op == OP_LOAD || w.op == OP_LOAD_DEP || w.op == OP_ALLOC || w.op == OP_LOAD_WAIT) && w.size > 0;
-        uint32_t first = 0, count = allocates ? w.size : 0;
+        const uint32_t count = allocates ? w.size : 0;
+        SlotList list{0, 0, count};
+        uint32_t first = 0;
         bool ok = true;
-        if (allocates) {  // in-order, first-fit contiguous allocation
-            uint32_t got = 0xffffffffu;
+        if (allocates) {  // in-order allocation: a contiguous run if one exists, else any free slots
+            uint32_t take = 0;
             if (lane == 0) {
                 const unsigned long long t0 = clock64();
                 ok = spin_until(c, [&] {
                     const uint32_t freebits = ~C.alloc_mask & budget_mask;
+                    if (uint32_t(__popc(freebits)) < count) return false;
                     uint32_t runs = freebits;
                     for (uint32_t k = 1; k < count && runs; ++k) runs &= freebits >> k;
-                    if (!runs) return false;
-                    got = __ffs(runs) - 1;
+                    if (runs) {
+                        take = (count >= 32 ? 0xffffffffu : ((1u << count) - 1u)) << (__ffs(runs) - 1);
+                    } else {
+                        take = 0;
+                        uint32_t f = freebits;
+                        for (uint32_t k = 0; k < count; ++k) {
+                            const uint32_t low = f & (0u - f);
+                            take |= low;
+                            f ^= low;
+                        }
+                    }
                     return true;
                 }, core, pc);
-                if (ok) {
-                    const uint32_t bits = (count >= 32 ? 0xffffffffu : ((1u << count) - 1u)) << got;
-                    atomicOr(const_cast<uint32_t*>(&C.alloc_mask), bits);
-                }
+                if (ok) atomicOr(const_cast<uint32_t*>(&C.alloc_mask), take);
                 c.P->stats[c.sm].cfu_stall_cycles += clock64() - t0;
             }
             ok = __shfl_sync(0xffffffffu, ok, 0);
-            first = __shfl_sync(0xffffffffu, got, 0);
+            take = __shfl_sync(0xffffffffu, take, 0);
             if (!ok) break;
+            if (count > 8) {
+                if (lane == 0) {
+                    P.status->fault_code = 5;
+                    P.status->fault_info = pc;
+                    atomicExch(&P.status->abort, 2);
+                }
+                break;
+            }
+            for (uint32_t k = 0; k < count; ++k) {
+                const uint32_t idx = __ffs(take) - 1;
+                take &= take - 1;
+                if (k < 4) list.lo |= idx << (8 * k); else list.hi |= idx << (8 * (k - 4));
+            }
+            first = list.at(0);
         }
         // m2c reservation (stream order per VCC)
         uint32_t m2c_idx = 0;
@@ -400,7 +432,7 @@ __device__ void cfu_role(Cta& c) {
                         parity = C.bar_uses[first] & 1;
                         C.bar_uses[first] += 1;
                     }
-                    e.slots = first | (count << 8);
+                    e.slots = list;
                     e.rows = t.rows_at;
                     e.cols = t.cols_at;
                     e.stride = t.tile_cols;
@@ -437,7 +469,7 @@ __device__ void cfu_role(Cta& c) {
                 q.dtype = uint8_t(t.dtype);
                 q.dep_id = uint16_t(w.dep);
                 q.size = uint16_t(w.size);
-                q.slots = first | (count << 8);
+                q.slots = list;
                 q.m2c = m2c_idx;
                 q.storage = t.storage;
                 q.bytes = (w.size == 0 && w.op != OP_LOAD_LOCAL) ? 0 : t.bytes;
@@ -468,31 +500,39 @@ __device__ void cfu_role(Cta& c) {
 // ---------------------------------------------------------------------------
 // load unit
 
-// copy one tile region global -> shared; completes the slot barrier
+// copy one tile region global -> shared; completes the first slot's barrier
 __device__ void copy_in(Cta& c, const UnitOp& q, uint32_t lane) {
     Control& C = *c.C;
-    const uint32_t first = q.slots & 0xff;
-    char* dst = c.slot_ptr(first);
+    const uint32_t first = q.slots.at(0);
     uint64_t* bar = &C.full_bar[first];
     const uint32_t row_bytes = uint32_t(q.cols_at) * q.elem;
     const uint32_t spitch = uint32_t(q.tile_cols) * q.elem;
     const bool contiguous = q.rows_at == 1 || (int64_t(row_bytes) == q.gpitch && row_bytes == spitch);
     const bool aligned = (reinterpret_cast<uintptr_t>(q.gptr) & 15) == 0;
+    const bool one_run = Cta::contiguous(q.slots);
+    const uint32_t ssz = c.P->slot_size;
     if (contiguous && aligned && (q.bytes & 15) == 0) {
         if (lane == 0) {
             mbar_expect_tx(bar, q.bytes);
-            bulk_g2s(dst, q.gptr, q.bytes, bar);
+            if (one_run) {
+                bulk_g2s(c.slot_ptr(first), q.gptr, q.bytes, bar);
+            } else {  // scattered slots: one bulk copy per slot-sized chunk
+                for (uint32_t off = 0, i = 0; off < q.bytes; off += ssz, ++i)
+                    bulk_g2s(c.slot_ptr(q.slots.at(i)), q.gptr + off, min(ssz, q.bytes - off), bar);
+            }
         }
-    } else if (aligned && (row_bytes & 15) == 0 && (q.gpitch & 15) == 0 && (spitch & 15) == 0) {
+    } else if (aligned && (row_bytes & 15) == 0 && (q.gpitch & 15) == 0 && (spitch & 15) == 0 &&
+               (one_run || (ssz % spitch == 0))) {
         if (lane == 0) mbar_expect_tx(bar, q.bytes);
         __syncwarp();
-        for (int r = int(lane); r < q.rows_at; r += 32) bulk_g2s(dst + size_t(r) * spitch, q.gptr + r * q.gpitch, row_bytes, bar);
+        for (int r = int(lane); r < q.rows_at; r += 32)
+            bulk_g2s(c.region_ptr(q.slots, uint32_t(r) * spitch), q.gptr + r * q.gpitch, row_bytes, bar);
     } else {  // odd geometry: cooperative element copy, then a plain arrive
         const int elems = q.rows_at * q.cols_at;
         for (int i = int(lane); i < elems; i += 32) {
             const int r = i / q.cols_at, col = i % q.cols_at;
             const char* s = q.gptr + r * q.gpitch + int64_t(col) * q.elem;
-            char* d = dst + size_t(r) * spitch + size_t(col) * q.elem;
+            char* d = c.region_ptr(q.slots, uint32_t(r) * spitch + uint32_t(col) * q.elem);
             if (q.elem == 4) *reinterpret_cast<uint32_t*>(d) = *reinterpret_cast<const volatile uint32_t*>(s);
             else if (q.elem == 2) *reinterpret_cast<uint16_t*>(d) = *reinterpret_cast<const volatile uint16_t*>(s);
             else *reinterpret_cast<uint64_t*>(d) = *reinterpret_cast<const volatile uint64_t*>(s);
@@ -528,12 +568,12 @@ __device__ void ldu_role(Cta& c, uint32_t u) {
         // dependency side
         if (q.op == OP_LOAD_DEP || q.op == OP_LOAD_LOCAL) {
             DepQueue* dq = &P.deps[q.dep_id];
-            uint32_t payload[4] = {0, 0, 0, 0};
+            uint32_t payload[6] = {0, 0, 0, 0, 0, 0};
             if (lane == 0) {
                 const uint32_t mine = dq->consumed;
                 ok = spin_until(c, [&] { return ld_acquire(&dq->produced) > mine; }, core, q.core_pc);
                 if (ok) {
-                    for (int i = 0; i < 4; ++i) payload[i] = reinterpret_cast<volatile uint32_t*>(dq->payload)[i];
+                    for (int i = 0; i < 6; ++i) payload[i] = reinterpret_cast<volatile uint32_t*>(dq->payload)[i];
                     st_release(&dq->consumed, mine + 1);
                 }
             }
@@ -541,10 +581,10 @@ __device__ void ldu_role(Cta& c, uint32_t u) {
             if (!ok) break;
             if (q.op == OP_LOAD_LOCAL) {  // slot ownership arrives with the token
                 if (lane == 0 && e) {
-                    e->slots = payload[0];
-                    e->rows = int32_t(payload[1]);
-                    e->cols = int32_t(payload[2]);
-                    e->stride = int32_t(payload[3]);
+                    e->slots = SlotList{payload[0], payload[1], payload[2]};
+                    e->rows = int32_t(payload[3]);
+                    e->cols = int32_t(payload[4]);
+                    e->stride = int32_t(payload[5]);
                     e->meta &= ~(1u << 9);  // no data movement to wait for
                     __threadfence_block();
                     e->ready = q.m2c + 1;
@@ -564,7 +604,7 @@ __device__ void ldu_role(Cta& c, uint32_t u) {
             ok = __shfl_sync(0xffffffffu, ok, 0);
             if (!ok) break;
         }
-        if (q.bytes > 0 && (q.slots >> 8) > 0) {
+        if (q.bytes > 0 && q.slots.count > 0) {
             copy_in(c, q, lane);
             bytes += q.bytes;
         }
@@ -583,24 +623,34 @@ __device__ void ldu_role(Cta& c, uint32_t u) {
 // ---------------------------------------------------------------------------
 // store unit
 
-__device__ __forceinline__ void free_slots(Control& C, uint32_t slots) {
-    const uint32_t first = slots & 0xff, count = slots >> 8;
-    if (!count) return;
-    const uint32_t bits = (count >= 32 ? 0xffffffffu : ((1u << count) - 1u)) << first;
-    atomicAnd(const_cast<uint32_t*>(&C.alloc_mask), ~bits);
+__device__ __forceinline__ void free_slots(Control& C, const SlotList& l) {
+    uint32_t bits = 0;
+    for (uint32_t i = 0; i < l.count; ++i) bits |= 1u << l.at(i);
+    if (bits) atomicAnd(const_cast<uint32_t*>(&C.alloc_mask), ~bits);
 }
 
 // slot -> global copy of the target tile (generic stores, warp-cooperative)
 __device__ void copy_out(Cta& c, const UnitOp& q, const C2M& m, uint32_t lane) {
-    const char* src = c.slot_ptr(m.slots & 0xff);
+    const bool one_run = Cta::contiguous(m.slots);
+    const char* src = c.slot_ptr(m.slots.at(0));
     const int rows = q.rows_at, cols = q.cols_at;
     const uint32_t spitch = uint32_t(q.tile_cols) * q.elem;
     const uint32_t row_bytes = uint32_t(cols) * q.elem;
     const bool contiguous = rows == 1 || (int64_t(row_bytes) == q.gpitch && row_bytes == spitch);
-    if (contiguous && (reinterpret_cast<uintptr_t>(q.gptr) & 15) == 0 && (q.bytes & 15) == 0) {
+    if (contiguous && one_run && (reinterpret_cast<uintptr_t>(q.gptr) & 15) == 0 && (q.bytes & 15) == 0) {
         const int n16 = int(q.bytes >> 4);
         for (int i = int(lane); i < n16; i += 32)
             reinterpret_cast<uint4*>(q.gptr)[i] = reinterpret_cast<const uint4*>(src)[i];
+    } else if (!one_run) {
+        const int elems = rows * cols;
+        for (int i = int(lane); i < elems; i += 32) {
+            const int r = i / cols, col = i % cols;
+            char* d = q.gptr + r * q.gpitch + int64_t(col) * q.elem;
+            const char* s = c.region_ptr(m.slots, uint32_t(r) * spitch + uint32_t(col) * q.elem);
+            if (q.elem == 4) *reinterpret_cast<uint32_t*>(d) = *reinterpret_cast<const uint32_t*>(s);
+            else if (q.elem == 2) *reinterpret_cast<uint16_t*>(d) = *reinterpret_cast<const uint16_t*>(s);
+            else *reinterpret_cast<uint64_t*>(d) = *reinterpret_cast<const uint64_t*>(s);
+        }
     } else {
         const int elems = rows * cols;
         for (int i = int(lane); i < elems; i += 32) {
@@ -650,7 +700,7 @@ __device__ void stu_role(Cta& c, uint32_t u) {
             if (!ok) break;
             __threadfence_block();
         }
-        C2M first_msg = need ? C.c2m[v][c2m_tail[v] % kC2mDepth] : C2M{0, 0, 0, 0};
+        C2M first_msg = need ? C.c2m[v][c2m_tail[v] % kC2mDepth] : C2M{SlotList{0, 0, 0}, 0, 0, 0};
         if (q.op == OP_FREE) {
             if (lane == 0)
                 for (uint32_t i = 0; i < need; ++i) free_slots(C, C.c2m[v][(c2m_tail[v] + i) % kC2mDepth].slots);
@@ -673,10 +723,12 @@ __device__ void stu_role(Cta& c, uint32_t u) {
                     if (ok) {
                         if (q.op == OP_STORE_LOCAL) {
                             volatile uint32_t* pl = dq->payload;
-                            pl[0] = first_msg.slots;
-                            pl[1] = uint32_t(first_msg.rows);
-                            pl[2] = uint32_t(first_msg.cols);
-                            pl[3] = uint32_t(first_msg.stride);
+                            pl[0] = first_msg.slots.lo;
+                            pl[1] = first_msg.slots.hi;
+                            pl[2] = first_msg.slots.count;
+                            pl[3] = uint32_t(first_msg.rows);
+                            pl[4] = uint32_t(first_msg.cols);
+                            pl[5] = uint32_t(first_msg.stride);
                         }
                         __threadfence();
                         st_release(&dq->produced, made + 1);
@@ -700,9 +752,11 @@ __device__ void stu_role(Cta& c, uint32_t u) {
 // compute virtual core
 
 struct Msg {
-    char* data;
+    char* data;  // first slot (1-slot tiles and contiguous runs)
     int32_t rows, cols, stride, row0, col0, dtype;
-    uint32_t slots;
+    SlotList slots;
+    const Cta* c;
+    __device__ char* ptr(uint32_t off) const { return c->region_ptr(slots, off); }
 };
 
 struct Vcc {
@@ -739,7 +793,8 @@ struct Vcc {
         m.row0 = e.row0;
         m.col0 = e.col0;
         m.dtype = int32_t(meta & 0xff);
-        m.data = c->slot_ptr(m.slots & 0xff);
+        m.data = c->slot_ptr(m.slots.at(0));
+        m.c = c;
         if (meta & (1u << 9)) {
             uint64_t* b = &C.full_bar[meta >> 16];
             const uint32_t parity = (meta >> 8) & 1;
@@ -775,7 +830,8 @@ struct Vcc {
         m.row0 = e.row0;
         m.col0 = e.col0;
         m.dtype = int32_t(meta & 0xff);
-        m.data = c->slot_ptr(m.slots & 0xff);
+        m.data = c->slot_ptr(m.slots.at(0));
+        m.c = c;
         if (meta & (1u << 9)) {
             uint64_t* b = &C.full_bar[meta >> 16];
             const uint32_t parity = (meta >> 8) & 1;
@@ -1033,14 +1089,17 @@ __device__ void h_gemv(Vcc& k, const Word& w, uint32_t pc) {
     for (int i = int(k.t); i < kAccRows; i += 32 * kVccWarps) acc[i] = 0.f;
     if (w.op == OP_RMS_GEMV) {  // x <- round(x * rsqrt(mean(x^2) + eps) * w), in place
         float ss = 0.f;
+        const int xe = x.dtype == VDC_DTYPE_BF16 ? 2 : 4, we = third.dtype == VDC_DTYPE_BF16 ? 2 : 4;
         for (int i = int(k.t); i < K; i += 32 * kVccWarps) {
-            const float v = load_elem(x.data, x.dtype, i);
+            const float v = load_elem(x.ptr(uint32_t(i * xe)), x.dtype, 0);
             ss += v * v;
         }
         ss = vcc_sum(k, ss);
         const float inv = 1.0f / sqrtf(ss / float(K) + hp[VDC_GEMV_P_EPS]);
-        for (int i = int(k.t); i < K; i += 32 * kVccWarps)
-            store_elem(x.data, x.dtype, i, load_elem(x.data, x.dtype, i) * inv * load_elem(third.data, third.dtype, i));
+        for (int i = int(k.t); i < K; i += 32 * kVccWarps) {
+            char* xp = x.ptr(uint32_t(i * xe));
+            store_elem(xp, x.dtype, 0, load_elem(xp, x.dtype, 0) * inv * load_elem(third.ptr(uint32_t(i * we)), third.dtype, 0));
+        }
     }
     k.sync();
     int job_row0 = -1, raw_rows = 0;
@@ -1051,16 +1110,23 @@ __device__ void h_gemv(Vcc& k, const Word& w, uint32_t pc) {
         raw_rows = max(raw_rows, rbase + g.rows);
         const bool fast = g.dtype == VDC_DTYPE_BF16 && x.dtype == VDC_DTYPE_BF16 && (g.cols & 7) == 0 &&
                           (g.stride & 7) == 0 && (g.col0 & 7) == 0;
+        const int xe = x.dtype == VDC_DTYPE_BF16 ? 2 : 4, ge = g.dtype == VDC_DTYPE_BF16 ? 2 : 4;
+        const uint32_t ssz = k.c->P->slot_size;
+        // the x segment of this tile lies in one slot unless it straddles a slot edge
+        const uint32_t xoff = uint32_t(g.col0) * uint32_t(xe);
+        const bool xseg = (xoff % ssz) + uint32_t(g.cols) * uint32_t(xe) <= ssz;
         for (int r = wp; r < g.rows; r += kVccWarps) {
             float s = 0.f;
-            if (fast) {
-                const uint4* wr = reinterpret_cast<const uint4*>(g.data + size_t(r) * g.stride * 2);
-                const uint4* xv = reinterpret_cast<const uint4*>(x.data + size_t(g.col0) * 2);
+            const uint32_t roff = uint32_t(r) * uint32_t(g.stride) * uint32_t(ge);
+            if (fast && xseg && (roff % ssz) + uint32_t(g.cols) * 2u <= ssz) {
+                const uint4* wr = reinterpret_cast<const uint4*>(g.ptr(roff));
+                const uint4* xv = reinterpret_cast<const uint4*>(x.ptr(xoff));
                 const int n8 = g.cols >> 3;
                 for (int ch = lane; ch < n8; ch += 32) s += dot_bf16x8(wr[ch], xv[ch]);
             } else {
                 for (int col = lane; col < g.cols; col += 32)
-                    s += load_elem(g.data, g.dtype, int64_t(r) * g.stride + col) * load_elem(x.data, x.dtype, g.col0 + col);
+                    s += load_elem(g.ptr(roff + uint32_t(col * ge)), g.dtype, 0) *
+                         load_elem(x.ptr(uint32_t((g.col0 + col) * xe)), x.dtype, 0);
             }
             s = warp_sum(s);
             if (lane == 0 && rbase + r < kAccRows) acc[rbase + r] += s;
@@ -1142,15 +1208,17 @@ __device__ void h_attn_decode(Vcc& k, const Word& w, uint32_t pc) {
                 float acc = 0.f;
                 if (kt.dtype == VDC_DTYPE_BF16 && q.dtype == VDC_DTYPE_BF16 && (hd & 7) == 0) {
                     const int nch = hd >> 3;
-                    const uint4* kr = reinterpret_cast<const uint4*>(kt.data + size_t(r) * kt.stride * 2);
+                    const uint4* kr = reinterpret_cast<const uint4*>(kt.ptr(uint32_t(r) * uint32_t(kt.stride) * 2u));
                     const uint4* qv = reinterpret_cast<const uint4*>(q.data + size_t(h) * hd * 2);
                     for (int cc = 0; cc < nch; ++cc) {
                         const int ch = (cc + lane) % nch;  // rotate to spread smem banks
                         acc += dot_bf16x8(kr[ch], qv[ch]);
                     }
                 } else {
+                    const int ke = kt.dtype == VDC_DTYPE_BF16 ? 2 : 4;
+                    const char* kr = kt.ptr(uint32_t(r) * uint32_t(kt.stride) * uint32_t(ke));
                     for (int d = 0; d < hd; ++d)
-                        acc += load_elem(q.data, q.dtype, int64_t(h) * hd + d) * load_elem(kt.data, kt.dtype, int64_t(r) * kt.stride + d);
+                        acc += load_elem(q.data, q.dtype, int64_t(h) * hd + d) * load_elem(kr, kt.dtype, d);
                 }
                 s[rr] = acc * scale;
             }
@@ -1166,8 +1234,8 @@ __device__ void h_attn_decode(Vcc& k, const Word& w, uint32_t pc) {
             for (int r = 0; r < vt.rows && r < 64; ++r) {
                 const float pr = __shfl_sync(0xffffffffu, p[r >> 5], r & 31);
                 if (pr == 0.f) continue;
-                for (int d = 0; d < dpl; ++d)
-                    o[hi][d] += pr * load_elem(vt.data, vt.dtype, int64_t(r) * vt.stride + lane * dpl + d);
+                const char* vr = vt.ptr(uint32_t(r) * uint32_t(vt.stride) * uint32_t(vt.dtype == VDC_DTYPE_BF16 ? 2 : 4));
+                for (int d = 0; d < dpl; ++d) o[hi][d] += pr * load_elem(vr, vt.dtype, lane * dpl + d);
             }
             m[hi] = mnew;
         }
@@ -1429,7 +1497,7 @@ int vdc_create(const vdc_profile* p, int device, vdc_ctx** out) {
     if (p->ldu_count < 1 || p->ldu_count > uint32_t(kMaxLdu)) return fail(VDC_ERR_INPUT, "ldu_count must be 1..2");
     if (p->stu_count < 1 || p->stu_count > uint32_t(kMaxStu)) return fail(VDC_ERR_INPUT, "stu_count must be 1..2");
     if (p->slot_budget < 1 || p->slot_budget > uint32_t(kMaxSlots)) return fail(VDC_ERR_INPUT, "slot_budget must be 1..32");
-    if (p->slot_size % 1024) return fail(VDC_ERR_INPUT, "slot_size must be a multiple of 1024");
+    if (p->slot_size < 1024 || (p->slot_size & (p->slot_size - 1))) return fail(VDC_ERR_INPUT, "slot_size must be a power of two >= 1024");
     CU(cudaSetDevice(device));
     cudaDeviceProp prop;
     CU(cudaGetDeviceProperties(&prop, device));
@@ -1628,6 +1696,7 @@ int vdc_launch(vdc_ctx* ctx, void* stream) {
     P.ldu_count = ctx->prof.ldu_count;
     P.stu_count = ctx->prof.stu_count;
     P.slot_size = ctx->prof.slot_size;
+    P.slot_shift = uint32_t(__builtin_ctz(ctx->prof.slot_size));
     P.slot_budget = ctx->prof.slot_budget;
     P.local_depth = ctx->local_depth;
     P.stats = ctx->d_stats;

@@ -23,7 +23,7 @@ constexpr int kMaxStu = 2;
 constexpr int kVccWarps = 4;
 constexpr int kM2cDepth = 64;   // >= any program's local_queue_depth (checked at load)
 constexpr int kC2mDepth = 64;
-constexpr int kUnitDepth = 32;
+constexpr int kUnitDepth = 16;
 constexpr int kCfuChunk = 64;   // words per stream prefetch chunk (1 KB)
 constexpr int kAccRows = 256;   // per-VCC fp32 accumulator scratch (streaming GEMV rows)
 constexpr int kMaxSlots = 32;
@@ -49,7 +49,7 @@ struct DepQueue {          // global FIFO per dep id (single producer / consumer
     uint32_t consumed;
     uint32_t depth;
     uint32_t local;
-    uint32_t payload[4];   // STORE_LOCAL slot handoff: first | count<<8 ; rows ; cols ; stride
+    uint32_t payload[6];   // STORE_LOCAL slot handoff: slots lo, hi, count ; rows ; cols ; stride
 };
 
 struct SmStats {
@@ -80,25 +80,36 @@ struct EngineParams {
     const int64_t* step;
     int32_t n_step;
     uint32_t sm_count, vcc_per_sm, ldu_count, stu_count;
-    uint32_t slot_size, slot_budget, local_depth;
+    uint32_t slot_size, slot_shift, slot_budget, local_depth;
     SmStats* stats;
     Status* status;
     unsigned long long watchdog_ns;
 };
 
+// A region of `count` slots, not necessarily contiguous (indices packed 8
+// bits each): the allocator prefers a contiguous run but falls back to any
+// free slots, so admission is exactly "free slots >= count" — the condition
+// the generator's certificate is computed with (contiguity-only allocation
+// can starve on fragmentation). Reference programs only use 1-slot tiles.
+struct SlotList {
+    uint32_t lo, hi;  // slot indices 0..3 / 4..7
+    uint32_t count;
+    __host__ __device__ uint32_t at(uint32_t i) const { return ((i < 4 ? lo >> (8 * i) : hi >> (8 * (i - 4))) & 0xff); }
+};
+
 // m2c message: one slot region handed from the VMC to a VCC.
 struct M2C {
-    uint32_t slots;     // first | count << 8
+    SlotList slots;
     int32_t rows, cols; // payload extents (edge-trimmed)
     int32_t stride;     // padded row stride in elements (tile_cols)
     int32_t row0, col0; // global first row / col of the tile (trailing dims)
-    uint32_t meta;      // dtype | (parity << 8) | (wait << 9) | (first_slot_bar << 16)
+    uint32_t meta;      // dtype | (parity << 8) | (wait << 9) | (barrier slot << 16)
     volatile uint32_t ready;  // entry index + 1 once the LDU has issued the data movement
 };
 
 // c2m message: a region released (or produced) by a VCC.
 struct C2M {
-    uint32_t slots;
+    SlotList slots;
     int32_t rows, cols, stride;
 };
 
@@ -106,7 +117,7 @@ struct C2M {
 struct UnitOp {
     uint8_t op, flags, reg1, dtype;
     uint16_t dep_id, size;
-    uint32_t slots;       // allocated / carried region
+    SlotList slots;       // allocated region
     uint32_t m2c;         // m2c entry index (send)
     int32_t storage;      // counter index of the resolved tensor (-1 none)
     uint32_t bytes;       // tile payload bytes (0 = no data movement)
@@ -116,7 +127,6 @@ struct UnitOp {
     char* gptr;           // first element of the tile in global memory
     int64_t gpitch;       // global row pitch in bytes
     uint32_t core_pc;
-    uint32_t pad;
 };
 
 struct Ring {

@@ -111,7 +111,18 @@ struct Builder {
         auto [tr, tc] = weight_tile(rows, cols, m.dtype, l);
         while (job_rows % tr) --tr;
         const InitKind init = m.scaled_init ? InitKind::centered : InitKind::random;
-        add(name, {rows, cols}, tr, tc, init, m.dtype, m.scaled_init ? float(1.0 / std::sqrt(double(fan_in))) : 1.0f);
+        const float scale = m.scaled_init ? float(1.0 / std::sqrt(double(fan_in))) : 1.0f;
+        // the word format encodes tile coordinates in 12 bits: tall matrices
+        // become (planes, rows/plane, K) — same row-major storage — with the
+        // fewest planes that keep every coordinate < 4096 and jobs inside a plane
+        int64_t planes = 1;
+        while (rows / planes / tr > 4095 || rows % planes || (rows / planes) % job_rows) {
+            if (++planes > rows) throw workload::WorkloadError(name + ": no plane split fits the 12-bit tile coordinates");
+        }
+        if (planes == 1)
+            add(name, {rows, cols}, tr, tc, init, m.dtype, scale);
+        else
+            add(name, {planes, rows / planes, cols}, tr, tc, init, m.dtype, scale);
         return name;
     }
     std::string norm(const std::string& name, int64_t rows) {

@@ -159,7 +159,10 @@ class DecodeLowering {
     void plan_gemv(const workload::OperatorNode& n, uint32_t ordinal) {
         const uint16_t w = idx(n.inputs[0]);
         const TileDescriptor& wd = desc_[w];
-        const int64_t M = wd.rows(), R = attr_int(n, "job_rows", 16);
+        // W is (M,K) or (P, M/P, K) planes of the same row-major storage
+        const int64_t plane_rows = wd.rows(), M = wd.elem_count() / wd.cols(), R = attr_int(n, "job_rows", 16);
+        const bool planar = wd.shape.size() == 3;
+        if (plane_rows % R) throw GeneratorError("node " + n.id + ": job_rows must divide the rows of a weight plane");
         const int64_t swiglu = attr_int(n, "swiglu", 0);
         const bool rope = attr_int(n, "rope", 0) != 0;
         if (R % wd.tile_rows) throw GeneratorError("node " + n.id + ": job_rows must be a multiple of the weight tile rows");
@@ -189,8 +192,11 @@ class DecodeLowering {
                 const uint16_t third = idx(n.inputs[2]);
                 jb.prologue.push_back(n.kind == OpKind::RMS_GEMV ? at(third, {0, 0}) : at(third, {uint16_t(j), 0}));
             }
-            for (int64_t rt = j * R / wd.tile_rows; rt < (j + 1) * R / wd.tile_rows; ++rt)
-                for (int64_t kt = 0; kt < ktiles; ++kt) jb.groups.push_back({at(w, {uint16_t(rt), uint16_t(kt)})});
+            const int64_t plane = (j * R) / plane_rows, prow = (j * R) % plane_rows;
+            for (int64_t rt = prow / wd.tile_rows; rt < (prow + R) / wd.tile_rows; ++rt)
+                for (int64_t kt = 0; kt < ktiles; ++kt)
+                    jb.groups.push_back({planar ? at(w, {uint16_t(plane), uint16_t(rt), uint16_t(kt)})
+                                                : at(w, {uint16_t(rt), uint16_t(kt)})});
             const int64_t r0 = j * R;
             if (n.outputs.size() == 3 && r0 >= qrows) {
                 const bool is_k = r0 < qrows + kvrows;
@@ -318,8 +324,10 @@ class DecodeLowering {
         for (const auto& f : j.prologue) out.push_back({fetch_word(f, j.vcc), meta});
         const int n = int(j.groups.size());
         for (int gi = 0; gi < n; ++gi) {
-            for (const auto& f : j.groups[size_t(gi)]) out.push_back({fetch_word(f, j.vcc), meta});
+            // release group gi-window before loading group gi: the job never
+            // holds more than prologue + window groups (+ result at the end)
             if (io.streaming && gi >= window) release(io.iter_pushes_c2m);
+            for (const auto& f : j.groups[size_t(gi)]) out.push_back({fetch_word(f, j.vcc), meta});
         }
         UopWord alloc;
         alloc.opcode = Opcode::ALLOC;
