@@ -42,7 +42,7 @@ def model_request(layers: int = 32, ctx: int = CTX) -> dict:
     pages = (ctx + 63) // 64
     return {
         "model": {"preset": "llama3-8b", "layers": layers},
-        "layout": {"ctx_pages": pages, "max_ctx": pages * 64, "pages_per_job": 2, "job_rows": 16, "gu_block": 32,
+        "layout": {"ctx_pages": pages, "max_ctx": pages * 64, "pages_per_job": 4, "job_rows": 16, "gu_block": 32,
                    "head_job_rows": 64},
         "profile": {"builtin": "b200"},
     }

@@ -47,7 +47,7 @@ struct LayoutConfig {
     int job_rows = 16;       // output rows per GEMV job (divides head_dim)
     int head_job_rows = 64;  // output rows per lm_head job
     int gu_block = 16;       // swiglu interleave block (== job_rows for the gu node)
-    int wtile_bytes = 16384; // target weight tile bytes
+    int wtile_bytes = 32768; // target weight tile bytes (32 KB: full 4096-wide rows)
 };
 
 ModelConfig llama3_8b();

@@ -84,6 +84,10 @@ typedef struct vdc_report {
     double elapsed_ms;         /* device time of the last launch                 */
     uint32_t stalled_core[16]; /* core index (CoreId order) of blocked cores     */
     uint32_t stalled_pc[16];
+    /* cycles spent at each engine wait site, summed over SMs (see
+     * engine.cuh WaitSite: cfu alloc/m2c/unit, ldu idle/dep, stu idle/c2m/dep,
+     * vcc ready/barrier/c2m, vcc compute, cfu total, vcc total, ldu issue) */
+    uint64_t wait_cycles[24];
     char message[256];
 } vdc_report;
 
@@ -113,6 +117,10 @@ int vdc_bind_step(vdc_ctx* ctx, int64_t* dptr, uint32_t n);
 int vdc_launch(vdc_ctx* ctx, void* stream);
 /* synchronise with the last launch and fill the report */
 int vdc_wait(vdc_ctx* ctx, vdc_report* report);
+/* device trace (optional): per VCC core `records_per_core` records of four
+ * uint64 {core << 32 | pc, t_enter, t_prologue_ready, t_done} in %globaltimer
+ * ns, written for each compute µop; dptr = NULL disables tracing */
+int vdc_bind_trace(vdc_ctx* ctx, void* dptr, uint32_t records_per_core);
 /* watchdog: abort a launch whose cores make no progress for `ms` (0 = off) */
 int vdc_set_watchdog(vdc_ctx* ctx, uint32_t ms);
 
@@ -122,8 +130,9 @@ int vdc_set_watchdog(vdc_ctx* ctx, uint32_t ms);
 int vdc_program_build(const char* request_json, vdc_program** out);
 int vdc_program_parse(const char* streams_json, const char* sidecar, vdc_program** out);
 void vdc_program_free(vdc_program* prog);
-/* JSON: {"streams":{core:text}, "sidecar":..., "words":{core:hex}?, "tilings":..., ...} */
-int vdc_program_text(const vdc_program* prog, int with_words, char** out_json);
+/* JSON: {"streams":{core:text}, "sidecar":..., "words":{core:hex}?, "tilings":..., ...}
+ * mode 0: streams + sidecar, 1: also encoded words, 2: summary (descriptors, params, geometry) */
+int vdc_program_text(const vdc_program* prog, int mode, char** out_json);
 int vdc_program_cores(const vdc_program* prog, uint32_t* n_cores, uint32_t* sm_count, uint32_t* vcc_per_sm);
 /* encoded stream of core i (CoreId order over sm_count x (1 + vcc_per_sm)) */
 int vdc_program_words(const vdc_program* prog, uint32_t core, const uint8_t** words, uint32_t* n_words);

@@ -62,6 +62,7 @@ class vdc_report(ctypes.Structure):
         ("elapsed_ms", ctypes.c_double),
         ("stalled_core", ctypes.c_uint32 * 16),
         ("stalled_pc", ctypes.c_uint32 * 16),
+        ("wait_cycles", ctypes.c_uint64 * 24),
         ("message", ctypes.c_char * 256),
     ]
 
@@ -69,7 +70,7 @@ class vdc_report(ctypes.Structure):
 # every symbol include/vdc.h declares (the CPU suite checks they are exported)
 EXPORTS = [
     "vdc_last_error", "vdc_version", "vdc_create", "vdc_destroy", "vdc_load_program", "vdc_set_params",
-    "vdc_bind_tensor", "vdc_bind_step", "vdc_launch", "vdc_wait", "vdc_set_watchdog", "vdc_program_build",
+    "vdc_bind_tensor", "vdc_bind_step", "vdc_bind_trace", "vdc_launch", "vdc_wait", "vdc_set_watchdog", "vdc_program_build",
     "vdc_program_parse", "vdc_program_free", "vdc_program_text", "vdc_program_cores", "vdc_program_words",
     "vdc_program_load", "vdc_free_string",
 ]
@@ -96,6 +97,7 @@ def lib() -> ctypes.CDLL:
         "vdc_set_params": ([vp, c.POINTER(c.c_float), c.c_uint32], c.c_int),
         "vdc_bind_tensor": ([vp, c.c_uint16, vp, c.c_size_t, c.c_int], c.c_int),
         "vdc_bind_step": ([vp, vp, c.c_uint32], c.c_int),
+        "vdc_bind_trace": ([vp, vp, c.c_uint32], c.c_int),
         "vdc_launch": ([vp, vp], c.c_int),
         "vdc_wait": ([vp, c.POINTER(vdc_report)], c.c_int),
         "vdc_set_watchdog": ([vp, c.c_uint32], c.c_int),
@@ -157,8 +159,11 @@ class Program:
         return json.loads(take_string(out))
 
     def info(self) -> dict:
+        """Summary (descriptors, params, geometry) without stream text."""
         if self._info is None:
-            self._info = self.text(False)
+            out = ctypes.c_void_p()
+            check(lib().vdc_program_text(self._h, 2, ctypes.byref(out)))
+            self._info = json.loads(take_string(out))
         return self._info
 
     def cores(self):

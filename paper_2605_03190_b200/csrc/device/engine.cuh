@@ -52,12 +52,20 @@ struct DepQueue {          // global FIFO per dep id (single producer / consumer
     uint32_t payload[6];   // STORE_LOCAL slot handoff: slots lo, hi, count ; rows ; cols ; stride
 };
 
+// wait-site accounting (cycles spent blocked, per SM, summed over roles)
+enum WaitSite : int {
+    W_CFU_ALLOC = 0, W_CFU_M2C, W_CFU_UNIT, W_LDU_IDLE, W_LDU_DEP, W_STU_IDLE, W_STU_C2M, W_STU_DEP,
+    W_VCC_READY, W_VCC_BAR, W_VCC_C2M, W_VCC_COMPUTE, W_CFU_TOTAL, W_VCC_TOTAL, W_LDU_ISSUE, W_CFU_RESOLVE,
+    W_VCC_SYNC, W_VCC_PUSH, W_VCC_PROLOGUE, W_VCC_EPILOGUE, W_VCC_POP, W_CFU_ALLOCLOOP, W_CFU_SYNCK, W_CFU_DISPATCH, W_NSITES
+};
+
 struct SmStats {
     unsigned long long uops;
     unsigned long long bytes_loaded;
     unsigned long long bytes_stored;
     unsigned long long cfu_stall_cycles;
-    unsigned long long pad[4];
+    unsigned long long wait[24];
+    unsigned long long cfu_phase[4];  // refill, resolve, m2c, unit push
 };
 
 struct Status {
@@ -84,6 +92,10 @@ struct EngineParams {
     SmStats* stats;
     Status* status;
     unsigned long long watchdog_ns;
+    // optional device trace: per VCC core, `trace_cap` records of
+    // {core << 32 | pc, t_enter, t_prologue_ready, t_done} (%globaltimer ns)
+    unsigned long long* trace;
+    uint32_t trace_cap;
 };
 
 // A region of `count` slots, not necessarily contiguous (indices packed 8
@@ -113,8 +125,8 @@ struct C2M {
     int32_t rows, cols, stride;
 };
 
-// CFU -> unit work item.
-struct UnitOp {
+// CFU -> unit work item (written with four 16-byte stores).
+struct alignas(16) UnitOp {
     uint8_t op, flags, reg1, dtype;
     uint16_t dep_id, size;
     SlotList slots;       // allocated region
@@ -134,6 +146,12 @@ struct Ring {
     volatile uint32_t tail;
 };
 
+// per-batch scratch of the warp-parallel CFU
+struct CfuScratch {
+    uint32_t info[32];    // per lane: count | send << 8 | vcc << 9 | (unit + 1) << 12
+    SlotList lists[32];   // slot lists chosen by lane 0's in-order allocation
+};
+
 struct alignas(16) Control {
     uint64_t full_bar[kMaxSlots];
     uint32_t bar_uses[kMaxSlots];
@@ -147,7 +165,12 @@ struct alignas(16) Control {
     C2M c2m[kMaxVcc][kC2mDepth];
     UnitOp ldu_q[kMaxLdu][kUnitDepth];
     UnitOp stu_q[kMaxStu][kUnitDepth];
-    uint4 cfu_buf[kCfuChunk];
+    CfuScratch cfu;
+    // per-role wait-site counters (cycles >> 6) and per-core accumulator
+    // registers live in shared memory: run-time indexed per-thread arrays
+    // would sit in local memory, which misses L1 after every gpu-scope fence
+    uint32_t stat[1 + kMaxLdu + kMaxStu + kMaxVcc][24];
+    long long acc_regs[1 + kMaxVcc][16];
     uint4 vcc_word[kMaxVcc];
     float acc[kMaxVcc][kAccRows];
     float red[kMaxVcc][32];

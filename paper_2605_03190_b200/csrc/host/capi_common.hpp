@@ -26,7 +26,7 @@ struct ProgramBox {
     std::vector<std::vector<uint8_t>> words;       // encode_stream per core
 
     void finish();
-    std::string text(bool with_words) const;
+    std::string text(int mode) const;  // 0 streams, 1 streams + words, 2 summary
 };
 
 ProgramBox* build(const std::string& request);

@@ -196,13 +196,14 @@ void ProgramBox::finish() {
     }
 }
 
-std::string ProgramBox::text(bool with_words) const {
+std::string ProgramBox::text(int mode) const {
+    const bool with_words = mode == 1, summary = mode == 2;
     json out;
     out["ok"] = true;
     out["tilings"] = json::parse(tilings_json.empty() ? "{}" : tilings_json);
     json streams = json::object(), hex = json::object();
     static const char* digits = "0123456789abcdef";
-    for (size_t i = 0; i < cores.size(); ++i) {
+    for (size_t i = 0; i < cores.size() && !summary; ++i) {
         const auto it = program.streams.find(cores[i]);
         if (it == program.streams.end()) continue;
         streams[cores[i].name()] = generator::serialize_stream(program, cores[i]);
@@ -218,13 +219,15 @@ std::string ProgramBox::text(bool with_words) const {
     }
     out["streams"] = streams;
     if (with_words) out["words"] = hex;
-    out["sidecar"] = generator::serialize_sidecar(program);
     out["total_uops"] = program.total_uops();
-    out["certificate_ok"] = generator::replay_certificate(program);
-    try {
-        out["makespan_estimate"] = generator::estimate_makespan(program, hw);
-    } catch (const std::exception&) {
-        out["makespan_estimate"] = nullptr;
+    if (!summary) {
+        out["sidecar"] = generator::serialize_sidecar(program);
+        out["certificate_ok"] = generator::replay_certificate(program);
+        try {
+            out["makespan_estimate"] = generator::estimate_makespan(program, hw);
+        } catch (const std::exception&) {
+            out["makespan_estimate"] = nullptr;
+        }
     }
     json descs = json::array();
     for (const auto& d : program.descriptors)
@@ -298,7 +301,7 @@ void vdc_program_free(vdc_program* prog) { delete reinterpret_cast<ProgramBox*>(
 int vdc_program_text(const vdc_program* prog, int with_words, char** out_json) {
     if (!prog || !out_json) return fail(VDC_ERR_INPUT, "null argument");
     try {
-        const std::string s = reinterpret_cast<const ProgramBox*>(prog)->text(with_words != 0);
+        const std::string s = reinterpret_cast<const ProgramBox*>(prog)->text(with_words);
         *out_json = static_cast<char*>(std::malloc(s.size() + 1));
         std::memcpy(*out_json, s.c_str(), s.size() + 1);
         return VDC_OK;

@@ -178,7 +178,8 @@ OperatorGraph build_decode_graph(const ModelConfig& m, const LayoutConfig& l) {
         b.node(L + "attn", OpKind::ATTN_DECODE, {b.view(L + "q", ".grp", grp * hd), L + "kc", L + "vc"}, {L + "part"},
                {{"ctx_pages", std::to_string(l.ctx_pages)}, {"pages_per_job", std::to_string(l.pages_per_job)}});
         b.vec(L + "attn", qrows, grp * hd, e);
-        b.node(L + "comb", OpKind::ATTN_COMBINE, {L + "part"}, {L + "attn"});
+        // the combine reads all partials of one kv head as a single tile
+        b.node(L + "comb", OpKind::ATTN_COMBINE, {b.view(L + "part", ".head", splits * grp)}, {L + "attn"});
         b.weight(L + "wo", d, qrows, R, float(qrows));
         b.vec(L + "x1", d, R, e);
         b.node(L + "o", OpKind::GEMV_ADD, {L + "wo", b.view(L + "attn", ".all", qrows), b.view(x, ".blk", R)}, {L + "x1"},

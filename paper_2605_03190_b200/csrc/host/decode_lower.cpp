@@ -237,14 +237,18 @@ class DecodeLowering {
 
     void plan_combine(const workload::OperatorNode& n, uint32_t ordinal) {
         const uint16_t part = idx(n.inputs[0]), out = idx(n.outputs[0]);
-        const int64_t splits = attn_splits_.at(part);
-        const int64_t grp = desc_[part].tile_rows, hd = desc_[part].tile_cols - 2;
-        const int64_t hkv = desc_[part].rows() / (splits * grp);
+        const int64_t splits = attn_splits_.at(uint16_t(storage(part)));
+        const TileDescriptor& pd = desc_[part];
+        const int64_t hd = pd.tile_cols - 2;
+        const int64_t per_tile = pd.tile_rows;  // partial rows per tile (splits * G when viewed per head)
+        const int64_t grp = desc_[storage(part)].tile_rows;
+        const int64_t hkv = pd.rows() / (splits * grp);
+        const int64_t tiles_per_head = (splits * grp) / per_tile;
         const int32_t pbase = param_block({float(hd), float(grp)});
         for (int64_t h = 0; h < hkv; ++h) {
             DJob& jb = job(Opcode::ATTN_COMBINE, ordinal);
             jb.imm = pbase << 8;
-            for (int64_t s = 0; s < splits; ++s) jb.groups.push_back({at(part, {uint16_t(h * splits + s), 0})});
+            for (int64_t s = 0; s < tiles_per_head; ++s) jb.groups.push_back({at(part, {uint16_t(h * tiles_per_head + s), 0})});
             jb.out = at(out, {uint16_t(h), 0});
         }
     }

@@ -27,6 +27,7 @@ class Report:
     elapsed_ms: float
     message: str
     stalled: list = field(default_factory=list)
+    wait_cycles: dict = field(default_factory=dict)
 
     @property
     def completed(self) -> bool:
@@ -38,6 +39,10 @@ def _torch():
 
     return torch
 
+
+WAIT_SITES = ["cfu_alloc", "cfu_m2c", "cfu_unit", "ldu_idle", "ldu_dep", "stu_idle", "stu_c2m", "stu_dep",
+              "vcc_ready", "vcc_barrier", "vcc_c2m", "vcc_compute", "cfu_total", "vcc_total", "ldu_issue", "cfu_resolve",
+              "vcc_sync", "vcc_push", "vcc_prologue", "vcc_epilogue", "vcc_pop", "cfu_allocloop", "cfu_synckick", "cfu_dispatch"]
 
 TORCH_DTYPE = {"f32": "float32", "bf16": "bfloat16", "i64": "int64"}
 
@@ -101,6 +106,20 @@ class Engine:
         check(lib().vdc_bind_step(self._h, ctypes.c_void_p(tensor.data_ptr()), tensor.numel()))
         self._step = tensor
 
+    def enable_trace(self, records_per_core: int = 512):
+        """Device trace of every compute µop (see vdc_bind_trace)."""
+        torch = _torch()
+        n_cores = self.program.cores()[0]
+        self._trace = torch.zeros(n_cores * records_per_core * 4, dtype=torch.int64, device=f"cuda:{self.device}")
+        self._trace_cap = records_per_core
+        check(lib().vdc_bind_trace(self._h, ctypes.c_void_p(self._trace.data_ptr()), records_per_core))
+
+    def trace(self):
+        """[(core, pc, t_enter, t_prologue, t_done)] of the last launch (ns)."""
+        a = self._trace.view(-1, 4).cpu().numpy()
+        a = a[a[:, 1] != 0]
+        return [(int(r[0]) >> 32, int(r[0]) & 0xffffffff, int(r[1]), int(r[2]), int(r[3])) for r in a]
+
     # -- execution ----------------------------------------------------------
     def launch(self, stream=None) -> None:
         s = ctypes.c_void_p(stream.cuda_stream if stream is not None else _torch().cuda.current_stream(self.device).cuda_stream)
@@ -112,7 +131,8 @@ class Engine:
         if rc not in (VDC_OK, VDC_ERR_DEADLOCK) and r.status == 0:
             check(rc)
         return Report(r.status, r.uops_executed, r.bytes_loaded, r.bytes_stored, r.elapsed_ms, r.message.decode(),
-                      [(r.stalled_core[i], r.stalled_pc[i]) for i in range(min(16, r.n_stalled))])
+                      [(r.stalled_core[i], r.stalled_pc[i]) for i in range(min(16, r.n_stalled))],
+                      {name: int(r.wait_cycles[i]) for i, name in enumerate(WAIT_SITES)})
 
     def run(self, stream=None) -> Report:
         self.launch(stream)
