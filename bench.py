@@ -38,8 +38,16 @@ METRIC = "Llama-3-8B bf16 decode tokens/s (1/2/4/8 B200) + HBM GB/s fraction of 
 CTX = 4096
 
 
-def model_request(layers: int = 32, ctx: int = CTX) -> dict:
+def model_request(layers: int = 32, ctx: int = CTX, engine: str = "ring", ring_slots: int = 11,
+                  pages_per_job: int = 4) -> dict:
     pages = (ctx + 63) // 64
+    if engine == "ring":
+        return {
+            "engine": "ring", "ring_slots": ring_slots,
+            "model": {"preset": "llama3-8b", "layers": layers},
+            "layout": {"ctx_pages": pages, "max_ctx": pages * 64, "pages_per_job": pages_per_job, "gu_block": 4},
+            "profile": {"builtin": "b200"},
+        }
     return {
         "model": {"preset": "llama3-8b", "layers": layers},
         "layout": {"ctx_pages": pages, "max_ctx": pages * 64, "pages_per_job": 4, "job_rows": 16, "gu_block": 32,
@@ -160,7 +168,7 @@ def cpu_oracle_tokens_per_s(timeout_s: int = 240) -> dict:
     times = {}
     with tempfile.TemporaryDirectory() as d:
         for layers in (1, 2):
-            prog = Program.build(model_request(layers))
+            prog = Program.build(model_request(layers, engine="reference"))
             pj = os.path.join(d, f"p{layers}.json")
             with open(pj, "w") as f:
                 json.dump(prog.text(True), f)
@@ -227,7 +235,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     torch.cuda.set_device(local_rank)
     t_build = time.time()
-    prog = Program.build(model_request(args.layers, args.ctx))
+    prog = Program.build(model_request(args.layers, args.ctx, args.engine, args.ring_slots, args.pages_per_job))
     build_s = time.time() - t_build
     eng = Engine(prog, device=local_rank, watchdog_ms=10000)
     tens = init_tensors(eng)
@@ -330,10 +338,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": committed_traffic(),
                      "peak_source": peak_src, "frac_of_8TBps_spec": round(achieved / 8000.0, 4),
-                     "bytes_per_step": nbytes, "kernel": "vdc_dev::engine_kernel (persistent, 1 CTA/SM)",
+                     "bytes_per_step": nbytes, "kernel": ("vdc_dev::ring::ring_kernel" if args.engine == "ring" else "vdc_dev::engine_kernel") + " (persistent, 1 CTA/SM)",
                      "kernel_ms_median": round(kernel_ms, 4)},
         "clocks": clocks,
-        "engine_report": {"uops_executed": rep.uops_executed, "bytes_loaded": rep.bytes_loaded,
+        "engine_report": {"engine": args.engine, "uops_executed": rep.uops_executed, "bytes_loaded": rep.bytes_loaded,
+                          "wait_cycles_sum_over_sms": rep.wait_cycles,
                           "bytes_stored": rep.bytes_stored},
     }
     return result
@@ -348,6 +357,9 @@ def main():
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--ctx", type=int, default=CTX)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--engine", default="ring", choices=["ring", "reference"])
+    ap.add_argument("--ring-slots", type=int, default=11)
+    ap.add_argument("--pages-per-job", type=int, default=4)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", 0))

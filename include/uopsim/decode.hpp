@@ -48,6 +48,7 @@ struct LayoutConfig {
     int head_job_rows = 64;  // output rows per lm_head job
     int gu_block = 16;       // swiglu interleave block (== job_rows for the gu node)
     int wtile_bytes = 32768; // target weight tile bytes (32 KB: full 4096-wide rows)
+    bool ring = false;       // ring-mode tiling: contiguous weight tiles of <= one ring slot
 };
 
 ModelConfig llama3_8b();

@@ -1,0 +1,69 @@
+/* Ring-mode µop programs: the operand block of a compute µop and the
+ * constants shared by the host lowering (ring_lower.cpp), the sm_100a ring
+ * engine (device/ring_engine.cu) and the tests.
+ *
+ * A ring-mode program is an ordinary LoweredProgram (per-core streams of
+ * 16-byte isa words, CoreId order sm<i>.vmc, sm<i>.vcc0) with the decoupled
+ * execution model of the paper (§3-4) specialised for decode:
+ *
+ *   sm<i>.vmc  : LOAD [send] size=1 words only. Each LOAD moves one tile
+ *                (contiguous, <= VDC_RING_SLOT_BYTES) into the next slot of
+ *                the SM's shared-memory ring with one cp.async.bulk; the
+ *                slot's `full` mbarrier is the m2c message. The memory core
+ *                never waits on data dependencies (weights and KV pages of
+ *                earlier steps are immutable during a launch), so it
+ *                prefetches across operator boundaries, bounded only by the
+ *                ring's `empty` mbarriers (slot release = the c2m FREE).
+ *   sm<i>.vcc0 : compute µops (GEMV / RMS_GEMV / GEMV_ADD / ATTN_DECODE /
+ *                ATTN_COMBINE / ELEMWISE) with size = ring tiles consumed and
+ *                imm = index of a vdc_job operand block. Activation operands
+ *                (the LOAD_WAIT of the reference-form decode program) are
+ *                read by the compute core itself after its readiness counter
+ *                reaches the target; results are stored by the compute core
+ *                and published with a release increment of the output
+ *                tensor's counter (the STORE_DEP of the reference form).
+ *
+ * Readiness counters are per storage tensor and monotonic across launches:
+ * launch e (1-based) waits for counter >= need * e.
+ */
+#ifndef UOPSIM_RING_ABI_H
+#define UOPSIM_RING_ABI_H
+
+#include <stdint.h>
+
+#define VDC_RING_SLOT_BYTES 16384
+#define VDC_RING_MAX_SLOTS 11  /* 11 x 16 KB ring + 32 KB staged x + scratch <= 227 KB */
+#define VDC_RING_COMPUTE_WARPS 8
+#define VDC_RING_MAX_JOB_ROWS 256  /* output rows per GEMV job (smem partials) */
+#define VDC_RING_MAX_TILE_ROWS 8   /* W rows per ring tile */
+#define VDC_RING_MAX_K 16384       /* GEMV reduction length held in registers */
+
+/* vdc_job.flags */
+#define VDC_JOB_RMS 0x01        /* x <- bf16/f32(x * rsqrt(mean(x^2)+eps) * a) */
+#define VDC_JOB_ROPE 0x02       /* interleaved-pair rotary on the output rows */
+#define VDC_JOB_SWIGLU 0x04     /* W rows in blocks [gate x B/2 | up x B/2] */
+#define VDC_JOB_RESID 0x08      /* out = a + W x */
+#define VDC_JOB_KV_APPEND 0x10  /* output row r -> cache[(r/hd)*T + pos][r%hd] */
+#define VDC_JOB_TOKEN_ROW 0x20  /* x offset += step[TOKEN] * k (embedding row) */
+
+typedef struct vdc_job {
+    int32_t op;               /* isa opcode of the compute µop                */
+    int32_t flags;            /* VDC_JOB_*                                    */
+    int32_t r0, r1;           /* GEMV: W rows; ATTN: pages; COMBINE: r1 = splits */
+    int32_t k;                /* GEMV reduction length; ATTN/COMBINE: head dim; copy: elements */
+    int32_t tile_rows;        /* ring tile rows (GEMV W rows / KV page rows)  */
+    int32_t tile_cols;        /* ring tile columns                            */
+    int32_t x_t, x_off, x_need; /* input vector: tensor, element offset, readiness target */
+    int32_t a_t, a_off, a_need; /* aux: rms weight / residual / K cache       */
+    int32_t b_t, b_off, b_need; /* aux 2: V cache                              */
+    int32_t o_t, o_off;       /* output tensor + element offset               */
+    int32_t out_row0;         /* W row of output row 0 (region start)         */
+    int32_t head_dim;         /* rope / attention head dim                    */
+    int32_t group;            /* attention: q heads per kv head               */
+    int32_t block;            /* swiglu block                                 */
+    int32_t cache_rows;       /* KV cache rows per kv head (T)                */
+    float eps, theta, scale;
+    int32_t pad[6];
+} vdc_job;  /* 128 bytes */
+
+#endif

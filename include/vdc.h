@@ -29,6 +29,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include "uopsim/ring_abi.h"
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -106,6 +108,11 @@ int vdc_destroy(vdc_ctx* ctx);
 int vdc_load_program(vdc_ctx* ctx, const uint8_t* words, const uint32_t* words_per_core, uint32_t n_cores,
                      const vdc_queue* queues, uint32_t n_queues, const vdc_desc* descs, uint32_t n_desc,
                      uint16_t slot_budget, uint16_t local_depth);
+/* ring-mode programs (uopsim/ring_abi.h): compute-µop operand blocks and the
+ * shared-memory ring depth; switches the context to the ring engine and
+ * zeroes its readiness counters. The context must have been created with
+ * slot_size = VDC_RING_SLOT_BYTES and vcc_per_sm = 1. */
+int vdc_load_jobs(vdc_ctx* ctx, const vdc_job* jobs, uint32_t n_jobs, uint32_t ring_slots);
 /* extension handler parameter table (LoweredProgram::params) */
 int vdc_set_params(vdc_ctx* ctx, const float* params, uint32_t n);
 /* device memory (row-major) backing descriptor `tensor`; the caller owns it */

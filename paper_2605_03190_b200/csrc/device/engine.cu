@@ -12,7 +12,9 @@
 #include <cstdio>
 
 #include "engine.cuh"
+#include "ptx.cuh"
 #include "uopsim/decode_abi.h"
+#include "uopsim/ring_abi.h"
 #include "vdc.h"
 
 namespace vdc_dev {
@@ -57,61 +59,6 @@ __device__ __forceinline__ Word decode(uint4 w) {
 
 __device__ __forceinline__ bool is_control(uint32_t op) { return op >= OP_LOOP; }
 __device__ __forceinline__ bool is_memory(uint32_t op) { return op < OP_MATVEC; }
-
-// ---------------------------------------------------------------------------
-// PTX helpers
-__device__ __forceinline__ uint32_t smem_addr(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
-}
-__device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
-        : "=r"(ok)
-        : "r"(smem_addr(b)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_addr(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-// polling loads: relaxed (no L1 invalidation per poll); the caller issues
-// one acquire fence after the condition is observed
-__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long now_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-__device__ __forceinline__ void named_bar(int id, int threads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory"); }
 
 __device__ __forceinline__ float bf16_to_f(uint16_t b) { return __uint_as_float(uint32_t(b) << 16); }
 __device__ __forceinline__ float load_elem(const char* p, int dtype, int64_t i) {
@@ -1891,6 +1838,13 @@ struct vdc_ctx {
     uint32_t trace_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaStream_t last_stream = nullptr;
+    // ring mode (ring-mode programs, include/uopsim/ring_abi.h)
+    bool ring = false;
+    uint32_t ring_slots = 0;
+    vdc_job* d_jobs = nullptr;
+    uint32_t n_jobs = 0;
+    uint32_t epoch = 0;
+    bool ring_attr_set = false;
 };
 
 namespace {
@@ -1919,7 +1873,8 @@ int vdc_create(const vdc_profile* p, int device, vdc_ctx** out) {
     if (p->ldu_count < 1 || p->ldu_count > uint32_t(kMaxLdu)) return fail(VDC_ERR_INPUT, "ldu_count must be 1..2");
     if (p->stu_count < 1 || p->stu_count > uint32_t(kMaxStu)) return fail(VDC_ERR_INPUT, "stu_count must be 1..2");
     if (p->slot_budget < 1 || p->slot_budget > uint32_t(kMaxSlots)) return fail(VDC_ERR_INPUT, "slot_budget must be 1..32");
-    if (p->slot_size != 8192) return fail(VDC_ERR_INPUT, "the engine is compiled for 8 KB slots");
+    if (p->slot_size != 8192 && p->slot_size != VDC_RING_SLOT_BYTES)
+        return fail(VDC_ERR_INPUT, "slot_size must be 8192 (reference-form programs) or 16384 (ring programs)");
     CU(cudaSetDevice(device));
     cudaDeviceProp prop;
     CU(cudaGetDeviceProperties(&prop, device));
@@ -1932,14 +1887,18 @@ int vdc_create(const vdc_profile* p, int device, vdc_ctx** out) {
         delete ctx;
         return fail(VDC_ERR_INPUT, "sm_count exceeds the device's multiprocessors");
     }
-    ctx->smem_bytes = size_t(p->slot_budget) * p->slot_size + control_bytes();
+    ctx->smem_bytes = p->slot_size == VDC_RING_SLOT_BYTES ? ring_smem_bytes(p->slot_budget)
+                                                          : size_t(p->slot_budget) * p->slot_size + control_bytes();
     if (ctx->smem_bytes > prop.sharedMemPerBlockOptin) {
         const size_t need = ctx->smem_bytes;
         delete ctx;
         return fail(VDC_ERR_INPUT, "slots + control block need " + std::to_string(need) + " B of shared memory, device allows " +
                                        std::to_string(prop.sharedMemPerBlockOptin));
     }
-    CU(cudaFuncSetAttribute(engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ctx->smem_bytes)));
+    if (p->slot_size == VDC_RING_SLOT_BYTES)
+        CU(cudaFuncSetAttribute(ring_kernel_entry(), cudaFuncAttributeMaxDynamicSharedMemorySize, int(ctx->smem_bytes)));
+    else
+        CU(cudaFuncSetAttribute(engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ctx->smem_bytes)));
     CU(cudaMalloc(&ctx->d_stats, sizeof(SmStats) * p->sm_count));
     CU(cudaMalloc(&ctx->d_status, sizeof(Status)));
     CU(cudaEventCreate(&ctx->ev0));
@@ -1956,6 +1915,7 @@ int vdc_destroy(vdc_ctx* ctx) {
     dfree(ctx->d_deps);
     dfree(ctx->d_counters);
     dfree(ctx->d_params);
+    dfree(ctx->d_jobs);
     dfree(ctx->d_stats);
     dfree(ctx->d_status);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -2060,6 +2020,33 @@ int vdc_set_params(vdc_ctx* ctx, const float* params, uint32_t n) {
     return VDC_OK;
 }
 
+int vdc_load_jobs(vdc_ctx* ctx, const vdc_job* jobs, uint32_t n_jobs, uint32_t ring_slots) {
+    if (!ctx || !ctx->loaded) return fail(VDC_ERR_INPUT, "load the program words first");
+    if (ctx->prof.slot_size != VDC_RING_SLOT_BYTES || ctx->prof.vcc_per_sm != 1)
+        return fail(VDC_ERR_INPUT, "ring programs need a context with 16 KB slots and one VCC per SM");
+    if (ring_slots < 2 || ring_slots > ctx->prof.slot_budget || ring_slots > VDC_RING_MAX_SLOTS)
+        return fail(VDC_ERR_INPUT, "ring_slots must be 2..min(slot_budget, 13)");
+    for (uint32_t i = 0; i < n_jobs; ++i) {
+        const vdc_job& j = jobs[i];
+        for (int32_t t : {j.x_t, j.a_t, j.b_t, j.o_t})
+            if (t >= int32_t(ctx->descs.size())) return fail(VDC_ERR_INPUT, "job " + std::to_string(i) + " names an unknown tensor");
+        if (j.tile_rows > VDC_RING_MAX_TILE_ROWS && (j.op == 0x27 || j.op == 0x28 || j.op == 0x29))
+            return fail(VDC_ERR_INPUT, "job " + std::to_string(i) + ": tile rows exceed the engine limit");
+        if (j.r1 - j.r0 > VDC_RING_MAX_JOB_ROWS && j.op >= 0x27 && j.op <= 0x29)
+            return fail(VDC_ERR_INPUT, "job " + std::to_string(i) + ": more output rows than the engine holds");
+    }
+    dfree(ctx->d_jobs);
+    CU(cudaMalloc(&ctx->d_jobs, sizeof(vdc_job) * std::max<uint32_t>(1, n_jobs)));
+    if (n_jobs) CU(cudaMemcpy(ctx->d_jobs, jobs, sizeof(vdc_job) * n_jobs, cudaMemcpyHostToDevice));
+    ctx->n_jobs = n_jobs;
+    ctx->ring = true;
+    ctx->ring_slots = ring_slots;
+    ctx->epoch = 0;
+    CU(cudaMemset(ctx->d_counters, 0, sizeof(uint32_t) * std::max<size_t>(1, ctx->descs.size())));
+    CU(cudaMemset(ctx->d_status, 0, sizeof(Status)));
+    return VDC_OK;
+}
+
 int vdc_bind_tensor(vdc_ctx* ctx, uint16_t tensor, void* dptr, size_t bytes, int dtype) {
     if (!ctx || !ctx->loaded) return fail(VDC_ERR_INPUT, "no program loaded");
     if (tensor >= ctx->descs.size()) return fail(VDC_ERR_INPUT, "tensor index out of range");
@@ -2105,6 +2092,28 @@ int vdc_launch(vdc_ctx* ctx, void* stream) {
     if (ctx->descs_dirty) {
         CU(cudaMemcpyAsync(ctx->d_descs, ctx->dev_descs.data(), sizeof(DevDesc) * ctx->dev_descs.size(), cudaMemcpyHostToDevice, s));
         ctx->descs_dirty = false;
+    }
+    if (ctx->ring) {
+        RingParams R{};
+        R.words = ctx->d_words;
+        R.core_off = ctx->d_core_off;
+        R.descs = ctx->d_descs;
+        R.jobs = ctx->d_jobs;
+        R.counters = ctx->d_counters;
+        R.step = ctx->d_step;
+        R.n_step = int32_t(ctx->d_step ? ctx->n_step : 0);
+        R.epoch = ++ctx->epoch;
+        R.ring_slots = ctx->ring_slots;
+        R.stats = ctx->d_stats;
+        R.status = ctx->d_status;
+        R.watchdog_ns = (unsigned long long)ctx->watchdog_ms * 1000000ull;
+        void* rargs[] = {&R};
+        CU(cudaEventRecord(ctx->ev0, s));
+        CU(cudaLaunchCooperativeKernel(ring_kernel_entry(), dim3(ctx->prof.sm_count), dim3(kRingThreads), rargs,
+                                       ring_smem_bytes(ctx->ring_slots), s));
+        CU(cudaEventRecord(ctx->ev1, s));
+        ctx->last_stream = s;
+        return VDC_OK;
     }
     CU(cudaMemcpyAsync(ctx->d_deps, ctx->dep_init.data(), sizeof(DepQueue) * ctx->dep_init.size(), cudaMemcpyHostToDevice, s));
     CU(cudaMemsetAsync(ctx->d_counters, 0, sizeof(uint32_t) * std::max<size_t>(1, ctx->dev_descs.size()), s));
@@ -2175,11 +2184,19 @@ int vdc_wait(vdc_ctx* ctx, vdc_report* r) {
         (void)ph;
         std::snprintf(r->message, sizeof r->message, "cfu phases: fetch %llu resolve %llu dispatch %llu sub-batches %llu",
                       (unsigned long long)ph[0], (unsigned long long)ph[1], (unsigned long long)ph[2], (unsigned long long)ph[3]);
+        if (ctx->ring) {
+            std::snprintf(r->message, sizeof r->message, "ring engine: %u slots x 16 KB, epoch %u", ctx->ring_slots, ctx->epoch);
+        }
         r->status = st.abort == 0 ? VDC_OK : st.abort == 1 ? VDC_ERR_DEADLOCK : VDC_ERR_INTERNAL;
         if (st.abort == 1)
             std::snprintf(r->message, sizeof r->message, "deadlock: %d core(s) made no progress for %u ms", st.n_stalled, ctx->watchdog_ms);
         else if (st.abort == 2)
             std::snprintf(r->message, sizeof r->message, "fault code %u info %u", st.fault_code, st.fault_info);
+    }
+    if (st.abort && ctx->ring) {  // counters are inconsistent after an aborted launch: restart the epochs
+        CU(cudaMemset(ctx->d_counters, 0, sizeof(uint32_t) * std::max<size_t>(1, ctx->descs.size())));
+        CU(cudaMemset(ctx->d_status, 0, sizeof(Status)));
+        ctx->epoch = 0;
     }
     if (st.abort == 1) return fail(VDC_ERR_DEADLOCK, "device watchdog: deadlock");
     if (st.abort == 2) return fail(VDC_ERR_INTERNAL, "device fault code " + std::to_string(st.fault_code));
@@ -2215,6 +2232,12 @@ int vdc_program_load(vdc_ctx* ctx, const vdc_program* prog) {
         int rc = vdc_load_program(ctx, words.data(), per_core.data(), uint32_t(per_core.size()), qs.data(), uint32_t(qs.size()),
                                   ds.data(), uint32_t(ds.size()), b->program.slot_budget, b->program.local_queue_depth);
         if (rc != VDC_OK) return rc;
+        if (b->program.ring_slots) {
+            rc = vdc_load_jobs(ctx, b->program.jobs.data(), uint32_t(b->program.jobs.size()), b->program.ring_slots);
+            if (rc != VDC_OK) return rc;
+        } else {
+            ctx->ring = false;
+        }
         return vdc_set_params(ctx, b->program.params.data(), uint32_t(b->program.params.size()));
     } catch (const std::exception& e) {
         return fail(VDC_ERR_INTERNAL, e.what());

@@ -15,6 +15,8 @@
 #pragma once
 #include <cstdint>
 
+#include "uopsim/ring_abi.h"
+
 namespace vdc_dev {
 
 constexpr int kMaxVcc = 2;
@@ -97,6 +99,26 @@ struct EngineParams {
     unsigned long long* trace;
     uint32_t trace_cap;
 };
+
+// Parameters of the ring engine (ring_engine.cu; ring-mode programs, see
+// include/uopsim/ring_abi.h). Cores in CoreId order: 2*sm = vmc, 2*sm+1 = vcc0.
+struct RingParams {
+    const uint4* words;
+    const uint32_t* core_off;
+    const DevDesc* descs;
+    const ::vdc_job* jobs;
+    uint32_t* counters;        // per storage descriptor, monotonic across launches
+    const int64_t* step;
+    int32_t n_step;
+    uint32_t epoch;            // 1-based launch ordinal since the counters were zeroed
+    uint32_t ring_slots;
+    SmStats* stats;            // written (not accumulated) by each SM
+    Status* status;
+    unsigned long long watchdog_ns;
+};
+size_t ring_smem_bytes(uint32_t ring_slots);
+const void* ring_kernel_entry();
+constexpr uint32_t kRingThreads = 32 * (8 + 1);
 
 // A region of `count` slots, not necessarily contiguous (indices packed 8
 // bits each): the allocator prefers a contiguous run but falls back to any

@@ -97,6 +97,7 @@ decode::LayoutConfig layout_from(const json& j) {
     l.head_job_rows = j.value("head_job_rows", l.head_job_rows);
     l.gu_block = j.value("gu_block", l.gu_block);
     l.wtile_bytes = j.value("wtile_bytes", l.wtile_bytes);
+    l.ring = j.value("ring", l.ring);
     return l;
 }
 
@@ -115,8 +116,11 @@ ProgramBox* build(const std::string& request) {
     opt.input_seed = jo.value("seed", uint64_t(0));
 
     workload::OperatorGraph g;
+    const bool ring = req.value("engine", std::string("reference")) == "ring";
     if (req.contains("model")) {
-        g = decode::build_decode_graph(model_from(req.at("model")), layout_from(req.value("layout", json::object())));
+        auto layout = layout_from(req.value("layout", json::object()));
+        layout.ring = layout.ring || ring;
+        g = decode::build_decode_graph(model_from(req.at("model")), layout);
     } else {
         g = workload::parse_workload(req.at("workload").dump());
     }
@@ -125,7 +129,11 @@ ProgramBox* build(const std::string& request) {
     bool decode_graph = false;
     for (const auto& n : g.nodes) decode_graph = decode_graph || workload::is_decode_kind(n.kind);
     std::map<std::string, workload::TilingChoice> tilings;
-    if (decode_graph) {
+    if (decode_graph && ring) {
+        box->program = generator::lower_decode_ring(g, hw, opt, req.value("ring_slots", 11));
+        const auto v = generator::validate_ring_program(box->program);
+        if (!v.empty()) throw generator::GeneratorError("ring program invalid: " + v.front().message);
+    } else if (decode_graph) {
         box->program = generator::generate(g, hw, opt);
     } else if (req.contains("tilings") || req.contains("passes")) {
         if (req.contains("tilings")) {
@@ -177,13 +185,13 @@ ProgramBox* build(const std::string& request) {
 
 void ProgramBox::finish() {
     generator::LoweredProgram& p = program;
-    p.slot_size = hw.slot_size;
-    p.vcc_per_sm = uint16_t(hw.vcc_per_sm);
+    if (!p.ring_slots) p.slot_size = hw.slot_size;
+    p.vcc_per_sm = p.ring_slots ? uint16_t(1) : uint16_t(hw.vcc_per_sm);
     p.sm_count = uint16_t(hw.sm_count);
     uint32_t sms = hw.sm_count;
     for (const auto& kv : p.streams) sms = std::max<uint32_t>(sms, uint32_t(kv.first.sm) + 1);
     sm_count = sms;
-    vcc_per_sm = hw.vcc_per_sm;
+    vcc_per_sm = p.vcc_per_sm;
     cores.clear();
     words.clear();
     for (uint32_t sm = 0; sm < sms; ++sm) {
@@ -222,9 +230,10 @@ std::string ProgramBox::text(int mode) const {
     out["total_uops"] = program.total_uops();
     if (!summary) {
         out["sidecar"] = generator::serialize_sidecar(program);
-        out["certificate_ok"] = generator::replay_certificate(program);
+        out["certificate_ok"] = program.ring_slots ? generator::validate_ring_program(program).empty()
+                                                   : generator::replay_certificate(program);
         try {
-            out["makespan_estimate"] = generator::estimate_makespan(program, hw);
+            out["makespan_estimate"] = program.ring_slots ? json(nullptr) : json(generator::estimate_makespan(program, hw));
         } catch (const std::exception&) {
             out["makespan_estimate"] = nullptr;
         }
@@ -237,12 +246,22 @@ std::string ProgramBox::text(int mode) const {
                          {"init", int(d.init)}, {"init_scale", d.init_scale}});
     out["descriptors"] = descs;
     out["params"] = program.params;
+    out["ring_slots"] = program.ring_slots;
+    json jobs = json::array();
+    for (const auto& jb : program.jobs)
+        jobs.push_back({{"op", jb.op}, {"flags", jb.flags}, {"r0", jb.r0}, {"r1", jb.r1}, {"k", jb.k},
+                        {"tile", {jb.tile_rows, jb.tile_cols}}, {"x", {jb.x_t, jb.x_off, jb.x_need}},
+                        {"a", {jb.a_t, jb.a_off, jb.a_need}}, {"b", {jb.b_t, jb.b_off, jb.b_need}},
+                        {"o", {jb.o_t, jb.o_off}}, {"out_row0", jb.out_row0}, {"head_dim", jb.head_dim},
+                        {"group", jb.group}, {"block", jb.block}, {"cache_rows", jb.cache_rows},
+                        {"eps", jb.eps}, {"theta", jb.theta}, {"scale", jb.scale}});
+    out["jobs"] = jobs;
     json queues = json::array();
     for (const auto& q : program.queues)
         queues.push_back({{"dep", q.dep_id}, {"depth", q.depth}, {"local", q.local}, {"producer_sm", q.producer.sm},
                           {"consumer_sm", q.consumer.sm}});
     out["queues"] = queues;
-    out["slot_size"] = hw.slot_size;
+    out["slot_size"] = program.slot_size;
     out["ldu_count"] = hw.ldu_count;
     out["stu_count"] = hw.stu_count;
     out["step_scalars"] = program.step_scalars;

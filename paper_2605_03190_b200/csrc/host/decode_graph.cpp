@@ -4,6 +4,7 @@
 
 #include "uopsim/decode.hpp"
 #include "uopsim/util.hpp"
+#include "uopsim/ring_abi.h"
 
 namespace uopsim::decode {
 
@@ -59,6 +60,25 @@ ModelConfig tiny_llama() {
 std::pair<int64_t, int64_t> weight_tile(int64_t rows, int64_t cols, ElemType e, const LayoutConfig& l) {
     (void)rows;
     const int64_t eb = workload::elem_bytes(e);
+    if (l.ring) {
+        // ring mode: every tile is one contiguous run of <= one slot, so the
+        // memory core moves it with a single cp.async.bulk: whole rows
+        // (power-of-two count <= VDC_RING_MAX_TILE_ROWS) when a row fits the
+        // slot, else equal column chunks of one row (multiples of 16 bytes)
+        const int64_t row_bytes = cols * eb;
+        if (row_bytes <= VDC_RING_SLOT_BYTES) {
+            int64_t tr = 1;
+            while (tr * 2 <= VDC_RING_MAX_TILE_ROWS && tr * 2 * row_bytes <= VDC_RING_SLOT_BYTES) tr *= 2;
+            return {tr, cols};
+        }
+        // rows longer than a slot: column chunks of 16/8/4 KB (a multiple of
+        // the compute core's 256 x 16-byte stride), stacked 1/2/4 rows high
+        for (int64_t chunk = VDC_RING_SLOT_BYTES; chunk >= 4096; chunk /= 2)
+            if ((cols * eb) % chunk == 0) return {VDC_RING_SLOT_BYTES / chunk, chunk / eb};
+        for (int64_t parts = (row_bytes + VDC_RING_SLOT_BYTES - 1) / VDC_RING_SLOT_BYTES; parts <= cols; ++parts)
+            if (cols % parts == 0 && ((cols / parts) * eb) % 16 == 0) return {1, cols / parts};
+        throw workload::WorkloadError("no ring tiling for a row of " + std::to_string(cols) + " elements");
+    }
     const int64_t tc = std::min<int64_t>(cols, std::max<int64_t>(1, l.wtile_bytes / (eb * 4)));
     int64_t tr = std::max<int64_t>(1, l.wtile_bytes / (tc * eb));
     return {tr, tc};

@@ -1,0 +1,414 @@
+// Ring-mode decode lowering (ext): decode-kind graphs -> per-SM memory and
+// compute µop streams for the sm_100a ring engine (include/uopsim/ring_abi.h).
+//
+// Relation to the reference-form decode lowering (decode_lower.cpp) and to
+// the reference's lower() (reference src/lower.cpp:48-260):
+//  * Same operator -> job decomposition idea (one compute µop per output row
+//    range, groups = per-tile fetches in pop order, generator.cpp:156-289),
+//    but each operator's rows are split into one contiguous, tile-aligned
+//    range per SM (equal tile counts +-1) instead of `chunk % pairs`: at
+//    batch 1 every SM streams weights and the slowest SM sets the step time.
+//  * Weight / KV-page tiles are the only memory µops: LOAD [send] size=1 in
+//    exactly the order the SM's compute µops consume them, so the memory
+//    core can run ahead across operator boundaries (the paper's decoupling,
+//    PAPER.md:588-626) — its only back-pressure is the ring's slot release.
+//  * Activation dependencies are per-tensor readiness counters (the
+//    broadcast dependency the reference lacks, SURVEY finding 3), carried in
+//    the compute µop's operand block (vdc_job) as (tensor, target).
+//  * Operators appear in every SM's streams in topological order, so every
+//    counter wait targets jobs that precede it on every SM: the program is
+//    deadlock-free by construction (checked by validate_ring_program).
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+
+#include "jobs.hpp"
+#include "uopsim/decode_abi.h"
+#include "uopsim/ring_abi.h"
+#include "uopsim/util.hpp"
+
+namespace uopsim::generator {
+
+using isa::Opcode;
+using isa::UopWord;
+using workload::OpKind;
+
+namespace {
+
+int64_t attr_int(const workload::OperatorNode& n, const char* key, int64_t dflt) {
+    const auto it = n.attrs.find(key);
+    return it == n.attrs.end() ? dflt : std::stoll(it->second);
+}
+double attr_num(const workload::OperatorNode& n, const char* key, double dflt) {
+    const auto it = n.attrs.find(key);
+    return it == n.attrs.end() ? dflt : std::stod(it->second);
+}
+
+struct Tile {
+    uint16_t tensor;
+    std::vector<uint16_t> coord;
+};
+
+struct RJob {
+    vdc_job j{};
+    std::vector<Tile> tiles;  // ring tiles in consumption order
+    uint32_t ordinal = 0;
+    uint32_t sm = 0;
+};
+
+class RingLowering {
+  public:
+    RingLowering(const workload::OperatorGraph& g, const costmodel::HardwareProfile& hw, int ring_slots)
+        : g_(g), hw_(hw), desc_(build_descriptors(g)), ring_slots_(ring_slots) {}
+
+    LoweredProgram run(const GenOptions& opt) {
+        if (hw_.vmc_per_sm != 1) throw GeneratorError("ring lowering assumes one VMC per SM");
+        sms_ = hw_.sm_count;
+        const auto order = detail::topo_nodes(g_);
+        uint32_t ordinal = 0;
+        for (const auto* n : order) plan(*n, ordinal++);
+        // readiness targets: jobs writing each storage tensor per launch
+        std::map<int32_t, int32_t> writers;
+        for (const auto& r : jobs_) ++writers[r.j.o_t];
+        for (auto& r : jobs_) {
+            auto need = [&](int32_t t) { return t >= 0 && writers.count(storage(uint16_t(t))) ? writers.at(storage(uint16_t(t))) : 0; };
+            r.j.x_need = need(r.j.x_t);
+            r.j.a_need = need(r.j.a_t);
+            r.j.b_need = need(r.j.b_t);
+        }
+        LoweredProgram p;
+        p.descriptors = desc_;
+        p.slot_budget = uint16_t(ring_slots_);
+        p.ring_slots = uint16_t(ring_slots_);
+        p.slot_size = VDC_RING_SLOT_BYTES;
+        p.operator_count = ordinal;
+        p.workload_hash = g_.content_hash();
+        p.profile_name = hw_.name;
+        p.input_seed = opt.input_seed;
+        p.step_scalars = VDC_STEP_MAX;
+        p.vcc_per_sm = 1;
+        p.sm_count = uint16_t(sms_);
+        p.local_queue_depth = uint16_t(ring_slots_);
+        emit(p);
+        return p;
+    }
+
+  private:
+    const workload::OperatorGraph& g_;
+    const costmodel::HardwareProfile& hw_;
+    std::vector<TileDescriptor> desc_;
+    int ring_slots_;
+    uint32_t sms_ = 1;
+    std::vector<RJob> jobs_;
+
+    int32_t storage(uint16_t t) const { return desc_[t].view_of >= 0 ? desc_[t].view_of : int32_t(t); }
+    uint16_t idx(const std::string& name) const { return g_.tensor_index(name); }
+
+    static vdc_job blank(Opcode op) {
+        vdc_job j{};
+        j.op = int32_t(op);
+        j.x_t = j.a_t = j.b_t = j.o_t = -1;
+        return j;
+    }
+
+    // contiguous, unit-aligned share of `units` for SM s
+    std::pair<int64_t, int64_t> share(int64_t units, uint32_t s) const {
+        return {units * s / sms_, units * (s + 1) / sms_};
+    }
+
+    void plan(const workload::OperatorNode& n, uint32_t ordinal) {
+        switch (n.kind) {
+            case OpKind::GEMV:
+            case OpKind::RMS_GEMV:
+            case OpKind::GEMV_ADD:
+                plan_gemv(n, ordinal);
+                break;
+            case OpKind::ATTN_DECODE:
+                plan_attention(n, ordinal);
+                break;
+            case OpKind::ATTN_COMBINE:
+                plan_combine(n, ordinal);
+                break;
+            case OpKind::EMBED_ROW: {
+                RJob r;
+                r.ordinal = ordinal;
+                r.sm = 0;
+                r.j = blank(Opcode::ELEMWISE);
+                r.j.flags = VDC_JOB_TOKEN_ROW;
+                const uint16_t tab = idx(n.inputs[0]);
+                r.j.x_t = storage(tab);
+                r.j.k = int32_t(desc_[tab].cols());
+                r.j.o_t = storage(idx(n.outputs[0]));
+                jobs_.push_back(std::move(r));
+                break;
+            }
+            default:
+                throw GeneratorError("node " + n.id + ": reference kinds cannot be lowered in ring mode");
+        }
+    }
+
+    void plan_gemv(const workload::OperatorNode& n, uint32_t ordinal) {
+        const uint16_t w = idx(n.inputs[0]);
+        const TileDescriptor& wd = desc_[w];
+        if (wd.view_of >= 0) throw GeneratorError("node " + n.id + ": weight must own its storage");
+        const int64_t K = wd.cols(), plane_rows = wd.rows(), M = wd.elem_count() / K;
+        const int64_t tr = wd.tile_rows, tc = wd.tile_cols, tpr = K / tc;
+        const int64_t eb = workload::elem_bytes(wd.elem);
+        if (K % tc || 8 % tr || uint64_t(tr * tc * eb) > VDC_RING_SLOT_BYTES)
+            throw GeneratorError("node " + n.id + ": weight tiles are not ring tiles (build the graph with layout.ring)");
+        if (K > VDC_RING_MAX_K || (K * eb) % 16 || (tc * eb) % 16)
+            throw GeneratorError("node " + n.id + ": reduction length unsupported by the ring engine");
+        const bool rope = attr_int(n, "rope", 0) != 0;
+        const int64_t swiglu = attr_int(n, "swiglu", 0);
+        int64_t unit = tr;
+        if (rope) unit = std::lcm(unit, int64_t(2));
+        if (swiglu) unit = std::lcm(unit, swiglu);
+        if (M % unit) throw GeneratorError("node " + n.id + ": rows not a multiple of the job alignment");
+        // output regions (qkv: q | k | v), each a separate job family
+        struct Region {
+            int64_t r0, r1;
+            uint16_t out;
+            bool kv;
+        };
+        std::vector<Region> regions;
+        int64_t head_dim = 0, qrows = M;
+        if (n.outputs.size() == 3) {
+            const TileDescriptor& kc = desc_[idx(n.outputs[1])];
+            head_dim = kc.shape.back();
+            const int64_t kvrows = kc.shape[0] * head_dim;
+            qrows = desc_[idx(n.outputs[0])].rows();
+            if (qrows + 2 * kvrows != M) throw GeneratorError("node " + n.id + ": q/k/v rows do not add up to W rows");
+            regions = {{0, qrows, idx(n.outputs[0]), false}, {qrows, qrows + kvrows, idx(n.outputs[1]), true},
+                       {qrows + kvrows, M, idx(n.outputs[2]), true}};
+            for (const auto& r : regions)
+                if (r.r0 % unit) throw GeneratorError("node " + n.id + ": q/k/v boundary not tile aligned");
+        } else {
+            regions = {{0, M, idx(n.outputs[0]), false}};
+        }
+        const int64_t max_rows = (VDC_RING_MAX_JOB_ROWS / unit) * unit;
+        const int64_t units = M / unit;
+        const TileDescriptor& xd = desc_[idx(n.inputs[1])];
+        for (uint32_t s = 0; s < sms_; ++s) {
+            const auto [u0, u1] = share(units, s);
+            for (const auto& reg : regions) {
+                int64_t a = std::max(u0 * unit, reg.r0), b = std::min(u1 * unit, reg.r1);
+                for (int64_t c0 = a; c0 < b; c0 += max_rows) {
+                    const int64_t c1 = std::min(b, c0 + max_rows);
+                    RJob r;
+                    r.ordinal = ordinal;
+                    r.sm = s;
+                    vdc_job& j = r.j;
+                    j = blank(n.kind == OpKind::GEMV ? Opcode::GEMV : n.kind == OpKind::RMS_GEMV ? Opcode::RMS_GEMV : Opcode::GEMV_ADD);
+                    j.r0 = int32_t(c0);
+                    j.r1 = int32_t(c1);
+                    j.k = int32_t(K);
+                    j.tile_rows = int32_t(tr);
+                    j.tile_cols = int32_t(tc);
+                    j.x_t = storage(idx(n.inputs[1]));
+                    j.x_off = 0;
+                    if (xd.elem_count() != K) throw GeneratorError("node " + n.id + ": input length != reduction length");
+                    if (n.kind == OpKind::RMS_GEMV) {
+                        j.flags |= VDC_JOB_RMS;
+                        j.a_t = storage(idx(n.inputs[2]));
+                        j.eps = float(attr_num(n, "eps", 1e-5));
+                    } else if (n.kind == OpKind::GEMV_ADD) {
+                        j.flags |= VDC_JOB_RESID;
+                        j.a_t = storage(idx(n.inputs[2]));
+                        j.a_off = 0;
+                    }
+                    j.o_t = storage(reg.out);
+                    j.out_row0 = int32_t(reg.r0);
+                    if (rope && (!reg.kv || reg.r0 == qrows)) {  // q and k rows rotate, v rows do not
+                        j.flags |= VDC_JOB_ROPE;
+                        j.theta = float(attr_num(n, "theta", 10000.0));
+                    }
+                    j.head_dim = int32_t(head_dim);
+                    if (reg.kv) {
+                        j.flags |= VDC_JOB_KV_APPEND;
+                        j.cache_rows = int32_t(desc_[reg.out].shape[1]);
+                    }
+                    if (swiglu) {
+                        j.flags |= VDC_JOB_SWIGLU;
+                        j.block = int32_t(swiglu);
+                    }
+                    // consumption order of the ring engine: batches of 8 output
+                    // rows, column tiles outer, row groups inner
+                    for (int64_t b0 = c0; b0 < c1; b0 += 8)
+                        for (int64_t ct = 0; ct < tpr; ++ct)
+                            for (int64_t row = b0; row < std::min(c1, b0 + 8); row += tr) {
+                                const int64_t plane = row / plane_rows, prow = row % plane_rows;
+                                if (wd.shape.size() == 3)
+                                    r.tiles.push_back({w, {uint16_t(plane), uint16_t(prow / tr), uint16_t(ct)}});
+                                else
+                                    r.tiles.push_back({w, {uint16_t(prow / tr), uint16_t(ct)}});
+                            }
+                    jobs_.push_back(std::move(r));
+                }
+            }
+        }
+    }
+
+    void plan_attention(const workload::OperatorNode& n, uint32_t ordinal) {
+        const uint16_t q = idx(n.inputs[0]), kc = idx(n.inputs[1]), vc = idx(n.inputs[2]), part = idx(n.outputs[0]);
+        const TileDescriptor& kd = desc_[kc];
+        const int64_t hkv = kd.shape[0], T = kd.shape[1], hd = kd.shape[2], page_rows = kd.tile_rows;
+        const int64_t grp = desc_[q].tile_rows / hd;
+        if (kd.tile_cols != hd || uint64_t(page_rows * hd * workload::elem_bytes(kd.elem)) > VDC_RING_SLOT_BYTES)
+            throw GeneratorError("node " + n.id + ": KV pages do not fit a ring slot");
+        if (grp < 1 || grp > VDC_RING_COMPUTE_WARPS || VDC_RING_COMPUTE_WARPS % grp || hd % 32 || hd > 256)
+            throw GeneratorError("node " + n.id + ": unsupported GQA group / head dim for the ring engine");
+        const int64_t pages = attr_int(n, "ctx_pages", 1), per = attr_int(n, "pages_per_job", 1);
+        const int64_t splits = ceil_div(pages, per);
+        int64_t k = 0;
+        for (int64_t h = 0; h < hkv; ++h)
+            for (int64_t s = 0; s < splits; ++s, ++k) {
+                RJob r;
+                r.ordinal = ordinal;
+                r.sm = uint32_t(k % sms_);
+                vdc_job& j = r.j;
+                j = blank(Opcode::ATTN_DECODE);
+                j.r0 = int32_t(s * per);
+                j.r1 = int32_t(std::min(pages, (s + 1) * per));
+                j.k = int32_t(hd);
+                j.head_dim = int32_t(hd);
+                j.group = int32_t(grp);
+                j.tile_rows = int32_t(page_rows);
+                j.tile_cols = int32_t(hd);
+                j.cache_rows = int32_t(T);
+                j.scale = float(1.0 / std::sqrt(double(hd)));
+                j.x_t = storage(q);
+                j.x_off = int32_t(h * grp * hd);
+                j.a_t = storage(kc);
+                j.a_off = int32_t(h * T * hd);
+                j.b_t = storage(vc);
+                j.b_off = int32_t(h * T * hd);
+                j.o_t = storage(part);
+                j.o_off = int32_t((h * splits + s) * grp * (hd + 2));
+                for (int64_t pg = j.r0; pg < j.r1; ++pg) {
+                    r.tiles.push_back({kc, {uint16_t(h), uint16_t(pg), 0}});
+                    r.tiles.push_back({vc, {uint16_t(h), uint16_t(pg), 0}});
+                }
+                jobs_.push_back(std::move(r));
+            }
+        attn_ = {hkv, splits, grp, hd, k};
+    }
+
+    void plan_combine(const workload::OperatorNode& n, uint32_t ordinal) {
+        const uint16_t part = idx(n.inputs[0]), out = idx(n.outputs[0]);
+        // combine jobs go to the SMs that had no attention job (idle during
+        // the split-KV sweep), else round-robin after the attention jobs
+        for (int64_t h = 0; h < attn_.hkv; ++h) {
+            RJob r;
+            r.ordinal = ordinal;
+            r.sm = uint32_t((attn_.jobs + h) % sms_);
+            vdc_job& j = r.j;
+            j = blank(Opcode::ATTN_COMBINE);
+            j.r0 = 0;
+            j.r1 = int32_t(attn_.splits);
+            j.k = int32_t(attn_.hd);
+            j.head_dim = int32_t(attn_.hd);
+            j.group = int32_t(attn_.grp);
+            j.x_t = storage(part);
+            j.x_off = int32_t(h * attn_.splits * attn_.grp * (attn_.hd + 2));
+            j.o_t = storage(out);
+            j.o_off = int32_t(h * attn_.grp * attn_.hd);
+            jobs_.push_back(std::move(r));
+        }
+    }
+
+    void emit(LoweredProgram& p) {
+        std::vector<std::vector<size_t>> per_sm(sms_);
+        for (size_t i = 0; i < jobs_.size(); ++i) per_sm[jobs_[i].sm].push_back(i);
+        for (uint32_t s = 0; s < sms_; ++s) {
+            std::stable_sort(per_sm[s].begin(), per_sm[s].end(),
+                             [&](size_t a, size_t b) { return jobs_[a].ordinal < jobs_[b].ordinal; });
+            auto& vs = p.streams[CoreId::vmc(uint16_t(s))];
+            auto& vm = p.meta[CoreId::vmc(uint16_t(s))];
+            auto& cs = p.streams[CoreId::vcc_id(uint16_t(s), 0)];
+            auto& cm = p.meta[CoreId::vcc_id(uint16_t(s), 0)];
+            for (size_t ji : per_sm[s]) {
+                const RJob& r = jobs_[ji];
+                const int32_t slot = int32_t(p.jobs.size());
+                p.jobs.push_back(r.j);
+                for (const Tile& t : r.tiles) {
+                    UopWord u;
+                    u.opcode = Opcode::LOAD;
+                    u.flags = isa::kFlagSend;
+                    u.flow = 1;
+                    u.size = 1;
+                    u.addr = isa::AddressSpec::tile(t.tensor, t.coord);
+                    vs.push_back(u);
+                    vm.push_back({r.ordinal, slot, -1});
+                }
+                UopWord c;
+                c.opcode = Opcode(r.j.op);
+                c.size = uint16_t(r.tiles.size());
+                c.imm = slot;
+                c.flow = 1;
+                cs.push_back(c);
+                cm.push_back({r.ordinal, slot, -1});
+            }
+            for (auto* st : {&vs, &cs}) {
+                UopWord h;
+                h.opcode = Opcode::HALT;
+                h.flags = isa::kFlagLast;
+                st->push_back(h);
+            }
+            vm.push_back({0, -1, -1});
+            cm.push_back({0, -1, -1});
+        }
+    }
+
+    struct AttnInfo {
+        int64_t hkv = 0, splits = 1, grp = 1, hd = 0, jobs = 0;
+    } attn_;
+};
+
+}  // namespace
+
+LoweredProgram lower_decode_ring(const workload::OperatorGraph& g, const costmodel::HardwareProfile& hw, const GenOptions& opt,
+                                 int ring_slots) {
+    if (ring_slots < 2 || ring_slots > VDC_RING_MAX_SLOTS) throw GeneratorError("ring_slots must be 2..11");
+    return RingLowering(g, hw, ring_slots).run(opt);
+}
+
+// Ring-program invariants (the ring analogue of validate + the certificate):
+// per SM, compute µops consume exactly the LOADs of its memory stream in
+// order, and every readiness wait targets an operator that precedes the
+// waiting µop on every SM (topological per-SM order => no cyclic waits).
+std::vector<isa::Violation> validate_ring_program(const LoweredProgram& p) {
+    std::vector<isa::Violation> v;
+    std::map<int32_t, uint32_t> writer_op;  // storage -> operator ordinal
+    for (const auto& [core, m] : p.meta) {
+        if (core.kind != isa::CoreKind::vcc) continue;
+        const auto& s = p.streams.at(core);
+        for (size_t i = 0; i < s.size(); ++i)
+            if (s[i].klass() == isa::OpClass::compute) writer_op[p.jobs.at(size_t(s[i].imm)).o_t] = m[i].op;
+    }
+    for (const auto& [core, s] : p.streams) {
+        if (core.kind != isa::CoreKind::vcc) continue;
+        const auto& vmc = p.streams.at(CoreId::vmc(core.sm));
+        size_t loads = 0;
+        for (const auto& u : vmc) loads += u.opcode == Opcode::LOAD;
+        size_t consumed = 0;
+        uint32_t last_op = 0;
+        const auto& m = p.meta.at(core);
+        for (size_t i = 0; i < s.size(); ++i) {
+            if (s[i].klass() != isa::OpClass::compute) continue;
+            consumed += s[i].size;
+            if (m[i].op < last_op) v.push_back({i, core.name() + ": operators out of topological order"});
+            last_op = m[i].op;
+            const vdc_job& j = p.jobs.at(size_t(s[i].imm));
+            for (int32_t t : {j.x_t, j.a_t, j.b_t}) {
+                const auto it = writer_op.find(t);
+                if (it != writer_op.end() && it->second >= m[i].op)
+                    v.push_back({i, core.name() + ": waits on an operator that does not precede it"});
+            }
+        }
+        if (consumed != loads) v.push_back({0, core.name() + ": compute µops consume " + std::to_string(consumed) +
+                                                   " ring tiles, memory stream loads " + std::to_string(loads)});
+    }
+    return v;
+}
+
+}  // namespace uopsim::generator

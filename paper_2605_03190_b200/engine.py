@@ -44,6 +44,8 @@ WAIT_SITES = ["cfu_alloc", "cfu_m2c", "cfu_unit", "ldu_idle", "ldu_dep", "stu_id
               "vcc_ready", "vcc_barrier", "vcc_c2m", "vcc_compute", "cfu_total", "vcc_total", "ldu_issue", "cfu_resolve",
               "vcc_sync", "vcc_push", "vcc_prologue", "vcc_epilogue", "vcc_pop", "cfu_allocloop", "cfu_synckick", "cfu_dispatch"]
 
+RING_SITES = ["vmc_empty_wait", "vcc_full_wait", "vcc_dep_wait", "vcc_epilogue", "vcc_total", "vmc_total", "jobs"]
+
 TORCH_DTYPE = {"f32": "float32", "bf16": "bfloat16", "i64": "int64"}
 
 
@@ -130,9 +132,10 @@ class Engine:
         rc = lib().vdc_wait(self._h, ctypes.byref(r))
         if rc not in (VDC_OK, VDC_ERR_DEADLOCK) and r.status == 0:
             check(rc)
+        names = RING_SITES if self.info.get("ring_slots") else WAIT_SITES
         return Report(r.status, r.uops_executed, r.bytes_loaded, r.bytes_stored, r.elapsed_ms, r.message.decode(),
                       [(r.stalled_core[i], r.stalled_pc[i]) for i in range(min(16, r.n_stalled))],
-                      {name: int(r.wait_cycles[i]) for i, name in enumerate(WAIT_SITES)})
+                      {name: int(r.wait_cycles[i]) for i, name in enumerate(names)})
 
     def run(self, stream=None) -> Report:
         self.launch(stream)
