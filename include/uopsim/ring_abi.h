@@ -38,6 +38,11 @@
 #define VDC_RING_MAX_TILE_ROWS 8   /* W rows per ring tile */
 #define VDC_RING_MAX_K 16384       /* GEMV reduction length held in registers */
 
+/* ATTN_DECODE in ring programs also performs the split-KV combine (the
+ * reference-form ATTN_COMBINE): every split job writes its partial
+ * (o, m, l per q head), increments the kv head's arrival counter, and the
+ * last arriving job merges the partials and publishes the output. */
+
 /* vdc_job.flags */
 #define VDC_JOB_RMS 0x01        /* x <- bf16/f32(x * rsqrt(mean(x^2)+eps) * a) */
 #define VDC_JOB_ROPE 0x02       /* interleaved-pair rotary on the output rows */
@@ -63,7 +68,11 @@ typedef struct vdc_job {
     int32_t block;            /* swiglu block                                 */
     int32_t cache_rows;       /* KV cache rows per kv head (T)                */
     float eps, theta, scale;
-    int32_t pad[6];
+    int32_t lead_pad;         /* ATTN: leading padding tiles (keeps K pages on even ring indices) */
+    int32_t arrive_ctr;       /* ATTN: per-kv-head arrival counter (index into the counter array) */
+    int32_t arrive_need;      /* ATTN: split jobs per kv head; the last to arrive combines */
+    int32_t o2_t, o2_off;     /* ATTN: combined output (attention vector of the head's q heads) */
+    int32_t split;            /* ATTN: split index of this job within its kv head */
 } vdc_job;  /* 128 bytes */
 
 #endif

@@ -128,6 +128,9 @@ int vdc_wait(vdc_ctx* ctx, vdc_report* report);
  * uint64 {core << 32 | pc, t_enter, t_prologue_ready, t_done} in %globaltimer
  * ns, written for each compute µop; dptr = NULL disables tracing */
 int vdc_bind_trace(vdc_ctx* ctx, void* dptr, uint32_t records_per_core);
+/* ring engine: L2 prefetch look-ahead of the memory core, in rounds of 8
+ * tiles (default 0 = off, <= 31) */
+int vdc_set_prefetch(vdc_ctx* ctx, uint32_t tiles);
 /* watchdog: abort a launch whose cores make no progress for `ms` (0 = off) */
 int vdc_set_watchdog(vdc_ctx* ctx, uint32_t ms);
 

@@ -1798,6 +1798,7 @@ __global__ void __launch_bounds__(32 * (1 + kMaxLdu + kMaxStu + kMaxVcc * kVccWa
 // host side of the device C-ABI
 
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -1844,6 +1845,9 @@ struct vdc_ctx {
     vdc_job* d_jobs = nullptr;
     uint32_t n_jobs = 0;
     uint32_t epoch = 0;
+    uint32_t ring_prefetch = 0;
+    size_t n_counters = 0;
+    unsigned long long* d_tile_trace = nullptr;
     bool ring_attr_set = false;
 };
 
@@ -2024,8 +2028,8 @@ int vdc_load_jobs(vdc_ctx* ctx, const vdc_job* jobs, uint32_t n_jobs, uint32_t r
     if (!ctx || !ctx->loaded) return fail(VDC_ERR_INPUT, "load the program words first");
     if (ctx->prof.slot_size != VDC_RING_SLOT_BYTES || ctx->prof.vcc_per_sm != 1)
         return fail(VDC_ERR_INPUT, "ring programs need a context with 16 KB slots and one VCC per SM");
-    if (ring_slots < 2 || ring_slots > ctx->prof.slot_budget || ring_slots > VDC_RING_MAX_SLOTS)
-        return fail(VDC_ERR_INPUT, "ring_slots must be 2..min(slot_budget, 13)");
+    if (ring_slots % VDC_RING_COMPUTE_WARPS || ring_slots > ctx->prof.slot_budget || ring_slots > VDC_RING_MAX_SLOTS)
+        return fail(VDC_ERR_INPUT, "ring_slots must be a multiple of 8 and <= min(slot_budget, VDC_RING_MAX_SLOTS)");
     for (uint32_t i = 0; i < n_jobs; ++i) {
         const vdc_job& j = jobs[i];
         for (int32_t t : {j.x_t, j.a_t, j.b_t, j.o_t})
@@ -2035,6 +2039,12 @@ int vdc_load_jobs(vdc_ctx* ctx, const vdc_job* jobs, uint32_t n_jobs, uint32_t r
         if (j.r1 - j.r0 > VDC_RING_MAX_JOB_ROWS && j.op >= 0x27 && j.op <= 0x29)
             return fail(VDC_ERR_INPUT, "job " + std::to_string(i) + ": more output rows than the engine holds");
     }
+    size_t n_ctr = std::max<size_t>(1, ctx->descs.size());
+    for (uint32_t i = 0; i < n_jobs; ++i)
+        if (jobs[i].arrive_ctr >= 0) n_ctr = std::max<size_t>(n_ctr, size_t(jobs[i].arrive_ctr) + 1);
+    dfree(ctx->d_counters);
+    CU(cudaMalloc(&ctx->d_counters, sizeof(uint32_t) * n_ctr));
+    ctx->n_counters = n_ctr;
     dfree(ctx->d_jobs);
     CU(cudaMalloc(&ctx->d_jobs, sizeof(vdc_job) * std::max<uint32_t>(1, n_jobs)));
     if (n_jobs) CU(cudaMemcpy(ctx->d_jobs, jobs, sizeof(vdc_job) * n_jobs, cudaMemcpyHostToDevice));
@@ -2042,7 +2052,7 @@ int vdc_load_jobs(vdc_ctx* ctx, const vdc_job* jobs, uint32_t n_jobs, uint32_t r
     ctx->ring = true;
     ctx->ring_slots = ring_slots;
     ctx->epoch = 0;
-    CU(cudaMemset(ctx->d_counters, 0, sizeof(uint32_t) * std::max<size_t>(1, ctx->descs.size())));
+    CU(cudaMemset(ctx->d_counters, 0, sizeof(uint32_t) * ctx->n_counters));
     CU(cudaMemset(ctx->d_status, 0, sizeof(Status)));
     return VDC_OK;
 }
@@ -2078,6 +2088,20 @@ int vdc_bind_trace(vdc_ctx* ctx, void* dptr, uint32_t records_per_core) {
     return VDC_OK;
 }
 
+// debug: copy the tile trace of the last launch (3 x u64 per tile) to host memory
+extern "C" int vdc_debug_tile_trace(vdc_ctx* ctx, void* host, uint32_t n) {
+    if (!ctx || !ctx->d_tile_trace) return fail(VDC_ERR_INPUT, "no tile trace (set VDC_RING_DEBUG bit 1)");
+    CU(cudaMemcpy(host, ctx->d_tile_trace, sizeof(unsigned long long) * 3 * std::min<uint32_t>(n, 65536), cudaMemcpyDeviceToHost));
+    return VDC_OK;
+}
+
+int vdc_set_prefetch(vdc_ctx* ctx, uint32_t tiles) {
+    if (!ctx) return fail(VDC_ERR_INPUT, "null ctx");
+    if (tiles > 31) return fail(VDC_ERR_INPUT, "prefetch look-ahead must be <= 31 tiles");
+    ctx->ring_prefetch = tiles;
+    return VDC_OK;
+}
+
 int vdc_set_watchdog(vdc_ctx* ctx, uint32_t ms) {
     if (!ctx) return fail(VDC_ERR_INPUT, "null ctx");
     ctx->watchdog_ms = ms;
@@ -2104,9 +2128,21 @@ int vdc_launch(vdc_ctx* ctx, void* stream) {
         R.n_step = int32_t(ctx->d_step ? ctx->n_step : 0);
         R.epoch = ++ctx->epoch;
         R.ring_slots = ctx->ring_slots;
+        R.prefetch = ctx->ring_prefetch;
+        R.debug = getenv("VDC_RING_DEBUG") ? uint32_t(atoi(getenv("VDC_RING_DEBUG"))) : 0u;
         R.stats = ctx->d_stats;
         R.status = ctx->d_status;
         R.watchdog_ns = (unsigned long long)ctx->watchdog_ms * 1000000ull;
+        R.trace = ctx->d_trace;
+        R.trace_cap = ctx->trace_cap;
+        if (R.debug & 2u) {
+            static unsigned long long* tt = nullptr;
+            if (!tt) cudaMalloc(&tt, sizeof(unsigned long long) * 3 * 65536);
+            cudaMemsetAsync(tt, 0, sizeof(unsigned long long) * 3 * 65536, s);
+            R.tile_trace = tt;
+            R.tile_trace_cap = 65536;
+            ctx->d_tile_trace = tt;
+        }
         void* rargs[] = {&R};
         CU(cudaEventRecord(ctx->ev0, s));
         CU(cudaLaunchCooperativeKernel(ring_kernel_entry(), dim3(ctx->prof.sm_count), dim3(kRingThreads), rargs,
@@ -2189,12 +2225,13 @@ int vdc_wait(vdc_ctx* ctx, vdc_report* r) {
         }
         r->status = st.abort == 0 ? VDC_OK : st.abort == 1 ? VDC_ERR_DEADLOCK : VDC_ERR_INTERNAL;
         if (st.abort == 1)
-            std::snprintf(r->message, sizeof r->message, "deadlock: %d core(s) made no progress for %u ms", st.n_stalled, ctx->watchdog_ms);
+            std::snprintf(r->message, sizeof r->message, "deadlock: %d core(s) made no progress for %u ms (core %u, info 0x%x)",
+                          st.n_stalled, ctx->watchdog_ms, st.stalled_core[0], st.fault_info);
         else if (st.abort == 2)
             std::snprintf(r->message, sizeof r->message, "fault code %u info %u", st.fault_code, st.fault_info);
     }
     if (st.abort && ctx->ring) {  // counters are inconsistent after an aborted launch: restart the epochs
-        CU(cudaMemset(ctx->d_counters, 0, sizeof(uint32_t) * std::max<size_t>(1, ctx->descs.size())));
+        CU(cudaMemset(ctx->d_counters, 0, sizeof(uint32_t) * ctx->n_counters));
         CU(cudaMemset(ctx->d_status, 0, sizeof(Status)));
         ctx->epoch = 0;
     }

@@ -112,9 +112,15 @@ struct RingParams {
     int32_t n_step;
     uint32_t epoch;            // 1-based launch ordinal since the counters were zeroed
     uint32_t ring_slots;
+    uint32_t prefetch;         // L2 prefetch look-ahead of the memory core, in tiles (0 = off)
+    uint32_t debug;            // bit 0: GEMV tiles are released without computing (bandwidth experiments)
+    unsigned long long* tile_trace;  // debug: per ring tile of SM `debug >> 8`: {t_issue, t_full, t_release}
+    uint32_t tile_trace_cap;
     SmStats* stats;            // written (not accumulated) by each SM
     Status* status;
     unsigned long long watchdog_ns;
+    unsigned long long* trace;  // optional: per VCC core trace_cap records {core<<32|pc, t_enter, t_ready, t_done}
+    uint32_t trace_cap;
 };
 size_t ring_smem_bytes(uint32_t ring_slots);
 const void* ring_kernel_entry();

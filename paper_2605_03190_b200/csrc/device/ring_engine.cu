@@ -127,10 +127,11 @@ struct Vcc {
     uint32_t ring;   // shared address of slot 0
     uint32_t sm;
     uint32_t ct, lane, w;
-    uint32_t slot = 0, phase = 0;  // ring position of the next tile (slot, full-barrier parity)
+    uint32_t kt = 0;  // ring tiles consumed so far (program order, uniform over the VCC)
     uint32_t R;
     bool ok = true;
     unsigned long long st_full = 0, st_dep = 0, st_epi = 0;
+    unsigned long long t_ready = 0;  // trace: when the last readiness wait of the running µop completed
     // x held in registers across jobs that share it
     int32_t xk_t = -2, xk_off = 0, xk_flags = 0, xk_a = 0;
 
@@ -149,8 +150,11 @@ struct Vcc {
 
     // all compute threads: wait for ring tile k (slot full)
     __device__ bool wait_full(uint32_t slot, uint32_t parity) {
-        if (mbar_try(&S->full[slot], parity)) return true;
         const long long c0 = clock64();
+        if (mbar_try(&S->full[slot], parity)) {
+            if (ct == 0) st_full += clock64() - c0;
+            return true;
+        }
         const unsigned long long t0 = now_ns();
         for (uint32_t n = 1;; ++n) {
             if (mbar_wait_hint(&S->full[slot], parity)) break;
@@ -201,6 +205,7 @@ struct Vcc {
             }
             S->flag = good ? 1 : 0;
             st_dep += clock64() - c0;
+            if (P->trace) t_ready = now_ns();
         }
         sync();
         return S->flag != 0;
@@ -212,14 +217,6 @@ struct Vcc {
         if (ct == 0 && t >= 0) {
             __threadfence();
             red_release_add(&P->counters[t], 1u);
-        }
-    }
-
-    // ring position of the next tile to consume
-    __device__ void advance() {
-        if (++slot == R) {
-            slot = 0;
-            phase ^= 1u;
         }
     }
 
@@ -276,7 +273,12 @@ struct Vcc {
             xk_a = J.a_t;
             sync();
         }
-        switch (J.tile_rows) {
+        const int cpt_all = J.tile_cols / (BF ? 8 : 4);
+        if (BF && J.tile_rows == 2 && cpt_all % 16 == 0)
+            tiles_mma<2>(J);
+        else if (BF && J.tile_rows == 4 && cpt_all % 8 == 0)
+            tiles_mma<4>(J);
+        else switch (J.tile_rows) {
             case 1: tiles<BF, 1>(J); break;
             case 2: tiles<BF, 2>(J); break;
             case 4: tiles<BF, 4>(J); break;
@@ -290,42 +292,161 @@ struct Vcc {
         publish(J.o_t);
     }
 
-    // Consume the job's W tiles in batches of 8 output rows. The lowering
-    // orders a batch column-major (for each column tile: its 8/TR row
-    // groups), so one x chunk from shared memory feeds 8 rows. The tiles of
-    // one column are released together once their products are accumulated;
-    // the 8 per-thread row partials of the batch are then reduced across the
-    // warp with a butterfly reduce-scatter (9 shuffles) into red[warp][row].
+    // bf16 GEMV tile on the tensor cores (mma.sync m16n8k16, fp32 accumulate).
+    // A TR-row x (cpt x 8)-column tile is viewed as 16 "virtual rows"
+    // v = r * NC + c (NC = 16 / TR chunk classes): virtual row v holds the
+    // 16-byte chunks c, c + NC, c + 2 NC, ... of W row r, so one ldmatrix.x4
+    // reads 8 consecutive chunks per matrix (bank-conflict free). B column n
+    // holds the matching x chunks of class n; the partial dot products of row
+    // r are the diagonal entries D[r * NC + c][c], summed over c. Tensor-core
+    // work is 8x redundant (only the diagonal is used) but the instruction
+    // count per 16 KB tile drops from ~1200 FFMA/unpack to ~100, which is
+    // what bounds the slot hold time of warp-per-tile consumption.
+    template <int TR>
+    __device__ void tiles_mma(const vdc_job& J) {
+        constexpr int NC = 16 / TR;
+        const int K = J.k, tc = J.tile_cols, tpr = K / tc, cpt = tc / 8;
+        const int rows = J.r1 - J.r0, ntiles = (rows / TR) * tpr;
+        const uint32_t row_bytes = uint32_t(cpt) * 16u;
+        const uint32_t xb = smem_addr(S->x);
+        const int ksteps = cpt / (2 * NC);
+        // ldmatrix source of this lane: matrix mi = lane / 8 -> (virtual row block, k half)
+        const int mi = int(lane) >> 3, vi = int(lane & 7u) + 8 * (mi & 1), kh = mi >> 1;
+        const uint32_t a_lane = uint32_t(vi / NC) * row_bytes + uint32_t(vi % NC + NC * kh) * 16u;
+        // B fragment: n = lane / 4 (class), k = (lane % 4) * 2
+        const int bn = int(lane) >> 2;
+        const uint32_t b_lane = uint32_t(bn % NC) * 16u + (lane & 3u) * 4u;
+        // diagonal ownership: lanes with lane % 4 == c / 2 hold D[v][c] for v = lane / 4 (+8)
+        const int c_lo = (int(lane) >> 2) % NC;
+        const bool diag = int(lane & 3u) == (c_lo >> 1);
+        const bool odd = c_lo & 1;
+        const int r_lo = (int(lane) >> 2) / NC, r_hi = ((int(lane) >> 2) + 8) / NC;
+        for (int i = int(lane); i < rows; i += 32) S->u.red[w][i] = 0.f;
+        __syncwarp();
+        int t = int((w + CW - kt % CW) % CW);
+        uint32_t g = kt + uint32_t(t);
+        const uint32_t SP = R / CW;
+        uint32_t wm = g / CW;
+        uint32_t wslot = w + CW * (wm % SP), wphase = (wm / SP) & 1u;
+        for (; t < ntiles; t += CW) {
+            const int rg = t / tpr, c = t - rg * tpr;
+            if (!wait_full(wslot, wphase)) {
+                ok = false;
+                return;
+            }
+            const bool ttr = P->tile_trace && sm == (P->debug >> 8) && g < P->tile_trace_cap && lane == 0;
+            if (ttr) P->tile_trace[3 * g + 1] = now_ns();
+            const uint32_t abase = ring + wslot * SLOT + a_lane;
+            const uint32_t bbase = xb + uint32_t(c * cpt) * 16u + b_lane;
+            float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
+            if (!(P->debug & 1u)) {
+                // groups of 4 k-steps: all fragment loads first, then the MMAs
+                // (volatile asm keeps program order, so the order is explicit)
+                int st = 0;
+                for (; st + 4 <= ksteps; st += 4) {
+                    uint32_t a[4][4], b[4][2];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const uint32_t off = uint32_t((st + u) * 2 * NC) * 16u;
+                        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                                     : "=r"(a[u][0]), "=r"(a[u][1]), "=r"(a[u][2]), "=r"(a[u][3])
+                                     : "r"(abase + off));
+                        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(b[u][0]) : "r"(bbase + off));
+                        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(b[u][1]) : "r"(bbase + off + uint32_t(NC) * 16u));
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        float* d = (u & 1) ? d1 : d0;
+                        asm volatile(
+                            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                            "{%0,%1,%2,%3};"
+                            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                            : "r"(a[u][0]), "r"(a[u][1]), "r"(a[u][2]), "r"(a[u][3]), "r"(b[u][0]), "r"(b[u][1]));
+                    }
+                }
+                for (; st < ksteps; ++st) {
+                    const uint32_t off = uint32_t(st * 2 * NC) * 16u;
+                    uint32_t a0, a1, a2, a3, b0, b1;
+                    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+                                 : "r"(abase + off));
+                    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(b0) : "r"(bbase + off));
+                    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(b1) : "r"(bbase + off + uint32_t(NC) * 16u));
+                    asm volatile(
+                        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                        "{%0,%1,%2,%3};"
+                        : "+f"(d0[0]), "+f"(d0[1]), "+f"(d0[2]), "+f"(d0[3])
+                        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+                }
+            }
+            __syncwarp();
+            if (ttr) P->tile_trace[3 * g + 2] = now_ns();
+            if (lane == 0) mbar_arrive(&S->empty[wslot]);  // the tile goes back to the memory core
+            const float vlo = diag ? (odd ? d0[1] + d1[1] : d0[0] + d1[0]) : 0.f;
+            const float vhi = diag ? (odd ? d0[3] + d1[3] : d0[2] + d1[2]) : 0.f;
+#pragma unroll
+            for (int r = 0; r < TR; ++r) {
+                const float v = warp_sum((r_lo == r ? vlo : 0.f) + (r_hi == r ? vhi : 0.f));
+                if (lane == 0) S->u.red[w][rg * TR + r] += v;
+            }
+            ++wm;
+            g += CW;
+            wslot = w + CW * (wm % SP);
+            wphase = (wm / SP) & 1u;
+        }
+        kt += uint32_t(ntiles);
+    }
+
+    // Consume the job's W tiles warp-per-tile: ring tile g (global consumption
+    // index) belongs to compute warp g % 8, so eight tiles are in the compute
+    // pipeline at once and each tile costs one full-wait and one release. A
+    // warp accumulates its tile's rows over its 32 lanes (x chunks from the
+    // staged vector in shared memory), releases the slot, reduces across the
+    // warp and adds the row sums to red[warp][row]; column-split rows (K
+    // larger than a slot) are summed over warps in the epilogue.
     template <bool BF, int TR>
     __device__ void tiles(const vdc_job& J) {
         constexpr int EPC = BF ? 8 : 4;
-        constexpr int NG = 8 / TR;
         const int K = J.k, tc = J.tile_cols, tpr = K / tc, cpt = tc / EPC;
-        const int rows = J.r1 - J.r0;
+        const int rows = J.r1 - J.r0, ntiles = (rows / TR) * tpr;
         const uint32_t row_bytes = uint32_t(cpt) * 16u;
         const uint32_t xb = smem_addr(S->x);
-        for (int b0 = 0; b0 < rows; b0 += 8) {
-            const int ng = min(8, rows - b0) / TR;
-            float acc[8];
+        for (int i = int(lane); i < rows; i += 32) S->u.red[w][i] = 0.f;
+        __syncwarp();
+        int t = int((w + CW - kt % CW) % CW);
+        uint32_t g = kt + uint32_t(t);
+        const uint32_t SP = R / CW;
+        uint32_t wm = g / CW;  // this warp's m-th tile
+        uint32_t wslot = w + CW * (wm % SP), wphase = (wm / SP) & 1u;
+        for (; t < ntiles; t += CW) {
+            const int rg = t / tpr, c = t - rg * tpr;
+            if (!wait_full(wslot, wphase)) {
+                ok = false;
+                return;
+            }
+            const uint32_t base = ring + wslot * SLOT;
+            const bool ttr = P->tile_trace && sm == (P->debug >> 8) && g < P->tile_trace_cap && lane == 0;
+            if (ttr) P->tile_trace[3 * g + 1] = now_ns();
+            if (P->debug & 1u) {
+                release(wslot);
+                ++wm;
+                g += CW;
+                wslot = w + CW * (wm % SP);
+                wphase = (wm / SP) & 1u;
+                continue;
+            }
+            // two independent accumulators per row (even / odd chunk steps)
+            // halve the FMA dependency chain of the 16-step sweep
+            float acc[2][TR];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) acc[r] = 0.f;
-            for (int c = 0; c < tpr; ++c) {
-                uint32_t base[NG];
-                uint32_t held[NG];
+            for (int r = 0; r < TR; ++r) acc[0][r] = acc[1][r] = 0.f;
+#pragma unroll 2
+            for (int j = int(lane); j < cpt; j += 64) {
 #pragma unroll
-                for (int g = 0; g < NG; ++g) {
-                    if (g < ng) {
-                        if (!wait_full(slot, phase)) {
-                            ok = false;
-                            return;
-                        }
-                        held[g] = slot;
-                        base[g] = ring + slot * SLOT;
-                        advance();
-                    }
-                }
-                for (int j = int(ct); j < cpt; j += NCT) {
-                    const uint4 xv = lds128(xb + uint32_t(c * cpt + j) * 16u);
+                for (int h = 0; h < 2; ++h) {
+                    const int jj = j + 32 * h;
+                    if (jj >= cpt) break;
+                    const uint4 xv = lds128(xb + uint32_t(c * cpt + jj) * 16u);
                     float x[EPC];
                     if constexpr (BF) {
                         x[0] = bf_lo(xv.x); x[1] = bf_hi(xv.x); x[2] = bf_lo(xv.y); x[3] = bf_hi(xv.y);
@@ -335,61 +456,42 @@ struct Vcc {
                         x[2] = __uint_as_float(xv.z); x[3] = __uint_as_float(xv.w);
                     }
 #pragma unroll
-                    for (int g = 0; g < NG; ++g) {
-                        if (g >= ng) break;
-#pragma unroll
-                        for (int r = 0; r < TR; ++r) {
-                            const uint4 wv = lds128(base[g] + uint32_t(r) * row_bytes + uint32_t(j) * 16u);
-                            float s = acc[g * TR + r];
-                            if constexpr (BF) {
-                                s = fmaf(bf_lo(wv.x), x[0], s);
-                                s = fmaf(bf_hi(wv.x), x[1], s);
-                                s = fmaf(bf_lo(wv.y), x[2], s);
-                                s = fmaf(bf_hi(wv.y), x[3], s);
-                                s = fmaf(bf_lo(wv.z), x[4], s);
-                                s = fmaf(bf_hi(wv.z), x[5], s);
-                                s = fmaf(bf_lo(wv.w), x[6], s);
-                                s = fmaf(bf_hi(wv.w), x[7], s);
-                            } else {
-                                s = fmaf(__uint_as_float(wv.x), x[0], s);
-                                s = fmaf(__uint_as_float(wv.y), x[1], s);
-                                s = fmaf(__uint_as_float(wv.z), x[2], s);
-                                s = fmaf(__uint_as_float(wv.w), x[3], s);
-                            }
-                            acc[g * TR + r] = s;
+                    for (int r = 0; r < TR; ++r) {
+                        const uint4 wv = lds128(base + uint32_t(r) * row_bytes + uint32_t(jj) * 16u);
+                        float s = acc[h][r];
+                        if constexpr (BF) {
+                            s = fmaf(bf_lo(wv.x), x[0], s);
+                            s = fmaf(bf_hi(wv.x), x[1], s);
+                            s = fmaf(bf_lo(wv.y), x[2], s);
+                            s = fmaf(bf_hi(wv.y), x[3], s);
+                            s = fmaf(bf_lo(wv.z), x[4], s);
+                            s = fmaf(bf_hi(wv.z), x[5], s);
+                            s = fmaf(bf_lo(wv.w), x[6], s);
+                            s = fmaf(bf_hi(wv.w), x[7], s);
+                        } else {
+                            s = fmaf(__uint_as_float(wv.x), x[0], s);
+                            s = fmaf(__uint_as_float(wv.y), x[1], s);
+                            s = fmaf(__uint_as_float(wv.z), x[2], s);
+                            s = fmaf(__uint_as_float(wv.w), x[3], s);
                         }
+                        acc[h][r] = s;
                     }
                 }
-                __syncwarp();
-                if (lane == 0) {
-#pragma unroll
-                    for (int g = 0; g < NG; ++g)
-                        if (g < ng) mbar_arrive(&S->empty[held[g]]);
-                }
             }
-            // butterfly reduce-scatter of acc[0..7] over the warp
-            {
-                const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4;
+            __syncwarp();
+            if (ttr) P->tile_trace[3 * g + 2] = now_ns();
+            if (lane == 0) mbar_arrive(&S->empty[wslot]);  // the tile goes back to the memory core
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const float send = u16 ? acc[i] : acc[i + 4], keep = u16 ? acc[i + 4] : acc[i];
-                    acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-                }
-#pragma unroll
-                for (int i = 0; i < 2; ++i) {
-                    const float send = u8 ? acc[i] : acc[i + 2], keep = u8 ? acc[i + 2] : acc[i];
-                    acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-                }
-                {
-                    const float send = u4 ? acc[0] : acc[1], keep = u4 ? acc[1] : acc[0];
-                    acc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-                }
-                acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 2);
-                acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
-                const int row = (u16 ? 4 : 0) + (u8 ? 2 : 0) + (u4 ? 1 : 0);
-                if ((lane & 3) == 0 && row < ng * TR) S->u.red[w][b0 + row] = acc[0];
+            for (int r = 0; r < TR; ++r) {
+                const float v = warp_sum(acc[0][r] + acc[1][r]);
+                if (lane == 0) S->u.red[w][rg * TR + r] += v;
             }
+            ++wm;
+            g += CW;
+            wslot = w + CW * (wm % SP);
+            wphase = (wm / SP) & 1u;
         }
+        kt += uint32_t(ntiles);
     }
 
     __device__ float row_sum(int i) const {
@@ -452,194 +554,316 @@ struct Vcc {
     }
 
     // ------------------------------------------------------ ATTN_DECODE
-    // split-KV q-len-1 attention over pages [r0, r1) of one kv head for its
-    // G q heads. Warp w serves head w / (CW/G) over its slice of each page.
-    template <bool BF>
+    // Split-KV q-len-1 attention of one kv head (G q heads) over pages
+    // [r0, r1), fused with the split combine.
+    //  * page i = ring tiles (K, V) at global indices kt0 + 2i, kt0 + 2i + 1
+    //    (kt0 even: lead_pad pads the stream), i.e. in the slots of compute
+    //    warps 2p and 2p + 1 (p = pair); the pair splits the page's rows in
+    //    halves and each warp keeps its own online-softmax state.
+    //  * lanes split the head dim (DPL dims each); q and the appended K/V row
+    //    (produced in this launch by the qkv µop, read from global) sit in
+    //    registers; 32/G rows x G heads of partial dot products are reduced
+    //    across the warp with one butterfly reduce-scatter.
+    //  * the 8 warp states are merged per head in shared memory and written
+    //    as this split's partial; the last split of the kv head to arrive
+    //    (per-head arrival counter) merges all partials in split order and
+    //    publishes the head's attention output (reference finalize,
+    //    handlers.cpp:155-168).
+    template <bool BF, int DPL, int G>
     __device__ void attn(const vdc_job& J) {
         constexpr int EB = BF ? 2 : 4;
+        constexpr int HD = 32 * DPL;
+        constexpr int RB = 32 / G;  // rows per reduce-scatter batch
         if (!wait_ready(J.x_t, J.x_need, J.a_t, J.a_need, J.b_t, J.b_need)) {
             ok = false;
             return;
         }
-        xk_t = -2;  // the union below overwrites nothing of x, but keep reuse conservative
-        const int hd = J.head_dim, G = J.group, PR = J.tile_rows;
-        const int nwh = CW / G, h = int(w) / nwh, sl = int(w) % nwh;
-        const int rpw = PR / nwh;                 // page rows per warp
-        const uint32_t rowb = uint32_t(hd * EB);  // bytes per K/V row
-        const int nchk = int(rowb / 16u);
-        const int dpl = hd / 32;
+        const int PR = J.tile_rows;
+        const uint32_t rowb = uint32_t(HD * EB);
         const int64_t pos = P->step[VDC_STEP_POS], ctx = P->step[VDC_STEP_CTX];
-        // q of the group -> smem (cache dtype, same chunk layout as a K row)
+        const int half = int(w & 1u), pair = int(w >> 1);
+        auto ld = [&](const char* base, int i) -> float {
+            return BF ? bf_lo(ldcg_u16(reinterpret_cast<const uint16_t*>(base) + i)) : ldcg_f32(reinterpret_cast<const float*>(base) + i);
+        };
+        float q[G][DPL], kn[DPL], vn[DPL];
         {
-            const uint4* qs = reinterpret_cast<const uint4*>(tptr(J.x_t) + size_t(J.x_off) * EB);
-            for (int c = int(ct); c < G * nchk; c += NCT) S->u.att.q[c] = ldcg128(qs + c);
-        }
-        sync();
-        const uint32_t qbase = smem_addr(S->u.att.q) + uint32_t(h) * rowb;
-        float m = -INFINITY, l = 0.f, o[MAX_DPL];
+            const char* qb = tptr(J.x_t) + size_t(J.x_off) * EB;
+            const char* kb = tptr(J.a_t) + (size_t(J.a_off) + size_t(pos) * HD) * EB;
+            const char* vb = tptr(J.b_t) + (size_t(J.b_off) + size_t(pos) * HD) * EB;
 #pragma unroll
-        for (int d = 0; d < MAX_DPL; ++d) o[d] = 0.f;
-        for (int pg = J.r0; pg < J.r1; ++pg) {
-            const uint32_t ks = slot, kp = phase;
-            advance();
-            const uint32_t vs = slot, vp = phase;
-            advance();
-            if (!wait_full(ks, kp) || !wait_full(vs, vp)) {
+            for (int d = 0; d < DPL; ++d) {
+#pragma unroll
+                for (int h = 0; h < G; ++h) q[h][d] = ld(qb, h * HD + int(lane) * DPL + d);
+                kn[d] = ld(kb, int(lane) * DPL + d);
+                vn[d] = ld(vb, int(lane) * DPL + d);
+            }
+        }
+        float m[G], l[G], o[G][DPL];
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            m[h] = -INFINITY;
+            l[h] = 0.f;
+#pragma unroll
+            for (int d = 0; d < DPL; ++d) o[h][d] = 0.f;
+        }
+        const uint32_t SP = R / CW;
+        auto slot_of = [&](uint32_t g, uint32_t& par) {
+            const uint32_t mm = g / CW;
+            par = (mm / SP) & 1u;
+            return g % CW + CW * (mm % SP);
+        };
+        const uint32_t npages = uint32_t(J.r1 - J.r0), ntiles = uint32_t(J.lead_pad) + 2u * npages;
+        if (J.lead_pad && (kt % CW) == w) {  // padding tile: wait for it and hand it back
+            uint32_t par;
+            const uint32_t s0 = slot_of(kt, par);
+            if (!wait_full(s0, par)) {
                 ok = false;
                 return;
             }
-            const uint32_t kb = ring + ks * SLOT, vb = ring + vs * SLOT;
-            const int64_t row0 = int64_t(pg) * PR;
-            const bool has_new = pos >= row0 && pos < row0 + PR;
-            if (has_new) {  // the appended row was produced in this launch: take it from global
-                if (w == 0) {
-                    const int r = int(pos - row0);
-                    const char* kn = tptr(J.a_t) + (size_t(J.a_off) + size_t(pos) * hd) * EB;
-                    const char* vn = tptr(J.b_t) + (size_t(J.b_off) + size_t(pos) * hd) * EB;
-                    for (int c = int(lane); c < 2 * nchk; c += 32) {
-                        const bool isk = c < nchk;
-                        const int cc = isk ? c : c - nchk;
-                        const uint4 v = ldcg128(reinterpret_cast<const uint4*>(isk ? kn : vn) + cc);
-                        const uint32_t dst = (isk ? kb : vb) + uint32_t(r) * rowb + uint32_t(cc) * 16u;
-                        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(dst), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
-                    }
-                    fence_proxy_async_smem();
-                }
-                sync();
-            }
-            // scores for this warp's rows: lane owns rows sl*rpw + lane + 32 j
-            constexpr int MAXJ = 2;  // rpw <= 64
-            float sc[MAXJ];
-            float pmax = -INFINITY;
-#pragma unroll
-            for (int j = 0; j < MAXJ; ++j) {
-                sc[j] = -INFINITY;
-                const int r = int(lane) + 32 * j;
-                if (r >= rpw) continue;
-                const int rr = sl * rpw + r;
-                if (row0 + rr >= ctx) continue;
-                const uint32_t ka = kb + uint32_t(rr) * rowb;
-                float a0 = 0.f, a1 = 0.f;
-                for (int cc = 0; cc < nchk; cc += 2) {
-                    const int c0 = (cc + int(lane)) % nchk, c1 = (cc + 1 + int(lane)) % nchk;
-                    a0 += dot16<BF>(lds128(ka + uint32_t(c0) * 16u), lds128(qbase + uint32_t(c0) * 16u));
-                    if (cc + 1 < nchk) a1 += dot16<BF>(lds128(ka + uint32_t(c1) * 16u), lds128(qbase + uint32_t(c1) * 16u));
-                }
-                sc[j] = (a0 + a1) * J.scale;
-                pmax = fmaxf(pmax, sc[j]);
-            }
-            pmax = warp_max(pmax);
-            if (pmax != -INFINITY) {
-                const float mn = fmaxf(m, pmax);
-                const float corr = m == -INFINITY ? 0.f : expf(m - mn);
-                float p[MAXJ], ps = 0.f;
-#pragma unroll
-                for (int j = 0; j < MAXJ; ++j) {
-                    p[j] = sc[j] == -INFINITY ? 0.f : expf(sc[j] - mn);
-                    ps += p[j];
-                }
-                l = l * corr + warp_sum(ps);
-#pragma unroll
-                for (int d = 0; d < MAX_DPL; ++d) o[d] *= corr;
-                const int nrow = min(rpw, int(ctx - row0) - sl * rpw);
-                for (int r = 0; r < nrow; ++r) {
-                    const float pr = __shfl_sync(0xffffffffu, r < 32 ? p[0] : p[1], r & 31);
-                    const uint32_t va = vb + uint32_t(sl * rpw + r) * rowb + uint32_t(lane * dpl * EB);
-                    if constexpr (BF) {
-                        if (dpl == 4) {
-                            const uint2 v = lds64(va);
-                            o[0] = fmaf(pr, bf_lo(v.x), o[0]);
-                            o[1] = fmaf(pr, bf_hi(v.x), o[1]);
-                            o[2] = fmaf(pr, bf_lo(v.y), o[2]);
-                            o[3] = fmaf(pr, bf_hi(v.y), o[3]);
-                            continue;
-                        }
-                    } else {
-                        if (dpl == 2) {
-                            const uint2 v = lds64(va);
-                            o[0] = fmaf(pr, __uint_as_float(v.x), o[0]);
-                            o[1] = fmaf(pr, __uint_as_float(v.y), o[1]);
-                            continue;
-                        }
-                    }
-#pragma unroll
-                    for (int d = 0; d < MAX_DPL; ++d) {
-                        if (d >= dpl) break;
-                        float e;
-                        if constexpr (BF) {
-                            unsigned short u;
-                            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(u) : "r"(va + uint32_t(d) * 2u));
-                            e = __uint_as_float(uint32_t(u) << 16);
-                        } else {
-                            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(e) : "r"(va + uint32_t(d) * 4u));
-                        }
-                        o[d] = fmaf(pr, e, o[d]);
-                    }
-                }
-                m = mn;
-            }
-            release(ks);
-            release(vs);
+            release(s0);
         }
-        // merge the warp slices of each head in slice order
-        float* st = S->u.att.st[w];
-        for (int d = 0; d < dpl; ++d) st[2 + lane * dpl + d] = o[d];
-        if (lane == 0) {
-            st[0] = m;
-            st[1] = l;
+        const uint32_t kt0 = kt + uint32_t(J.lead_pad);
+        const int my_row0 = half * (PR / 2);
+        for (uint32_t i = 0; i < npages; ++i) {
+            const uint32_t gk = kt0 + 2u * i;
+            if (int((gk % CW) >> 1) != pair) continue;
+            uint32_t pk, pv;
+            const uint32_t sk = slot_of(gk, pk), sv = slot_of(gk + 1u, pv);
+            if (!wait_full(sk, pk) || !wait_full(sv, pv)) {
+                ok = false;
+                return;
+            }
+            const uint32_t kb = ring + sk * SLOT, vb = ring + sv * SLOT;
+            const int64_t prow0 = int64_t(J.r0 + int(i)) * PR + my_row0;  // global row of this warp's first row
+            // ---- scores: G batches of RB rows; lane l ends with (row l / G, head l % G) of each batch
+            float sc[G];
+#pragma unroll
+            for (int b = 0; b < G; ++b) {
+                float part[32];
+#pragma unroll
+                for (int rr = 0; rr < RB; ++rr) {
+                    const int r = b * RB + rr;
+                    float kv[DPL];
+                    if (prow0 + r == pos) {
+#pragma unroll
+                        for (int d = 0; d < DPL; ++d) kv[d] = kn[d];
+                    } else {
+                        const uint32_t a = kb + uint32_t(my_row0 + r) * rowb + lane * uint32_t(DPL * EB);
+                        load_row<BF, DPL>(a, kv);
+                    }
+#pragma unroll
+                    for (int h = 0; h < G; ++h) {
+                        float acc = 0.f;
+#pragma unroll
+                        for (int d = 0; d < DPL; ++d) acc = fmaf(q[h][d], kv[d], acc);
+                        part[rr * G + h] = acc;
+                    }
+                }
+                const float v = reduce_scatter32(part);
+                const int row = b * RB + int(lane) / G;
+                sc[b] = (prow0 + row < ctx) ? v * J.scale : -INFINITY;
+            }
+            // ---- online softmax per head (lane l serves head l % G)
+            float mx = sc[0];
+#pragma unroll
+            for (int b = 1; b < G; ++b) mx = fmaxf(mx, sc[b]);
+#pragma unroll
+            for (int off = G; off < 32; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+            const int myh = int(lane) % G;
+            float mnew_mine = fmaxf(m[0], mx);
+            float mnew[G], corr[G];
+#pragma unroll
+            for (int h = 0; h < G; ++h) {
+                const float mh = __shfl_sync(0xffffffffu, mx, h);
+                mnew[h] = fmaxf(m[h], mh);
+                corr[h] = (m[h] == -INFINITY || mnew[h] == -INFINITY) ? (m[h] == mnew[h] ? 1.f : 0.f) : expf(m[h] - mnew[h]);
+                if (h == myh) mnew_mine = mnew[h];
+            }
+            float p[G], ps = 0.f;
+#pragma unroll
+            for (int b = 0; b < G; ++b) {
+                p[b] = sc[b] == -INFINITY ? 0.f : expf(sc[b] - mnew_mine);
+                ps += p[b];
+            }
+#pragma unroll
+            for (int off = G; off < 32; off <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
+#pragma unroll
+            for (int h = 0; h < G; ++h) {
+                l[h] = l[h] * corr[h] + __shfl_sync(0xffffffffu, ps, h);
+                m[h] = mnew[h];
+#pragma unroll
+                for (int d = 0; d < DPL; ++d) o[h][d] *= corr[h];
+            }
+            // ---- o += p V over this warp's rows
+#pragma unroll
+            for (int b = 0; b < G; ++b) {
+#pragma unroll 4
+                for (int rr = 0; rr < RB; ++rr) {
+                    const int r = b * RB + rr;
+                    if (prow0 + r >= ctx) break;
+                    float vv[DPL];
+                    if (prow0 + r == pos) {
+#pragma unroll
+                        for (int d = 0; d < DPL; ++d) vv[d] = vn[d];
+                    } else {
+                        load_row<BF, DPL>(vb + uint32_t(my_row0 + r) * rowb + lane * uint32_t(DPL * EB), vv);
+                    }
+#pragma unroll
+                    for (int h = 0; h < G; ++h) {
+                        const float ph = __shfl_sync(0xffffffffu, p[b], rr * G + h);
+#pragma unroll
+                        for (int d = 0; d < DPL; ++d) o[h][d] = fmaf(ph, vv[d], o[h][d]);
+                    }
+                }
+            }
+            // both warps of the pair are done with K and V: each returns its slot
+            named_bar(2 + pair, 64);
+            release(half ? sv : sk);
+        }
+        kt += ntiles;
+        // ---- merge the 8 warp states per head (slice order), write this split's partial
+        float* part = reinterpret_cast<float*>(tptr(J.o_t)) + J.o_off;
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            float* st = S->u.att.st[w];
+            if (lane == 0) {
+                st[0] = m[h];
+                st[1] = l[h];
+            }
+#pragma unroll
+            for (int d = 0; d < DPL; ++d) st[2 + lane * DPL + d] = o[h][d];
+            sync();
+            if (int(w) == h % CW) {
+                float M = -INFINITY;
+                for (int q2 = 0; q2 < CW; ++q2) M = fmaxf(M, S->u.att.st[q2][0]);
+                float L = 0.f, O[DPL];
+#pragma unroll
+                for (int d = 0; d < DPL; ++d) O[d] = 0.f;
+                for (int q2 = 0; q2 < CW; ++q2) {
+                    const float* t = S->u.att.st[q2];
+                    if (t[0] == -INFINITY) continue;
+                    const float f = expf(t[0] - M);
+                    L = fmaf(t[1], f, L);
+#pragma unroll
+                    for (int d = 0; d < DPL; ++d) O[d] = fmaf(t[2 + lane * DPL + d], f, O[d]);
+                }
+                float* out = part + h * (HD + 2);
+#pragma unroll
+                for (int d = 0; d < DPL; ++d) out[lane * DPL + d] = O[d];
+                if (lane == 0) {
+                    out[HD] = M;
+                    out[HD + 1] = L;
+                }
+            }
+            sync();
+        }
+        // ---- arrival: the last split of this kv head combines
+        if (ct == 0) {
+            __threadfence();
+            const uint32_t old = atomicAdd(&P->counters[J.arrive_ctr], 1u);
+            S->flag = (old + 1u == uint32_t(J.arrive_need) * P->epoch) ? 1 : 0;
+            __threadfence();
         }
         sync();
-        if (sl == 0) {
-            float M = -INFINITY;
-            for (int s2 = 0; s2 < nwh; ++s2) M = fmaxf(M, S->u.att.st[w + s2][0]);
-            float L = 0.f, O[MAX_DPL];
-#pragma unroll
-            for (int d = 0; d < MAX_DPL; ++d) O[d] = 0.f;
-            for (int s2 = 0; s2 < nwh; ++s2) {
-                const float* t = S->u.att.st[w + s2];
-                if (t[0] == -INFINITY) continue;
-                const float f = expf(t[0] - M);
-                L = fmaf(t[1], f, L);
-                for (int d = 0; d < dpl; ++d) O[d] = fmaf(t[2 + lane * dpl + d], f, O[d]);
-            }
-            float* out = reinterpret_cast<float*>(tptr(J.o_t)) + J.o_off + h * (hd + 2);
-            for (int d = 0; d < dpl; ++d) out[lane * dpl + d] = O[d];
-            if (lane == 0) {
-                out[hd] = M;
-                out[hd + 1] = L;
-            }
-        }
-        publish(J.o_t);
+        if (!S->flag) return;
+        if (int(w) < G) combine_head<DPL, HD>(J, int(w));
+        publish(J.o2_t);
     }
 
-    // --------------------------------------------------- ATTN_COMBINE
-    __device__ void combine(const vdc_job& J) {
-        if (!wait_ready(J.x_t, J.x_need, -1, 0, -1, 0)) {
-            ok = false;
-            return;
-        }
-        const int hd = J.head_dim, G = J.group, S2 = J.r1, dpl = hd / 32;
-        if (int(w) < G) {
-            const int h = int(w);
-            const float* part = reinterpret_cast<const float*>(tptr(J.x_t)) + J.x_off;
-            float M = -INFINITY, L = 0.f, O[MAX_DPL];
+    template <bool BF, int DPL>
+    __device__ __forceinline__ void load_row(uint32_t a, float (&v)[DPL]) const {
+        if constexpr (BF) {
+            if constexpr (DPL == 4) {
+                const uint2 u = lds64(a);
+                v[0] = bf_lo(u.x); v[1] = bf_hi(u.x); v[2] = bf_lo(u.y); v[3] = bf_hi(u.y);
+            } else if constexpr (DPL == 8) {
+                const uint4 u = lds128(a);
+                v[0] = bf_lo(u.x); v[1] = bf_hi(u.x); v[2] = bf_lo(u.y); v[3] = bf_hi(u.y);
+                v[4] = bf_lo(u.z); v[5] = bf_hi(u.z); v[6] = bf_lo(u.w); v[7] = bf_hi(u.w);
+            } else {
 #pragma unroll
-            for (int d = 0; d < MAX_DPL; ++d) O[d] = 0.f;
-            for (int s = 0; s < S2; ++s) {
-                const float* pr = part + size_t(s * G + h) * (hd + 2);
-                const float ms = ldcg_f32(pr + hd), ls = ldcg_f32(pr + hd + 1);
-                if (ms == -INFINITY || !(ls > 0.f)) continue;
-                const float mn = fmaxf(M, ms);
-                const float a = M == -INFINITY ? 0.f : expf(M - mn), b = expf(ms - mn);
-                for (int d = 0; d < dpl; ++d) O[d] = O[d] * a + ldcg_f32(pr + lane * dpl + d) * b;
-                L = L * a + ls * b;
-                M = mn;
+                for (int d = 0; d < DPL; ++d) {
+                    unsigned short x;
+                    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(x) : "r"(a + uint32_t(d) * 2u));
+                    v[d] = __uint_as_float(uint32_t(x) << 16);
+                }
             }
-            char* ob = tptr(J.o_t);
-            const bool obf = tdtype(J.o_t) == VDC_DTYPE_BF16;
-            for (int d = 0; d < dpl; ++d) store_out(ob, obf, int64_t(J.o_off) + h * hd + lane * dpl + d, L > 0.f ? O[d] / L : 0.f);
+        } else {
+            if constexpr (DPL == 2) {
+                const uint2 u = lds64(a);
+                v[0] = __uint_as_float(u.x); v[1] = __uint_as_float(u.y);
+            } else if constexpr (DPL == 4) {
+                const uint4 u = lds128(a);
+                v[0] = __uint_as_float(u.x); v[1] = __uint_as_float(u.y); v[2] = __uint_as_float(u.z); v[3] = __uint_as_float(u.w);
+            } else {
+#pragma unroll
+                for (int d = 0; d < DPL; ++d) {
+                    float x;
+                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(a + uint32_t(d) * 4u));
+                    v[d] = x;
+                }
+            }
         }
-        publish(J.o_t);
+    }
+
+    // butterfly reduce-scatter: 32 values per lane -> lane l holds the warp
+    // sum of value l
+    __device__ __forceinline__ float reduce_scatter32(float (&v)[32]) const {
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            const bool up = lane & uint32_t(step);
+#pragma unroll
+            for (int i = 0; i < step; ++i) {
+                const float send = up ? v[i] : v[i + step], keep = up ? v[i + step] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, step);
+            }
+        }
+        return v[0];
+    }
+
+    // merge all split partials of q head h of this kv head (warp-wide): the
+    // splits' (m, l) are loaded in parallel across lanes, then o in split order
+    template <int DPL, int HD>
+    __device__ void combine_head(const vdc_job& J, int h) {
+        const int S2 = J.arrive_need, G = J.group;
+        const float* part0 = reinterpret_cast<const float*>(tptr(J.o_t)) + (J.o_off - J.split * G * (HD + 2));
+        float M = -INFINITY;
+        for (int s0 = 0; s0 < S2; s0 += 32) {
+            const int s = s0 + int(lane);
+            if (s < S2) {
+                const float* pr = part0 + size_t(s * G + h) * (HD + 2);
+                const float ms = ldcg_f32(pr + HD), ls = ldcg_f32(pr + HD + 1);
+                if (ms != -INFINITY && ls > 0.f) M = fmaxf(M, ms);
+            }
+        }
+        M = warp_max(M);
+        float L = 0.f, O[DPL];
+#pragma unroll
+        for (int d = 0; d < DPL; ++d) O[d] = 0.f;
+        for (int s0 = 0; s0 < S2; s0 += 32) {
+            const int s = s0 + int(lane);
+            float wsum = 0.f, wl = 0.f;
+            if (s < S2) {
+                const float* pr = part0 + size_t(s * G + h) * (HD + 2);
+                const float ms = ldcg_f32(pr + HD), ls = ldcg_f32(pr + HD + 1);
+                wsum = (ms != -INFINITY && ls > 0.f) ? expf(ms - M) : 0.f;
+                wl = ls * wsum;
+            }
+            L += warp_sum(wl);
+            const int n = min(32, S2 - s0);
+#pragma unroll 8
+            for (int k2 = 0; k2 < n; ++k2) {
+                const float wk = __shfl_sync(0xffffffffu, wsum, k2);
+                const float* pr = part0 + size_t((s0 + k2) * G + h) * (HD + 2) + lane * DPL;
+#pragma unroll
+                for (int d = 0; d < DPL; ++d) O[d] = fmaf(ldcg_f32(pr + d), wk, O[d]);
+            }
+        }
+        char* ob = tptr(J.o2_t);
+        const bool obf = tdtype(J.o2_t) == VDC_DTYPE_BF16;
+#pragma unroll
+        for (int d = 0; d < DPL; ++d)
+            store_out(ob, obf, int64_t(J.o2_off) + h * HD + lane * DPL + d, L > 0.f ? O[d] / L : 0.f);
     }
 
     // ------------------------------------------- ELEMWISE copy (embedding row)
@@ -674,21 +898,44 @@ __device__ void vcc_role(const RingParams& P, Shared& S, char* ring) {
         if (op == OP_HALT) break;
         const vdc_job J = P.jobs[raw.z];
         const bool bf = v.tdtype(J.x_t) == VDC_DTYPE_BF16;
+        const unsigned long long t_enter = P.trace ? now_ns() : 0;
+        v.t_ready = 0;
         switch (op) {
             case OP_GEMV:
             case OP_RMS_GEMV:
             case OP_GEMV_ADD:
                 if (bf) v.gemv<true>(J); else v.gemv<false>(J);
                 break;
-            case OP_ATTN_DECODE:
-                if (v.tdtype(J.a_t) == VDC_DTYPE_BF16) v.attn<true>(J); else v.attn<false>(J);
+            case OP_ATTN_DECODE: {
+                const bool kbf = v.tdtype(J.a_t) == VDC_DTYPE_BF16;
+                const int dpl = J.head_dim / 32, G = J.group;
+#define VDC_ATTN_CASE(B, D, GG) \
+    if (kbf == B && dpl == D && G == GG) { v.attn<B, D, GG>(J); break; }
+                VDC_ATTN_CASE(true, 4, 4)
+                VDC_ATTN_CASE(true, 4, 8)
+                VDC_ATTN_CASE(true, 4, 1)
+                VDC_ATTN_CASE(true, 4, 2)
+                VDC_ATTN_CASE(false, 2, 1)
+                VDC_ATTN_CASE(false, 2, 4)
+                VDC_ATTN_CASE(false, 4, 1)
+                VDC_ATTN_CASE(false, 4, 4)
+#undef VDC_ATTN_CASE
+                if (v.ct == 0) v.fire(6, (core << 16) | pc);  // unsupported head geometry
+                v.ok = false;
                 break;
-            case OP_ATTN_COMBINE: v.combine(J); break;
+            }
             case OP_ELEMWISE: v.copy_row(J); break;
             default:
                 if (v.ct == 0) v.fire(4, (core << 16) | pc);
                 v.ok = false;
                 break;
+        }
+        if (P.trace && v.ct == 0 && jobs < P.trace_cap) {
+            unsigned long long* rec = P.trace + (size_t(core) * P.trace_cap + jobs) * 4;
+            rec[0] = (static_cast<unsigned long long>(core) << 32) | pc;
+            rec[1] = t_enter;
+            rec[2] = v.t_ready ? v.t_ready : t_enter;
+            rec[3] = now_ns();
         }
         ++jobs;
     }
@@ -702,108 +949,157 @@ __device__ void vcc_role(const RingParams& P, Shared& S, char* ring) {
     }
 }
 
+// One LOAD word resolved to its global runs: `copies` runs of `run` bytes,
+// `pitch` apart (whole-row tiles are a single run).
+struct Tile {
+    const char* src = nullptr;
+    uint32_t copies = 0, run = 0, pitch = 0;
+    bool bad = false, halt = false;
+    __device__ uint32_t bytes() const { return copies * run; }
+};
+
+__device__ __forceinline__ Tile resolve_load(const RingParams& P, uint4 raw) {
+    Tile t;
+    const uint32_t op = raw.x & 0xff;
+    if (op == OP_HALT) {
+        t.halt = true;
+        return t;
+    }
+    if (op != OP_LOAD) {
+        t.bad = true;
+        return t;
+    }
+    const uint32_t b1 = (raw.x >> 8) & 0xff;
+    const uint32_t kind = (b1 >> 4) & 3, rank = (b1 >> 6) + 1;
+    const uint32_t ti = raw.z & 0xffff;
+    const uint64_t pl = uint64_t(raw.z >> 16) | (uint64_t(raw.w) << 16);
+    const DevDesc& d = P.descs[ti];
+    if (kind != 2 || int32_t(rank) != d.grid_rank) {
+        t.bad = true;
+        return t;
+    }
+    const int64_t c0 = int64_t(pl & 0xfff), c1 = int64_t((pl >> 12) & 0xfff), c2 = int64_t((pl >> 24) & 0xfff);
+    const int64_t rt = rank == 3 ? c1 : c0, ctile = rank == 3 ? c2 : c1, plane = rank == 3 ? c0 : 0;
+    const int64_t off = plane * d.lead_stride[0] + rt * d.tile_rows * d.cols + ctile * d.tile_cols;
+    const int64_t rows_at = min(d.tile_rows, d.rows - rt * d.tile_rows);
+    t.src = d.ptr + off * d.elem;
+    t.copies = d.tile_cols == d.cols ? 1u : uint32_t(rows_at);
+    t.run = uint32_t((d.tile_cols == d.cols ? rows_at * d.cols : d.tile_cols) * d.elem);
+    t.pitch = uint32_t(d.cols * d.elem);
+    t.bad = t.bytes() == 0 || t.bytes() > SLOT || (reinterpret_cast<uintptr_t>(t.src) & 15) || (t.run & 15) ||
+            (t.copies > 1 && (t.pitch & 15));
+    return t;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_addr(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+// The memory core: eight issuing lanes, one per compute warp. Ring tile g
+// is consumed by compute warp g % 8 and lives in slot (g % 8) + 8 * ((g / 8)
+// % S) (S = ring_slots / 8), so lane w walks tiles w, w + 8, w + 16, ... of
+// the stream and refills only warp w's slots: each (issuing lane, compute
+// warp) pair is an independent pipeline and a slow tile never blocks the
+// refill of another warp's slot. Lanes poll their own slot's `empty`
+// barrier (non-blocking test_wait) in one converged loop and issue the bulk
+// copy of their next tile as soon as it is free; optional L2 prefetch of
+// the tile `prefetch` rounds ahead.
 __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t core = 2 * blockIdx.x;
     const uint32_t w0 = P.core_off[core], n = P.core_off[core + 1] - w0;
-    const uint32_t R = P.ring_slots;
-    uint32_t k = 0;
+    const uint32_t SP = P.ring_slots / CW;  // slots per issuing lane
+    const uint32_t PF = P.prefetch;
+    // the stream is LOAD words followed by one HALT
+    const uint32_t ntiles = n && ((__ldg(&P.words[w0 + n - 1]).x & 0xff) == OP_HALT) ? n - 1 : n;
+    const bool issuer = lane < uint32_t(CW);
+    uint32_t g = lane, m = 0;
     unsigned long long st_empty = 0, bytes = 0, uops = 0;
     const long long t_start = clock64();
-    bool stop = false;
-    uint4 nxt = lane < n ? __ldg(&P.words[w0 + lane]) : make_uint4(0, 0, 0, 0);
-    for (uint32_t base = 0; base < n && !stop; base += 32) {
-        const uint4 raw = nxt;
-        if (base + 32 + lane < n) nxt = __ldg(&P.words[w0 + base + 32 + lane]);  // prefetch the next batch
-        const uint32_t cnt = min(32u, n - base);
-        const uint32_t op = raw.x & 0xff;
-        // resolve this lane's word: LOAD addr=t@(coords) -> global pointer + bytes
-        const char* src = nullptr;
-        uint32_t bytes_l = 0, copies = 1, run = 0, pitch = 0;
-        bool bad = false;
-        if (lane < cnt && op == OP_LOAD) {
-            const uint32_t b1 = (raw.x >> 8) & 0xff;
-            const uint32_t kind = (b1 >> 4) & 3, rank = (b1 >> 6) + 1;
-            const uint32_t t = raw.z & 0xffff;
-            const uint64_t pl = uint64_t(raw.z >> 16) | (uint64_t(raw.w) << 16);
-            const DevDesc& d = P.descs[t];
-            if (kind != 2 || int32_t(rank) != d.grid_rank) {
-                bad = true;
+    uint4 raw = issuer && g < ntiles ? __ldg(&P.words[w0 + g]) : make_uint4(0, 0, 0, 0);
+    if (issuer && PF)
+        for (uint32_t a = 1; a <= PF; ++a) {
+            const uint32_t ga = g + CW * a;
+            if (ga >= ntiles) break;
+            const Tile t = resolve_load(P, __ldg(&P.words[w0 + ga]));
+            if (!t.bad && !t.halt)
+                for (uint32_t q = 0; q < t.copies; ++q) prefetch_l2(t.src + size_t(q) * t.pitch, t.run);
+        }
+    long long idle_since = 0;
+    unsigned long long t_idle = 0;
+    for (;;) {
+        const bool pending = issuer && g < ntiles;
+        if (!__any_sync(0xffffffffu, pending)) break;
+        bool ready = false;
+        uint32_t slot = 0;
+        if (pending) {
+            slot = lane + CW * (m % SP);
+            ready = m < SP || mbar_test(&S.empty[slot], ((m / SP) - 1u) & 1u);
+        }
+        if (ready) {
+            const Tile t = resolve_load(P, raw);
+            if (t.bad || t.halt) {
+                if (atomicCAS(&P.status->abort, 0, 2) == 0) {
+                    P.status->fault_code = 5;
+                    P.status->fault_info = g;
+                    P.status->stalled_core[0] = core;
+                }
             } else {
-                const int64_t c0 = int64_t(pl & 0xfff), c1 = int64_t((pl >> 12) & 0xfff), c2 = int64_t((pl >> 24) & 0xfff);
-                const int64_t rt = rank == 3 ? c1 : c0, ctile = rank == 3 ? c2 : c1, plane = rank == 3 ? c0 : 0;
-                const int64_t off = plane * d.lead_stride[0] + rt * d.tile_rows * d.cols + ctile * d.tile_cols;
-                const int64_t rows_at = min(d.tile_rows, d.rows - rt * d.tile_rows);
-                src = d.ptr + off * d.elem;
-                // whole rows: one contiguous run; column chunks: one run per row
-                copies = d.tile_cols == d.cols ? 1u : uint32_t(rows_at);
-                run = uint32_t((d.tile_cols == d.cols ? rows_at * d.cols : d.tile_cols) * d.elem);
-                pitch = uint32_t(d.cols * d.elem);
-                bytes_l = run * copies;
-                bad = bytes_l == 0 || bytes_l > SLOT || (reinterpret_cast<uintptr_t>(src) & 15) || (run & 15) ||
-                      (copies > 1 && (pitch & 15));
+                if (P.tile_trace && blockIdx.x == (P.debug >> 8) && g < P.tile_trace_cap) P.tile_trace[3 * g] = now_ns();
+                mbar_expect_tx(&S.full[slot], t.bytes());
+                char* dst = ring + size_t(slot) * SLOT;
+                for (uint32_t q = 0; q < t.copies; ++q)
+                    bulk_g2s(dst + q * t.run, t.src + size_t(q) * t.pitch, t.run, &S.full[slot]);
+                bytes += t.bytes();
+                ++uops;
             }
-        } else if (lane < cnt && op != OP_HALT) {
-            bad = true;
-        }
-        const uint32_t badm = __ballot_sync(0xffffffffu, bad);
-        const uint32_t haltm = __ballot_sync(0xffffffffu, lane < cnt && op == OP_HALT);
-        if (badm) {
-            if (lane == 0 && atomicCAS(&P.status->abort, 0, 2) == 0) {
-                P.status->fault_code = 5;
-                P.status->fault_info = base + __ffs(badm) - 1;
-                P.status->stalled_core[0] = core;
-            }
-            break;
-        }
-        const uint32_t m = haltm ? min(cnt, uint32_t(__ffs(haltm) - 1)) : cnt;
-        for (uint32_t i = 0; i < m; ++i) {
-            const uint64_t sp = __shfl_sync(0xffffffffu, reinterpret_cast<uint64_t>(src), i);
-            const uint32_t nb = __shfl_sync(0xffffffffu, bytes_l, i);
-            const uint32_t ncp = __shfl_sync(0xffffffffu, copies, i);
-            const uint32_t nrun = __shfl_sync(0xffffffffu, run, i);
-            const uint32_t npitch = __shfl_sync(0xffffffffu, pitch, i);
-            if (lane == 0) {
-                const uint32_t slot = k % R;
-                if (k >= R) {
-                    const uint32_t par = ((k / R) - 1u) & 1u;
-                    if (!mbar_try(&S.empty[slot], par)) {
-                        const long long c0 = clock64();
-                        const unsigned long long t0 = now_ns();
-                        for (uint32_t spin = 1;; ++spin) {
-                            if (mbar_wait_hint(&S.empty[slot], par)) break;
-                            if ((spin & 15) == 0) {
-                                if (*reinterpret_cast<volatile int32_t*>(&P.status->abort)) {
-                                    stop = true;
-                                    break;
-                                }
-                                if (P.watchdog_ns && now_ns() - t0 > P.watchdog_ns) {
-                                    if (atomicCAS(&P.status->abort, 0, 1) == 0) {
-                                        P.status->stalled_core[0] = core;
-                                        P.status->n_stalled = 1;
-                                    }
-                                    stop = true;
-                                    break;
-                                }
-                            }
-                        }
-                        st_empty += clock64() - c0;
-                    }
-                }
-                if (!stop) {
-                    mbar_expect_tx(&S.full[slot], nb);
-                    const char* g = reinterpret_cast<const char*>(sp);
-                    char* dst = ring + size_t(slot) * SLOT;
-                    for (uint32_t q = 0; q < ncp; ++q) bulk_g2s(dst + q * nrun, g + size_t(q) * npitch, nrun, &S.full[slot]);
-                    bytes += nb;
+            if (PF) {
+                const uint32_t ga = g + CW * (PF + 1);
+                if (ga < ntiles) {
+                    const Tile ta = resolve_load(P, __ldg(&P.words[w0 + ga]));
+                    if (!ta.bad && !ta.halt)
+                        for (uint32_t q = 0; q < ta.copies; ++q) prefetch_l2(ta.src + size_t(q) * ta.pitch, ta.run);
                 }
             }
-            stop = __shfl_sync(0xffffffffu, stop, 0);
-            if (stop) break;
-            ++k;
-            ++uops;
+            g += CW;
+            ++m;
+            raw = g < ntiles ? __ldg(&P.words[w0 + g]) : make_uint4(0, 0, 0, 0);
         }
-        if (haltm) break;
+        if (!__any_sync(0xffffffffu, ready)) {
+            const long long now = clock64();
+            if (!idle_since) {
+                idle_since = now;
+                t_idle = now_ns();
+            }
+            __nanosleep(32);
+            if (*reinterpret_cast<volatile int32_t*>(&P.status->abort)) break;
+            if (P.watchdog_ns && now_ns() - t_idle > P.watchdog_ns) {
+                if (lane == 0 && atomicCAS(&P.status->abort, 0, 1) == 0) {
+                    P.status->stalled_core[0] = core;
+                    P.status->n_stalled = 1;
+                    P.status->fault_info = 0x30000u | (g & 0xffffu);
+                }
+                break;
+            }
+        } else if (idle_since) {
+            st_empty += clock64() - idle_since;
+            idle_since = 0;
+        }
+    }
+    if (idle_since) st_empty += clock64() - idle_since;
+    for (int o = 16; o; o >>= 1) {
+        bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+        uops += __shfl_xor_sync(0xffffffffu, uops, o);
     }
     if (lane == 0) {
         SmStats& st = P.stats[blockIdx.x];
@@ -822,7 +1118,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(const __grid_cons
     if (threadIdx.x == 0) {
         for (uint32_t i = 0; i < P.ring_slots; ++i) {
             mbar_init(&S.full[i], 1);
-            mbar_init(&S.empty[i], CW);
+            mbar_init(&S.empty[i], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }

@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cmath>
 #include <numeric>
+#include <set>
 
 #include "jobs.hpp"
 #include "uopsim/decode_abi.h"
@@ -51,6 +52,7 @@ struct Tile {
 
 struct RJob {
     vdc_job j{};
+    int32_t head = -1;        // attention: kv head
     std::vector<Tile> tiles;  // ring tiles in consumption order
     uint32_t ordinal = 0;
     uint32_t sm = 0;
@@ -69,7 +71,11 @@ class RingLowering {
         for (const auto* n : order) plan(*n, ordinal++);
         // readiness targets: jobs writing each storage tensor per launch
         std::map<int32_t, int32_t> writers;
-        for (const auto& r : jobs_) ++writers[r.j.o_t];
+        std::set<std::pair<int32_t, int32_t>> combined;
+        for (const auto& r : jobs_) {
+            ++writers[r.j.o_t];
+            if (r.j.o2_t >= 0 && combined.insert({r.j.o2_t, r.j.o2_off}).second) ++writers[r.j.o2_t];  // one combiner per kv head
+        }
         for (auto& r : jobs_) {
             auto need = [&](int32_t t) { return t >= 0 && writers.count(storage(uint16_t(t))) ? writers.at(storage(uint16_t(t))) : 0; };
             r.j.x_need = need(r.j.x_t);
@@ -107,7 +113,8 @@ class RingLowering {
     static vdc_job blank(Opcode op) {
         vdc_job j{};
         j.op = int32_t(op);
-        j.x_t = j.a_t = j.b_t = j.o_t = -1;
+        j.x_t = j.a_t = j.b_t = j.o_t = j.o2_t = -1;
+        j.arrive_ctr = -1;
         return j;
     }
 
@@ -231,17 +238,16 @@ class RingLowering {
                         j.flags |= VDC_JOB_SWIGLU;
                         j.block = int32_t(swiglu);
                     }
-                    // consumption order of the ring engine: batches of 8 output
-                    // rows, column tiles outer, row groups inner
-                    for (int64_t b0 = c0; b0 < c1; b0 += 8)
-                        for (int64_t ct = 0; ct < tpr; ++ct)
-                            for (int64_t row = b0; row < std::min(c1, b0 + 8); row += tr) {
-                                const int64_t plane = row / plane_rows, prow = row % plane_rows;
-                                if (wd.shape.size() == 3)
-                                    r.tiles.push_back({w, {uint16_t(plane), uint16_t(prow / tr), uint16_t(ct)}});
-                                else
-                                    r.tiles.push_back({w, {uint16_t(prow / tr), uint16_t(ct)}});
-                            }
+                    // consumption order of the ring engine: row groups outer,
+                    // column tiles inner (tile t -> compute warp t mod 8)
+                    for (int64_t row = c0; row < c1; row += tr)
+                        for (int64_t ct = 0; ct < tpr; ++ct) {
+                            const int64_t plane = row / plane_rows, prow = row % plane_rows;
+                            if (wd.shape.size() == 3)
+                                r.tiles.push_back({w, {uint16_t(plane), uint16_t(prow / tr), uint16_t(ct)}});
+                            else
+                                r.tiles.push_back({w, {uint16_t(prow / tr), uint16_t(ct)}});
+                        }
                     jobs_.push_back(std::move(r));
                 }
             }
@@ -260,11 +266,13 @@ class RingLowering {
         const int64_t pages = attr_int(n, "ctx_pages", 1), per = attr_int(n, "pages_per_job", 1);
         const int64_t splits = ceil_div(pages, per);
         int64_t k = 0;
-        for (int64_t h = 0; h < hkv; ++h)
+        for (int64_t h = 0; h < hkv; ++h) {
+            const int32_t ctr = int32_t(desc_.size()) + n_arrive_++;  // per-kv-head arrival counter
             for (int64_t s = 0; s < splits; ++s, ++k) {
                 RJob r;
                 r.ordinal = ordinal;
                 r.sm = uint32_t(k % sms_);
+                r.head = int32_t(h);
                 vdc_job& j = r.j;
                 j = blank(Opcode::ATTN_DECODE);
                 j.r0 = int32_t(s * per);
@@ -284,36 +292,29 @@ class RingLowering {
                 j.b_off = int32_t(h * T * hd);
                 j.o_t = storage(part);
                 j.o_off = int32_t((h * splits + s) * grp * (hd + 2));
+                j.split = int32_t(s);
+                j.arrive_ctr = ctr;
+                j.arrive_need = int32_t(splits);
                 for (int64_t pg = j.r0; pg < j.r1; ++pg) {
                     r.tiles.push_back({kc, {uint16_t(h), uint16_t(pg), 0}});
                     r.tiles.push_back({vc, {uint16_t(h), uint16_t(pg), 0}});
                 }
                 jobs_.push_back(std::move(r));
             }
+        }
         attn_ = {hkv, splits, grp, hd, k};
     }
 
+    // ring mode fuses the combine into the attention jobs (last arriver per kv
+    // head merges); the node only names the output the combiner writes
     void plan_combine(const workload::OperatorNode& n, uint32_t ordinal) {
-        const uint16_t part = idx(n.inputs[0]), out = idx(n.outputs[0]);
-        // combine jobs go to the SMs that had no attention job (idle during
-        // the split-KV sweep), else round-robin after the attention jobs
-        for (int64_t h = 0; h < attn_.hkv; ++h) {
-            RJob r;
-            r.ordinal = ordinal;
-            r.sm = uint32_t((attn_.jobs + h) % sms_);
-            vdc_job& j = r.j;
-            j = blank(Opcode::ATTN_COMBINE);
-            j.r0 = 0;
-            j.r1 = int32_t(attn_.splits);
-            j.k = int32_t(attn_.hd);
-            j.head_dim = int32_t(attn_.hd);
-            j.group = int32_t(attn_.grp);
-            j.x_t = storage(part);
-            j.x_off = int32_t(h * attn_.splits * attn_.grp * (attn_.hd + 2));
-            j.o_t = storage(out);
-            j.o_off = int32_t(h * attn_.grp * attn_.hd);
-            jobs_.push_back(std::move(r));
-        }
+        (void)ordinal;
+        const int32_t part = storage(idx(n.inputs[0])), out = storage(idx(n.outputs[0]));
+        for (auto& r : jobs_)
+            if (r.j.op == int32_t(Opcode::ATTN_DECODE) && r.j.o_t == part) {
+                r.j.o2_t = out;
+                r.j.o2_off = r.head * r.j.group * r.j.head_dim;
+            }
     }
 
     void emit(LoweredProgram& p) {
@@ -326,8 +327,15 @@ class RingLowering {
             auto& vm = p.meta[CoreId::vmc(uint16_t(s))];
             auto& cs = p.streams[CoreId::vcc_id(uint16_t(s), 0)];
             auto& cm = p.meta[CoreId::vcc_id(uint16_t(s), 0)];
+            size_t tiles_so_far = 0;
             for (size_t ji : per_sm[s]) {
-                const RJob& r = jobs_[ji];
+                RJob r = jobs_[ji];
+                if (r.j.op == int32_t(Opcode::ATTN_DECODE) && (tiles_so_far & 1)) {
+                    // K pages must start on an even ring index (warp pairs): pad
+                    r.j.lead_pad = 1;
+                    r.tiles.insert(r.tiles.begin(), r.tiles.front());
+                }
+                tiles_so_far += r.tiles.size();
                 const int32_t slot = int32_t(p.jobs.size());
                 p.jobs.push_back(r.j);
                 for (const Tile& t : r.tiles) {
@@ -359,6 +367,7 @@ class RingLowering {
         }
     }
 
+    int32_t n_arrive_ = 0;
     struct AttnInfo {
         int64_t hkv = 0, splits = 1, grp = 1, hd = 0, jobs = 0;
     } attn_;
@@ -368,7 +377,11 @@ class RingLowering {
 
 LoweredProgram lower_decode_ring(const workload::OperatorGraph& g, const costmodel::HardwareProfile& hw, const GenOptions& opt,
                                  int ring_slots) {
-    if (ring_slots < 2 || ring_slots > VDC_RING_MAX_SLOTS) throw GeneratorError("ring_slots must be 2..11");
+    // ring tile g is consumed by compute warp g % 8, so every slot must have a
+    // single consumer warp (a slot shared by two warps could be waited on one
+    // phase ahead, which mbarrier parity waits cannot distinguish)
+    if (ring_slots % VDC_RING_COMPUTE_WARPS || ring_slots > VDC_RING_MAX_SLOTS)
+        throw GeneratorError("ring_slots must be a multiple of 8 (one consumer warp per slot) and <= the smem limit");
     return RingLowering(g, hw, ring_slots).run(opt);
 }
 

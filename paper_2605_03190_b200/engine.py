@@ -69,6 +69,10 @@ class Engine:
         self.descs = {d["name"]: d for d in info["descriptors"]}
 
     # -- memory -------------------------------------------------------------
+    def set_prefetch(self, tiles: int) -> None:
+        """Ring engine: L2 prefetch look-ahead of the memory core (tiles)."""
+        check(lib().vdc_set_prefetch(self._h, tiles))
+
     def storage_names(self):
         return [d["name"] for d in self.info["descriptors"] if d["view_of"] < 0]
 
