@@ -50,6 +50,7 @@
 #define VDC_JOB_RESID 0x08      /* out = a + W x */
 #define VDC_JOB_KV_APPEND 0x10  /* output row r -> cache[(r/hd)*T + pos][r%hd] */
 #define VDC_JOB_TOKEN_ROW 0x20  /* x offset += step[TOKEN] * k (embedding row) */
+#define VDC_JOB_TOKEN_AUX 0x40  /* aux offset += step[TOKEN] * cache_rows (residual = embedding row) */
 
 typedef struct vdc_job {
     int32_t op;               /* isa opcode of the compute µop                */

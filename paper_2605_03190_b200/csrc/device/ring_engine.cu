@@ -64,10 +64,11 @@ struct alignas(16) Shared {
         float red[CW][RMAX];  // per-warp row partials of a GEMV job
         struct {
             float st[CW][2 + MAX_HD];   // per-warp online-softmax state (m, l, o)
-            uint4 q[1024 * 4 / 16];     // q heads of the group (cache dtype, <= 4 KB)
+            float qf[1024];             // q heads of the group, fp32 (G x head_dim <= 1024)
         } att;
     } u;
     float bc[2 * CW];
+    float rope_cs[MAX_HD / 2], rope_sn[MAX_HD / 2];  // rotary table of the launch's position
     int32_t flag;
     alignas(16) uint4 x[XBUF / 16];  // GEMV input vector (normalised, model dtype), reused across jobs
 };
@@ -132,6 +133,9 @@ struct Vcc {
     bool ok = true;
     unsigned long long st_full = 0, st_dep = 0, st_epi = 0;
     unsigned long long t_ready = 0;  // trace: when the last readiness wait of the running µop completed
+    float resid = 0.f;               // GEMV_ADD: this thread's residual element, loaded before the tile sweep
+    int32_t rope_hd = 0;             // head dim of the cached rotary table (0 = none)
+    float rope_theta = 0.f;
     // x held in registers across jobs that share it
     int32_t xk_t = -2, xk_off = 0, xk_flags = 0, xk_a = 0;
 
@@ -146,6 +150,7 @@ struct Vcc {
         }
     }
     __device__ char* tptr(int32_t t) const { return P->descs[t].ptr; }
+    __device__ int64_t token() const { return P->n_step > VDC_STEP_TOKEN ? P->step[VDC_STEP_TOKEN] : 0; }
     __device__ int32_t tdtype(int32_t t) const { return P->descs[t].dtype; }
 
     // all compute threads: wait for ring tile k (slot full)
@@ -214,10 +219,7 @@ struct Vcc {
     // after all threads stored the job's outputs
     __device__ void publish(int32_t t) {
         sync();
-        if (ct == 0 && t >= 0) {
-            __threadfence();
-            red_release_add(&P->counters[t], 1u);
-        }
+        if (ct == 0 && t >= 0) red_release_add(&P->counters[t], 1u);  // release is cumulative over the CTA barrier
     }
 
     // ---------------------------------------------------------------- GEMV
@@ -232,7 +234,8 @@ struct Vcc {
             return;
         }
         if (!reuse) {  // stage x (RMS-normalised, rounded to the model dtype) in shared memory
-            const uint4* xs = reinterpret_cast<const uint4*>(tptr(J.x_t)) + (J.x_off / EPC);
+            const uint4* xs = reinterpret_cast<const uint4*>(tptr(J.x_t)) +
+                              (J.x_off + (J.flags & VDC_JOB_TOKEN_ROW ? token() * int64_t(K) : 0)) / EPC;
             float inv = 1.f;
             if (rmsf) {
                 float ss = 0.f;
@@ -271,6 +274,28 @@ struct Vcc {
             xk_off = J.x_off;
             xk_flags = rmsf;
             xk_a = J.a_t;
+            sync();
+        }
+        if (J.flags & VDC_JOB_RESID) {  // residual element of this thread's output row (hidden behind the sweep)
+            const int i = int(ct);
+            resid = 0.f;
+            if (i < J.r1 - J.r0) {
+                const char* ab = tptr(J.a_t);
+                const int64_t ai = int64_t(J.a_off) + (J.r0 - J.out_row0) + i + (J.flags & VDC_JOB_TOKEN_AUX ? token() * int64_t(J.cache_rows) : 0);
+                resid = tdtype(J.a_t) == VDC_DTYPE_BF16 ? bf_lo(ldcg_u16(reinterpret_cast<const uint16_t*>(ab) + ai))
+                                                        : ldcg_f32(reinterpret_cast<const float*>(ab) + ai);
+            }
+        }
+        if ((J.flags & VDC_JOB_ROPE) && (rope_hd != J.head_dim || rope_theta != J.theta)) {
+            // rotary table of this launch's position: cos/sin per dim pair, angles in double precision
+            const int64_t pos = P->n_step > VDC_STEP_POS ? P->step[VDC_STEP_POS] : 0;
+            for (int d2 = int(ct); d2 < J.head_dim / 2; d2 += NCT) {
+                const double ang = double(pos) * pow(double(J.theta), -double(2 * d2) / double(J.head_dim));
+                S->rope_cs[d2] = float(cos(ang));
+                S->rope_sn[d2] = float(sin(ang));
+            }
+            rope_hd = J.head_dim;
+            rope_theta = J.theta;
             sync();
         }
         const int cpt_all = J.tile_cols / (BF ? 8 : 4);
@@ -526,29 +551,21 @@ struct Vcc {
                 store_out(ob, obf, int64_t(J.o_off) + lr0 / 2 + j, gt / (1.0f + expf(-gt)) * up);
             }
         } else if (J.flags & VDC_JOB_ROPE) {
-            const double theta = double(J.theta);
             for (int p = int(ct); p < rows / 2; p += NCT) {
                 const int lr = lr0 + 2 * p;
                 float a = row_sum(2 * p), b = row_sum(2 * p + 1);
                 const int d = lr % J.head_dim;
-                const double ang = double(pos) * pow(theta, -double(d) / double(J.head_dim));
-                const float cs = float(cos(ang)), sn = float(sin(ang));
+                const float cs = S->rope_cs[d / 2], sn = S->rope_sn[d / 2];
                 const float na = a * cs - b * sn, nb = a * sn + b * cs;
                 store_out(ob, obf, out_index(lr), na);
                 store_out(ob, obf, out_index(lr + 1), nb);
             }
         } else {
-            const char* ab = (J.flags & VDC_JOB_RESID) ? tptr(J.a_t) : nullptr;
-            const bool abf = ab && tdtype(J.a_t) == VDC_DTYPE_BF16;
+            const bool res = J.flags & VDC_JOB_RESID;
             for (int i = int(ct); i < rows; i += NCT) {
                 float v = row_sum(i);
-                const int lr = lr0 + i;
-                if (ab) {
-                    const int64_t ai = int64_t(J.a_off) + lr;
-                    v += abf ? bf_lo(ldcg_u16(reinterpret_cast<const uint16_t*>(ab) + ai))
-                             : ldcg_f32(reinterpret_cast<const float*>(ab) + ai);
-                }
-                store_out(ob, obf, out_index(lr), v);
+                if (res) v += resid;
+                store_out(ob, obf, out_index(lr0 + i), v);
             }
         }
     }
@@ -573,7 +590,7 @@ struct Vcc {
     __device__ void attn(const vdc_job& J) {
         constexpr int EB = BF ? 2 : 4;
         constexpr int HD = 32 * DPL;
-        constexpr int RB = 32 / G;  // rows per reduce-scatter batch
+        constexpr int NCH = HD * EB / 16;  // 16-byte chunks per K/V row
         if (!wait_ready(J.x_t, J.x_need, J.a_t, J.a_need, J.b_t, J.b_need)) {
             ok = false;
             return;
@@ -582,22 +599,17 @@ struct Vcc {
         const uint32_t rowb = uint32_t(HD * EB);
         const int64_t pos = P->step[VDC_STEP_POS], ctx = P->step[VDC_STEP_CTX];
         const int half = int(w & 1u), pair = int(w >> 1);
-        auto ld = [&](const char* base, int i) -> float {
-            return BF ? bf_lo(ldcg_u16(reinterpret_cast<const uint16_t*>(base) + i)) : ldcg_f32(reinterpret_cast<const float*>(base) + i);
-        };
-        float q[G][DPL], kn[DPL], vn[DPL];
+        const int rows_w = PR / 2;  // rows per warp (<= 32: one per lane)
+        // q of the group -> shared memory in the cache dtype, same 16-byte chunk
+        // layout as a K row: the rotated chunk reads of the score loop hit 8
+        // consecutive chunks per phase (bank-conflict free)
+        const uint32_t qs = smem_addr(S->u.att.qf);
         {
-            const char* qb = tptr(J.x_t) + size_t(J.x_off) * EB;
-            const char* kb = tptr(J.a_t) + (size_t(J.a_off) + size_t(pos) * HD) * EB;
-            const char* vb = tptr(J.b_t) + (size_t(J.b_off) + size_t(pos) * HD) * EB;
-#pragma unroll
-            for (int d = 0; d < DPL; ++d) {
-#pragma unroll
-                for (int h = 0; h < G; ++h) q[h][d] = ld(qb, h * HD + int(lane) * DPL + d);
-                kn[d] = ld(kb, int(lane) * DPL + d);
-                vn[d] = ld(vb, int(lane) * DPL + d);
-            }
+            const uint4* qb = reinterpret_cast<const uint4*>(tptr(J.x_t) + size_t(J.x_off) * EB);
+            uint4* qd = reinterpret_cast<uint4*>(S->u.att.qf);
+            for (int i = int(ct); i < G * NCH; i += NCT) qd[i] = ldcg128(qb + i);
         }
+        sync();
         float m[G], l[G], o[G][DPL];
 #pragma unroll
         for (int h = 0; h < G; ++h) {
@@ -623,7 +635,7 @@ struct Vcc {
             release(s0);
         }
         const uint32_t kt0 = kt + uint32_t(J.lead_pad);
-        const int my_row0 = half * (PR / 2);
+        const int my_row0 = half * rows_w;
         for (uint32_t i = 0; i < npages; ++i) {
             const uint32_t gk = kt0 + 2u * i;
             if (int((gk % CW) >> 1) != pair) continue;
@@ -633,95 +645,79 @@ struct Vcc {
                 ok = false;
                 return;
             }
-            const uint32_t kb = ring + sk * SLOT, vb = ring + sv * SLOT;
+            const bool ttr = P->tile_trace && sm == (P->debug >> 8) && gk < P->tile_trace_cap && lane == 0;
+            if (ttr) P->tile_trace[3 * (gk + half) + 1] = now_ns();
+            const uint32_t kb = ring + sk * SLOT + uint32_t(my_row0) * rowb, vb = ring + sv * SLOT + uint32_t(my_row0) * rowb;
             const int64_t prow0 = int64_t(J.r0 + int(i)) * PR + my_row0;  // global row of this warp's first row
-            // ---- scores: G batches of RB rows; lane l ends with (row l / G, head l % G) of each batch
-            float sc[G];
+            const bool fresh = pos >= prow0 && pos < prow0 + rows_w;
+            if (fresh) {
+                // the appended row was produced in this launch (after the page's
+                // bulk copy may have been issued): patch it into the slots
+                const int r = int(pos - prow0);
+                const char* kn = tptr(J.a_t) + (size_t(J.a_off) + size_t(pos) * HD) * EB;
+                const char* vn = tptr(J.b_t) + (size_t(J.b_off) + size_t(pos) * HD) * EB;
+                for (int c = int(lane); c < 2 * NCH; c += 32) {
+                    const bool isk = c < NCH;
+                    const int cc = isk ? c : c - NCH;
+                    const uint4 v = ldcg128(reinterpret_cast<const uint4*>(isk ? kn : vn) + cc);
+                    const uint32_t dst = (isk ? kb : vb) + uint32_t(r) * rowb + uint32_t(cc) * 16u;
+                    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(dst), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+                }
+                fence_proxy_async_smem();  // these generic writes precede the slot's next bulk refill
+                __syncwarp();
+            }
+            // ---- scores: lane = row; chunks rotated by lane (conflict-free K reads)
+            const bool valid = int(lane) < rows_w && prow0 + int(lane) < ctx;
+            float s[G];
 #pragma unroll
-            for (int b = 0; b < G; ++b) {
-                float part[32];
-#pragma unroll
-                for (int rr = 0; rr < RB; ++rr) {
-                    const int r = b * RB + rr;
-                    float kv[DPL];
-                    if (prow0 + r == pos) {
-#pragma unroll
-                        for (int d = 0; d < DPL; ++d) kv[d] = kn[d];
-                    } else {
-                        const uint32_t a = kb + uint32_t(my_row0 + r) * rowb + lane * uint32_t(DPL * EB);
-                        load_row<BF, DPL>(a, kv);
-                    }
+            for (int h = 0; h < G; ++h) s[h] = 0.f;
+            if (int(lane) < rows_w) {
+                const uint32_t krow = kb + lane * rowb;
+#pragma unroll 4
+                for (int c = 0; c < NCH; ++c) {
+                    const int cc = (c + int(lane)) & (NCH - 1);
+                    const uint4 kv = lds128(krow + uint32_t(cc) * 16u);
 #pragma unroll
                     for (int h = 0; h < G; ++h) {
-                        float acc = 0.f;
-#pragma unroll
-                        for (int d = 0; d < DPL; ++d) acc = fmaf(q[h][d], kv[d], acc);
-                        part[rr * G + h] = acc;
+                        const uint4 qv = lds128(qs + uint32_t(h * NCH + cc) * 16u);
+                        s[h] += dot16<BF>(qv, kv);
                     }
                 }
-                const float v = reduce_scatter32(part);
-                const int row = b * RB + int(lane) / G;
-                sc[b] = (prow0 + row < ctx) ? v * J.scale : -INFINITY;
             }
-            // ---- online softmax per head (lane l serves head l % G)
-            float mx = sc[0];
-#pragma unroll
-            for (int b = 1; b < G; ++b) mx = fmaxf(mx, sc[b]);
-#pragma unroll
-            for (int off = G; off < 32; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-            const int myh = int(lane) % G;
-            float mnew_mine = fmaxf(m[0], mx);
-            float mnew[G], corr[G];
+            // ---- online softmax per head over the warp's rows
+            float p[G];
 #pragma unroll
             for (int h = 0; h < G; ++h) {
-                const float mh = __shfl_sync(0xffffffffu, mx, h);
-                mnew[h] = fmaxf(m[h], mh);
-                corr[h] = (m[h] == -INFINITY || mnew[h] == -INFINITY) ? (m[h] == mnew[h] ? 1.f : 0.f) : expf(m[h] - mnew[h]);
-                if (h == myh) mnew_mine = mnew[h];
+                const float sc = valid ? s[h] * J.scale : -INFINITY;
+                const float mx = warp_max(sc);
+                const float mn = fmaxf(m[h], mx);
+                const float corr = (mn == -INFINITY) ? 1.f : (m[h] == -INFINITY ? 0.f : expf(m[h] - mn));
+                p[h] = valid ? expf(sc - mn) : 0.f;
+                l[h] = l[h] * corr + warp_sum(p[h]);
+                m[h] = mn;
+#pragma unroll
+                for (int d = 0; d < DPL; ++d) o[h][d] *= corr;
             }
-            float p[G], ps = 0.f;
-#pragma unroll
-            for (int b = 0; b < G; ++b) {
-                p[b] = sc[b] == -INFINITY ? 0.f : expf(sc[b] - mnew_mine);
-                ps += p[b];
-            }
-#pragma unroll
-            for (int off = G; off < 32; off <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
-#pragma unroll
-            for (int h = 0; h < G; ++h) {
-                l[h] = l[h] * corr[h] + __shfl_sync(0xffffffffu, ps, h);
-                m[h] = mnew[h];
-#pragma unroll
-                for (int d = 0; d < DPL; ++d) o[h][d] *= corr[h];
-            }
-            // ---- o += p V over this warp's rows
-#pragma unroll
-            for (int b = 0; b < G; ++b) {
+            // ---- o += p V (lanes own DPL dims)
+            const int nrow = int(ctx - prow0 < int64_t(rows_w) ? ctx - prow0 : int64_t(rows_w));
 #pragma unroll 4
-                for (int rr = 0; rr < RB; ++rr) {
-                    const int r = b * RB + rr;
-                    if (prow0 + r >= ctx) break;
-                    float vv[DPL];
-                    if (prow0 + r == pos) {
+            for (int r = 0; r < nrow; ++r) {
+                float vv[DPL];
+                load_row<BF, DPL>(vb + uint32_t(r) * rowb + lane * uint32_t(DPL * EB), vv);
 #pragma unroll
-                        for (int d = 0; d < DPL; ++d) vv[d] = vn[d];
-                    } else {
-                        load_row<BF, DPL>(vb + uint32_t(my_row0 + r) * rowb + lane * uint32_t(DPL * EB), vv);
-                    }
+                for (int h = 0; h < G; ++h) {
+                    const float ph = __shfl_sync(0xffffffffu, p[h], r);
 #pragma unroll
-                    for (int h = 0; h < G; ++h) {
-                        const float ph = __shfl_sync(0xffffffffu, p[b], rr * G + h);
-#pragma unroll
-                        for (int d = 0; d < DPL; ++d) o[h][d] = fmaf(ph, vv[d], o[h][d]);
-                    }
+                    for (int d = 0; d < DPL; ++d) o[h][d] = fmaf(ph, vv[d], o[h][d]);
                 }
             }
             // both warps of the pair are done with K and V: each returns its slot
+            if (ttr) P->tile_trace[3 * (gk + half) + 2] = now_ns();
             named_bar(2 + pair, 64);
             release(half ? sv : sk);
         }
         kt += ntiles;
-        // ---- merge the 8 warp states per head (slice order), write this split's partial
+        // ---- merge the 8 warp states per head (warp order), write this split's partial
         float* part = reinterpret_cast<float*>(tptr(J.o_t)) + J.o_off;
 #pragma unroll
         for (int h = 0; h < G; ++h) {
@@ -759,10 +755,9 @@ struct Vcc {
         }
         // ---- arrival: the last split of this kv head combines
         if (ct == 0) {
-            __threadfence();
-            const uint32_t old = atomicAdd(&P->counters[J.arrive_ctr], 1u);
+            uint32_t old;
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&P->counters[J.arrive_ctr]) : "memory");
             S->flag = (old + 1u == uint32_t(J.arrive_need) * P->epoch) ? 1 : 0;
-            __threadfence();
         }
         sync();
         if (!S->flag) return;
@@ -827,37 +822,47 @@ struct Vcc {
     __device__ void combine_head(const vdc_job& J, int h) {
         const int S2 = J.arrive_need, G = J.group;
         const float* part0 = reinterpret_cast<const float*>(tptr(J.o_t)) + (J.o_off - J.split * G * (HD + 2));
-        float M = -INFINITY;
-        for (int s0 = 0; s0 < S2; s0 += 32) {
-            const int s = s0 + int(lane);
-            if (s < S2) {
-                const float* pr = part0 + size_t(s * G + h) * (HD + 2);
-                const float ms = ldcg_f32(pr + HD), ls = ldcg_f32(pr + HD + 1);
-                if (ms != -INFINITY && ls > 0.f) M = fmaxf(M, ms);
-            }
-        }
-        M = warp_max(M);
-        float L = 0.f, O[DPL];
+        float M = -INFINITY, L = 0.f, O[DPL];
 #pragma unroll
         for (int d = 0; d < DPL; ++d) O[d] = 0.f;
         for (int s0 = 0; s0 < S2; s0 += 32) {
-            const int s = s0 + int(lane);
-            float wsum = 0.f, wl = 0.f;
-            if (s < S2) {
-                const float* pr = part0 + size_t(s * G + h) * (HD + 2);
-                const float ms = ldcg_f32(pr + HD), ls = ldcg_f32(pr + HD + 1);
-                wsum = (ms != -INFINITY && ls > 0.f) ? expf(ms - M) : 0.f;
-                wl = ls * wsum;
-            }
-            L += warp_sum(wl);
             const int n = min(32, S2 - s0);
-#pragma unroll 8
-            for (int k2 = 0; k2 < n; ++k2) {
-                const float wk = __shfl_sync(0xffffffffu, wsum, k2);
-                const float* pr = part0 + size_t((s0 + k2) * G + h) * (HD + 2) + lane * DPL;
-#pragma unroll
-                for (int d = 0; d < DPL; ++d) O[d] = fmaf(ldcg_f32(pr + d), wk, O[d]);
+            // all loads of this block of splits are independent: one L2 round trip
+            float ms = -INFINITY, ls = 0.f;
+            if (int(lane) < n) {
+                const float* pr = part0 + size_t((s0 + int(lane)) * G + h) * (HD + 2);
+                ms = ldcg_f32(pr + HD);
+                ls = ldcg_f32(pr + HD + 1);
             }
+            const bool ok_s = ms != -INFINITY && ls > 0.f;
+            const float bm = warp_max(ok_s ? ms : -INFINITY);
+            const float mn = fmaxf(M, bm);
+            if (mn == -INFINITY) continue;
+            const float a = M == -INFINITY ? 0.f : expf(M - mn);
+            const float ws = ok_s ? expf(ms - mn) : 0.f;
+            L = L * a + warp_sum(ls * ws);
+#pragma unroll
+            for (int d = 0; d < DPL; ++d) O[d] *= a;
+            // o slices in groups of 8 splits: 8 x DPL independent loads per round trip
+            for (int k0 = 0; k0 < n; k0 += 8) {
+                float ov[8][DPL];
+#pragma unroll
+                for (int k2 = 0; k2 < 8; ++k2) {
+                    const int kk = min(k0 + k2, n - 1);
+                    const float* pr = part0 + size_t((s0 + kk) * G + h) * (HD + 2) + lane * DPL;
+#pragma unroll
+                    for (int d = 0; d < DPL; ++d) ov[k2][d] = ldcg_f32(pr + d);
+                }
+#pragma unroll
+                for (int k2 = 0; k2 < 8; ++k2) {
+                    const float wk = __shfl_sync(0xffffffffu, ws, (k0 + k2) & 31);
+                    if (k0 + k2 < n) {
+#pragma unroll
+                        for (int d = 0; d < DPL; ++d) O[d] = fmaf(ov[k2][d], wk, O[d]);
+                    }
+                }
+            }
+            M = mn;
         }
         char* ob = tptr(J.o2_t);
         const bool obf = tdtype(J.o2_t) == VDC_DTYPE_BF16;
@@ -1027,14 +1032,7 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
     unsigned long long st_empty = 0, bytes = 0, uops = 0;
     const long long t_start = clock64();
     uint4 raw = issuer && g < ntiles ? __ldg(&P.words[w0 + g]) : make_uint4(0, 0, 0, 0);
-    if (issuer && PF)
-        for (uint32_t a = 1; a <= PF; ++a) {
-            const uint32_t ga = g + CW * a;
-            if (ga >= ntiles) break;
-            const Tile t = resolve_load(P, __ldg(&P.words[w0 + ga]));
-            if (!t.bad && !t.halt)
-                for (uint32_t q = 0; q < t.copies; ++q) prefetch_l2(t.src + size_t(q) * t.pitch, t.run);
-        }
+    uint32_t pf_g = g + CW * SP;  // next tile of this lane to prefetch into L2 (beyond its slots)
     long long idle_since = 0;
     unsigned long long t_idle = 0;
     for (;;) {
@@ -1063,17 +1061,19 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
                 bytes += t.bytes();
                 ++uops;
             }
-            if (PF) {
-                const uint32_t ga = g + CW * (PF + 1);
-                if (ga < ntiles) {
-                    const Tile ta = resolve_load(P, __ldg(&P.words[w0 + ga]));
-                    if (!ta.bad && !ta.halt)
-                        for (uint32_t q = 0; q < ta.copies; ++q) prefetch_l2(ta.src + size_t(q) * ta.pitch, ta.run);
-                }
-            }
             g += CW;
+            if (pf_g < g + CW * SP) pf_g = g + CW * SP;
             ++m;
             raw = g < ntiles ? __ldg(&P.words[w0 + g]) : make_uint4(0, 0, 0, 0);
+        }
+        if (PF && pending && !ready && pf_g < ntiles && pf_g < g + CW * (SP + PF)) {
+            // slot busy (the compute core is behind or waiting on a dependency):
+            // keep DRAM busy by pulling this lane's upcoming tiles into L2
+            const Tile ta = resolve_load(P, __ldg(&P.words[w0 + pf_g]));
+            if (!ta.bad && !ta.halt)
+                for (uint32_t q = 0; q < ta.copies; ++q) prefetch_l2(ta.src + size_t(q) * ta.pitch, ta.run);
+            pf_g += CW;
+            ready = true;  // made progress: skip the back-off
         }
         if (!__any_sync(0xffffffffu, ready)) {
             const long long now = clock64();

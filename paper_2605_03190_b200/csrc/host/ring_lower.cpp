@@ -137,16 +137,12 @@ class RingLowering {
                 plan_combine(n, ordinal);
                 break;
             case OpKind::EMBED_ROW: {
-                RJob r;
-                r.ordinal = ordinal;
-                r.sm = 0;
-                r.j = blank(Opcode::ELEMWISE);
-                r.j.flags = VDC_JOB_TOKEN_ROW;
+                // no µop: consumers read the embedding row in place (TOKEN_ROW /
+                // TOKEN_AUX operands), which removes one global dependency hop
                 const uint16_t tab = idx(n.inputs[0]);
-                r.j.x_t = storage(tab);
-                r.j.k = int32_t(desc_[tab].cols());
-                r.j.o_t = storage(idx(n.outputs[0]));
-                jobs_.push_back(std::move(r));
+                embed_out_ = storage(idx(n.outputs[0]));
+                embed_tab_ = storage(tab);
+                embed_len_ = int32_t(desc_[tab].cols());
                 break;
             }
             default:
@@ -213,6 +209,10 @@ class RingLowering {
                     j.tile_cols = int32_t(tc);
                     j.x_t = storage(idx(n.inputs[1]));
                     j.x_off = 0;
+                    if (j.x_t == embed_out_) {
+                        j.x_t = embed_tab_;
+                        j.flags |= VDC_JOB_TOKEN_ROW;
+                    }
                     if (xd.elem_count() != K) throw GeneratorError("node " + n.id + ": input length != reduction length");
                     if (n.kind == OpKind::RMS_GEMV) {
                         j.flags |= VDC_JOB_RMS;
@@ -222,6 +222,11 @@ class RingLowering {
                         j.flags |= VDC_JOB_RESID;
                         j.a_t = storage(idx(n.inputs[2]));
                         j.a_off = 0;
+                        if (j.a_t == embed_out_) {
+                            j.a_t = embed_tab_;
+                            j.flags |= VDC_JOB_TOKEN_AUX;
+                            j.cache_rows = embed_len_;
+                        }
                     }
                     j.o_t = storage(reg.out);
                     j.out_row0 = int32_t(reg.r0);
@@ -368,6 +373,7 @@ class RingLowering {
     }
 
     int32_t n_arrive_ = 0;
+    int32_t embed_out_ = -2, embed_tab_ = -1, embed_len_ = 0;
     struct AttnInfo {
         int64_t hkv = 0, splits = 1, grp = 1, hd = 0, jobs = 0;
     } attn_;
