@@ -1,0 +1,111 @@
+"""Device parity of the ring engine (the decode hot path: one persistent
+sm_100a kernel, include/uopsim/ring_abi.h) through the C-ABI.
+
+Checks, on identical synthetic inputs:
+  * against the dense numpy decode (tests/decode_ref.py; itself pinned to
+    the CPU oracle by test_decode_oracle.py): logits and the appended K/V
+    rows. Tolerances: fp32 model (C1 tiny) max|d| <= 1e-5 *
+    max|ref|; bf16 models max|d logits| <= 2e-2 * rms(ref logits), KV rows
+    rel <= 1e-2 (one bf16 ulp is 7.8e-3), argmax equal.
+  * against the CPU oracle interpreter running the reference-form µop
+    program of the same graph (oracle/_ref/oracle_interp): same bound.
+  * a multi-step decode (device KV cache carried across launches, positions
+    advancing) against the dense reference step by step.
+"""
+import numpy as np
+import pytest
+
+import decode_ref
+import harness
+import ring_cases as rc
+from paper_2605_03190_b200 import Program
+
+pytestmark = pytest.mark.gpu
+
+LLAMA_1L = {"model": {"preset": "llama3-8b", "layers": 1, "vocab": 32000},
+            "layout": {"ctx_pages": 16, "max_ctx": 1024, "pages_per_job": 4, "gu_block": 4}}
+
+
+def run(base, sms=None, steps=((17, 40),), seed=0):
+    from paper_2605_03190_b200.engine import Engine
+    import torch
+
+    req = rc.request(base, sms)
+    prog = Program.build(req)
+    info = prog.info()
+    ins = rc.synth_inputs(info, seed)
+    eng = Engine(prog, watchdog_ms=5000)
+    tens = eng.bind_inputs(ins)
+    st = torch.zeros(8, dtype=torch.int64, device="cuda")
+    eng.bind_step(st)
+    outs = []
+    state = {k: v.copy() for k, v in ins.items()}
+    for token, pos in steps:
+        st[0], st[1], st[2] = token, pos, pos + 1
+        rep = eng.run()
+        assert rep.status == 0, rep.message
+        host = {k: v.float().cpu().numpy() for k, v in tens.items()}
+        res = rc.check_against_dense(info, req, state, host, token, pos)
+        outs.append((res, host))
+        state = {k: v.copy() for k, v in host.items()}  # the device caches feed the next step
+    return info, req, ins, outs
+
+
+def assert_close(res, fp32):
+    if fp32:
+        assert res["logits_max_abs"] <= 1e-5 * res["logits_max"], res
+        assert res["kv_rel"] <= 1e-5, res
+    else:
+        assert res["logits_max_abs"] <= 2e-2 * res["logits_rms"], res
+        assert res["kv_rel"] <= 1e-2, res
+    assert res["argmax_equal"], res
+
+
+@pytest.mark.parametrize("sms", [4, 148])
+@pytest.mark.parametrize("token,pos", [(17, 40), (3, 0), (500, 63)])
+def test_tiny_fp32_matches_dense(cuda, sms, token, pos):
+    _, _, _, outs = run(rc.TINY, sms, ((token, pos),))
+    assert_close(outs[0][0], fp32=True)
+
+
+@pytest.mark.parametrize("token,pos", [(17, 300), (3, 0), (4095, 511)])
+def test_mid_bf16_matches_dense(cuda, token, pos):
+    _, _, _, outs = run(rc.MID, None, ((token, pos),))
+    assert_close(outs[0][0], fp32=False)
+
+
+def test_llama3_8b_layer_matches_dense(cuda):
+    _, _, _, outs = run(LLAMA_1L, None, ((1234, 777),))
+    assert_close(outs[0][0], fp32=False)
+
+
+def test_multi_step_decode_carries_the_kv_cache(cuda):
+    steps = [(17, 100), (5, 101), (99, 102), (7, 103)]
+    _, _, _, outs = run(rc.MID, None, steps)
+    for res, _ in outs:
+        assert_close(res, fp32=False)
+
+
+@pytest.mark.skipif(not harness.oracle_available(), reason="oracle/_ref not built")
+def test_tiny_matches_oracle_interpreter(cuda):
+    """ring device result vs the CPU oracle executing the reference-form
+    program (LOAD_WAIT/ALLOC/FREE/STORE streams + reference handlers)"""
+    token, pos = 21, 33
+    info, req, ins, outs = run(rc.TINY, None, ((token, pos),))
+    ref_req = {"model": req["model"], "layout": {k: v for k, v in req["layout"].items()},
+               "profile": {"builtin": "b200", "sm_count": 4}}
+    ref_req["layout"]["job_rows"] = 16
+    ref_prog = Program.build(ref_req)
+    rinfo = ref_prog.info()
+    names = [d["name"] for d in rinfo["descriptors"] if d["view_of"] < 0]
+    blob = b"".join(np.ascontiguousarray(ins[n], np.float32).tobytes() for n in names)
+    idx, _, ref_out = harness.run_oracle(ref_prog.text(True), step=[token, pos, pos + 1], inputs=blob)
+    assert idx["returncode"] == 0 and idx["completed"]
+    host = outs[0][1]
+    scale = np.abs(ref_out["logits"]).max()
+    assert np.abs(host["logits"] - ref_out["logits"]).max() <= 1e-5 * scale
+    for l in range(2):
+        for c in ("kc", "vc"):
+            a = host[f"L{l}.{c}"].reshape(4, 64, 64)[:, pos]
+            b = ref_out[f"L{l}.{c}"].reshape(4, 64, 64)[:, pos]
+            assert np.abs(a - b).max() <= 1e-5 * max(1.0, np.abs(b).max())
