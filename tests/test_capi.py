@@ -29,3 +29,11 @@ def test_errors_cross_the_boundary_as_status_codes():
     rc = _native.lib().vdc_program_build(json.dumps({"workload": {"tensors": [], "operators": []}, "profile": {"builtin": "nope"}}).encode(), ctypes.byref(h))
     assert rc == _native.VDC_ERR_INPUT
     assert _native.lib().vdc_last_error()
+
+
+def test_cpp_dropin_header_compiles(tmp_path):
+    """include/uopsim/machine.hpp (the reference executor API over the
+    C-ABI) builds against libvdc.so from a C++ caller (examples/)."""
+    import subprocess
+    r = subprocess.run(["make", "-B", "-C", str(ROOT / "examples"), "machine_demo"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]

@@ -109,3 +109,14 @@ def test_tiny_matches_oracle_interpreter(cuda):
             a = host[f"L{l}.{c}"].reshape(4, 64, 64)[:, pos]
             b = ref_out[f"L{l}.{c}"].reshape(4, 64, 64)[:, pos]
             assert np.abs(a - b).max() <= 1e-5 * max(1.0, np.abs(b).max())
+
+
+def test_cpp_machine_dropin_runs(cuda):
+    """the reference's simulate()/Machine call sites, unchanged, on the device"""
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    subprocess.run(["make", "-C", str(root / "examples"), "machine_demo"], check=True, capture_output=True)
+    r = subprocess.run([str(root / "examples" / "machine_demo")], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "fig4: status=completed" in r.stdout and "tiny decode (ring): status=completed" in r.stdout
