@@ -12,7 +12,7 @@ import os
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "lib" / "libvdc.so"
+LIB_PATH = Path(os.environ.get("VDC_LIB", str(PKG / "lib" / "libvdc.so")))  # VDC_LIB: A/B experiments only
 
 VDC_OK, VDC_ERR_INTERNAL, VDC_ERR_INPUT, VDC_ERR_DEADLOCK = 0, 1, 2, 3
 DTYPE = {"f32": 0, "bf16": 1, "i64": 2}

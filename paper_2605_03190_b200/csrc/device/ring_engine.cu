@@ -298,16 +298,19 @@ struct Vcc {
             rope_theta = J.theta;
             sync();
         }
-        const int cpt_all = J.tile_cols / (BF ? 8 : 4);
-        if (BF && J.tile_rows == 2 && cpt_all % 16 == 0)
-            tiles_mma<2>(J);
-        else if (BF && J.tile_rows == 4 && cpt_all % 8 == 0)
-            tiles_mma<4>(J);
-        else switch (J.tile_rows) {
-            case 1: tiles<BF, 1>(J); break;
-            case 2: tiles<BF, 2>(J); break;
-            case 4: tiles<BF, 4>(J); break;
-            default: tiles<BF, 8>(J); break;
+        if constexpr (BF) {
+            switch (J.tile_rows) {  // lowering guarantees 2/4/8-row tiles with 16 * (16 / TR) | chunks per row
+                case 2: tiles_mma<2>(J); break;
+                case 4: tiles_mma<4>(J); break;
+                default: tiles_mma<8>(J); break;
+            }
+        } else {
+            switch (J.tile_rows) {
+                case 1: tiles<false, 1>(J); break;
+                case 2: tiles<false, 2>(J); break;
+                case 4: tiles<false, 4>(J); break;
+                default: tiles<false, 8>(J); break;
+            }
         }
         if (!ok) return;
         sync();
@@ -364,6 +367,7 @@ struct Vcc {
             const uint32_t abase = ring + wslot * SLOT + a_lane;
             const uint32_t bbase = xb + uint32_t(c * cpt) * 16u + b_lane;
             float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
+            float d2[4] = {0.f, 0.f, 0.f, 0.f}, d3[4] = {0.f, 0.f, 0.f, 0.f};
             if (!(P->debug & 1u)) {
                 // groups of 4 k-steps: all fragment loads first, then the MMAs
                 // (volatile asm keeps program order, so the order is explicit)
@@ -381,7 +385,7 @@ struct Vcc {
                     }
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        float* d = (u & 1) ? d1 : d0;
+                        float* d = u == 0 ? d0 : u == 1 ? d1 : u == 2 ? d2 : d3;
                         asm volatile(
                             "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
                             "{%0,%1,%2,%3};"
@@ -407,8 +411,10 @@ struct Vcc {
             __syncwarp();
             if (ttr) P->tile_trace[3 * g + 2] = now_ns();
             if (lane == 0) mbar_arrive(&S->empty[wslot]);  // the tile goes back to the memory core
-            const float vlo = diag ? (odd ? d0[1] + d1[1] : d0[0] + d1[0]) : 0.f;
-            const float vhi = diag ? (odd ? d0[3] + d1[3] : d0[2] + d1[2]) : 0.f;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) d0[e] = (d0[e] + d1[e]) + (d2[e] + d3[e]);
+            const float vlo = diag ? (odd ? d0[1] : d0[0]) : 0.f;
+            const float vhi = diag ? (odd ? d0[3] : d0[2]) : 0.f;
 #pragma unroll
             for (int r = 0; r < TR; ++r) {
                 const float v = warp_sum((r_lo == r ? vlo : 0.f) + (r_hi == r ? vhi : 0.f));
@@ -918,12 +924,7 @@ __device__ void vcc_role(const RingParams& P, Shared& S, char* ring) {
     if (kbf == B && dpl == D && G == GG) { v.attn<B, D, GG>(J); break; }
                 VDC_ATTN_CASE(true, 4, 4)
                 VDC_ATTN_CASE(true, 4, 8)
-                VDC_ATTN_CASE(true, 4, 1)
-                VDC_ATTN_CASE(true, 4, 2)
                 VDC_ATTN_CASE(false, 2, 1)
-                VDC_ATTN_CASE(false, 2, 4)
-                VDC_ATTN_CASE(false, 4, 1)
-                VDC_ATTN_CASE(false, 4, 4)
 #undef VDC_ATTN_CASE
                 if (v.ct == 0) v.fire(6, (core << 16) | pc);  // unsupported head geometry
                 v.ok = false;

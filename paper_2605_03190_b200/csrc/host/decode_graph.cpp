@@ -73,7 +73,8 @@ std::pair<int64_t, int64_t> weight_tile(int64_t rows, int64_t cols, ElemType e, 
         }
         // rows longer than a slot: column chunks of 16/8/4 KB (a multiple of
         // the compute core's 256 x 16-byte stride), stacked 1/2/4 rows high
-        for (int64_t chunk = VDC_RING_SLOT_BYTES; chunk >= 4096; chunk /= 2)
+        // (prefer 8 KB x 2 rows: the tensor-core GEMV tiles take 2/4/8 rows)
+        for (int64_t chunk : {int64_t(8192), int64_t(4096), int64_t(VDC_RING_SLOT_BYTES)})
             if ((cols * eb) % chunk == 0) return {VDC_RING_SLOT_BYTES / chunk, chunk / eb};
         for (int64_t parts = (row_bytes + VDC_RING_SLOT_BYTES - 1) / VDC_RING_SLOT_BYTES; parts <= cols; ++parts)
             if (cols % parts == 0 && ((cols / parts) * eb) % 16 == 0) return {1, cols / parts};

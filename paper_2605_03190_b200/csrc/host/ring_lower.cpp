@@ -161,6 +161,11 @@ class RingLowering {
             throw GeneratorError("node " + n.id + ": weight tiles are not ring tiles (build the graph with layout.ring)");
         if (K > VDC_RING_MAX_K || (K * eb) % 16 || (tc * eb) % 16)
             throw GeneratorError("node " + n.id + ": reduction length unsupported by the ring engine");
+        if (wd.elem == workload::ElemType::bf16) {  // tensor-core tiles: 2/4/8 rows, whole k-steps of 16 * (16 / rows) chunks
+            const int64_t nc = 16 / std::max<int64_t>(1, tr), cpt = tc / 8;
+            if ((tr != 2 && tr != 4 && tr != 8) || cpt % (2 * nc))
+                throw GeneratorError("node " + n.id + ": bf16 weight tile shape unsupported by the tensor-core GEMV");
+        }
         const bool rope = attr_int(n, "rope", 0) != 0;
         const int64_t swiglu = attr_int(n, "swiglu", 0);
         int64_t unit = tr;
@@ -266,8 +271,11 @@ class RingLowering {
         const int64_t grp = desc_[q].tile_rows / hd;
         if (kd.tile_cols != hd || uint64_t(page_rows * hd * workload::elem_bytes(kd.elem)) > VDC_RING_SLOT_BYTES)
             throw GeneratorError("node " + n.id + ": KV pages do not fit a ring slot");
-        if (grp < 1 || grp > VDC_RING_COMPUTE_WARPS || VDC_RING_COMPUTE_WARPS % grp || hd % 32 || hd > 256)
-            throw GeneratorError("node " + n.id + ": unsupported GQA group / head dim for the ring engine");
+        const bool bf = kd.elem == workload::ElemType::bf16;
+        if (!(bf ? (hd == 128 && (grp == 4 || grp == 8)) : (hd == 64 && grp == 1)))
+            throw GeneratorError("node " + n.id + ": ring attention is built for bf16 head_dim 128 with GQA group 4/8 "
+                                 "and fp32 head_dim 64 with group 1");
+        if (page_rows != 64) throw GeneratorError("node " + n.id + ": ring attention pages are 64 rows");
         const int64_t pages = attr_int(n, "ctx_pages", 1), per = attr_int(n, "pages_per_job", 1);
         const int64_t splits = ceil_div(pages, per);
         int64_t k = 0;
