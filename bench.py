@@ -38,7 +38,7 @@ METRIC = "Llama-3-8B bf16 decode tokens/s (1/2/4/8 B200) + HBM GB/s fraction of 
 CTX = 4096
 
 
-def model_request(layers: int = 32, ctx: int = CTX, engine: str = "ring", ring_slots: int = 8,
+def model_request(layers: int = 32, ctx: int = CTX, engine: str = "ring", ring_slots: int = 12,
                   pages_per_job: int = 4) -> dict:
     pages = (ctx + 63) // 64
     if engine == "ring":
@@ -358,7 +358,7 @@ def main():
     ap.add_argument("--ctx", type=int, default=CTX)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--engine", default="ring", choices=["ring", "reference"])
-    ap.add_argument("--ring-slots", type=int, default=8)
+    ap.add_argument("--ring-slots", type=int, default=12)
     ap.add_argument("--pages-per-job", type=int, default=4)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -32,11 +32,11 @@
 #include <stdint.h>
 
 #define VDC_RING_SLOT_BYTES 16384
-#define VDC_RING_MAX_SLOTS 11  /* 11 x 16 KB ring + 32 KB staged x + scratch <= 227 KB */
+#define VDC_RING_MAX_SLOTS 12  /* 12 x 16 KB ring + 28 KB staged x + scratch <= 227 KB */
 #define VDC_RING_COMPUTE_WARPS 8
-#define VDC_RING_MAX_JOB_ROWS 256  /* output rows per GEMV job (smem partials) */
+#define VDC_RING_MAX_JOB_ROWS 128  /* output rows per GEMV job (smem partials) */
 #define VDC_RING_MAX_TILE_ROWS 8   /* W rows per ring tile */
-#define VDC_RING_MAX_K 16384       /* GEMV reduction length held in registers */
+#define VDC_RING_MAX_K 14336       /* GEMV reduction length (bf16) staged in shared memory */
 
 /* ATTN_DECODE in ring programs also performs the split-KV combine (the
  * reference-form ATTN_COMBINE): every split job writes its partial

@@ -2028,8 +2028,9 @@ int vdc_load_jobs(vdc_ctx* ctx, const vdc_job* jobs, uint32_t n_jobs, uint32_t r
     if (!ctx || !ctx->loaded) return fail(VDC_ERR_INPUT, "load the program words first");
     if (ctx->prof.slot_size != VDC_RING_SLOT_BYTES || ctx->prof.vcc_per_sm != 1)
         return fail(VDC_ERR_INPUT, "ring programs need a context with 16 KB slots and one VCC per SM");
-    if (ring_slots % VDC_RING_COMPUTE_WARPS || ring_slots > ctx->prof.slot_budget || ring_slots > VDC_RING_MAX_SLOTS)
-        return fail(VDC_ERR_INPUT, "ring_slots must be a multiple of 8 and <= min(slot_budget, VDC_RING_MAX_SLOTS)");
+    if (ring_slots < VDC_RING_COMPUTE_WARPS || ring_slots == VDC_RING_COMPUTE_WARPS + 1 || ring_slots > ctx->prof.slot_budget ||
+        ring_slots > VDC_RING_MAX_SLOTS)
+        return fail(VDC_ERR_INPUT, "ring_slots must be 8, 10, 11 or 12 (<= slot_budget)");
     for (uint32_t i = 0; i < n_jobs; ++i) {
         const vdc_job& j = jobs[i];
         for (int32_t t : {j.x_t, j.a_t, j.b_t, j.o_t})

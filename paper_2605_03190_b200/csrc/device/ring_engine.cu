@@ -46,7 +46,7 @@ constexpr int XBUF = VDC_RING_MAX_K * 2;  // bytes of the staged GEMV input vect
 constexpr int RMAX = VDC_RING_MAX_JOB_ROWS;
 constexpr uint32_t SLOT = VDC_RING_SLOT_BYTES;
 constexpr int BAR_VCC = 1;
-constexpr int MAX_HD = 256;
+constexpr int MAX_HD = 128;
 constexpr int MAX_DPL = MAX_HD / 32;
 
 enum : uint32_t {
@@ -60,13 +60,7 @@ enum : int { S_VMC_EMPTY = 0, S_VCC_FULL = 1, S_VCC_DEP = 2, S_VCC_EPI = 3, S_VC
 struct alignas(16) Shared {
     uint64_t full[VDC_RING_MAX_SLOTS];
     uint64_t empty[VDC_RING_MAX_SLOTS];
-    union {
-        float red[CW][RMAX];  // per-warp row partials of a GEMV job
-        struct {
-            float st[CW][2 + MAX_HD];   // per-warp online-softmax state (m, l, o)
-            float qf[1024];             // q heads of the group, fp32 (G x head_dim <= 1024)
-        } att;
-    } u;
+    float red[CW][RMAX];  // per-warp row partials of a GEMV job
     float bc[2 * CW];
     float rope_cs[MAX_HD / 2], rope_sn[MAX_HD / 2];  // rotary table of the launch's position
     int32_t flag;
@@ -349,14 +343,18 @@ struct Vcc {
         const bool diag = int(lane & 3u) == (c_lo >> 1);
         const bool odd = c_lo & 1;
         const int r_lo = (int(lane) >> 2) / NC, r_hi = ((int(lane) >> 2) + 8) / NC;
-        for (int i = int(lane); i < rows; i += 32) S->u.red[w][i] = 0.f;
+        for (int i = int(lane); i < rows; i += 32) S->red[w][i] = 0.f;
         __syncwarp();
-        int t = int((w + CW - kt % CW) % CW);
-        uint32_t g = kt + uint32_t(t);
-        const uint32_t SP = R / CW;
-        uint32_t wm = g / CW;
-        uint32_t wslot = w + CW * (wm % SP), wphase = (wm / SP) & 1u;
-        for (; t < ntiles; t += CW) {
+        uint32_t g = kt - 1u, gs = kt % R, gph = (kt / R) & 1u;
+        for (int t = 0; t < ntiles; ++t) {
+            // ring tile g lives in slot g % R and belongs to compute warp (g % R) % 8
+            const uint32_t wslot = gs, wphase = gph;
+            ++g;
+            if (++gs == R) {
+                gs = 0;
+                gph ^= 1u;
+            }
+            if ((wslot & uint32_t(CW - 1)) != w) continue;
             const int rg = t / tpr, c = t - rg * tpr;
             if (!wait_full(wslot, wphase)) {
                 ok = false;
@@ -418,12 +416,8 @@ struct Vcc {
 #pragma unroll
             for (int r = 0; r < TR; ++r) {
                 const float v = warp_sum((r_lo == r ? vlo : 0.f) + (r_hi == r ? vhi : 0.f));
-                if (lane == 0) S->u.red[w][rg * TR + r] += v;
+                if (lane == 0) S->red[w][rg * TR + r] += v;
             }
-            ++wm;
-            g += CW;
-            wslot = w + CW * (wm % SP);
-            wphase = (wm / SP) & 1u;
         }
         kt += uint32_t(ntiles);
     }
@@ -442,14 +436,18 @@ struct Vcc {
         const int rows = J.r1 - J.r0, ntiles = (rows / TR) * tpr;
         const uint32_t row_bytes = uint32_t(cpt) * 16u;
         const uint32_t xb = smem_addr(S->x);
-        for (int i = int(lane); i < rows; i += 32) S->u.red[w][i] = 0.f;
+        for (int i = int(lane); i < rows; i += 32) S->red[w][i] = 0.f;
         __syncwarp();
-        int t = int((w + CW - kt % CW) % CW);
-        uint32_t g = kt + uint32_t(t);
-        const uint32_t SP = R / CW;
-        uint32_t wm = g / CW;  // this warp's m-th tile
-        uint32_t wslot = w + CW * (wm % SP), wphase = (wm / SP) & 1u;
-        for (; t < ntiles; t += CW) {
+        uint32_t g = kt - 1u, gs = kt % R, gph = (kt / R) & 1u;
+        for (int t = 0; t < ntiles; ++t) {
+            // ring tile g lives in slot g % R and belongs to compute warp (g % R) % 8
+            const uint32_t wslot = gs, wphase = gph;
+            ++g;
+            if (++gs == R) {
+                gs = 0;
+                gph ^= 1u;
+            }
+            if ((wslot & uint32_t(CW - 1)) != w) continue;
             const int rg = t / tpr, c = t - rg * tpr;
             if (!wait_full(wslot, wphase)) {
                 ok = false;
@@ -460,10 +458,6 @@ struct Vcc {
             if (ttr) P->tile_trace[3 * g + 1] = now_ns();
             if (P->debug & 1u) {
                 release(wslot);
-                ++wm;
-                g += CW;
-                wslot = w + CW * (wm % SP);
-                wphase = (wm / SP) & 1u;
                 continue;
             }
             // two independent accumulators per row (even / odd chunk steps)
@@ -515,12 +509,8 @@ struct Vcc {
 #pragma unroll
             for (int r = 0; r < TR; ++r) {
                 const float v = warp_sum(acc[0][r] + acc[1][r]);
-                if (lane == 0) S->u.red[w][rg * TR + r] += v;
+                if (lane == 0) S->red[w][rg * TR + r] += v;
             }
-            ++wm;
-            g += CW;
-            wslot = w + CW * (wm % SP);
-            wphase = (wm / SP) & 1u;
         }
         kt += uint32_t(ntiles);
     }
@@ -528,7 +518,7 @@ struct Vcc {
     __device__ float row_sum(int i) const {
         float v = 0.f;
 #pragma unroll
-        for (int q = 0; q < CW; ++q) v += S->u.red[q][i];
+        for (int q = 0; q < CW; ++q) v += S->red[q][i];
         return v;
     }
 
@@ -579,14 +569,14 @@ struct Vcc {
     // ------------------------------------------------------ ATTN_DECODE
     // Split-KV q-len-1 attention of one kv head (G q heads) over pages
     // [r0, r1), fused with the split combine.
-    //  * page i = ring tiles (K, V) at global indices kt0 + 2i, kt0 + 2i + 1
-    //    (kt0 even: lead_pad pads the stream), i.e. in the slots of compute
-    //    warps 2p and 2p + 1 (p = pair); the pair splits the page's rows in
-    //    halves and each warp keeps its own online-softmax state.
-    //  * lanes split the head dim (DPL dims each); q and the appended K/V row
-    //    (produced in this launch by the qkv µop, read from global) sit in
-    //    registers; 32/G rows x G heads of partial dot products are reduced
-    //    across the warp with one butterfly reduce-scatter.
+    //  * page i = ring tiles (K, V) at global indices kt + 2i, kt + 2i + 1,
+    //    i.e. slots sk, sv owned by compute warps sk % 8 and sv % 8; that
+    //    pair splits the page's rows in halves (K owner: first half) and
+    //    each warp keeps its own online-softmax state.
+    //  * scores: a lane owns a row (q staged in shared memory in the cache
+    //    dtype, chunks rotated per lane: conflict free); P.V: lanes own head
+    //    dim slices. The appended K/V row was produced in this launch by the
+    //    qkv µop, so it is patched into the slots from global.
     //  * the 8 warp states are merged per head in shared memory and written
     //    as this split's partial; the last split of the kv head to arrive
     //    (per-head arrival counter) merges all partials in split order and
@@ -604,15 +594,15 @@ struct Vcc {
         const int PR = J.tile_rows;
         const uint32_t rowb = uint32_t(HD * EB);
         const int64_t pos = P->step[VDC_STEP_POS], ctx = P->step[VDC_STEP_CTX];
-        const int half = int(w & 1u), pair = int(w >> 1);
         const int rows_w = PR / 2;  // rows per warp (<= 32: one per lane)
         // q of the group -> shared memory in the cache dtype, same 16-byte chunk
         // layout as a K row: the rotated chunk reads of the score loop hit 8
         // consecutive chunks per phase (bank-conflict free)
-        const uint32_t qs = smem_addr(S->u.att.qf);
+        xk_t = -2;  // the staged-x buffer holds q (and the merge scratch) now
+        const uint32_t qs = smem_addr(S->x);
         {
             const uint4* qb = reinterpret_cast<const uint4*>(tptr(J.x_t) + size_t(J.x_off) * EB);
-            uint4* qd = reinterpret_cast<uint4*>(S->u.att.qf);
+            uint4* qd = S->x;
             for (int i = int(ct); i < G * NCH; i += NCT) qd[i] = ldcg128(qb + i);
         }
         sync();
@@ -624,29 +614,14 @@ struct Vcc {
 #pragma unroll
             for (int d = 0; d < DPL; ++d) o[h][d] = 0.f;
         }
-        const uint32_t SP = R / CW;
-        auto slot_of = [&](uint32_t g, uint32_t& par) {
-            const uint32_t mm = g / CW;
-            par = (mm / SP) & 1u;
-            return g % CW + CW * (mm % SP);
-        };
-        const uint32_t npages = uint32_t(J.r1 - J.r0), ntiles = uint32_t(J.lead_pad) + 2u * npages;
-        if (J.lead_pad && (kt % CW) == w) {  // padding tile: wait for it and hand it back
-            uint32_t par;
-            const uint32_t s0 = slot_of(kt, par);
-            if (!wait_full(s0, par)) {
-                ok = false;
-                return;
-            }
-            release(s0);
-        }
-        const uint32_t kt0 = kt + uint32_t(J.lead_pad);
-        const int my_row0 = half * rows_w;
+        const uint32_t npages = uint32_t(J.r1 - J.r0), ntiles = 2u * npages;
         for (uint32_t i = 0; i < npages; ++i) {
-            const uint32_t gk = kt0 + 2u * i;
-            if (int((gk % CW) >> 1) != pair) continue;
-            uint32_t pk, pv;
-            const uint32_t sk = slot_of(gk, pk), sv = slot_of(gk + 1u, pv);
+            const uint32_t gk = kt + 2u * i;
+            const uint32_t sk = gk % R, pk = (gk / R) & 1u, sv = (gk + 1u) % R, pv = ((gk + 1u) / R) & 1u;
+            const uint32_t ok_k = sk & uint32_t(CW - 1), ok_v = sv & uint32_t(CW - 1);
+            if (w != ok_k && w != ok_v) continue;
+            const int half = w == ok_v ? 1 : 0;
+            const int my_row0 = half * rows_w;
             if (!wait_full(sk, pk) || !wait_full(sv, pv)) {
                 ok = false;
                 return;
@@ -719,30 +694,42 @@ struct Vcc {
             }
             // both warps of the pair are done with K and V: each returns its slot
             if (ttr) P->tile_trace[3 * (gk + half) + 2] = now_ns();
-            named_bar(2 + pair, 64);
+            // both owners are done with K and V: each returns its slot. Named
+            // barrier per owner pair: (w, w+1) -> 2 + w; the wrap pair of the
+            // last slot (owner (R-1) % 8) with slot 0 -> 10
+            named_bar(ok_v == ((ok_k + 1u) & uint32_t(CW - 1)) ? 2 + int(ok_k) : 10, 64);
             release(half ? sv : sk);
         }
         kt += ntiles;
-        // ---- merge the 8 warp states per head (warp order), write this split's partial
+        // ---- merge the 8 warp states per head (warp order), write this split's partial;
+        // scratch = the staged-x buffer, up to 4 heads per round (2 barriers per round)
         float* part = reinterpret_cast<float*>(tptr(J.o_t)) + J.o_off;
+        float* scr = reinterpret_cast<float*>(S->x) + G * HD;  // after the staged q
+        constexpr int HPR = G < 4 ? G : 4;
+        constexpr int SST = HD + 2;
 #pragma unroll
-        for (int h = 0; h < G; ++h) {
-            float* st = S->u.att.st[w];
-            if (lane == 0) {
-                st[0] = m[h];
-                st[1] = l[h];
+        for (int h0 = 0; h0 < G; h0 += HPR) {
+#pragma unroll
+            for (int hh = 0; hh < HPR; ++hh) {
+                float* st = scr + (size_t(hh) * CW + w) * SST;
+                if (lane == 0) {
+                    st[0] = m[h0 + hh];
+                    st[1] = l[h0 + hh];
+                }
+#pragma unroll
+                for (int d = 0; d < DPL; ++d) st[2 + lane * DPL + d] = o[h0 + hh][d];
             }
-#pragma unroll
-            for (int d = 0; d < DPL; ++d) st[2 + lane * DPL + d] = o[h][d];
             sync();
-            if (int(w) == h % CW) {
+            if (int(w) < HPR) {
+                const int h = h0 + int(w);
+                const float* base = scr + size_t(w) * CW * SST;
                 float M = -INFINITY;
-                for (int q2 = 0; q2 < CW; ++q2) M = fmaxf(M, S->u.att.st[q2][0]);
+                for (int q2 = 0; q2 < CW; ++q2) M = fmaxf(M, base[q2 * SST]);
                 float L = 0.f, O[DPL];
 #pragma unroll
                 for (int d = 0; d < DPL; ++d) O[d] = 0.f;
                 for (int q2 = 0; q2 < CW; ++q2) {
-                    const float* t = S->u.att.st[q2];
+                    const float* t = base + q2 * SST;
                     if (t[0] == -INFINITY) continue;
                     const float f = expf(t[0] - M);
                     L = fmaf(t[1], f, L);
@@ -1024,16 +1011,16 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t core = 2 * blockIdx.x;
     const uint32_t w0 = P.core_off[core], n = P.core_off[core + 1] - w0;
-    const uint32_t SP = P.ring_slots / CW;  // slots per issuing lane
+    const uint32_t R = P.ring_slots;
     const uint32_t PF = P.prefetch;
     // the stream is LOAD words followed by one HALT
     const uint32_t ntiles = n && ((__ldg(&P.words[w0 + n - 1]).x & 0xff) == OP_HALT) ? n - 1 : n;
-    const bool issuer = lane < uint32_t(CW);
-    uint32_t g = lane, m = 0;
+    const bool issuer = lane < R;
+    uint32_t g = lane, m = 0;  // lane s issues tiles s, s + R, s + 2R, ... into slot s
     unsigned long long st_empty = 0, bytes = 0, uops = 0;
     const long long t_start = clock64();
     uint4 raw = issuer && g < ntiles ? __ldg(&P.words[w0 + g]) : make_uint4(0, 0, 0, 0);
-    uint32_t pf_g = g + CW * SP;  // next tile of this lane to prefetch into L2 (beyond its slots)
+    uint32_t pf_g = g + R;  // next tile of this lane to prefetch into L2 (beyond its slot)
     long long idle_since = 0;
     unsigned long long t_idle = 0;
     for (;;) {
@@ -1042,8 +1029,8 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
         bool ready = false;
         uint32_t slot = 0;
         if (pending) {
-            slot = lane + CW * (m % SP);
-            ready = m < SP || mbar_test(&S.empty[slot], ((m / SP) - 1u) & 1u);
+            slot = lane;
+            ready = m == 0 || mbar_test(&S.empty[slot], (m - 1u) & 1u);
         }
         if (ready) {
             const Tile t = resolve_load(P, raw);
@@ -1062,18 +1049,18 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
                 bytes += t.bytes();
                 ++uops;
             }
-            g += CW;
-            if (pf_g < g + CW * SP) pf_g = g + CW * SP;
+            g += R;
+            if (pf_g < g + R) pf_g = g + R;
             ++m;
             raw = g < ntiles ? __ldg(&P.words[w0 + g]) : make_uint4(0, 0, 0, 0);
         }
-        if (PF && pending && !ready && pf_g < ntiles && pf_g < g + CW * (SP + PF)) {
+        if (PF && pending && !ready && pf_g < ntiles && pf_g < g + R * (1 + PF)) {
             // slot busy (the compute core is behind or waiting on a dependency):
             // keep DRAM busy by pulling this lane's upcoming tiles into L2
             const Tile ta = resolve_load(P, __ldg(&P.words[w0 + pf_g]));
             if (!ta.bad && !ta.halt)
                 for (uint32_t q = 0; q < ta.copies; ++q) prefetch_l2(ta.src + size_t(q) * ta.pitch, ta.run);
-            pf_g += CW;
+            pf_g += R;
             ready = true;  // made progress: skip the back-off
         }
         if (!__any_sync(0xffffffffu, ready)) {

@@ -130,7 +130,7 @@ ProgramBox* build(const std::string& request) {
     for (const auto& n : g.nodes) decode_graph = decode_graph || workload::is_decode_kind(n.kind);
     std::map<std::string, workload::TilingChoice> tilings;
     if (decode_graph && ring) {
-        box->program = generator::lower_decode_ring(g, hw, opt, req.value("ring_slots", 8));
+        box->program = generator::lower_decode_ring(g, hw, opt, req.value("ring_slots", 12));
         const auto v = generator::validate_ring_program(box->program);
         if (!v.empty()) throw generator::GeneratorError("ring program invalid: " + v.front().message);
     } else if (decode_graph) {

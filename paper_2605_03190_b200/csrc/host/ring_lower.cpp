@@ -159,7 +159,7 @@ class RingLowering {
         const int64_t eb = workload::elem_bytes(wd.elem);
         if (K % tc || 8 % tr || uint64_t(tr * tc * eb) > VDC_RING_SLOT_BYTES)
             throw GeneratorError("node " + n.id + ": weight tiles are not ring tiles (build the graph with layout.ring)");
-        if (K > VDC_RING_MAX_K || (K * eb) % 16 || (tc * eb) % 16)
+        if (K * eb > 2 * VDC_RING_MAX_K || (K * eb) % 16 || (tc * eb) % 16)
             throw GeneratorError("node " + n.id + ": reduction length unsupported by the ring engine");
         if (wd.elem == workload::ElemType::bf16) {  // tensor-core tiles: 2/4/8 rows, whole k-steps of 16 * (16 / rows) chunks
             const int64_t nc = 16 / std::max<int64_t>(1, tr), cpt = tc / 8;
@@ -343,11 +343,6 @@ class RingLowering {
             size_t tiles_so_far = 0;
             for (size_t ji : per_sm[s]) {
                 RJob r = jobs_[ji];
-                if (r.j.op == int32_t(Opcode::ATTN_DECODE) && (tiles_so_far & 1)) {
-                    // K pages must start on an even ring index (warp pairs): pad
-                    r.j.lead_pad = 1;
-                    r.tiles.insert(r.tiles.begin(), r.tiles.front());
-                }
                 tiles_so_far += r.tiles.size();
                 const int32_t slot = int32_t(p.jobs.size());
                 p.jobs.push_back(r.j);
@@ -391,11 +386,13 @@ class RingLowering {
 
 LoweredProgram lower_decode_ring(const workload::OperatorGraph& g, const costmodel::HardwareProfile& hw, const GenOptions& opt,
                                  int ring_slots) {
-    // ring tile g is consumed by compute warp g % 8, so every slot must have a
-    // single consumer warp (a slot shared by two warps could be waited on one
-    // phase ahead, which mbarrier parity waits cannot distinguish)
-    if (ring_slots % VDC_RING_COMPUTE_WARPS || ring_slots > VDC_RING_MAX_SLOTS)
-        throw GeneratorError("ring_slots must be a multiple of 8 (one consumer warp per slot) and <= the smem limit");
+    // ring tile g lives in slot g % R and is consumed by compute warp
+    // (g % R) % 8: every slot has a single consumer warp (a slot shared by
+    // two warps could be waited on one phase ahead, which mbarrier parity
+    // waits cannot distinguish); R = 9 would give an attention page's K and
+    // V slots the same owner
+    if (ring_slots < VDC_RING_COMPUTE_WARPS || ring_slots > VDC_RING_MAX_SLOTS || ring_slots == VDC_RING_COMPUTE_WARPS + 1)
+        throw GeneratorError("ring_slots must be 8, 10, 11 or 12");
     return RingLowering(g, hw, ring_slots).run(opt);
 }
 

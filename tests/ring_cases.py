@@ -13,7 +13,7 @@ MID = {"model": {"preset": "llama3-8b", "layers": 2, "hidden": 1024, "heads": 8,
        "layout": {"ctx_pages": 8, "max_ctx": 512, "pages_per_job": 2, "gu_block": 4}}
 
 
-def request(base: dict, sm_count: int | None = None, ring_slots: int = 8) -> dict:
+def request(base: dict, sm_count: int | None = None, ring_slots: int = 12) -> dict:
     r = {"engine": "ring", "model": dict(base["model"]), "layout": dict(base["layout"]), "ring_slots": ring_slots,
          "profile": {"builtin": "b200"}}
     if sm_count:

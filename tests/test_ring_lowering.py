@@ -94,8 +94,9 @@ def test_ring_balance(name):
         assert (max(loads) - min(loads)) / mean < 0.05, (min(loads), max(loads), mean)
 
 
-def test_ring_slots_must_be_a_multiple_of_the_compute_warps():
-    req = dict(CASES["tiny"], ring_slots=6)
+@pytest.mark.parametrize("slots", [6, 9, 13])
+def test_ring_slots_give_every_slot_one_consumer_warp(slots):
+    req = dict(CASES["tiny"], ring_slots=slots)
     with pytest.raises(VdcError):
         Program.build(req)
 

@@ -6,7 +6,7 @@ import bench
 from paper_2605_03190_b200 import Program
 from paper_2605_03190_b200.engine import Engine
 layers = int(sys.argv[1]) if len(sys.argv) > 1 else 32
-slots = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+slots = int(sys.argv[2]) if len(sys.argv) > 2 else 12
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 200
 prog = Program.build(bench.model_request(layers, ring_slots=slots))
 eng = Engine(prog, watchdog_ms=2000)
