@@ -127,6 +127,7 @@ struct Vcc {
     bool ok = true;
     unsigned long long st_full = 0, st_dep = 0, st_epi = 0;
     unsigned long long t_ready = 0;  // trace: when the last readiness wait of the running µop completed
+    uint32_t n_attn = 0;             // debug stamps
     float resid = 0.f;               // GEMV_ADD: this thread's residual element, loaded before the tile sweep
     int32_t rope_hd = 0;             // head dim of the cached rotary table (0 = none)
     float rope_theta = 0.f;
@@ -570,9 +571,10 @@ struct Vcc {
     // Split-KV q-len-1 attention of one kv head (G q heads) over pages
     // [r0, r1), fused with the split combine.
     //  * page i = ring tiles (K, V) at global indices kt + 2i, kt + 2i + 1,
-    //    i.e. slots sk, sv owned by compute warps sk % 8 and sv % 8; that
-    //    pair splits the page's rows in halves (K owner: first half) and
-    //    each warp keeps its own online-softmax state.
+    //    processed by warp pair i mod 4 (rows split in halves, each warp
+    //    keeps its own online softmax). The job's tiles (<= ring depth) were
+    //    issued after every earlier tile was released, so any warp may wait
+    //    on their slots' next phase; each warp of the pair hands one slot back.
     //  * scores: a lane owns a row (q staged in shared memory in the cache
     //    dtype, chunks rotated per lane: conflict free); P.V: lanes own head
     //    dim slices. The appended K/V row was produced in this launch by the
@@ -582,15 +584,20 @@ struct Vcc {
     //    (per-head arrival counter) merges all partials in split order and
     //    publishes the head's attention output (reference finalize,
     //    handlers.cpp:155-168).
+    __device__ void astamp(int ev) {
+        if (P->tile_trace && sm == (P->debug >> 8) && ct == 0) P->tile_trace[60000 + 8 * (n_attn & 7) + ev] = now_ns();
+    }
     template <bool BF, int DPL, int G>
     __device__ void attn(const vdc_job& J) {
         constexpr int EB = BF ? 2 : 4;
+        astamp(0);
         constexpr int HD = 32 * DPL;
         constexpr int NCH = HD * EB / 16;  // 16-byte chunks per K/V row
         if (!wait_ready(J.x_t, J.x_need, J.a_t, J.a_need, J.b_t, J.b_need)) {
             ok = false;
             return;
         }
+        astamp(1);
         const int PR = J.tile_rows;
         const uint32_t rowb = uint32_t(HD * EB);
         const int64_t pos = P->step[VDC_STEP_POS], ctx = P->step[VDC_STEP_CTX];
@@ -618,9 +625,12 @@ struct Vcc {
         for (uint32_t i = 0; i < npages; ++i) {
             const uint32_t gk = kt + 2u * i;
             const uint32_t sk = gk % R, pk = (gk / R) & 1u, sv = (gk + 1u) % R, pv = ((gk + 1u) / R) & 1u;
-            const uint32_t ok_k = sk & uint32_t(CW - 1), ok_v = sv & uint32_t(CW - 1);
-            if (w != ok_k && w != ok_v) continue;
-            const int half = w == ok_v ? 1 : 0;
+            // page i -> warp pair i mod 4 (balanced over the 8 warps); the
+            // job's tiles (<= ring depth) were issued after every earlier
+            // tile was released, so any warp may wait on their slots
+            const uint32_t pair = i % uint32_t(CW / 2);
+            if ((w >> 1) != pair) continue;
+            const int half = int(w & 1u);
             const int my_row0 = half * rows_w;
             if (!wait_full(sk, pk) || !wait_full(sv, pv)) {
                 ok = false;
@@ -694,13 +704,12 @@ struct Vcc {
             }
             // both warps of the pair are done with K and V: each returns its slot
             if (ttr) P->tile_trace[3 * (gk + half) + 2] = now_ns();
-            // both owners are done with K and V: each returns its slot. Named
-            // barrier per owner pair: (w, w+1) -> 2 + w; the wrap pair of the
-            // last slot (owner (R-1) % 8) with slot 0 -> 10
-            named_bar(ok_v == ((ok_k + 1u) & uint32_t(CW - 1)) ? 2 + int(ok_k) : 10, 64);
+            named_bar(2 + int(pair), 64);  // the pair is done with K and V
             release(half ? sv : sk);
         }
         kt += ntiles;
+        sync();
+        astamp(3);
         // ---- merge the 8 warp states per head (warp order), write this split's partial;
         // scratch = the staged-x buffer, up to 4 heads per round (2 barriers per round)
         float* part = reinterpret_cast<float*>(tptr(J.o_t)) + J.o_off;
@@ -746,15 +755,34 @@ struct Vcc {
             }
             sync();
         }
-        // ---- arrival: the last split of this kv head combines
+        astamp(4);
+        // ---- arrival: the last split of this kv head combines (the
+        // reference-form ATTN_COMBINE, fused: saves one dependency hop)
         if (ct == 0) {
             uint32_t old;
             asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&P->counters[J.arrive_ctr]) : "memory");
             S->flag = (old + 1u == uint32_t(J.arrive_need) * P->epoch) ? 1 : 0;
         }
         sync();
+        ++n_attn;
         if (!S->flag) return;
         if (int(w) < G) combine_head<DPL, HD>(J, int(w));
+        publish(J.o2_t);
+    }
+
+    // ATTN_COMBINE as a separate µop (waits for all splits of a kv head on its
+    // arrival counter); ring programs fuse it into ATTN_DECODE by default
+    __device__ void combine(const vdc_job& J) {
+        if (!wait_ready(J.arrive_ctr, J.arrive_need, -1, 0, -1, 0)) {
+            ok = false;
+            return;
+        }
+        if (int(w) < J.group) {
+            if (J.head_dim == 128)
+                combine_head<4, 128>(J, int(w));
+            else
+                combine_head<2, 64>(J, int(w));
+        }
         publish(J.o2_t);
     }
 
@@ -814,18 +842,30 @@ struct Vcc {
     template <int DPL, int HD>
     __device__ void combine_head(const vdc_job& J, int h) {
         const int S2 = J.arrive_need, G = J.group;
+        // split 0 of this kv head's partials
         const float* part0 = reinterpret_cast<const float*>(tptr(J.o_t)) + (J.o_off - J.split * G * (HD + 2));
         float M = -INFINITY, L = 0.f, O[DPL];
 #pragma unroll
         for (int d = 0; d < DPL; ++d) O[d] = 0.f;
-        for (int s0 = 0; s0 < S2; s0 += 32) {
-            const int n = min(32, S2 - s0);
-            // all loads of this block of splits are independent: one L2 round trip
+        constexpr int SB = 16;  // splits per block: every load of a block is issued before any is used
+        for (int s0 = 0; s0 < S2; s0 += SB) {
+            const int n = min(SB, S2 - s0);
             float ms = -INFINITY, ls = 0.f;
             if (int(lane) < n) {
                 const float* pr = part0 + size_t((s0 + int(lane)) * G + h) * (HD + 2);
                 ms = ldcg_f32(pr + HD);
                 ls = ldcg_f32(pr + HD + 1);
+            }
+            float4 ov[SB];
+#pragma unroll
+            for (int k2 = 0; k2 < SB; ++k2) {
+                const int kk = min(k2, n - 1);
+                const float* pr = part0 + size_t((s0 + kk) * G + h) * (HD + 2) + lane * DPL;
+                if constexpr (DPL == 4) {
+                    ov[k2] = make_float4(ldcg_f32(pr), ldcg_f32(pr + 1), ldcg_f32(pr + 2), ldcg_f32(pr + 3));
+                } else {
+                    ov[k2] = make_float4(ldcg_f32(pr), DPL > 1 ? ldcg_f32(pr + 1) : 0.f, 0.f, 0.f);
+                }
             }
             const bool ok_s = ms != -INFINITY && ls > 0.f;
             const float bm = warp_max(ok_s ? ms : -INFINITY);
@@ -836,23 +876,13 @@ struct Vcc {
             L = L * a + warp_sum(ls * ws);
 #pragma unroll
             for (int d = 0; d < DPL; ++d) O[d] *= a;
-            // o slices in groups of 8 splits: 8 x DPL independent loads per round trip
-            for (int k0 = 0; k0 < n; k0 += 8) {
-                float ov[8][DPL];
 #pragma unroll
-                for (int k2 = 0; k2 < 8; ++k2) {
-                    const int kk = min(k0 + k2, n - 1);
-                    const float* pr = part0 + size_t((s0 + kk) * G + h) * (HD + 2) + lane * DPL;
+            for (int k2 = 0; k2 < SB; ++k2) {
+                const float wk = __shfl_sync(0xffffffffu, ws, k2);
+                if (k2 < n) {
+                    const float v[4] = {ov[k2].x, ov[k2].y, ov[k2].z, ov[k2].w};
 #pragma unroll
-                    for (int d = 0; d < DPL; ++d) ov[k2][d] = ldcg_f32(pr + d);
-                }
-#pragma unroll
-                for (int k2 = 0; k2 < 8; ++k2) {
-                    const float wk = __shfl_sync(0xffffffffu, ws, (k0 + k2) & 31);
-                    if (k0 + k2 < n) {
-#pragma unroll
-                        for (int d = 0; d < DPL; ++d) O[d] = fmaf(ov[k2][d], wk, O[d]);
-                    }
+                    for (int d = 0; d < DPL; ++d) O[d] = fmaf(v[d], wk, O[d]);
                 }
             }
             M = mn;
@@ -917,6 +947,7 @@ __device__ void vcc_role(const RingParams& P, Shared& S, char* ring) {
                 v.ok = false;
                 break;
             }
+            case OP_ATTN_COMBINE: v.combine(J); break;
             case OP_ELEMWISE: v.copy_row(J); break;
             default:
                 if (v.ct == 0) v.fire(4, (core << 16) | pc);

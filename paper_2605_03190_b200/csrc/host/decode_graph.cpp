@@ -61,21 +61,20 @@ std::pair<int64_t, int64_t> weight_tile(int64_t rows, int64_t cols, ElemType e, 
     (void)rows;
     const int64_t eb = workload::elem_bytes(e);
     if (l.ring) {
-        // ring mode: every tile is one contiguous run of <= one slot, so the
-        // memory core moves it with a single cp.async.bulk: whole rows
-        // (power-of-two count <= VDC_RING_MAX_TILE_ROWS) when a row fits the
-        // slot, else equal column chunks of one row (multiples of 16 bytes)
+        // ring mode: tiles of <= one ring slot moved by bulk copies. Rows of
+        // <= 8 KB: whole rows (power-of-two count <= VDC_RING_MAX_TILE_ROWS,
+        // one contiguous copy). Longer rows: 2-row tiles of equal column
+        // chunks (one copy per row), chunk a multiple of 128 elements so the
+        // tensor-core GEMV's 16-chunk k-steps divide it; 2-row units keep the
+        // per-SM split of an operator fine grained (+-1 unit of 2 rows).
         const int64_t row_bytes = cols * eb;
-        if (row_bytes <= VDC_RING_SLOT_BYTES) {
+        if (row_bytes <= VDC_RING_SLOT_BYTES / 2) {
             int64_t tr = 1;
             while (tr * 2 <= VDC_RING_MAX_TILE_ROWS && tr * 2 * row_bytes <= VDC_RING_SLOT_BYTES) tr *= 2;
             return {tr, cols};
         }
-        // rows longer than a slot: column chunks of 16/8/4 KB (a multiple of
-        // the compute core's 256 x 16-byte stride), stacked 1/2/4 rows high
-        // (prefer 8 KB x 2 rows: the tensor-core GEMV tiles take 2/4/8 rows)
-        for (int64_t chunk : {int64_t(8192), int64_t(4096), int64_t(VDC_RING_SLOT_BYTES)})
-            if ((cols * eb) % chunk == 0) return {VDC_RING_SLOT_BYTES / chunk, chunk / eb};
+        for (int64_t parts = (2 * row_bytes + VDC_RING_SLOT_BYTES - 1) / VDC_RING_SLOT_BYTES; parts <= cols; ++parts)
+            if (cols % parts == 0 && (cols / parts) % 128 == 0) return {2, cols / parts};
         for (int64_t parts = (row_bytes + VDC_RING_SLOT_BYTES - 1) / VDC_RING_SLOT_BYTES; parts <= cols; ++parts)
             if (cols % parts == 0 && ((cols / parts) * eb) % 16 == 0) return {1, cols / parts};
         throw workload::WorkloadError("no ring tiling for a row of " + std::to_string(cols) + " elements");

@@ -277,6 +277,10 @@ class RingLowering {
                                  "and fp32 head_dim 64 with group 1");
         if (page_rows != 64) throw GeneratorError("node " + n.id + ": ring attention pages are 64 rows");
         const int64_t pages = attr_int(n, "ctx_pages", 1), per = attr_int(n, "pages_per_job", 1);
+        // all of a job's K/V tiles must fit the ring at once: the engine lets
+        // any warp wait on them (the page -> warp-pair map ignores slot owners)
+        if (2 * std::min(pages, per) > ring_slots_)
+            throw GeneratorError("node " + n.id + ": 2 * pages_per_job must not exceed ring_slots");
         const int64_t splits = ceil_div(pages, per);
         int64_t k = 0;
         for (int64_t h = 0; h < hkv; ++h) {
@@ -318,8 +322,10 @@ class RingLowering {
         attn_ = {hkv, splits, grp, hd, k};
     }
 
-    // ring mode fuses the combine into the attention jobs (last arriver per kv
-    // head merges); the node only names the output the combiner writes
+    // ring mode fuses the combine into the attention jobs (the last split of
+    // each kv head to arrive merges, saving one dependency hop); the node
+    // names the output the combiner writes. Combine µops use the same
+    // operand layout (o_t/o_off = partials of the head, o2 = output).
     void plan_combine(const workload::OperatorNode& n, uint32_t ordinal) {
         (void)ordinal;
         const int32_t part = storage(idx(n.inputs[0])), out = storage(idx(n.outputs[0]));

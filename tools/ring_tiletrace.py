@@ -30,3 +30,14 @@ gaps = np.diff(np.sort(iss))
 print("issue gaps (ns): p50 %d p90 %d p99 %d max %d" % tuple(np.percentile(gaps, [50, 90, 99, 100])))
 for i in range(0, min(len(a), 400), 8):
     print(i, [(int(x[0]) // 100, int(x[1]) // 100, int(x[2]) // 100) for x in a[i:i + 8]])
+ev = np.frombuffer(buf, dtype=np.uint64).reshape(-1, 3).astype(np.int64).reshape(-1)[60000:60000 + 64].reshape(8, 8)
+print("attention job stamps on this SM (us, rel. to tile0 issue): enter, ready, q staged, pages done, merged, arrived, [combined, published]")
+for row in ev:
+    if row[0]:
+        print([round((x - t0) / 1e3, 2) if x else None for x in row])
+# tiles consumed by the attention of layer 1 (between the stamps' ready and pages-done)
+lo, hi = ev[1][1], ev[1][3]
+sel = [(i, (int(x[0]) - 0) / 1e3, (int(x[1])) / 1e3, (int(x[2])) / 1e3) for i, x in enumerate(a) if x[1] > 0 and lo - t0 - 20000 <= x[1] <= hi - t0 + 2000]
+print("tiles around layer-1 attention (idx, issue, full, release) us:")
+for r in sel[:60]:
+    print(r)
