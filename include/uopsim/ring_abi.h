@@ -34,7 +34,8 @@
 #define VDC_RING_SLOT_BYTES 16384
 #define VDC_RING_MAX_SLOTS 12  /* 12 x 16 KB ring + 28 KB staged x + scratch <= 227 KB */
 #define VDC_RING_COMPUTE_WARPS 8
-#define VDC_RING_MAX_JOB_ROWS 128  /* output rows per GEMV job (smem partials) */
+#define VDC_RING_MAX_JOB_ROWS 256  /* output rows per GEMV job (smem partials) */
+#define VDC_RING_MAX_COL_TILES 4   /* column tiles per W row group (one partial plane each) */
 #define VDC_RING_MAX_TILE_ROWS 8   /* W rows per ring tile */
 #define VDC_RING_MAX_K 14336       /* GEMV reduction length (bf16) staged in shared memory */
 
@@ -51,6 +52,8 @@
 #define VDC_JOB_KV_APPEND 0x10  /* output row r -> cache[(r/hd)*T + pos][r%hd] */
 #define VDC_JOB_TOKEN_ROW 0x20  /* x offset += step[TOKEN] * k (embedding row) */
 #define VDC_JOB_TOKEN_AUX 0x40  /* aux offset += step[TOKEN] * cache_rows (residual = embedding row) */
+#define VDC_JOB_QKV 0x80        /* fused q|k|v rows: q -> o_t, k -> cache b_t, v -> cache o2_t;
+                                   block = q rows, split = k (= v) rows; rotary on q and k */
 
 typedef struct vdc_job {
     int32_t op;               /* isa opcode of the compute µop                */

@@ -43,7 +43,9 @@ namespace ring {
 constexpr int CW = VDC_RING_COMPUTE_WARPS;
 constexpr int NCT = CW * 32;
 constexpr int XBUF = VDC_RING_MAX_K * 2;  // bytes of the staged GEMV input vector
+constexpr int XPT = (XBUF / 16 + CW * 32 - 1) / (CW * 32);  // 16-byte chunks of x per compute thread
 constexpr int RMAX = VDC_RING_MAX_JOB_ROWS;
+constexpr int MAX_TPR = VDC_RING_MAX_COL_TILES;
 constexpr uint32_t SLOT = VDC_RING_SLOT_BYTES;
 constexpr int BAR_VCC = 1;
 constexpr int MAX_HD = 128;
@@ -60,7 +62,7 @@ enum : int { S_VMC_EMPTY = 0, S_VCC_FULL = 1, S_VCC_DEP = 2, S_VCC_EPI = 3, S_VC
 struct alignas(16) Shared {
     uint64_t full[VDC_RING_MAX_SLOTS];
     uint64_t empty[VDC_RING_MAX_SLOTS];
-    float red[CW][RMAX];  // per-warp row partials of a GEMV job
+    float red[MAX_TPR][RMAX];  // GEMV row partials, one plane per column tile (fixed summation order)
     float bc[2 * CW];
     float rope_cs[MAX_HD / 2], rope_sn[MAX_HD / 2];  // rotary table of the launch's position
     int32_t flag;
@@ -178,24 +180,27 @@ struct Vcc {
     // false (everywhere) if the launch aborted
     __device__ bool wait_ready(int32_t t0, int32_t n0, int32_t t1, int32_t n1, int32_t t2, int32_t n2) {
         if (ct == 0) {
+            // the (up to three) counters are polled together: one L2 round
+            // trip per poll, not one per counter; one acquire fence at the end
             const long long c0 = clock64();
-            const int32_t ts[3] = {t0, t1, t2}, ns[3] = {n0, n1, n2};
+            const bool u0 = t0 >= 0 && n0 > 0, u1 = t1 >= 0 && n1 > 0, u2 = t2 >= 0 && n2 > 0;
+            const uint32_t g0 = uint32_t(n0) * P->epoch, g1 = uint32_t(n1) * P->epoch, g2 = uint32_t(n2) * P->epoch;
+            const uint32_t* c0p = &P->counters[u0 ? t0 : 0];
+            const uint32_t* c1p = &P->counters[u1 ? t1 : 0];
+            const uint32_t* c2p = &P->counters[u2 ? t2 : 0];
             bool good = true;
-            for (int i = 0; i < 3 && good; ++i) {
-                if (ts[i] < 0 || ns[i] <= 0) continue;
-                const uint32_t target = uint32_t(ns[i]) * P->epoch;
-                const uint32_t* ctr = &P->counters[ts[i]];
-                if (ld_acquire(ctr) >= target) continue;
+            if (u0 || u1 || u2) {
                 const unsigned long long w0 = now_ns();
                 for (uint32_t n = 1;; ++n) {
-                    if (ld_relaxed(ctr) >= target) break;
+                    const uint32_t v0 = u0 ? ld_relaxed(c0p) : 0u, v1 = u1 ? ld_relaxed(c1p) : 0u, v2 = u2 ? ld_relaxed(c2p) : 0u;
+                    if ((!u0 || v0 >= g0) && (!u1 || v1 >= g1) && (!u2 || v2 >= g2)) break;
                     if ((n & 255) == 0) {
                         if (aborted()) {
                             good = false;
                             break;
                         }
                         if (P->watchdog_ns && now_ns() - w0 > P->watchdog_ns) {
-                            fire(0, 0x20000u | uint32_t(ts[i]));
+                            fire(0, 0x20000u | uint32_t(u0 ? t0 : u1 ? t1 : t2));
                             good = false;
                             break;
                         }
@@ -229,15 +234,23 @@ struct Vcc {
             return;
         }
         if (!reuse) {  // stage x (RMS-normalised, rounded to the model dtype) in shared memory
+            // every chunk of x (and of the norm weight) is requested before any
+            // is used: one L2 round trip instead of one per loop iteration
             const uint4* xs = reinterpret_cast<const uint4*>(tptr(J.x_t)) +
                               (J.x_off + (J.flags & VDC_JOB_TOKEN_ROW ? token() * int64_t(K) : 0)) / EPC;
+            const uint4* ws = rmsf ? reinterpret_cast<const uint4*>(tptr(J.a_t)) : nullptr;
+            uint4 xr[XPT], gr[XPT];
+#pragma unroll
+            for (int i = 0; i < XPT; ++i) {
+                const int c = int(ct) + i * NCT;
+                xr[i] = c < nch ? ldcg128(xs + c) : make_uint4(0, 0, 0, 0);
+                gr[i] = (rmsf && c < nch) ? __ldg(ws + c) : make_uint4(0, 0, 0, 0);
+            }
             float inv = 1.f;
             if (rmsf) {
                 float ss = 0.f;
-                for (int c = int(ct); c < nch; c += NCT) {
-                    const uint4 v = ldcg128(xs + c);
-                    ss += dot16<BF>(v, v);
-                }
+#pragma unroll
+                for (int i = 0; i < XPT; ++i) ss += dot16<BF>(xr[i], xr[i]);
                 ss = warp_sum(ss);
                 if (lane == 0) S->bc[w] = ss;
                 sync();
@@ -246,11 +259,13 @@ struct Vcc {
                 for (int i = 0; i < CW; ++i) tot += S->bc[i];
                 inv = 1.0f / sqrtf(tot / float(K) + J.eps);
             }
-            const uint4* ws = rmsf ? reinterpret_cast<const uint4*>(tptr(J.a_t)) : nullptr;
-            for (int c = int(ct); c < nch; c += NCT) {
-                uint4 v = ldcg128(xs + c);
+#pragma unroll
+            for (int i = 0; i < XPT; ++i) {
+                const int c = int(ct) + i * NCT;
+                if (c >= nch) break;
+                uint4 v = xr[i];
                 if (rmsf) {
-                    const uint4 g = __ldg(ws + c);
+                    const uint4 g = gr[i];
                     if constexpr (BF) {
                         v.x = pack2(bf_lo(v.x) * inv * bf_lo(g.x), bf_hi(v.x) * inv * bf_hi(g.x));
                         v.y = pack2(bf_lo(v.y) * inv * bf_lo(g.y), bf_hi(v.y) * inv * bf_hi(g.y));
@@ -281,7 +296,7 @@ struct Vcc {
                                                         : ldcg_f32(reinterpret_cast<const float*>(ab) + ai);
             }
         }
-        if ((J.flags & VDC_JOB_ROPE) && (rope_hd != J.head_dim || rope_theta != J.theta)) {
+        if ((J.flags & (VDC_JOB_ROPE | VDC_JOB_QKV)) && (rope_hd != J.head_dim || rope_theta != J.theta)) {
             // rotary table of this launch's position: cos/sin per dim pair, angles in double precision
             const int64_t pos = P->n_step > VDC_STEP_POS ? P->step[VDC_STEP_POS] : 0;
             for (int d2 = int(ct); d2 < J.head_dim / 2; d2 += NCT) {
@@ -312,7 +327,17 @@ struct Vcc {
         const long long e0 = clock64();
         gemv_epilogue(J, J.r1 - J.r0);
         if (ct == 0) st_epi += clock64() - e0;
-        publish(J.o_t);
+        if (J.flags & VDC_JOB_QKV) {
+            const int qrows = J.block, kvr = J.split;
+            sync();
+            if (ct == 0) {
+                if (J.r0 < qrows) red_release_add(&P->counters[J.o_t], 1u);
+                if (J.r0 < qrows + kvr && J.r1 > qrows) red_release_add(&P->counters[J.b_t], 1u);
+                if (J.r1 > qrows + kvr) red_release_add(&P->counters[J.o2_t], 1u);
+            }
+        } else {
+            publish(J.o_t);
+        }
     }
 
     // bf16 GEMV tile on the tensor cores (mma.sync m16n8k16, fp32 accumulate).
@@ -344,8 +369,6 @@ struct Vcc {
         const bool diag = int(lane & 3u) == (c_lo >> 1);
         const bool odd = c_lo & 1;
         const int r_lo = (int(lane) >> 2) / NC, r_hi = ((int(lane) >> 2) + 8) / NC;
-        for (int i = int(lane); i < rows; i += 32) S->red[w][i] = 0.f;
-        __syncwarp();
         uint32_t g = kt - 1u, gs = kt % R, gph = (kt / R) & 1u;
         for (int t = 0; t < ntiles; ++t) {
             // ring tile g lives in slot g % R and belongs to compute warp (g % R) % 8
@@ -417,7 +440,7 @@ struct Vcc {
 #pragma unroll
             for (int r = 0; r < TR; ++r) {
                 const float v = warp_sum((r_lo == r ? vlo : 0.f) + (r_hi == r ? vhi : 0.f));
-                if (lane == 0) S->red[w][rg * TR + r] += v;
+                if (lane == 0) S->red[c][rg * TR + r] = v;
             }
         }
         kt += uint32_t(ntiles);
@@ -437,8 +460,6 @@ struct Vcc {
         const int rows = J.r1 - J.r0, ntiles = (rows / TR) * tpr;
         const uint32_t row_bytes = uint32_t(cpt) * 16u;
         const uint32_t xb = smem_addr(S->x);
-        for (int i = int(lane); i < rows; i += 32) S->red[w][i] = 0.f;
-        __syncwarp();
         uint32_t g = kt - 1u, gs = kt % R, gph = (kt / R) & 1u;
         for (int t = 0; t < ntiles; ++t) {
             // ring tile g lives in slot g % R and belongs to compute warp (g % R) % 8
@@ -510,16 +531,15 @@ struct Vcc {
 #pragma unroll
             for (int r = 0; r < TR; ++r) {
                 const float v = warp_sum(acc[0][r] + acc[1][r]);
-                if (lane == 0) S->red[w][rg * TR + r] += v;
+                if (lane == 0) S->red[c][rg * TR + r] = v;
             }
         }
         kt += uint32_t(ntiles);
     }
 
-    __device__ float row_sum(int i) const {
-        float v = 0.f;
-#pragma unroll
-        for (int q = 0; q < CW; ++q) v += S->red[q][i];
+    __device__ float row_sum(int i, int tpr) const {
+        float v = S->red[0][i];
+        for (int c = 1; c < tpr; ++c) v += S->red[c][i];
         return v;
     }
 
@@ -531,6 +551,7 @@ struct Vcc {
     }
 
     __device__ void gemv_epilogue(const vdc_job& J, int rows) {
+        const int tpr = J.k / J.tile_cols;
         char* ob = tptr(J.o_t);
         const bool obf = tdtype(J.o_t) == VDC_DTYPE_BF16;
         const int lr0 = J.r0 - J.out_row0;  // first output row (region-local)
@@ -540,17 +561,44 @@ struct Vcc {
                 return (int64_t(lr / J.head_dim) * J.cache_rows + pos) * J.head_dim + lr % J.head_dim;
             return int64_t(J.o_off) + lr;
         };
-        if (J.flags & VDC_JOB_SWIGLU) {
+        if (J.flags & VDC_JOB_QKV) {
+            // fused q | k | v rows of one SM's share: rotary on q and k rows,
+            // k and v rows appended to the caches at the step position
+            const int qrows = J.block, kvr = J.split, hd = J.head_dim;
+            char* kb = tptr(J.b_t);
+            char* vb = tptr(J.o2_t);
+            for (int p = int(ct); p < rows / 2; p += NCT) {
+                const int wr = J.r0 + 2 * p;  // W row (pairs never straddle a region boundary)
+                float a = row_sum(2 * p, tpr), b = row_sum(2 * p + 1, tpr);
+                if (wr < qrows + kvr) {
+                    const int d = (wr < qrows ? wr : wr - qrows) % hd;
+                    const float cs = S->rope_cs[d / 2], sn = S->rope_sn[d / 2];
+                    const float na = a * cs - b * sn, nb = a * sn + b * cs;
+                    a = na;
+                    b = nb;
+                }
+                if (wr < qrows) {
+                    store_out(ob, obf, int64_t(J.o_off) + wr, a);
+                    store_out(ob, obf, int64_t(J.o_off) + wr + 1, b);
+                } else {
+                    const bool isk = wr < qrows + kvr;
+                    const int lr = isk ? wr - qrows : wr - qrows - kvr;
+                    const int64_t at = (int64_t(lr / hd) * J.cache_rows + pos) * hd + lr % hd;
+                    store_out(isk ? kb : vb, obf, at, a);
+                    store_out(isk ? kb : vb, obf, at + 1, b);
+                }
+            }
+        } else if (J.flags & VDC_JOB_SWIGLU) {
             const int B = J.block, hb = B / 2;
             for (int j = int(ct); j < rows / 2; j += NCT) {
                 const int blk = j / hb, jj = j % hb;
-                const float gt = row_sum(blk * B + jj), up = row_sum(blk * B + hb + jj);
+                const float gt = row_sum(blk * B + jj, tpr), up = row_sum(blk * B + hb + jj, tpr);
                 store_out(ob, obf, int64_t(J.o_off) + lr0 / 2 + j, gt / (1.0f + expf(-gt)) * up);
             }
         } else if (J.flags & VDC_JOB_ROPE) {
             for (int p = int(ct); p < rows / 2; p += NCT) {
                 const int lr = lr0 + 2 * p;
-                float a = row_sum(2 * p), b = row_sum(2 * p + 1);
+                float a = row_sum(2 * p, tpr), b = row_sum(2 * p + 1, tpr);
                 const int d = lr % J.head_dim;
                 const float cs = S->rope_cs[d / 2], sn = S->rope_sn[d / 2];
                 const float na = a * cs - b * sn, nb = a * sn + b * cs;
@@ -560,7 +608,7 @@ struct Vcc {
         } else {
             const bool res = J.flags & VDC_JOB_RESID;
             for (int i = int(ct); i < rows; i += NCT) {
-                float v = row_sum(i);
+                float v = row_sum(i, tpr);
                 if (res) v += resid;
                 store_out(ob, obf, out_index(lr0 + i), v);
             }

@@ -252,7 +252,8 @@ std::string ProgramBox::text(int mode) const {
         jobs.push_back({{"op", jb.op}, {"flags", jb.flags}, {"r0", jb.r0}, {"r1", jb.r1}, {"k", jb.k},
                         {"tile", {jb.tile_rows, jb.tile_cols}}, {"x", {jb.x_t, jb.x_off, jb.x_need}},
                         {"a", {jb.a_t, jb.a_off, jb.a_need}}, {"b", {jb.b_t, jb.b_off, jb.b_need}},
-                        {"o", {jb.o_t, jb.o_off}}, {"out_row0", jb.out_row0}, {"head_dim", jb.head_dim},
+                        {"o", {jb.o_t, jb.o_off}}, {"o2", {jb.o2_t, jb.o2_off}}, {"out_row0", jb.out_row0}, {"head_dim", jb.head_dim},
+                        {"split", jb.split}, {"arrive", {jb.arrive_ctr, jb.arrive_need}},
                         {"group", jb.group}, {"block", jb.block}, {"cache_rows", jb.cache_rows},
                         {"eps", jb.eps}, {"theta", jb.theta}, {"scale", jb.scale}});
     out["jobs"] = jobs;

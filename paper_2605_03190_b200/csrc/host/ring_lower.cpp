@@ -52,6 +52,7 @@ struct Tile {
 
 struct RJob {
     vdc_job j{};
+    std::vector<int32_t> publishes;  // counters bumped when the µop completes (default: o_t)
     int32_t head = -1;        // attention: kv head
     std::vector<Tile> tiles;  // ring tiles in consumption order
     uint32_t ordinal = 0;
@@ -73,8 +74,10 @@ class RingLowering {
         std::map<int32_t, int32_t> writers;
         std::set<std::pair<int32_t, int32_t>> combined;
         for (const auto& r : jobs_) {
-            ++writers[r.j.o_t];
-            if (r.j.o2_t >= 0 && combined.insert({r.j.o2_t, r.j.o2_off}).second) ++writers[r.j.o2_t];  // one combiner per kv head
+            if (r.publishes.empty()) ++writers[r.j.o_t];
+            for (int32_t t : r.publishes) ++writers[t];
+            if (r.j.op == int32_t(Opcode::ATTN_DECODE) && r.j.o2_t >= 0 && combined.insert({r.j.o2_t, r.j.o2_off}).second)
+                ++writers[r.j.o2_t];  // one combiner per kv head
         }
         for (auto& r : jobs_) {
             auto need = [&](int32_t t) { return t >= 0 && writers.count(storage(uint16_t(t))) ? writers.at(storage(uint16_t(t))) : 0; };
@@ -179,20 +182,23 @@ class RingLowering {
             bool kv;
         };
         std::vector<Region> regions;
-        int64_t head_dim = 0, qrows = M;
-        if (n.outputs.size() == 3) {
+        int64_t head_dim = 0, qrows = M, kvrows = 0;
+        const bool qkv = n.outputs.size() == 3;
+        if (qkv) {
+            // one job per SM share even across the q | k | v boundaries (the
+            // engine routes each row: VDC_JOB_QKV), so no SM pays two epilogues
             const TileDescriptor& kc = desc_[idx(n.outputs[1])];
             head_dim = kc.shape.back();
-            const int64_t kvrows = kc.shape[0] * head_dim;
+            kvrows = kc.shape[0] * head_dim;
             qrows = desc_[idx(n.outputs[0])].rows();
             if (qrows + 2 * kvrows != M) throw GeneratorError("node " + n.id + ": q/k/v rows do not add up to W rows");
-            regions = {{0, qrows, idx(n.outputs[0]), false}, {qrows, qrows + kvrows, idx(n.outputs[1]), true},
-                       {qrows + kvrows, M, idx(n.outputs[2]), true}};
-            for (const auto& r : regions)
-                if (r.r0 % unit) throw GeneratorError("node " + n.id + ": q/k/v boundary not tile aligned");
+            if (qrows % unit || kvrows % unit || !rope)
+                throw GeneratorError("node " + n.id + ": q/k/v boundaries must be tile aligned and rotary enabled");
+            regions = {{0, M, idx(n.outputs[0]), false}};
         } else {
             regions = {{0, M, idx(n.outputs[0]), false}};
         }
+        if (tpr > VDC_RING_MAX_COL_TILES) throw GeneratorError("node " + n.id + ": more column tiles per row than the engine keeps");
         const int64_t max_rows = (VDC_RING_MAX_JOB_ROWS / unit) * unit;
         const int64_t units = M / unit;
         const TileDescriptor& xd = desc_[idx(n.inputs[1])];
@@ -235,14 +241,20 @@ class RingLowering {
                     }
                     j.o_t = storage(reg.out);
                     j.out_row0 = int32_t(reg.r0);
-                    if (rope && (!reg.kv || reg.r0 == qrows)) {  // q and k rows rotate, v rows do not
-                        j.flags |= VDC_JOB_ROPE;
-                        j.theta = float(attr_num(n, "theta", 10000.0));
-                    }
                     j.head_dim = int32_t(head_dim);
-                    if (reg.kv) {
-                        j.flags |= VDC_JOB_KV_APPEND;
-                        j.cache_rows = int32_t(desc_[reg.out].shape[1]);
+                    if (qkv) {
+                        j.flags |= VDC_JOB_QKV;
+                        j.theta = float(attr_num(n, "theta", 10000.0));
+                        j.block = int32_t(qrows);
+                        j.split = int32_t(kvrows);
+                        j.b_t = storage(idx(n.outputs[1]));
+                        j.o2_t = storage(idx(n.outputs[2]));
+                        j.cache_rows = int32_t(desc_[idx(n.outputs[1])].shape[1]);
+                        if (c0 < qrows) r.publishes.push_back(j.o_t);
+                        if (c0 < qrows + kvrows && c1 > qrows) r.publishes.push_back(j.b_t);
+                        if (c1 > qrows + kvrows) r.publishes.push_back(j.o2_t);
+                    } else {
+                        r.publishes.push_back(j.o_t);
                     }
                     if (swiglu) {
                         j.flags |= VDC_JOB_SWIGLU;
@@ -413,7 +425,11 @@ std::vector<isa::Violation> validate_ring_program(const LoweredProgram& p) {
         if (core.kind != isa::CoreKind::vcc) continue;
         const auto& s = p.streams.at(core);
         for (size_t i = 0; i < s.size(); ++i)
-            if (s[i].klass() == isa::OpClass::compute) writer_op[p.jobs.at(size_t(s[i].imm)).o_t] = m[i].op;
+            if (s[i].klass() == isa::OpClass::compute) {
+                const vdc_job& j = p.jobs.at(size_t(s[i].imm));
+                writer_op[j.o_t] = m[i].op;
+                if (j.flags & VDC_JOB_QKV) writer_op[j.b_t] = writer_op[j.o2_t] = m[i].op;
+            }
     }
     for (const auto& [core, s] : p.streams) {
         if (core.kind != isa::CoreKind::vcc) continue;
@@ -429,7 +445,8 @@ std::vector<isa::Violation> validate_ring_program(const LoweredProgram& p) {
             if (m[i].op < last_op) v.push_back({i, core.name() + ": operators out of topological order"});
             last_op = m[i].op;
             const vdc_job& j = p.jobs.at(size_t(s[i].imm));
-            for (int32_t t : {j.x_t, j.a_t, j.b_t}) {
+            const int32_t b_in = (j.flags & VDC_JOB_QKV) ? -1 : j.b_t;  // QKV: b_t is an output (K cache)
+            for (int32_t t : {j.x_t, j.a_t, b_in}) {
                 const auto it = writer_op.find(t);
                 if (it != writer_op.end() && it->second >= m[i].op)
                     v.push_back({i, core.name() + ": waits on an operator that does not precede it"});

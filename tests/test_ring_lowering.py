@@ -67,14 +67,25 @@ def test_ring_program_invariants(name):
     cover = collections.defaultdict(list)
     for j in jobs:
         if j["op"] in (OP["GEMV"], OP["RMS_GEMV"], OP["GEMV_ADD"]):
-            key = (j["o"][0] if j["flags"] & 0x10 == 0 else -1, j["k"], j["flags"] & 0x1, j["x"][0])
+            key = (j["o"][0], j["k"], j["flags"] & 0x1, j["x"][0])
             cover[key].append((j["r0"], j["r1"]))
     for key, rs in cover.items():
         rs.sort()
         for (a0, a1), (b0, b1) in zip(rs, rs[1:]):
             assert a1 <= b0, f"overlapping GEMV rows {rs}"
     # readiness targets: number of µops producing the storage tensor
-    writers = collections.Counter(j["o"][0] for j in jobs)
+    writers = collections.Counter()
+    for j in jobs:
+        if j["flags"] & 0x80:  # fused q|k|v rows: publishes every region it touches
+            qrows, kvr = j["block"], j["split"]
+            if j["r0"] < qrows:
+                writers[j["o"][0]] += 1
+            if j["r0"] < qrows + kvr and j["r1"] > qrows:
+                writers[j["b"][0]] += 1
+            if j["r1"] > qrows + kvr:
+                writers[j["o2"][0]] += 1
+        else:
+            writers[j["o"][0]] += 1
     for j in jobs:
         for key in ("x", "a", "b"):
             t, _, need = j[key]
