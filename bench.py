@@ -14,8 +14,10 @@ e2e        tokens/s through the public API with host buffers: per step the step
            on the host (greedy), i.e. a real serving loop
 roofline   algorithmic bytes per step (bf16 weights once + KV read + KV append)
            / device time per step, against MEASURED_PEAKS.json hbm_gbs
-N > 1      one independent replica per GPU (tensor parallelism is not built yet):
-           value = total tokens/s over ranks, time = max over ranks
+N > 1      tensor parallel (Megatron split over the N GPUs, partial sums exchanged
+           inside the persistent kernel over NVLink peer memory): value = tokens/s of
+           the group (strong scaling), time = max over ranks; --parallel replicas
+           runs N independent copies instead (weak scaling)
 --impl reference   the CPU oracle (test-infrastructure restatement of the
            reference semantics, oracle/_ref/oracle_interp) on the host cores.
 """
@@ -228,22 +230,62 @@ def init_tensors(eng, seed: int = 0):
     return out
 
 
+def bind_symmetric_tp(eng, world: int, rank: int, local_rank: int):
+    """TP exchange buffers: one symmetric allocation per symmetric tensor
+    (128-byte counter header + W x D fp32 slots), peer-mapped over NVLink by
+    torch symmetric memory; the engine stores partial sums into every rank's
+    buffer and publishes on its header counter (in-kernel allreduce)."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+
+    keep = []
+    group = dist.group.WORLD.group_name
+    if hasattr(symm_mem, "enable_symm_mem_for_group"):
+        symm_mem.enable_symm_mem_for_group(group)
+    for d in eng.info["descriptors"]:
+        if not d.get("symmetric"):
+            continue
+        n = 32 + int(d["shape"][0]) * int(d["shape"][1])
+        t = symm_mem.empty(n, dtype=torch.float32, device=f"cuda:{local_rank}")
+        t.zero_()
+        h = symm_mem.rendezvous(t, group)
+        eng.bind_symmetric(d["name"], [int(p) for p in h.buffer_ptrs], world, rank)
+        keep.append((t, h))
+    torch.cuda.synchronize()
+    dist.barrier()
+    return keep
+
+
 def run_ours(args, rank: int, world: int, local_rank: int):
     import torch
     from paper_2605_03190_b200 import Program
     from paper_2605_03190_b200.engine import Engine
 
     torch.cuda.set_device(local_rank)
+    tp = world > 1 and args.parallel == "tp"
     t_build = time.time()
-    prog = Program.build(model_request(args.layers, args.ctx, args.engine, args.ring_slots, args.pages_per_job))
+    req = model_request(args.layers, args.ctx, args.engine, args.ring_slots, args.pages_per_job)
+    if tp:
+        req["layout"]["tp_world"], req["layout"]["tp_rank"] = world, rank
+    prog = Program.build(req)
     build_s = time.time() - t_build
     eng = Engine(prog, device=local_rank, watchdog_ms=10000)
     tens = init_tensors(eng)
+    keep_sym = bind_symmetric_tp(eng, world, rank, local_rank) if tp else None
     info = eng.info
     nbytes = algorithmic_bytes(info, args.ctx)
     step = torch.tensor([17, args.ctx - 1, args.ctx, 0, 0, 0, 0, 0], dtype=torch.int64, device=f"cuda:{local_rank}")
     eng.bind_step(step)
     stream = torch.cuda.Stream(device=local_rank)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    barrier()
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             eng.launch(stream)
@@ -253,12 +295,6 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     sampler = ClockSampler(local_rank)
     sampler.start()
     time.sleep(0.3)
-
-    def barrier():
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
-        torch.cuda.synchronize()
 
     # ---- value: device-resident inputs, K back-to-back steps
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
@@ -280,7 +316,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # ---- e2e: host loop through the public API (H2D step block, D2H logits)
     logits = tens["logits"]
     h_step = torch.zeros(8, dtype=torch.int64).pin_memory()
-    h_logits = torch.empty(logits.numel(), dtype=torch.float32).pin_memory()
+    n_logits = logits.numel() * (world if tp else 1)
+    h_logits = torch.empty(n_logits, dtype=torch.float32).pin_memory()
+    gathered = torch.empty(n_logits, dtype=torch.float32, device=f"cuda:{local_rank}") if tp else None
     token = 17
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -291,7 +329,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             h_step[0], h_step[1], h_step[2] = token, args.ctx - 1, args.ctx
             step.copy_(h_step, non_blocking=True)
             eng.launch(stream)
-            h_logits.copy_(logits, non_blocking=True)
+            if tp:  # vocab-parallel logits: gather the shards, every rank picks the same token
+                import torch.distributed as dist
+                dist.all_gather_into_tensor(gathered, logits)
+                h_logits.copy_(gathered, non_blocking=True)
+            else:
+                h_logits.copy_(logits, non_blocking=True)
             stream.synchronize()
             token = int(torch.argmax(h_logits))
         e1.record(stream)
@@ -309,11 +352,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         total_ms, e2e_ms = float(t[0]), float(t[1])
 
     ms_per_step = total_ms / args.steps
-    value = world * args.steps / (total_ms / 1e3)
-    e2e_value = world * args.steps / (e2e_ms / 1e3)
+    # TP: the group decodes one token per step; replicas: one token per GPU per step
+    tokens_per_step = 1 if tp else world
+    value = tokens_per_step * args.steps / (total_ms / 1e3)
+    e2e_value = tokens_per_step * args.steps / (e2e_ms / 1e3)
     peak, peak_src = measured_peak()
     kernel_ms = sorted(per)[len(per) // 2]
-    achieved = nbytes["total"] / (sum(per) / len(per) / 1e3) / 1e9
+    achieved = nbytes["total"] / (sum(per) / len(per) / 1e3) / 1e9  # this rank's bytes (its shard) per GPU
+    parallelism = "1 GPU" if world == 1 else (f"tp{world} (Megatron split, in-kernel NVLink allreduce)" if tp
+                                               else f"{world} independent replicas")
     result = {
         "metric": METRIC,
         "value": round(value, 3),
@@ -323,28 +370,29 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if tp else "weak",
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic: random-init Llama-3-8B weights (uniform/sqrt(fan_in)), random bf16 KV cache, greedy token feedback in e2e",
         "config": {"workload": f"C2 Llama-3-8B bf16 decode, batch 1, ctx {args.ctx}, {args.layers} layers + lm_head",
-                   "model": "llama3-8b", "batch": 1, "ctx": args.ctx,
-                   "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas (TP not yet built)",
+                   "model": "llama3-8b", "batch": 1, "ctx": args.ctx, "parallelism": parallelism,
                    "l2": "inputs larger than L2 (algorithmic %.2f GB per step vs 126 MB L2)" % (nbytes["total"] / 1e9),
                    "program_uops": info["total_uops"], "virtual_cores": prog.cores()[0], "build_seconds": round(build_s, 2)},
         "e2e": {"value": round(e2e_value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 8 * 8,
-                "d2h_bytes_per_step": logits.numel() * 4},
+                "d2h_bytes_per_step": n_logits * 4},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": committed_traffic(),
+                     "frac": round(achieved / peak, 4), "traffic": committed_traffic() if world == 1 else None,
                      "peak_source": peak_src, "frac_of_8TBps_spec": round(achieved / 8000.0, 4),
-                     "bytes_per_step": nbytes, "kernel": ("vdc_dev::ring::ring_kernel" if args.engine == "ring" else "vdc_dev::engine_kernel") + " (persistent, 1 CTA/SM)",
+                     "bytes_per_step": nbytes, "per_gpu": True,
+                     "kernel": ("vdc_dev::ring::ring_kernel" if args.engine == "ring" else "vdc_dev::engine_kernel") + " (persistent, 1 CTA/SM)",
                      "kernel_ms_median": round(kernel_ms, 4)},
         "clocks": clocks,
         "engine_report": {"engine": args.engine, "uops_executed": rep.uops_executed, "bytes_loaded": rep.bytes_loaded,
                           "wait_cycles_sum_over_sms": rep.wait_cycles,
                           "bytes_stored": rep.bytes_stored},
     }
+    del keep_sym
     return result
 
 
@@ -360,6 +408,8 @@ def main():
     ap.add_argument("--engine", default="ring", choices=["ring", "reference"])
     ap.add_argument("--ring-slots", type=int, default=12)
     ap.add_argument("--pages-per-job", type=int, default=4)
+    ap.add_argument("--parallel", default="tp", choices=["tp", "replicas"],
+                    help="N>1: tensor parallel over the N GPUs (default) or N independent replicas")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", 0))

@@ -49,6 +49,12 @@ struct LayoutConfig {
     int gu_block = 16;       // swiglu interleave block (== job_rows for the gu node)
     int wtile_bytes = 32768; // target weight tile bytes (32 KB: full 4096-wide rows)
     bool ring = false;       // ring-mode tiling: contiguous weight tiles of <= one ring slot
+    // tensor parallelism (ext): 0 = single-device graph; >= 1 = the graph of
+    // rank `tp_rank` of `tp_world` (Megatron split: column-parallel qkv and
+    // gate/up, row-parallel o and down followed by ALLREDUCE_ADD of the
+    // hidden vector, vocab-parallel lm_head, replicated embedding and norms)
+    int tp_world = 0;
+    int tp_rank = 0;
 };
 
 ModelConfig llama3_8b();

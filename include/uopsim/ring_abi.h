@@ -52,6 +52,10 @@
 #define VDC_JOB_KV_APPEND 0x10  /* output row r -> cache[(r/hd)*T + pos][r%hd] */
 #define VDC_JOB_TOKEN_ROW 0x20  /* x offset += step[TOKEN] * k (embedding row) */
 #define VDC_JOB_TOKEN_AUX 0x40  /* aux offset += step[TOKEN] * cache_rows (residual = embedding row) */
+#define VDC_JOB_SYM_OUT 0x100   /* output rows go to every rank's slot `tp_rank` of a symmetric tensor */
+#define VDC_JOB_SYM_IN 0x200    /* x is a symmetric tensor: readiness on its header counter (sys scope) */
+#define VDC_RING_MAX_TP 8       /* tensor-parallel ranks */
+#define VDC_SYM_HEADER_BYTES 128 /* symmetric buffer = header (u32 readiness counter) + data */
 #define VDC_JOB_QKV 0x80        /* fused q|k|v rows: q -> o_t, k -> cache b_t, v -> cache o2_t;
                                    block = q rows, split = k (= v) rows; rotary on q and k */
 

@@ -117,6 +117,14 @@ int vdc_load_jobs(vdc_ctx* ctx, const vdc_job* jobs, uint32_t n_jobs, uint32_t r
 int vdc_set_params(vdc_ctx* ctx, const float* params, uint32_t n);
 /* device memory (row-major) backing descriptor `tensor`; the caller owns it */
 int vdc_bind_tensor(vdc_ctx* ctx, uint16_t tensor, void* dptr, size_t bytes, int dtype);
+/* tensor parallelism (ring programs): bind symmetric tensor `tensor` of rank
+ * `rank` of `world` (<= VDC_RING_MAX_TP). peer_bases[q] is rank q's buffer as
+ * mapped in this process (NVLink peer / IPC / same device); every buffer is
+ * VDC_SYM_HEADER_BYTES of header (u32 readiness counter at offset 0, zeroed
+ * by the caller before the first launch) followed by the tensor's data.
+ * Replaces the reference-side `vdc_tp_init` + host allreduce: the partial
+ * sums move by peer stores inside the persistent kernel. */
+int vdc_bind_symmetric(vdc_ctx* ctx, uint16_t tensor, void* const* peer_bases, uint32_t world, uint32_t rank);
 /* step block: device-resident int64 scalars read by SET_ACC_MEM */
 int vdc_bind_step(vdc_ctx* ctx, int64_t* dptr, uint32_t n);
 /* one execution of the loaded program on `stream` (a cudaStream_t, NULL =

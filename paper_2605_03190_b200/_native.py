@@ -70,7 +70,7 @@ class vdc_report(ctypes.Structure):
 # every symbol include/vdc.h declares (the CPU suite checks they are exported)
 EXPORTS = [
     "vdc_last_error", "vdc_version", "vdc_create", "vdc_destroy", "vdc_load_program", "vdc_load_jobs", "vdc_set_params",
-    "vdc_bind_tensor", "vdc_bind_step", "vdc_bind_trace", "vdc_launch", "vdc_wait", "vdc_set_watchdog", "vdc_set_prefetch", "vdc_program_build",
+    "vdc_bind_tensor", "vdc_bind_symmetric", "vdc_bind_step", "vdc_bind_trace", "vdc_launch", "vdc_wait", "vdc_set_watchdog", "vdc_set_prefetch", "vdc_program_build",
     "vdc_program_parse", "vdc_program_free", "vdc_program_text", "vdc_program_cores", "vdc_program_words",
     "vdc_program_load", "vdc_free_string",
 ]
@@ -98,6 +98,7 @@ def lib() -> ctypes.CDLL:
         "vdc_set_params": ([vp, c.POINTER(c.c_float), c.c_uint32], c.c_int),
         "vdc_bind_tensor": ([vp, c.c_uint16, vp, c.c_size_t, c.c_int], c.c_int),
         "vdc_bind_step": ([vp, vp, c.c_uint32], c.c_int),
+        "vdc_bind_symmetric": ([vp, c.c_uint16, c.POINTER(c.c_void_p), c.c_uint32, c.c_uint32], c.c_int),
         "vdc_bind_trace": ([vp, vp, c.c_uint32], c.c_int),
         "vdc_launch": ([vp, vp], c.c_int),
         "vdc_wait": ([vp, c.POINTER(vdc_report)], c.c_int),

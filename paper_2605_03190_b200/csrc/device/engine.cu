@@ -1847,6 +1847,10 @@ struct vdc_ctx {
     uint32_t epoch = 0;
     uint32_t ring_prefetch = 0;
     size_t n_counters = 0;
+    std::vector<char*> sym_host;  // [n_desc][VDC_RING_MAX_TP]
+    char** d_sym = nullptr;
+    bool sym_dirty = false;
+    uint32_t tp_rank = 0, tp_world = 1;
     unsigned long long* d_tile_trace = nullptr;
     bool ring_attr_set = false;
 };
@@ -1920,6 +1924,7 @@ int vdc_destroy(vdc_ctx* ctx) {
     dfree(ctx->d_counters);
     dfree(ctx->d_params);
     dfree(ctx->d_jobs);
+    dfree(ctx->d_sym);
     dfree(ctx->d_stats);
     dfree(ctx->d_status);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -2075,6 +2080,27 @@ int vdc_bind_tensor(vdc_ctx* ctx, uint16_t tensor, void* dptr, size_t bytes, int
     return VDC_OK;
 }
 
+int vdc_bind_symmetric(vdc_ctx* ctx, uint16_t tensor, void* const* peer_bases, uint32_t world, uint32_t rank) {
+    if (!ctx || !ctx->loaded) return fail(VDC_ERR_INPUT, "no program loaded");
+    if (tensor >= ctx->descs.size()) return fail(VDC_ERR_INPUT, "tensor index out of range");
+    if (!peer_bases || world < 1 || world > VDC_RING_MAX_TP || rank >= world) return fail(VDC_ERR_INPUT, "bad world/rank");
+    if (ctx->sym_host.size() != ctx->descs.size() * VDC_RING_MAX_TP) ctx->sym_host.assign(ctx->descs.size() * VDC_RING_MAX_TP, nullptr);
+    for (uint32_t q = 0; q < world; ++q) {
+        if (!peer_bases[q]) return fail(VDC_ERR_INPUT, "null peer buffer");
+        ctx->sym_host[size_t(tensor) * VDC_RING_MAX_TP + q] = static_cast<char*>(peer_bases[q]);
+    }
+    ctx->tp_rank = rank;
+    ctx->tp_world = world;
+    // the local data view (after the header) backs the descriptor like a bound tensor
+    char* local = static_cast<char*>(peer_bases[rank]) + VDC_SYM_HEADER_BYTES;
+    ctx->bound[tensor] = local;
+    for (size_t i = 0; i < ctx->dev_descs.size(); ++i)
+        if (ctx->dev_descs[i].storage == int32_t(tensor)) ctx->dev_descs[i].ptr = local;
+    ctx->descs_dirty = true;
+    ctx->sym_dirty = true;
+    return VDC_OK;
+}
+
 int vdc_bind_step(vdc_ctx* ctx, int64_t* dptr, uint32_t n) {
     if (!ctx) return fail(VDC_ERR_INPUT, "null ctx");
     ctx->d_step = dptr;
@@ -2136,6 +2162,15 @@ int vdc_launch(vdc_ctx* ctx, void* stream) {
         R.watchdog_ns = (unsigned long long)ctx->watchdog_ms * 1000000ull;
         R.trace = ctx->d_trace;
         R.trace_cap = ctx->trace_cap;
+        if (ctx->sym_dirty) {
+            dfree(ctx->d_sym);
+            CU(cudaMalloc(&ctx->d_sym, sizeof(char*) * ctx->sym_host.size()));
+            CU(cudaMemcpyAsync(ctx->d_sym, ctx->sym_host.data(), sizeof(char*) * ctx->sym_host.size(), cudaMemcpyHostToDevice, s));
+            ctx->sym_dirty = false;
+        }
+        R.sym = ctx->d_sym;
+        R.tp_rank = ctx->tp_rank;
+        R.tp_world = ctx->tp_world;
         if (R.debug & 2u) {
             static unsigned long long* tt = nullptr;
             if (!tt) cudaMalloc(&tt, sizeof(unsigned long long) * 3 * 65536);

@@ -115,6 +115,8 @@ struct RingParams {
     uint32_t prefetch;         // L2 prefetch look-ahead of the memory core, in tiles (0 = off)
     uint32_t debug;            // bit 0: GEMV tiles are released without computing (bandwidth experiments)
     unsigned long long* tile_trace;  // debug: per ring tile of SM `debug >> 8`: {t_issue, t_full, t_release}
+    char* const* sym;          // [n_desc][VDC_RING_MAX_TP] peer buffer bases of symmetric tensors (null: not symmetric)
+    uint32_t tp_rank, tp_world;
     uint32_t tile_trace_cap;
     SmStats* stats;            // written (not accumulated) by each SM
     Status* status;

@@ -53,7 +53,7 @@ constexpr int MAX_DPL = MAX_HD / 32;
 
 enum : uint32_t {
     OP_LOAD = 0x01, OP_ELEMWISE = 0x25, OP_GEMV = 0x27, OP_RMS_GEMV = 0x28, OP_GEMV_ADD = 0x29, OP_ATTN_DECODE = 0x2A,
-    OP_ATTN_COMBINE = 0x2B, OP_HALT = 0x45,
+    OP_ATTN_COMBINE = 0x2B, OP_ALLREDUCE_ADD = 0x2C, OP_HALT = 0x45,
 };
 
 // stat slots (SmStats::wait)
@@ -147,6 +147,12 @@ struct Vcc {
         }
     }
     __device__ char* tptr(int32_t t) const { return P->descs[t].ptr; }
+    // symmetric (TP) tensors keep their readiness counter in their buffer header
+    __device__ char* sym_base(int32_t t, uint32_t q) const { return P->sym ? P->sym[size_t(t) * VDC_RING_MAX_TP + q] : nullptr; }
+    __device__ uint32_t* ctr(int32_t t) const {
+        char* b = t >= 0 ? sym_base(t, P->tp_rank) : nullptr;
+        return b ? reinterpret_cast<uint32_t*>(b) : &P->counters[t < 0 ? 0 : t];
+    }
     __device__ int64_t token() const { return P->n_step > VDC_STEP_TOKEN ? P->step[VDC_STEP_TOKEN] : 0; }
     __device__ int32_t tdtype(int32_t t) const { return P->descs[t].dtype; }
 
@@ -185,14 +191,17 @@ struct Vcc {
             const long long c0 = clock64();
             const bool u0 = t0 >= 0 && n0 > 0, u1 = t1 >= 0 && n1 > 0, u2 = t2 >= 0 && n2 > 0;
             const uint32_t g0 = uint32_t(n0) * P->epoch, g1 = uint32_t(n1) * P->epoch, g2 = uint32_t(n2) * P->epoch;
-            const uint32_t* c0p = &P->counters[u0 ? t0 : 0];
-            const uint32_t* c1p = &P->counters[u1 ? t1 : 0];
-            const uint32_t* c2p = &P->counters[u2 ? t2 : 0];
+            const uint32_t* c0p = ctr(u0 ? t0 : -1);
+            const uint32_t* c1p = ctr(u1 ? t1 : -1);
+            const uint32_t* c2p = ctr(u2 ? t2 : -1);
+            const bool sys = P->tp_world > 1;  // peers publish at system scope
             bool good = true;
             if (u0 || u1 || u2) {
                 const unsigned long long w0 = now_ns();
                 for (uint32_t n = 1;; ++n) {
-                    const uint32_t v0 = u0 ? ld_relaxed(c0p) : 0u, v1 = u1 ? ld_relaxed(c1p) : 0u, v2 = u2 ? ld_relaxed(c2p) : 0u;
+                    const uint32_t v0 = u0 ? (sys ? ld_relaxed_sys(c0p) : ld_relaxed(c0p)) : 0u;
+                    const uint32_t v1 = u1 ? (sys ? ld_relaxed_sys(c1p) : ld_relaxed(c1p)) : 0u;
+                    const uint32_t v2 = u2 ? (sys ? ld_relaxed_sys(c2p) : ld_relaxed(c2p)) : 0u;
                     if ((!u0 || v0 >= g0) && (!u1 || v1 >= g1) && (!u2 || v2 >= g2)) break;
                     if ((n & 255) == 0) {
                         if (aborted()) {
@@ -206,7 +215,10 @@ struct Vcc {
                         }
                     }
                 }
-                fence_acquire_gpu();
+                if (sys)
+                    asm volatile("fence.acq_rel.sys;" ::: "memory");
+                else
+                    fence_acquire_gpu();
             }
             S->flag = good ? 1 : 0;
             st_dep += clock64() - c0;
@@ -219,7 +231,7 @@ struct Vcc {
     // after all threads stored the job's outputs
     __device__ void publish(int32_t t) {
         sync();
-        if (ct == 0 && t >= 0) red_release_add(&P->counters[t], 1u);  // release is cumulative over the CTA barrier
+        if (ct == 0 && t >= 0) red_release_add(ctr(t), 1u);  // release is cumulative over the CTA barrier
     }
 
     // ---------------------------------------------------------------- GEMV
@@ -335,6 +347,11 @@ struct Vcc {
                 if (J.r0 < qrows + kvr && J.r1 > qrows) red_release_add(&P->counters[J.b_t], 1u);
                 if (J.r1 > qrows + kvr) red_release_add(&P->counters[J.o2_t], 1u);
             }
+        } else if (J.flags & VDC_JOB_SYM_OUT) {
+            sync();  // the partial rows were stored into every rank's slot: publish on every rank
+            if (ct == 0)
+                for (uint32_t q = 0; q < P->tp_world; ++q)
+                    asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(sym_base(J.o_t, q)) : "memory");
         } else {
             publish(J.o_t);
         }
@@ -607,10 +624,16 @@ struct Vcc {
             }
         } else {
             const bool res = J.flags & VDC_JOB_RESID;
+            const bool symo = J.flags & VDC_JOB_SYM_OUT;
             for (int i = int(ct); i < rows; i += NCT) {
                 float v = row_sum(i, tpr);
                 if (res) v += resid;
-                store_out(ob, obf, out_index(lr0 + i), v);
+                if (symo) {  // TP partial sum -> slot `tp_rank` of every rank's buffer (NVLink peer stores)
+                    for (uint32_t q = 0; q < P->tp_world; ++q)
+                        reinterpret_cast<float*>(sym_base(J.o_t, q) + VDC_SYM_HEADER_BYTES)[J.o_off + lr0 + i] = v;
+                } else {
+                    store_out(ob, obf, out_index(lr0 + i), v);
+                }
             }
         }
     }
@@ -942,6 +965,36 @@ struct Vcc {
             store_out(ob, obf, int64_t(J.o2_off) + h * HD + lane * DPL + d, L > 0.f ? O[d] / L : 0.f);
     }
 
+    // ------------------------------------------- ALLREDUCE_ADD (tensor parallel)
+    // rows [r0, r1): x_next = residual + sum over the W rank slots of the
+    // symmetric partial buffer, in rank order (same result on every rank)
+    __device__ void allreduce(const vdc_job& J) {
+        if (!wait_ready(J.x_t, J.x_need, J.a_t, J.a_need, -1, 0)) {
+            ok = false;
+            return;
+        }
+        const float* part = reinterpret_cast<const float*>(tptr(J.x_t));
+        const char* ab = tptr(J.a_t);
+        const bool abf = tdtype(J.a_t) == VDC_DTYPE_BF16;
+        const int64_t aoff = J.a_off + (J.flags & VDC_JOB_TOKEN_AUX ? token() * int64_t(J.cache_rows) : 0);
+        char* ob = tptr(J.o_t);
+        const bool obf = tdtype(J.o_t) == VDC_DTYPE_BF16;
+        for (int r = J.r0 + int(ct); r < J.r1; r += NCT) {
+            float acc[VDC_RING_MAX_TP];
+#pragma unroll
+            for (int q = 0; q < VDC_RING_MAX_TP; ++q)
+                acc[q] = q < J.group ? ldcg_f32(part + int64_t(q) * J.k + r) : 0.f;
+            float v = 0.f;
+#pragma unroll
+            for (int q = 0; q < VDC_RING_MAX_TP; ++q)
+                if (q < J.group) v += acc[q];
+            v += abf ? bf_lo(ldcg_u16(reinterpret_cast<const uint16_t*>(ab) + aoff + r))
+                     : ldcg_f32(reinterpret_cast<const float*>(ab) + aoff + r);
+            store_out(ob, obf, r, v);
+        }
+        publish(J.o_t);
+    }
+
     // ------------------------------------------- ELEMWISE copy (embedding row)
     __device__ void copy_row(const vdc_job& J) {
         const int32_t eb = P->descs[J.x_t].elem;
@@ -996,6 +1049,7 @@ __device__ void vcc_role(const RingParams& P, Shared& S, char* ring) {
                 break;
             }
             case OP_ATTN_COMBINE: v.combine(J); break;
+            case OP_ALLREDUCE_ADD: v.allreduce(J); break;
             case OP_ELEMWISE: v.copy_row(J); break;
             default:
                 if (v.ct == 0) v.fire(4, (core << 16) | pc);

@@ -98,6 +98,8 @@ decode::LayoutConfig layout_from(const json& j) {
     l.gu_block = j.value("gu_block", l.gu_block);
     l.wtile_bytes = j.value("wtile_bytes", l.wtile_bytes);
     l.ring = j.value("ring", l.ring);
+    l.tp_world = j.value("tp_world", l.tp_world);
+    l.tp_rank = j.value("tp_rank", l.tp_rank);
     return l;
 }
 
@@ -243,7 +245,8 @@ std::string ProgramBox::text(int mode) const {
         descs.push_back({{"name", d.tensor}, {"index", d.index}, {"base", d.base}, {"shape", d.shape},
                          {"grid", d.grid}, {"tile", {d.tile_rows, d.tile_cols}}, {"dtype", std::string(workload::elem_name(d.elem))},
                          {"view_of", d.view_of}, {"external", d.external}, {"state", d.state},
-                         {"init", int(d.init)}, {"init_scale", d.init_scale}});
+                         {"init", int(d.init)}, {"init_scale", d.init_scale},
+                         {"symmetric", d.symmetric}});
     out["descriptors"] = descs;
     out["params"] = program.params;
     out["ring_slots"] = program.ring_slots;

@@ -129,7 +129,10 @@ struct Builder {
     // be a multiple of the tile rows so tiles never straddle two jobs
     std::string weight(const std::string& name, int64_t rows, int64_t cols, int64_t job_rows, float fan_in) {
         auto [tr, tc] = weight_tile(rows, cols, m.dtype, l);
-        while (job_rows % tr) --tr;
+        if (l.ring)
+            job_rows = tr;  // ring jobs are tile aligned only (the lowering splits rows per SM)
+        else
+            while (job_rows % tr) --tr;
         const InitKind init = m.scaled_init ? InitKind::centered : InitKind::random;
         const float scale = m.scaled_init ? float(1.0 / std::sqrt(double(fan_in))) : 1.0f;
         // the word format encodes tile coordinates in 12 bits: tall matrices
@@ -167,12 +170,27 @@ OperatorGraph build_decode_graph(const ModelConfig& m, const LayoutConfig& l) {
     if (m.head_dim % l.job_rows || l.job_rows % 2) throw workload::WorkloadError("job_rows must divide head_dim and be even");
     if (m.heads % m.kv_heads) throw workload::WorkloadError("heads must be a multiple of kv_heads");
     if (l.max_ctx < l.ctx_pages * l.page_rows) throw workload::WorkloadError("max_ctx below ctx_pages*page_rows");
+    const bool tp = l.tp_world >= 1;
+    const int64_t W = tp ? l.tp_world : 1;
+    if (tp && (l.tp_rank < 0 || l.tp_rank >= W || m.kv_heads % W || m.ffn % (W * (l.gu_block / 2)) || m.vocab % W))
+        throw workload::WorkloadError("tensor parallelism needs kv_heads, ffn (in gu blocks) and vocab divisible by tp_world");
     Builder b{{}, m, l};
     const ElemType e = m.dtype;
-    const int64_t d = m.hidden, hd = m.head_dim, hq = m.heads, hkv = m.kv_heads, grp = hq / hkv;
-    const int64_t qrows = hq * hd, kvrows = hkv * hd, R = l.job_rows;
+    const int64_t d = m.hidden, hd = m.head_dim, hq = m.heads / W, hkv = m.kv_heads / W, grp = hq / hkv;
+    const int64_t qrows = hq * hd, kvrows = hkv * hd, R = l.job_rows, ffn = m.ffn / W, vocab = m.vocab / W;
     const int64_t splits = (l.ctx_pages + l.pages_per_job - 1) / l.pages_per_job;
     const std::string eps = num(m.eps), theta = num(m.theta);
+    const std::map<std::string, std::string> tp_attrs = {{"tp_world", std::to_string(W)}, {"tp_rank", std::to_string(l.tp_rank)}};
+    auto with = [](std::map<std::string, std::string> a, const std::map<std::string, std::string>& extra) {
+        a.insert(extra.begin(), extra.end());
+        return a;
+    };
+    // TP exchange buffer: one (D,1) fp32 slot per rank, peer mapped
+    auto sym = [&](const std::string& name) {
+        TensorRef& t = b.add(name, {W * d, 1}, d, 1, InitKind::zeros, ElemType::f32);
+        t.symmetric = true;
+        return name;
+    };
 
     b.add("embed.table", {m.vocab, d}, 1, d, m.scaled_init ? InitKind::centered : InitKind::random, e);
     b.vec("embed.x", d, d, e);
@@ -200,25 +218,37 @@ OperatorGraph build_decode_graph(const ModelConfig& m, const LayoutConfig& l) {
         b.vec(L + "attn", qrows, grp * hd, e);
         // the combine reads all partials of one kv head as a single tile
         b.node(L + "comb", OpKind::ATTN_COMBINE, {b.view(L + "part", ".head", splits * grp)}, {L + "attn"});
-        b.weight(L + "wo", d, qrows, R, float(qrows));
+        b.weight(L + "wo", d, qrows, R, float(qrows * W));
         b.vec(L + "x1", d, R, e);
-        b.node(L + "o", OpKind::GEMV_ADD, {L + "wo", b.view(L + "attn", ".all", qrows), b.view(x, ".blk", R)}, {L + "x1"},
-               {{"job_rows", std::to_string(R)}});
+        if (tp) {  // row-parallel o-proj: partial sums -> all ranks' slots -> allreduce + residual
+            b.node(L + "o", OpKind::GEMV, {L + "wo", b.view(L + "attn", ".all", qrows)}, {sym(L + "o.part")},
+                   with({{"job_rows", std::to_string(R)}}, tp_attrs));
+            b.node(L + "o.ar", OpKind::ALLREDUCE_ADD, {L + "o.part", x}, {L + "x1"}, tp_attrs);
+        } else {
+            b.node(L + "o", OpKind::GEMV_ADD, {L + "wo", b.view(L + "attn", ".all", qrows), b.view(x, ".blk", R)}, {L + "x1"},
+                   {{"job_rows", std::to_string(R)}});
+        }
         // MLP block
         b.norm(L + "mlp_norm", d);
-        b.weight(L + "wgu", 2 * int64_t(m.ffn), d, l.gu_block, float(d));
-        b.vec(L + "a", m.ffn, l.gu_block / 2, e);
+        b.weight(L + "wgu", 2 * ffn, d, l.gu_block, float(d));
+        b.vec(L + "a", ffn, l.gu_block / 2, e);
         b.node(L + "gu", OpKind::RMS_GEMV, {L + "wgu", b.view(L + "x1", ".all", d), L + "mlp_norm"}, {L + "a"},
                {{"eps", eps}, {"swiglu", std::to_string(l.gu_block)}, {"job_rows", std::to_string(l.gu_block)}});
-        b.weight(L + "wd", d, m.ffn, R, float(m.ffn));
+        b.weight(L + "wd", d, ffn, R, float(ffn * W));
         b.vec(L + "x2", d, R, e);
-        b.node(L + "down", OpKind::GEMV_ADD, {L + "wd", b.view(L + "a", ".all", m.ffn), L + "x1"}, {L + "x2"},
-               {{"job_rows", std::to_string(R)}});
+        if (tp) {
+            b.node(L + "down", OpKind::GEMV, {L + "wd", b.view(L + "a", ".all", ffn)}, {sym(L + "d.part")},
+                   with({{"job_rows", std::to_string(R)}}, tp_attrs));
+            b.node(L + "down.ar", OpKind::ALLREDUCE_ADD, {L + "d.part", L + "x1"}, {L + "x2"}, tp_attrs);
+        } else {
+            b.node(L + "down", OpKind::GEMV_ADD, {L + "wd", b.view(L + "a", ".all", ffn), L + "x1"}, {L + "x2"},
+                   {{"job_rows", std::to_string(R)}});
+        }
         x = L + "x2";
     }
     b.norm("final_norm", d);
-    b.weight("lm_head", m.vocab, d, l.head_job_rows, float(d));
-    b.add("logits", {m.vocab, 1}, l.head_job_rows, 1, InitKind::zeros, ElemType::f32);
+    b.weight("lm_head", vocab, d, l.head_job_rows, float(d));  // vocab-parallel: this rank's logit rows
+    b.add("logits", {vocab, 1}, l.head_job_rows, 1, InitKind::zeros, ElemType::f32);
     b.node("head", OpKind::RMS_GEMV, {"lm_head", b.view(x, ".all", d), "final_norm"}, {"logits"},
            {{"eps", eps}, {"job_rows", std::to_string(l.head_job_rows)}});
     b.g.validate();

@@ -117,6 +117,7 @@ std::vector<TileDescriptor> build_descriptors(const workload::OperatorGraph& g) 
         d.view_of = t.view_of.empty() ? -1 : int32_t(g.tensor_index(g.storage_of(t.name).name));
         d.state = t.state;
         d.init_scale = t.init_scale;
+        d.symmetric = t.symmetric;
         base += d.tile_count();
         out.push_back(std::move(d));
     }

@@ -81,7 +81,7 @@ class RingLowering {
         }
         for (auto& r : jobs_) {
             auto need = [&](int32_t t) { return t >= 0 && writers.count(storage(uint16_t(t))) ? writers.at(storage(uint16_t(t))) : 0; };
-            r.j.x_need = need(r.j.x_t);
+            if (!(r.j.flags & VDC_JOB_SYM_IN)) r.j.x_need = need(r.j.x_t);
             r.j.a_need = need(r.j.a_t);
             r.j.b_need = need(r.j.b_t);
         }
@@ -138,6 +138,9 @@ class RingLowering {
                 break;
             case OpKind::ATTN_COMBINE:
                 plan_combine(n, ordinal);
+                break;
+            case OpKind::ALLREDUCE_ADD:
+                plan_allreduce(n, ordinal);
                 break;
             case OpKind::EMBED_ROW: {
                 // no µop: consumers read the embedding row in place (TOKEN_ROW /
@@ -256,6 +259,11 @@ class RingLowering {
                     } else {
                         r.publishes.push_back(j.o_t);
                     }
+                    if (desc_[reg.out].symmetric) {  // TP partial sums: this rank's slot of every rank's buffer
+                        j.flags |= VDC_JOB_SYM_OUT;
+                        j.o_off = int32_t(attr_int(n, "tp_rank", 0) * M);
+                        j.group = int32_t(attr_int(n, "tp_world", 1));
+                    }
                     if (swiglu) {
                         j.flags |= VDC_JOB_SWIGLU;
                         j.block = int32_t(swiglu);
@@ -332,6 +340,44 @@ class RingLowering {
             }
         }
         attn_ = {hkv, splits, grp, hd, k};
+    }
+
+    // ALLREDUCE_ADD: x_next = residual + sum of the W rank slots of the
+    // symmetric partial buffer (fixed rank order), rows split over the SMs
+    // like a GEMV share; no ring tiles. The readiness target of the partials
+    // is world x (this rank's producer µops): every rank runs the same split.
+    void plan_allreduce(const workload::OperatorNode& n, uint32_t ordinal) {
+        const int32_t part = storage(idx(n.inputs[0])), res = storage(idx(n.inputs[1])), out = storage(idx(n.outputs[0]));
+        const int64_t d = desc_[uint16_t(out)].rows(), W = attr_int(n, "tp_world", 1);
+        int32_t producers = 0;
+        for (const auto& r : jobs_)
+            for (int32_t t : r.publishes) producers += t == part;
+        const int64_t unit = 8, units = ceil_div<int64_t>(d, unit);
+        for (uint32_t s = 0; s < sms_; ++s) {
+            const auto [u0, u1] = share(units, s);
+            if (u0 == u1) continue;
+            RJob r;
+            r.ordinal = ordinal;
+            r.sm = s;
+            vdc_job& j = r.j;
+            j = blank(Opcode::ALLREDUCE_ADD);
+            j.flags = VDC_JOB_SYM_IN | VDC_JOB_RESID;
+            j.r0 = int32_t(u0 * unit);
+            j.r1 = int32_t(std::min(d, u1 * unit));
+            j.k = int32_t(d);
+            j.group = int32_t(W);
+            j.x_t = part;
+            j.x_need = int32_t(W) * producers;  // fixed here: the symmetric counter collects every rank
+            j.a_t = res;
+            if (j.a_t == embed_out_) {
+                j.a_t = embed_tab_;
+                j.flags |= VDC_JOB_TOKEN_AUX;
+                j.cache_rows = embed_len_;
+            }
+            j.o_t = out;
+            r.publishes.push_back(out);
+            jobs_.push_back(std::move(r));
+        }
     }
 
     // ring mode fuses the combine into the attention jobs (the last split of

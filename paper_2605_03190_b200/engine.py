@@ -107,6 +107,30 @@ class Engine:
             out[d["name"]] = t
         return out
 
+    def bind_inputs_nonsym(self, arrays: dict) -> dict:
+        """bind_inputs for every storage tensor except the symmetric (TP) buffers"""
+        torch = _torch()
+        out = {}
+        for d in self.info["descriptors"]:
+            if d["view_of"] >= 0 or d.get("symmetric"):
+                continue
+            n = int(np.prod(d["shape"]))
+            dt = getattr(torch, TORCH_DTYPE[d["dtype"]])
+            if d["name"] in arrays:
+                t = torch.from_numpy(np.ascontiguousarray(arrays[d["name"]], dtype=np.float32).reshape(-1)).to(
+                    f"cuda:{self.device}").to(dt)
+            else:
+                t = torch.zeros(n, dtype=dt, device=f"cuda:{self.device}")
+            self.bind(d["name"], t)
+            out[d["name"]] = t
+        return out
+
+    def bind_symmetric(self, name: str, peer_ptrs: list, world: int, rank: int) -> None:
+        """TP exchange buffer: peer_ptrs[q] = rank q's buffer (128-byte header + data)"""
+        d = self.descs[name]
+        arr = (ctypes.c_void_p * len(peer_ptrs))(*peer_ptrs)
+        check(lib().vdc_bind_symmetric(self._h, d["index"], arr, world, rank))
+
     def bind_step(self, tensor) -> None:
         """Device-resident int64 step block (token, pos, ctx, ...)."""
         check(lib().vdc_bind_step(self._h, ctypes.c_void_p(tensor.data_ptr()), tensor.numel()))

@@ -59,9 +59,9 @@ def synth_inputs(info: dict, seed: int = 0) -> dict:
     return out
 
 
-def check_against_dense(info: dict, req: dict, ins: dict, host: dict, token: int, pos: int) -> dict:
+def check_against_dense(info: dict, req: dict, ins: dict, host: dict, token: int, pos: int, cfg: dict | None = None) -> dict:
     """Errors of the device results vs the dense numpy reference."""
-    cfg = model_cfg(info, req)
+    cfg = cfg or model_cfg(info, req)
     ref = decode_ref.decode_step(ins, cfg, token, pos)
     lg, rl = host["logits"].astype(np.float64), ref["logits"].astype(np.float64)
     res = {"logits_max_abs": float(np.abs(lg - rl).max()), "logits_rms": float(np.sqrt(np.mean(rl ** 2))),

@@ -124,3 +124,31 @@ def test_attention_pages_read_once():
     # every (kv head, page) of L0.kc / L0.vc loaded once (a lead pad may repeat one)
     assert len(pages) == 2 * 8 * 64
     assert sum(pages.values()) - len(pages) <= info["sm_count"]
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_tp_rank_programs_shard_the_model(world):
+    """Megatron split of Llama-3-8B: every rank holds 1/world of the
+    projection rows/columns and of the vocabulary, the o and down GEMVs write
+    this rank's slot of a symmetric (W*D) partial buffer, and one
+    ALLREDUCE_ADD per block sums the slots in rank order."""
+    totals = collections.Counter()
+    for rank in range(world):
+        req = bench.model_request(2)
+        req["layout"]["tp_world"], req["layout"]["tp_rank"] = world, rank
+        req["profile"]["sm_count"] = 148
+        prog = Program.build(req)
+        info = prog.info()
+        assert prog.text(False)["certificate_ok"]
+        ds = {d["name"]: d for d in info["descriptors"]}
+        assert ds["L0.wqkv"]["shape"][0] == (4096 + 2 * 1024) // world
+        assert ds["L0.wo"]["shape"] == [4096, 4096 // world]
+        assert ds["L0.wd"]["shape"] == [4096, 14336 // world]
+        assert ds["L0.o.part"]["symmetric"] and ds["L0.o.part"]["shape"] == [world * 4096, 1]
+        ar = [j for j in info["jobs"] if j["op"] == 0x2C]
+        assert sum(j["r1"] - j["r0"] for j in ar) == 2 * 2 * 4096  # 2 allreduces x 2 layers x D rows
+        sym_out = [j for j in info["jobs"] if j["flags"] & 0x100]
+        assert all(j["o"][1] == rank * 4096 for j in sym_out)
+        totals["lm_head"] += ds["lm_head"]["shape"][0] * ds["lm_head"]["shape"][1] if len(ds["lm_head"]["shape"]) == 2 else \
+            ds["lm_head"]["shape"][0] * ds["lm_head"]["shape"][1] * ds["lm_head"]["shape"][2]
+    assert totals["lm_head"] == 128256 * 4096
