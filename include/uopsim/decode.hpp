@@ -19,6 +19,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "uopsim/workload.hpp"
 
@@ -55,6 +56,15 @@ struct LayoutConfig {
     // hidden vector, vocab-parallel lm_head, replicated embedding and norms)
     int tp_world = 0;
     int tp_rank = 0;
+    // batched decode (ext): batch >= 1 builds the graph of
+    // `batch` concurrent requests: activations (npad, width) with the
+    // request index as the row, 128 x 64 weight tiles for the tcgen05 GEMM
+    // µops (BGEMM), KV caches as page pools (pool_pages, kv_heads * 64, hd)
+    // addressed through a page table; request b covers req_pages[b] logical
+    // pages (its context capacity in this program), allocated contiguously
+    // in the pool (the page table is part of the lowered program).
+    int batch = 0;
+    std::vector<int> req_pages;
 };
 
 ModelConfig llama3_8b();
@@ -63,6 +73,8 @@ ModelConfig llama3_70b();
 ModelConfig tiny_llama();
 
 workload::OperatorGraph build_decode_graph(const ModelConfig& m, const LayoutConfig& l);
+workload::OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfig& l);
+int batch_npad(int batch);  // MMA N of a batch: 16, 32 or 64
 
 // weight tile shape (rows, cols) used for a (M,K) matrix under `l`
 std::pair<int64_t, int64_t> weight_tile(int64_t rows, int64_t cols, workload::ElemType e, const LayoutConfig& l);

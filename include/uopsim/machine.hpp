@@ -194,6 +194,7 @@ class Machine {
             x.tile_cols = d.tile_cols;
             x.dtype = uint32_t(d.elem);
             x.view_of = d.view_of;
+            x.tma = d.tma;
             ds.push_back(x);
         }
         detail::check(vdc_load_program(ctx_, words.data(), per_core.data(), uint32_t(per_core.size()), qs.data(),

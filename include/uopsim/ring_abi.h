@@ -58,6 +58,22 @@
 #define VDC_SYM_HEADER_BYTES 128 /* symmetric buffer = header (u32 readiness counter) + data */
 #define VDC_JOB_QKV 0x80        /* fused q|k|v rows: q -> o_t, k -> cache b_t, v -> cache o2_t;
                                    block = q rows, split = k (= v) rows; rotary on q and k */
+#define VDC_JOB_BATCH 0x400     /* batched program (nb requests): per-request token / pos / ctx in
+                                   the step block (3 int64 each), paged KV pools, page table at
+                                   step[ptab + b * maxp + logical page] */
+
+/* Batched programs (BGEMM and friends, layout.batch > 1):
+ *  - activations are (npad, K) bf16 row-major, request b = row b; rows
+ *    >= nb stay zero. npad in {16, 32, 64} is the tcgen05 MMA N.
+ *  - weight tiles are 128 rows x 64 columns moved by TMA tensor copies
+ *    with 128-byte swizzle (vdc_desc.tma = 128), the canonical K-major
+ *    operand layout of tcgen05.mma; activation chunks (npad x 64) are
+ *    loaded by the compute core's MMA issuer after the readiness wait
+ *    (vdc_desc.tma = npad).
+ *  - KV caches are page pools (pages, hkv * 64, hd): tile (page, head). */
+#define VDC_RING_BGEMM_ROWS 128  /* output rows per BGEMM job (MMA M) */
+#define VDC_RING_BGEMM_KT 64     /* reduction columns per weight tile (128-byte swizzle atom) */
+#define VDC_RING_MAX_BATCH 64
 
 typedef struct vdc_job {
     int32_t op;               /* isa opcode of the compute µop                */
@@ -80,7 +96,18 @@ typedef struct vdc_job {
     int32_t arrive_ctr;       /* ATTN: per-kv-head arrival counter (index into the counter array) */
     int32_t arrive_need;      /* ATTN: split jobs per kv head; the last to arrive combines */
     int32_t o2_t, o2_off;     /* ATTN: combined output (attention vector of the head's q heads) */
-    int32_t split;            /* ATTN: split index of this job within its kv head */
-} vdc_job;  /* 128 bytes */
+    int32_t split;            /* ATTN: split index of this job within its kv head;
+                                 BGEMM: piece index within its row block */
+    /* ---- batched programs (VDC_JOB_BATCH) ---- */
+    int32_t kt0, kt1;         /* BGEMM: reduction tiles [kt0, kt1) of this piece (stream-K share) */
+    int32_t nb, npad;         /* requests in the batch; MMA N (activation rows incl. padding) */
+    int32_t x2_t, x2_need;    /* BGEMM + RMS: raw activations the per-request rms scale is taken from */
+    int32_t o3_t, w3_t;       /* BGEMM + RESID: second output o3 = bf16(out * w3) (next RMSNorm's operand) */
+    int32_t part_t, part_off; /* BGEMM stream-K: fp32 partial buffer, this piece's slot (npad x 128 floats) */
+    int32_t req;              /* ATTN / ELEMWISE: request index (first request of an embed job) */
+    int32_t ptab, maxp;       /* page table: step-block offset and pages per request row */
+    int32_t kvrows;           /* BGEMM + QKV: k (= v) rows */
+    int32_t rsv[2];
+} vdc_job;  /* 192 bytes */
 
 #endif

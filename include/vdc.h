@@ -65,7 +65,8 @@ typedef struct vdc_desc {
     uint32_t rank;      /* rank of shape == rank of grid                  */
     uint32_t dtype;     /* VDC_DTYPE_*                                    */
     int32_t view_of;    /* storage owner descriptor, -1 = owns storage    */
-    uint32_t pad;
+    uint32_t tma;       /* ext: >0 = TMA tensor map with a {64 x tma} box, 128-byte swizzle
+                           (batched ring programs: weights tma=128, activations tma=npad) */
 } vdc_desc;
 
 /* Dependency queue wiring (generator::QueueInfo). */

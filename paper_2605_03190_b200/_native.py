@@ -38,7 +38,7 @@ class vdc_desc(ctypes.Structure):
         ("rank", ctypes.c_uint32),
         ("dtype", ctypes.c_uint32),
         ("view_of", ctypes.c_int32),
-        ("pad", ctypes.c_uint32),
+        ("tma", ctypes.c_uint32),
     ]
 
 

@@ -1853,6 +1853,11 @@ struct vdc_ctx {
     uint32_t tp_rank = 0, tp_world = 1;
     unsigned long long* d_tile_trace = nullptr;
     bool ring_attr_set = false;
+    // batched ring programs: TMA tensor maps of the descriptors with vdc_desc.tma > 0
+    std::vector<CUtensorMap> tmaps_host;
+    CUtensorMap* d_tmaps = nullptr;
+    bool tmaps_dirty = false;
+    bool batched = false;
 };
 
 namespace {
@@ -1925,6 +1930,7 @@ int vdc_destroy(vdc_ctx* ctx) {
     dfree(ctx->d_params);
     dfree(ctx->d_jobs);
     dfree(ctx->d_sym);
+    dfree(ctx->d_tmaps);
     dfree(ctx->d_stats);
     dfree(ctx->d_status);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -1979,6 +1985,7 @@ int vdc_load_program(vdc_ctx* ctx, const uint8_t* words, const uint32_t* words_p
     ctx->bound.assign(n_desc, nullptr);
     ctx->bound_bytes.assign(n_desc, 0);
     ctx->dev_descs.assign(n_desc, DevDesc{});
+    uint32_t n_tmaps = 0;
     for (uint32_t i = 0; i < n_desc; ++i) {
         const vdc_desc& s = descs[i];
         DevDesc& d = ctx->dev_descs[i];
@@ -2005,7 +2012,17 @@ int vdc_load_program(vdc_ctx* ctx, const uint8_t* words, const uint32_t* words_p
         d.elem = s.dtype == VDC_DTYPE_BF16 ? 2 : s.dtype == VDC_DTYPE_I64 ? 8 : 4;
         d.storage = s.view_of >= 0 ? s.view_of : int32_t(i);
         d.ptr = nullptr;
+        d.tmap = -1;
+        if (s.tma) {
+            if (s.view_of >= 0 || s.rank != 2 || s.dtype != VDC_DTYPE_BF16 || s.tma > 256 || s.shape[1] % 64)
+                return fail(VDC_ERR_INPUT, "TMA descriptors must be owned rank-2 bf16 tensors with 64-column tiles");
+            d.tmap = int32_t(n_tmaps++);
+        }
     }
+    ctx->tmaps_host.assign(n_tmaps, CUtensorMap{});
+    dfree(ctx->d_tmaps);
+    if (n_tmaps) CU(cudaMalloc(&ctx->d_tmaps, sizeof(CUtensorMap) * n_tmaps));
+    ctx->tmaps_dirty = n_tmaps > 0;
     ctx->max_dep = 0;
     for (uint32_t i = 0; i < n_queues; ++i) ctx->max_dep = std::max<uint32_t>(ctx->max_dep, queues[i].dep_id);
     ctx->dep_init.assign(ctx->max_dep + 1, DepQueue{0, 0, 4, 0, {0, 0, 0, 0}});
@@ -2036,9 +2053,21 @@ int vdc_load_jobs(vdc_ctx* ctx, const vdc_job* jobs, uint32_t n_jobs, uint32_t r
     if (ring_slots < VDC_RING_COMPUTE_WARPS || ring_slots == VDC_RING_COMPUTE_WARPS + 1 || ring_slots > ctx->prof.slot_budget ||
         ring_slots > VDC_RING_MAX_SLOTS)
         return fail(VDC_ERR_INPUT, "ring_slots must be 8, 10, 11 or 12 (<= slot_budget)");
+    bool batched = false;
     for (uint32_t i = 0; i < n_jobs; ++i) {
         const vdc_job& j = jobs[i];
-        for (int32_t t : {j.x_t, j.a_t, j.b_t, j.o_t})
+        if (j.flags & VDC_JOB_BATCH) {
+            batched = true;
+            if (j.npad != 16 && j.npad != 32 && j.npad != 64) return fail(VDC_ERR_INPUT, "batched jobs need npad 16, 32 or 64");
+            if (j.nb < 1 || j.nb > j.npad) return fail(VDC_ERR_INPUT, "batched job request count out of range");
+        }
+        if (j.op == 0x2D) {
+            for (int32_t t : {j.x_t})
+                if (t < 0 || t >= int32_t(ctx->descs.size()) || ctx->dev_descs[size_t(t)].tmap < 0 ||
+                    ctx->descs[size_t(t)].tma != uint32_t(j.npad))
+                    return fail(VDC_ERR_INPUT, "job " + std::to_string(i) + ": BGEMM activations need an npad-row tensor map");
+        }
+        for (int32_t t : {j.x_t, j.a_t, j.b_t, j.o_t, j.o2_t, j.x2_t, j.o3_t, j.w3_t, j.part_t})
             if (t >= int32_t(ctx->descs.size())) return fail(VDC_ERR_INPUT, "job " + std::to_string(i) + " names an unknown tensor");
         if (j.tile_rows > VDC_RING_MAX_TILE_ROWS && (j.op == 0x27 || j.op == 0x28 || j.op == 0x29))
             return fail(VDC_ERR_INPUT, "job " + std::to_string(i) + ": tile rows exceed the engine limit");
@@ -2056,6 +2085,7 @@ int vdc_load_jobs(vdc_ctx* ctx, const vdc_job* jobs, uint32_t n_jobs, uint32_t r
     if (n_jobs) CU(cudaMemcpy(ctx->d_jobs, jobs, sizeof(vdc_job) * n_jobs, cudaMemcpyHostToDevice));
     ctx->n_jobs = n_jobs;
     ctx->ring = true;
+    ctx->batched = batched;
     ctx->ring_slots = ring_slots;
     ctx->epoch = 0;
     CU(cudaMemset(ctx->d_counters, 0, sizeof(uint32_t) * ctx->n_counters));
@@ -2077,6 +2107,30 @@ int vdc_bind_tensor(vdc_ctx* ctx, uint16_t tensor, void* dptr, size_t bytes, int
     for (size_t i = 0; i < ctx->dev_descs.size(); ++i)
         if (ctx->dev_descs[i].storage == int32_t(tensor)) ctx->dev_descs[i].ptr = static_cast<char*>(dptr);
     ctx->descs_dirty = true;
+    if (d.tmap >= 0) {
+        // {64 columns x tma rows} boxes, 128-byte swizzle: the K-major SW128
+        // operand layout of tcgen05.mma (ring_engine.cu, bgemm)
+        using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+        static EncodeFn enc = nullptr;
+        if (!enc) {
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q) !=
+                    cudaSuccess || !enc)
+                return fail(VDC_ERR_INTERNAL, "cuTensorMapEncodeTiled unavailable");
+        }
+        if (reinterpret_cast<uintptr_t>(dptr) & 15) return fail(VDC_ERR_INPUT, "TMA tensors must be 16-byte aligned");
+        const cuuint64_t dims[2] = {cuuint64_t(d.cols), cuuint64_t(d.rows)};
+        const cuuint64_t strides[1] = {cuuint64_t(d.cols) * 2};
+        const cuuint32_t box[2] = {64, s.tma};
+        const cuuint32_t es[2] = {1, 1};
+        const CUresult r = enc(&ctx->tmaps_host[size_t(d.tmap)], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dptr, dims, strides, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(VDC_ERR_INPUT, "tensor map encode failed for tensor " + std::to_string(tensor));
+        ctx->tmaps_dirty = true;
+    }
     return VDC_OK;
 }
 
@@ -2171,6 +2225,13 @@ int vdc_launch(vdc_ctx* ctx, void* stream) {
         R.sym = ctx->d_sym;
         R.tp_rank = ctx->tp_rank;
         R.tp_world = ctx->tp_world;
+        if (ctx->tmaps_dirty) {
+            CU(cudaMemcpyAsync(ctx->d_tmaps, ctx->tmaps_host.data(), sizeof(CUtensorMap) * ctx->tmaps_host.size(),
+                               cudaMemcpyHostToDevice, s));
+            ctx->tmaps_dirty = false;
+        }
+        R.tmaps = ctx->d_tmaps;
+        R.batched = ctx->batched ? 1u : 0u;
         if (R.debug & 2u) {
             static unsigned long long* tt = nullptr;
             if (!tt) cudaMalloc(&tt, sizeof(unsigned long long) * 3 * 65536);
@@ -2300,6 +2361,7 @@ int vdc_program_load(vdc_ctx* ctx, const vdc_program* prog) {
             x.tile_cols = d.tile_cols;
             x.dtype = uint32_t(d.elem);
             x.view_of = d.view_of;
+            x.tma = d.tma;
             ds.push_back(x);
         }
         int rc = vdc_load_program(ctx, words.data(), per_core.data(), uint32_t(per_core.size()), qs.data(), uint32_t(qs.size()),

@@ -44,6 +44,8 @@ struct DevDesc {
     int32_t elem;         // bytes per element
     int32_t dtype;        // VDC_DTYPE_*
     int32_t storage;      // counter index (owner descriptor)
+    int32_t tmap;         // index into RingParams::tmaps (batched ring programs), -1 = none
+    int32_t pad_;
 };
 
 struct DepQueue {          // global FIFO per dep id (single producer / consumer site)
@@ -123,6 +125,8 @@ struct RingParams {
     unsigned long long watchdog_ns;
     unsigned long long* trace;  // optional: per VCC core trace_cap records {core<<32|pc, t_enter, t_ready, t_done}
     uint32_t trace_cap;
+    uint32_t batched;           // batched program: TMEM accumulator + X ring for BGEMM µops
+    const void* tmaps;          // CUtensorMap[] (64-byte aligned), indexed by DevDesc::tmap
 };
 size_t ring_smem_bytes(uint32_t ring_slots);
 const void* ring_kernel_entry();

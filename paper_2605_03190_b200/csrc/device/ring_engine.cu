@@ -53,8 +53,10 @@ constexpr int MAX_DPL = MAX_HD / 32;
 
 enum : uint32_t {
     OP_LOAD = 0x01, OP_ELEMWISE = 0x25, OP_GEMV = 0x27, OP_RMS_GEMV = 0x28, OP_GEMV_ADD = 0x29, OP_ATTN_DECODE = 0x2A,
-    OP_ATTN_COMBINE = 0x2B, OP_ALLREDUCE_ADD = 0x2C, OP_HALT = 0x45,
+    OP_ATTN_COMBINE = 0x2B, OP_ALLREDUCE_ADD = 0x2C, OP_BGEMM = 0x2D, OP_HALT = 0x45,
 };
+constexpr int NXMAX = 8;            // activation-chunk ring depth of batched GEMMs
+constexpr uint32_t TMEM_COLS = 64;  // fp32 accumulator columns (>= npad)
 
 // stat slots (SmStats::wait)
 enum : int { S_VMC_EMPTY = 0, S_VCC_FULL = 1, S_VCC_DEP = 2, S_VCC_EPI = 3, S_VCC_TOTAL = 4, S_VMC_TOTAL = 5, S_NJOBS = 6 };
@@ -66,7 +68,12 @@ struct alignas(16) Shared {
     float bc[2 * CW];
     float rope_cs[MAX_HD / 2], rope_sn[MAX_HD / 2];  // rotary table of the launch's position
     int32_t flag;
-    alignas(16) uint4 x[XBUF / 16];  // GEMV input vector (normalised, model dtype), reused across jobs
+    // batched programs: activation-chunk ring (in x), MMA completion, TMEM base, rms scales
+    uint64_t xfull[NXMAX], xempty[NXMAX], mma_bar;
+    uint32_t tmem_base;
+    float binv[VDC_RING_MAX_BATCH];
+    alignas(1024) uint4 x[XBUF / 16];  // GEMV input vector (normalised, model dtype), reused across jobs;
+                                       // batched programs: activation chunks (128-byte swizzle, 1 KB aligned)
 };
 
 size_t smem_bytes(uint32_t slots) { return size_t(slots) * SLOT + ((sizeof(Shared) + 127) & ~size_t(127)); }
@@ -638,6 +645,319 @@ struct Vcc {
         }
     }
 
+    // ------------------------------------------------------------ BGEMM
+    // Batched GEMM µop (batched programs): out[b][r] = sum_k W[r][k] X[b][k]
+    // for the 128 W rows [r0, r0 + 128) and the nb requests, reduction tiles
+    // [kt0, kt1) (a stream-K piece of the row block).
+    //  * W tiles (128 x 64 bf16, 128-byte swizzle) arrive in the ring from
+    //    the memory core (TMA tensor copies, prefetched across operators).
+    //  * activation chunks (npad x 64) are loaded by the MMA issuer (thread 0)
+    //    after the readiness wait, into a small ring in the x buffer; the
+    //    issuer keeps NX - 1 chunks in flight.
+    //  * thread 0 issues 4 tcgen05.mma (M=128, N=npad, K=16) per tile into the
+    //    TMEM accumulator; tcgen05.commit hands the W slot back to the memory
+    //    core (its empty barrier) and the chunk buffer back to the issuer once
+    //    the MMAs that read them completed.
+    //  * epilogue: tcgen05.ld (warp w: TMEM lanes 32 (w % 4) .. , columns
+    //    (w / 4) * npad / 2 ..); pieces of a split row block add their fp32
+    //    partials in piece order (the last to arrive finishes the block);
+    //    per-request rms scale, rotary / KV append / SwiGLU / residual, stores.
+    uint32_t tmem = 0;
+    uint32_t xq = 0, xd = 0;  // activation chunks issued / consumed (issuer thread)
+    uint32_t nmma = 0;        // BGEMM µops completed (mma_bar phase)
+    int32_t binv_t = -2;      // activations the cached rms scales belong to
+
+    __device__ float* f32p(int32_t t) const { return reinterpret_cast<float*>(tptr(t)); }
+    __device__ uint16_t* u16p(int32_t t) const { return reinterpret_cast<uint16_t*>(tptr(t)); }
+    __device__ int64_t req_pos(int b) const { return P->step[3 * b + 1]; }
+
+    __device__ bool spin(uint64_t* bar, uint32_t parity) {
+        if (mbar_try(bar, parity)) return true;
+        const unsigned long long t0 = now_ns();
+        for (uint32_t n = 1;; ++n) {
+            if (mbar_wait_hint(bar, parity)) return true;
+            if ((n & 15) == 0) {
+                if (aborted()) return false;
+                if (P->watchdog_ns && now_ns() - t0 > P->watchdog_ns) {
+                    fire(0, 0x40000u);
+                    return false;
+                }
+            }
+        }
+    }
+
+    __device__ void bgemm(const vdc_job& J) {
+        const int n = J.kt1 - J.kt0, K = J.k, nb = J.nb, npad = J.npad;
+        const bool rms = J.flags & VDC_JOB_RMS;
+        if (!wait_ready(J.x_t, J.x_need, rms ? J.x2_t : -1, J.x2_need, (J.flags & VDC_JOB_RESID) ? J.a_t : -1, J.a_need)) {
+            ok = false;
+            return;
+        }
+        if (rms && binv_t != J.x2_t) {  // per-request 1 / rms of the raw activations (warp per request)
+            const uint16_t* xr = u16p(J.x2_t);
+            for (int b = int(w); b < nb; b += CW) {
+                const uint4* row = reinterpret_cast<const uint4*>(xr + int64_t(b) * K);
+                float ss = 0.f;
+                for (int c = int(lane); c < K / 8; c += 32) {
+                    const uint4 u = ldcg128(row + c);
+                    ss += dot16<true>(u, u);
+                }
+                ss = warp_sum(ss);
+                if (lane == 0) S->binv[b] = 1.0f / sqrtf(ss / float(K) + J.eps);
+            }
+            binv_t = J.x2_t;
+            sync();
+        }
+        const uint32_t xbytes = uint32_t(npad) * 128u;
+        const uint32_t NX = min(uint32_t(NXMAX), uint32_t(XBUF) / xbytes);
+        const uint32_t xb0 = smem_addr(S->x);
+        if (ct == 0) {
+            // generic writes (other SMs' epilogues, this CTA's scratch) before async-proxy reads / writes
+            fence_proxy_async_global();
+            fence_proxy_async_smem();
+            const void* xm = static_cast<const char*>(P->tmaps) + size_t(P->descs[J.x_t].tmap) * 128;
+            const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(npad >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+            auto issue_x = [&](int j) -> bool {
+                const uint32_t i = xq % NX;
+                if (xq >= NX && !spin(&S->xempty[i], ((xq / NX) - 1u) & 1u)) return false;
+                mbar_expect_tx(&S->xfull[i], xbytes);
+                tma_2d(xb0 + i * xbytes, xm, (J.kt0 + j) * VDC_RING_BGEMM_KT, 0, &S->xfull[i]);
+                ++xq;
+                return true;
+            };
+            bool good = true;
+            const int pre = min(n, int(NX) - 1);
+            for (int j = 0; j < pre && good; ++j) good = issue_x(j);
+            uint32_t g = kt;
+            for (int t = 0; t < n && good; ++t, ++g) {
+                if (t + int(NX) - 1 < n && !issue_x(t + int(NX) - 1)) {
+                    good = false;
+                    break;
+                }
+                const uint32_t xi = xd % NX;
+                const uint32_t slot = g % R;
+                if (!spin(&S->xfull[xi], (xd / NX) & 1u) || !wait_full(slot, (g / R) & 1u)) {
+                    good = false;
+                    break;
+                }
+                tc_fence_after();
+                if (!(P->debug & 1u)) {
+                    const uint32_t a0 = ring + slot * SLOT, b0 = xb0 + xi * xbytes;
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        umma_bf16(tmem, umma_sw128_desc(a0 + kk * 32), umma_sw128_desc(b0 + kk * 32), idesc, (t | kk) ? 1u : 0u);
+                }
+                umma_commit(&S->empty[slot]);  // W slot -> memory core when the MMAs are done
+                umma_commit(&S->xempty[xi]);
+                ++xd;
+            }
+            if (good) umma_commit(&S->mma_bar);
+            S->flag = good ? 1 : 0;
+        }
+        kt += uint32_t(n);
+        sync();
+        if (!S->flag) {
+            ok = false;
+            return;
+        }
+        if (!spin(&S->mma_bar, nmma & 1u)) {
+            ok = false;
+            return;
+        }
+        ++nmma;
+        tc_fence_after();
+        const long long e0 = clock64();
+        bool fin = false;
+        switch (npad) {
+            case 16: fin = bgemm_epilogue<8>(J); break;
+            case 32: fin = bgemm_epilogue<16>(J); break;
+            default: fin = bgemm_epilogue<32>(J); break;
+        }
+        if (ct == 0) st_epi += clock64() - e0;
+        if (!fin) return;  // a piece of a split row block that was not the last to arrive
+        fence_proxy_async_global();  // consumers read these activations with TMA (async proxy)
+        sync();
+        if (ct == 0) {
+            red_release_add(ctr(J.o_t), 1u);
+            if (J.flags & VDC_JOB_QKV) {
+                red_release_add(ctr(J.b_t), 1u);
+                red_release_add(ctr(J.o2_t), 1u);
+            }
+            if (J.o3_t >= 0) red_release_add(ctr(J.o3_t), 1u);
+        }
+    }
+
+    template <int NH>
+    __device__ __forceinline__ void tmem_ld(uint32_t addr, float (&v)[NH]) const {
+        uint32_t r[NH];
+        if constexpr (NH == 8) {
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                         : "r"(addr));
+        } else {
+#pragma unroll
+            for (int c = 0; c < NH; c += 16)
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                    : "=r"(r[c]), "=r"(r[c + 1]), "=r"(r[c + 2]), "=r"(r[c + 3]), "=r"(r[c + 4]), "=r"(r[c + 5]), "=r"(r[c + 6]),
+                      "=r"(r[c + 7]), "=r"(r[c + 8]), "=r"(r[c + 9]), "=r"(r[c + 10]), "=r"(r[c + 11]), "=r"(r[c + 12]),
+                      "=r"(r[c + 13]), "=r"(r[c + 14]), "=r"(r[c + 15])
+                    : "r"(addr + uint32_t(c)));
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int c = 0; c < NH; ++c) v[c] = __uint_as_float(r[c]);
+    }
+
+    // returns false when this piece is not the one that finishes its row block
+    template <int NH>
+    __device__ bool bgemm_epilogue(const vdc_job& J) {
+        const int q = int(w & 3u);
+        const int row = q * 32 + int(lane);  // row within the 128-row block (TMEM lane)
+        const int c0 = int(w >> 2) * NH;     // first request column of this thread
+        const int nb = J.nb, npad = J.npad;
+        const int64_t M = J.cache_rows;      // output row stride (elements per request)
+        const int rg = J.r0 + row;           // global W row
+        float v[NH];
+        tmem_ld<NH>(tmem + (uint32_t(q * 32) << 16) + uint32_t(c0), v);
+        tc_fence_before();  // the accumulator may be overwritten after the next barrier
+        if (J.arrive_need > 1) {
+            // stream-K: this piece's partial -> global; the last piece of the
+            // row block to arrive adds all partials in piece order
+            float* part = f32p(J.part_t);
+            float* mine = part + size_t(J.part_off) * size_t(npad) * 128;
+#pragma unroll
+            for (int c = 0; c < NH; ++c) mine[(c0 + c) * 128 + row] = v[c];
+            sync();
+            if (ct == 0) {
+                uint32_t old;
+                asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&P->counters[J.arrive_ctr]) : "memory");
+                S->flag = (old + 1u == uint32_t(J.arrive_need) * P->epoch) ? 1 : 0;
+            }
+            sync();
+            if (!S->flag) return false;
+            const float* p0 = part + size_t(J.part_off - J.split) * size_t(npad) * 128;
+            float acc[NH];
+#pragma unroll
+            for (int c = 0; c < NH; ++c) acc[c] = 0.f;
+            for (int s = 0; s < J.arrive_need; ++s) {
+                float t[NH];
+                if (s == J.split) {
+#pragma unroll
+                    for (int c = 0; c < NH; ++c) t[c] = v[c];
+                } else {
+                    const float* ps = p0 + size_t(s) * size_t(npad) * 128;
+#pragma unroll
+                    for (int c = 0; c < NH; ++c) t[c] = ldcg_f32(ps + (c0 + c) * 128 + row);
+                }
+#pragma unroll
+                for (int c = 0; c < NH; ++c) acc[c] += t[c];
+            }
+#pragma unroll
+            for (int c = 0; c < NH; ++c) v[c] = acc[c];
+        }
+        if (J.flags & VDC_JOB_RMS) {
+#pragma unroll
+            for (int c = 0; c < NH; ++c) v[c] *= S->binv[min(c0 + c, VDC_RING_MAX_BATCH - 1)];
+        }
+        if (J.flags & VDC_JOB_QKV) {
+            const int qrows = J.block, kvr = J.kvrows, hd = J.head_dim, hkv = kvr / hd;
+            const bool isq = rg < qrows, isk = !isq && rg < qrows + kvr;
+            const int lr = isq ? rg : isk ? rg - qrows : rg - qrows - kvr;
+            const int d = lr % hd;
+            const double invf = pow(double(J.theta), -double(d & ~1) / double(hd));
+            const bool even = (lane & 1u) == 0;
+#pragma unroll
+            for (int c = 0; c < NH; ++c) {
+                const int b = c0 + c;
+                const float other = __shfl_xor_sync(0xffffffffu, v[c], 1);
+                if (b >= nb) continue;
+                const int64_t pos = req_pos(b);
+                if (isq || isk) {
+                    double ang = double(pos) * invf;
+                    ang -= 6.283185307179586 * rint(ang * 0.15915494309189535);
+                    float sn, cs;
+                    sincosf(float(ang), &sn, &cs);
+                    v[c] = even ? v[c] * cs - other * sn : other * sn + v[c] * cs;
+                }
+                if (isq) {
+                    u16p(J.o_t)[int64_t(b) * qrows + rg] = f2bf(v[c]);
+                } else {
+                    const int64_t page = P->step[J.ptab + int64_t(b) * J.maxp + pos / 64];
+                    const int64_t at = ((page * hkv + lr / hd) * 64 + pos % 64) * hd + d;
+                    u16p(isk ? J.b_t : J.o2_t)[at] = f2bf(v[c]);
+                }
+            }
+        } else if (J.flags & VDC_JOB_SWIGLU) {
+            // 128-row blocks = [64 gate rows | 64 up rows]: up rows go through shared memory
+            float* scr = reinterpret_cast<float*>(S->x);
+            if (row >= 64) {
+#pragma unroll
+                for (int c = 0; c < NH; ++c) scr[(c0 + c) * 64 + (row - 64)] = v[c];
+            }
+            sync();
+            if (row < 64) {
+                const int64_t orow = int64_t(J.r0 / 128) * 64 + row;
+#pragma unroll
+                for (int c = 0; c < NH; ++c) {
+                    const int b = c0 + c;
+                    if (b >= nb) continue;
+                    const float gt = v[c], up = scr[(c0 + c) * 64 + row];
+                    u16p(J.o_t)[int64_t(b) * M + orow] = f2bf(gt / (1.0f + expf(-gt)) * up);
+                }
+            }
+        } else if (J.flags & VDC_JOB_RESID) {
+            const uint16_t* res = u16p(J.a_t);
+            const float wn = J.o3_t >= 0 ? bf_lo(u16p(J.w3_t)[rg]) : 0.f;
+            float r[NH];
+#pragma unroll
+            for (int c = 0; c < NH; ++c) r[c] = c0 + c < nb ? bf_lo(ldcg_u16(res + int64_t(c0 + c) * M + rg)) : 0.f;
+#pragma unroll
+            for (int c = 0; c < NH; ++c) {
+                const int b = c0 + c;
+                if (b >= nb) continue;
+                const uint16_t xo = f2bf(v[c] + r[c]);
+                u16p(J.o_t)[int64_t(b) * M + rg] = xo;
+                if (J.o3_t >= 0) u16p(J.o3_t)[int64_t(b) * M + rg] = f2bf(bf_lo(xo) * wn);
+            }
+        } else {
+            const bool obf = tdtype(J.o_t) == VDC_DTYPE_BF16;
+#pragma unroll
+            for (int c = 0; c < NH; ++c)
+                if (c0 + c < nb) store_out(tptr(J.o_t), obf, int64_t(c0 + c) * M + rg, v[c]);
+        }
+        (void)npad;
+        return true;
+    }
+
+    // ELEMWISE (batched): embedding rows of requests [r0, r1) -> x, and the
+    // normalised-weight copy x * w3 the first layer's qkv GEMM reads
+    __device__ void embed_rows(const vdc_job& J) {
+        const int d = J.k, nch = d / 8;
+        const uint4* tab = reinterpret_cast<const uint4*>(tptr(J.x_t));
+        const uint4* wv = reinterpret_cast<const uint4*>(tptr(J.w3_t));
+        uint4* xo = reinterpret_cast<uint4*>(tptr(J.o_t));
+        uint4* xn = reinterpret_cast<uint4*>(tptr(J.o3_t));
+        for (int i = int(ct); i < (J.r1 - J.r0) * nch; i += NCT) {
+            const int b = J.r0 + i / nch, c = i % nch;
+            const int64_t tok = P->step[3 * b];
+            const uint4 u = __ldg(tab + tok * nch + c), g = __ldg(wv + c);
+            xo[int64_t(b) * nch + c] = u;
+            uint4 o;
+            o.x = pack2(bf_lo(u.x) * bf_lo(g.x), bf_hi(u.x) * bf_hi(g.x));
+            o.y = pack2(bf_lo(u.y) * bf_lo(g.y), bf_hi(u.y) * bf_hi(g.y));
+            o.z = pack2(bf_lo(u.z) * bf_lo(g.z), bf_hi(u.z) * bf_hi(g.z));
+            o.w = pack2(bf_lo(u.w) * bf_lo(g.w), bf_hi(u.w) * bf_hi(g.w));
+            xn[int64_t(b) * nch + c] = o;
+        }
+        fence_proxy_async_global();
+        sync();
+        if (ct == 0) {
+            red_release_add(ctr(J.o_t), 1u);
+            red_release_add(ctr(J.o3_t), 1u);
+        }
+    }
+
     // ------------------------------------------------------ ATTN_DECODE
     // Split-KV q-len-1 attention of one kv head (G q heads) over pages
     // [r0, r1), fused with the split combine.
@@ -671,7 +991,24 @@ struct Vcc {
         astamp(1);
         const int PR = J.tile_rows;
         const uint32_t rowb = uint32_t(HD * EB);
-        const int64_t pos = P->step[VDC_STEP_POS], ctx = P->step[VDC_STEP_CTX];
+        // batched programs: per-request position / context, paged pools, and
+        // pages mapped to warp pairs by ring slot (slot s -> pair (s % 8) / 2,
+        // K on even slots: a leading pad tile aligns the job), so every slot
+        // keeps a single consumer pair and jobs may span more than the ring
+        const bool batched = J.flags & VDC_JOB_BATCH;
+        const int64_t pos = batched ? P->step[3 * J.req + 1] : P->step[VDC_STEP_POS];
+        const int64_t ctx = batched ? P->step[3 * J.req + 2] : P->step[VDC_STEP_CTX];
+        if (J.lead_pad) {
+            const uint32_t s0 = kt % R;
+            if ((s0 & uint32_t(CW - 1)) == w) {
+                if (!wait_full(s0, (kt / R) & 1u)) {
+                    ok = false;
+                    return;
+                }
+                release(s0);
+            }
+            kt += 1;
+        }
         const int rows_w = PR / 2;  // rows per warp (<= 32: one per lane)
         // q of the group -> shared memory in the cache dtype, same 16-byte chunk
         // layout as a K row: the rotated chunk reads of the score loop hit 8
@@ -699,7 +1036,7 @@ struct Vcc {
             // page i -> warp pair i mod 4 (balanced over the 8 warps); the
             // job's tiles (<= ring depth) were issued after every earlier
             // tile was released, so any warp may wait on their slots
-            const uint32_t pair = i % uint32_t(CW / 2);
+            const uint32_t pair = batched ? ((sk & uint32_t(CW - 1)) >> 1) : i % uint32_t(CW / 2);
             if ((w >> 1) != pair) continue;
             const int half = int(w & 1u);
             const int my_row0 = half * rows_w;
@@ -716,8 +1053,13 @@ struct Vcc {
                 // the appended row was produced in this launch (after the page's
                 // bulk copy may have been issued): patch it into the slots
                 const int r = int(pos - prow0);
-                const char* kn = tptr(J.a_t) + (size_t(J.a_off) + size_t(pos) * HD) * EB;
-                const char* vn = tptr(J.b_t) + (size_t(J.b_off) + size_t(pos) * HD) * EB;
+                // cache row of the appended position: (hkv, T, hd) cache, or
+                // page pool (pages, hkv * 64, hd) through the page table
+                const size_t crow = batched ? size_t(P->step[J.ptab + int64_t(J.req) * J.maxp + pos / PR]) * size_t(J.cache_rows) +
+                                                  size_t(pos % PR)
+                                            : size_t(pos);
+                const char* kn = tptr(J.a_t) + (size_t(J.a_off) + crow * HD) * EB;
+                const char* vn = tptr(J.b_t) + (size_t(J.b_off) + crow * HD) * EB;
                 for (int c = int(lane); c < 2 * NCH; c += 32) {
                     const bool isk = c < NCH;
                     const int cc = isk ? c : c - NCH;
@@ -1017,6 +1359,7 @@ __device__ void vcc_role(const RingParams& P, Shared& S, char* ring) {
     v.lane = threadIdx.x & 31;
     v.w = threadIdx.x >> 5;
     v.R = P.ring_slots;
+    v.tmem = S.tmem_base;
     const uint32_t core = 2 * blockIdx.x + 1;
     const uint32_t w0 = P.core_off[core], n = P.core_off[core + 1] - w0;
     const long long t0 = clock64();
@@ -1025,8 +1368,8 @@ __device__ void vcc_role(const RingParams& P, Shared& S, char* ring) {
         const uint4 raw = __ldg(&P.words[w0 + pc]);
         const uint32_t op = raw.x & 0xff;
         if (op == OP_HALT) break;
-        const vdc_job J = P.jobs[raw.z];
-        const bool bf = v.tdtype(J.x_t) == VDC_DTYPE_BF16;
+        const vdc_job& J = P.jobs[raw.z];
+        const bool bf = J.x_t >= 0 && v.tdtype(J.x_t) == VDC_DTYPE_BF16;
         const unsigned long long t_enter = P.trace ? now_ns() : 0;
         v.t_ready = 0;
         switch (op) {
@@ -1050,7 +1393,10 @@ __device__ void vcc_role(const RingParams& P, Shared& S, char* ring) {
             }
             case OP_ATTN_COMBINE: v.combine(J); break;
             case OP_ALLREDUCE_ADD: v.allreduce(J); break;
-            case OP_ELEMWISE: v.copy_row(J); break;
+            case OP_BGEMM: v.bgemm(J); break;
+            case OP_ELEMWISE:
+                if (J.flags & VDC_JOB_BATCH) v.embed_rows(J); else v.copy_row(J);
+                break;
             default:
                 if (v.ct == 0) v.fire(4, (core << 16) | pc);
                 v.ok = false;
@@ -1079,6 +1425,8 @@ __device__ void vcc_role(const RingParams& P, Shared& S, char* ring) {
 // `pitch` apart (whole-row tiles are a single run).
 struct Tile {
     const char* src = nullptr;
+    const void* tmap = nullptr;  // TMA tensor tile (batched weights): box at (cx, cy)
+    int32_t cx = 0, cy = 0;
     uint32_t copies = 0, run = 0, pitch = 0;
     bool bad = false, halt = false;
     __device__ uint32_t bytes() const { return copies * run; }
@@ -1105,6 +1453,15 @@ __device__ __forceinline__ Tile resolve_load(const RingParams& P, uint4 raw) {
         return t;
     }
     const int64_t c0 = int64_t(pl & 0xfff), c1 = int64_t((pl >> 12) & 0xfff), c2 = int64_t((pl >> 24) & 0xfff);
+    if (d.tmap >= 0) {  // one 2-D tensor copy: 64 columns x tile_rows rows, 128-byte swizzle
+        t.tmap = static_cast<const char*>(P.tmaps) + size_t(d.tmap) * 128;
+        t.cx = int32_t(c1 * d.tile_cols);
+        t.cy = int32_t(c0 * d.tile_rows);
+        t.copies = 1;
+        t.run = uint32_t(d.tile_rows * d.tile_cols * d.elem);
+        t.bad = t.run > SLOT || rank != 2 || c0 >= d.grid[0] || c1 >= d.grid[1];
+        return t;
+    }
     const int64_t rt = rank == 3 ? c1 : c0, ctile = rank == 3 ? c2 : c1, plane = rank == 3 ? c0 : 0;
     const int64_t off = plane * d.lead_stride[0] + rt * d.tile_rows * d.cols + ctile * d.tile_cols;
     const int64_t rows_at = min(d.tile_rows, d.rows - rt * d.tile_rows);
@@ -1177,8 +1534,11 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
                 if (P.tile_trace && blockIdx.x == (P.debug >> 8) && g < P.tile_trace_cap) P.tile_trace[3 * g] = now_ns();
                 mbar_expect_tx(&S.full[slot], t.bytes());
                 char* dst = ring + size_t(slot) * SLOT;
-                for (uint32_t q = 0; q < t.copies; ++q)
-                    bulk_g2s(dst + q * t.run, t.src + size_t(q) * t.pitch, t.run, &S.full[slot]);
+                if (t.tmap)
+                    tma_2d(smem_addr(dst), t.tmap, t.cx, t.cy, &S.full[slot]);
+                else
+                    for (uint32_t q = 0; q < t.copies; ++q)
+                        bulk_g2s(dst + q * t.run, t.src + size_t(q) * t.pitch, t.run, &S.full[slot]);
                 bytes += t.bytes();
                 ++uops;
             }
@@ -1191,7 +1551,7 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
             // slot busy (the compute core is behind or waiting on a dependency):
             // keep DRAM busy by pulling this lane's upcoming tiles into L2
             const Tile ta = resolve_load(P, __ldg(&P.words[w0 + pf_g]));
-            if (!ta.bad && !ta.halt)
+            if (!ta.bad && !ta.halt && !ta.tmap)
                 for (uint32_t q = 0; q < ta.copies; ++q) prefetch_l2(ta.src + size_t(q) * ta.pitch, ta.run);
             pf_g += R;
             ready = true;  // made progress: skip the back-off
@@ -1241,13 +1601,33 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(const __grid_cons
             mbar_init(&S.full[i], 1);
             mbar_init(&S.empty[i], 1);
         }
+        for (int i = 0; i < NXMAX; ++i) {
+            mbar_init(&S.xfull[i], 1);
+            mbar_init(&S.xempty[i], 1);
+        }
+        mbar_init(&S.mma_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (P.batched && threadIdx.x < 32) {  // TMEM accumulator of the batched GEMM µops (one CTA per SM)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&S.tmem_base)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
     __syncthreads();
-    if (threadIdx.x < NCT)
+    tc_fence_after();
+    if (threadIdx.x < NCT) {
         vcc_role(P, S, ring);
-    else
+        if (P.batched) {
+            tc_fence_before();
+            named_bar(BAR_VCC, NCT);
+            tc_fence_after();
+            if (threadIdx.x < 32)
+                asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(S.tmem_base), "r"(TMEM_COLS));
+        }
+    } else {
         vmc_role(P, S, ring);
+    }
 }
 
 }  // namespace ring

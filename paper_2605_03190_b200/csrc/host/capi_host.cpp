@@ -100,6 +100,8 @@ decode::LayoutConfig layout_from(const json& j) {
     l.ring = j.value("ring", l.ring);
     l.tp_world = j.value("tp_world", l.tp_world);
     l.tp_rank = j.value("tp_rank", l.tp_rank);
+    l.batch = j.value("batch", l.batch);
+    l.req_pages = j.value("req_pages", l.req_pages);
     return l;
 }
 
@@ -132,7 +134,8 @@ ProgramBox* build(const std::string& request) {
     for (const auto& n : g.nodes) decode_graph = decode_graph || workload::is_decode_kind(n.kind);
     std::map<std::string, workload::TilingChoice> tilings;
     if (decode_graph && ring) {
-        box->program = generator::lower_decode_ring(g, hw, opt, req.value("ring_slots", 12));
+        const bool batched = req.value("layout", json::object()).value("batch", 0) >= 1;
+        box->program = generator::lower_decode_ring(g, hw, opt, req.value("ring_slots", batched ? 8 : 12));
         const auto v = generator::validate_ring_program(box->program);
         if (!v.empty()) throw generator::GeneratorError("ring program invalid: " + v.front().message);
     } else if (decode_graph) {
@@ -246,7 +249,7 @@ std::string ProgramBox::text(int mode) const {
                          {"grid", d.grid}, {"tile", {d.tile_rows, d.tile_cols}}, {"dtype", std::string(workload::elem_name(d.elem))},
                          {"view_of", d.view_of}, {"external", d.external}, {"state", d.state},
                          {"init", int(d.init)}, {"init_scale", d.init_scale},
-                         {"symmetric", d.symmetric}});
+                         {"symmetric", d.symmetric}, {"tma", d.tma}});
     out["descriptors"] = descs;
     out["params"] = program.params;
     out["ring_slots"] = program.ring_slots;
@@ -258,8 +261,13 @@ std::string ProgramBox::text(int mode) const {
                         {"o", {jb.o_t, jb.o_off}}, {"o2", {jb.o2_t, jb.o2_off}}, {"out_row0", jb.out_row0}, {"head_dim", jb.head_dim},
                         {"split", jb.split}, {"arrive", {jb.arrive_ctr, jb.arrive_need}},
                         {"group", jb.group}, {"block", jb.block}, {"cache_rows", jb.cache_rows},
-                        {"eps", jb.eps}, {"theta", jb.theta}, {"scale", jb.scale}});
+                        {"eps", jb.eps}, {"theta", jb.theta}, {"scale", jb.scale}, {"kt", {jb.kt0, jb.kt1}},
+                        {"req", jb.req}, {"part", {jb.part_t, jb.part_off}}, {"x2", {jb.x2_t, jb.x2_need}},
+                        {"o3", {jb.o3_t, jb.w3_t}}, {"lead_pad", jb.lead_pad}});
     out["jobs"] = jobs;
+    if (program.batch)
+        out["batch"] = {{"nb", program.batch}, {"npad", program.npad}, {"maxp", program.maxp},
+                        {"page_table_off", program.page_table_off}, {"page_table", program.page_table}};
     json queues = json::array();
     for (const auto& q : program.queues)
         queues.push_back({{"dep", q.dep_id}, {"depth", q.depth}, {"local", q.local}, {"producer_sm", q.producer.sm},

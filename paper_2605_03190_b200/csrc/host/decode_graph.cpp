@@ -167,6 +167,7 @@ std::string num(double v) {
 }  // namespace
 
 OperatorGraph build_decode_graph(const ModelConfig& m, const LayoutConfig& l) {
+    if (l.batch >= 1) return build_decode_graph_batched(m, l);
     if (m.head_dim % l.job_rows || l.job_rows % 2) throw workload::WorkloadError("job_rows must divide head_dim and be even");
     if (m.heads % m.kv_heads) throw workload::WorkloadError("heads must be a multiple of kv_heads");
     if (l.max_ctx < l.ctx_pages * l.page_rows) throw workload::WorkloadError("max_ctx below ctx_pages*page_rows");
@@ -252,6 +253,111 @@ OperatorGraph build_decode_graph(const ModelConfig& m, const LayoutConfig& l) {
     b.node("head", OpKind::RMS_GEMV, {"lm_head", b.view(x, ".all", d), "final_norm"}, {"logits"},
            {{"eps", eps}, {"job_rows", std::to_string(l.head_job_rows)}});
     b.g.validate();
+    return std::move(b.g);
+}
+
+int batch_npad(int batch) {
+    if (batch < 1 || batch > VDC_RING_MAX_BATCH) throw workload::WorkloadError("batch must be 1..64");
+    return batch <= 16 ? 16 : batch <= 32 ? 32 : 64;
+}
+
+// Batched decode graph (see LayoutConfig::batch). Node kinds label the
+// operators for the ring lowering's batched planner (attr "batch"); the
+// tensor shapes are batched, so the single-request shape rules of
+// check_node_shapes do not apply and are not run.
+//   embed   [embed.table, L0.attn_norm]            -> [embed.x, embed.xn]
+//   L.qkv   [L.wqkv, xn, x]                        -> [L.q, L.kc, L.vc]
+//   L.attn  [L.q, L.kc, L.vc]                      -> [L.part]
+//   L.comb  [L.part]                               -> [L.attn]
+//   L.o     [L.wo, L.attn, x, L.mlp_norm]          -> [L.x1, L.x1n]
+//   L.gu    [L.wgu, L.x1n, L.x1]                   -> [L.a]
+//   L.down  [L.wd, L.a, L.x1, next norm]           -> [L.x2, L.x2n]
+//   head    [lm_head, xn, x]                       -> [logits]
+// xn = bf16(x * w_norm) of the next RMSNorm (its per-request 1/rms is
+// applied in the consuming GEMM's epilogue); gate/up rows come in blocks of
+// 128 = [64 gate | 64 up] (gu_block 128: one MMA row block).
+OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfig& l) {
+    const int B = l.batch, N = batch_npad(B);
+    if (m.dtype != ElemType::bf16 || m.head_dim != 128 || l.page_rows != 64)
+        throw workload::WorkloadError("batched decode is built for bf16 models with head_dim 128 and 64-row pages");
+    if (int(l.req_pages.size()) != B) throw workload::WorkloadError("layout.req_pages needs one entry per request");
+    if (l.gu_block != 128) throw workload::WorkloadError("batched decode uses gu_block 128");
+    const int64_t d = m.hidden, hd = m.head_dim, hq = m.heads, hkv = m.kv_heads, grp = hq / hkv;
+    const int64_t qrows = hq * hd, kvrows = hkv * hd, ffn = m.ffn;
+    if (d % 128 || qrows % 128 || kvrows % 128 || ffn % 64 || m.vocab % 128 || hq % hkv)
+        throw workload::WorkloadError("batched decode needs 128-row aligned projections");
+    int64_t pool = 0, jobs = 0;
+    for (int p : l.req_pages) {
+        if (p < 1) throw workload::WorkloadError("every request covers at least one page");
+        pool += p;
+        jobs += (p + l.pages_per_job - 1) / l.pages_per_job;
+    }
+    if (pool > 4095) throw workload::WorkloadError("KV pool exceeds 4095 pages (12-bit tile coordinates)");
+    Builder b{{}, m, l};
+    const ElemType e = m.dtype;
+    const InitKind winit = m.scaled_init ? InitKind::centered : InitKind::random;
+    const std::string eps = num(m.eps), theta = num(m.theta), bs = std::to_string(B);
+    std::string rp;
+    for (int p : l.req_pages) rp += (rp.empty() ? "" : ",") + std::to_string(p);
+    auto act = [&](const std::string& name, int64_t width, bool tma) {
+        TensorRef& t = b.add(name, {N, width}, N, 64, InitKind::zeros, e);
+        t.tma = tma ? uint32_t(N) : 0u;
+        return name;
+    };
+    auto wgt = [&](const std::string& name, int64_t rows, int64_t cols, double fan_in) {
+        TensorRef& t = b.add(name, {rows, cols}, VDC_RING_BGEMM_ROWS, VDC_RING_BGEMM_KT, winit, e,
+                             m.scaled_init ? float(1.0 / std::sqrt(fan_in)) : 1.0f);
+        t.tma = VDC_RING_BGEMM_ROWS;
+        return name;
+    };
+    auto sk = [&](const std::string& name, int64_t row_blocks) {  // stream-K partials (shared by all layers)
+        b.add(name, {(row_blocks + 256) * N * 128, 1}, N * 128, 1, InitKind::zeros, ElemType::f32);
+        return name;
+    };
+    b.add("ring.pad", {1, 8}, 1, 8, InitKind::zeros, e);  // 16-byte tile that realigns attention jobs in the ring
+    b.add("embed.table", {m.vocab, d}, 1, d, winit, e);
+    sk("qkv.sk", (qrows + 2 * kvrows) / 128);
+    sk("o.sk", d / 128);
+    sk("gu.sk", 2 * ffn / 128);
+    sk("down.sk", d / 128);
+    sk("head.sk", m.vocab / 128);
+    std::string x = act("embed.x", d, false), xn = act("embed.xn", d, true);
+    b.norm("L0.attn_norm", d);
+    b.node("embed", OpKind::EMBED_ROW, {"embed.table", "L0.attn_norm"}, {x, xn}, {{"batch", bs}});
+    for (int li = 0; li < m.layers; ++li) {
+        const std::string L = "L" + std::to_string(li) + ".";
+        wgt(L + "wqkv", qrows + 2 * kvrows, d, double(d));
+        b.add(L + "q", {B, qrows}, 1, qrows, InitKind::zeros, e);
+        for (const char* c : {"kc", "vc"}) {
+            TensorRef& t = b.add(L + c, {pool, hkv * l.page_rows, hd}, l.page_rows, hd, winit, e);
+            t.state = true;
+        }
+        b.node(L + "qkv", OpKind::RMS_GEMV, {L + "wqkv", xn, x}, {L + "q", L + "kc", L + "vc"},
+               {{"eps", eps}, {"theta", theta}, {"rope", "1"}, {"batch", bs}});
+        b.add(L + "part", {jobs * hkv * grp, hd + 2}, grp, hd + 2, InitKind::zeros, ElemType::f32);
+        b.node(L + "attn", OpKind::ATTN_DECODE, {L + "q", L + "kc", L + "vc"}, {L + "part"},
+               {{"pages_per_job", std::to_string(l.pages_per_job)}, {"batch", bs}, {"req_pages", rp}});
+        act(L + "attn", qrows, true);
+        b.node(L + "comb", OpKind::ATTN_COMBINE, {L + "part"}, {L + "attn"}, {{"batch", bs}});
+        wgt(L + "wo", d, qrows, double(qrows));
+        b.norm(L + "mlp_norm", d);
+        act(L + "x1", d, false);
+        act(L + "x1n", d, true);
+        b.node(L + "o", OpKind::GEMV_ADD, {L + "wo", L + "attn", x, L + "mlp_norm"}, {L + "x1", L + "x1n"}, {{"batch", bs}});
+        wgt(L + "wgu", 2 * ffn, d, double(d));
+        act(L + "a", ffn, true);
+        b.node(L + "gu", OpKind::RMS_GEMV, {L + "wgu", L + "x1n", L + "x1"}, {L + "a"},
+               {{"eps", eps}, {"swiglu", "128"}, {"batch", bs}});
+        wgt(L + "wd", d, ffn, double(ffn));
+        const std::string next_norm = li + 1 < m.layers ? "L" + std::to_string(li + 1) + ".attn_norm" : "final_norm";
+        b.norm(next_norm, d);
+        x = act(L + "x2", d, false);
+        xn = act(L + "x2n", d, true);
+        b.node(L + "down", OpKind::GEMV_ADD, {L + "wd", L + "a", L + "x1", next_norm}, {x, xn}, {{"batch", bs}});
+    }
+    wgt("lm_head", m.vocab, d, double(d));
+    b.add("logits", {B, m.vocab}, 1, m.vocab, InitKind::zeros, ElemType::f32);
+    b.node("head", OpKind::RMS_GEMV, {"lm_head", xn, x}, {"logits"}, {{"eps", eps}, {"batch", bs}});
     return std::move(b.g);
 }
 

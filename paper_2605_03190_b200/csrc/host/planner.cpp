@@ -118,6 +118,7 @@ std::vector<TileDescriptor> build_descriptors(const workload::OperatorGraph& g) 
         d.state = t.state;
         d.init_scale = t.init_scale;
         d.symmetric = t.symmetric;
+        d.tma = t.tma;
         base += d.tile_count();
         out.push_back(std::move(d));
     }

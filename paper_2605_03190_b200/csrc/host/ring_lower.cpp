@@ -24,6 +24,7 @@
 #include <set>
 
 #include "jobs.hpp"
+#include "uopsim/decode.hpp"
 #include "uopsim/decode_abi.h"
 #include "uopsim/ring_abi.h"
 #include "uopsim/util.hpp"
@@ -57,6 +58,7 @@ struct RJob {
     std::vector<Tile> tiles;  // ring tiles in consumption order
     uint32_t ordinal = 0;
     uint32_t sm = 0;
+    bool counts = true;       // counted in the readiness targets of its outputs (stream-K: one piece per row block)
 };
 
 class RingLowering {
@@ -74,6 +76,7 @@ class RingLowering {
         std::map<int32_t, int32_t> writers;
         std::set<std::pair<int32_t, int32_t>> combined;
         for (const auto& r : jobs_) {
+            if (!r.counts) continue;
             if (r.publishes.empty()) ++writers[r.j.o_t];
             for (int32_t t : r.publishes) ++writers[t];
             if (r.j.op == int32_t(Opcode::ATTN_DECODE) && r.j.o2_t >= 0 && combined.insert({r.j.o2_t, r.j.o2_off}).second)
@@ -84,6 +87,8 @@ class RingLowering {
             if (!(r.j.flags & VDC_JOB_SYM_IN)) r.j.x_need = need(r.j.x_t);
             r.j.a_need = need(r.j.a_t);
             r.j.b_need = need(r.j.b_t);
+            r.j.x2_need = need(r.j.x2_t);
+            if (r.j.flags & VDC_JOB_BATCH) r.j.maxp = maxp_;
         }
         LoweredProgram p;
         p.descriptors = desc_;
@@ -98,6 +103,18 @@ class RingLowering {
         p.vcc_per_sm = 1;
         p.sm_count = uint16_t(sms_);
         p.local_queue_depth = uint16_t(ring_slots_);
+        if (batched_) {
+            if (ring_slots_ != VDC_RING_COMPUTE_WARPS)
+                throw GeneratorError("batched ring programs use 8 ring slots (attention pages map to warp pairs by slot)");
+            p.batch = nb_;
+            p.npad = npad_;
+            p.maxp = maxp_;
+            p.page_table_off = 3 * nb_;
+            p.page_table.assign(size_t(nb_) * size_t(maxp_), 0);
+            for (size_t b = 0; b < pages_.size(); ++b)
+                for (size_t i = 0; i < pages_[b].size(); ++i) p.page_table[b * size_t(maxp_) + i] = pages_[b][i];
+            p.step_scalars = uint16_t(3 * nb_ + nb_ * maxp_);
+        }
         emit(p);
         return p;
     }
@@ -117,6 +134,7 @@ class RingLowering {
         vdc_job j{};
         j.op = int32_t(op);
         j.x_t = j.a_t = j.b_t = j.o_t = j.o2_t = -1;
+        j.x2_t = j.o3_t = j.w3_t = j.part_t = -1;
         j.arrive_ctr = -1;
         return j;
     }
@@ -127,6 +145,10 @@ class RingLowering {
     }
 
     void plan(const workload::OperatorNode& n, uint32_t ordinal) {
+        if (n.attrs.count("batch")) {
+            plan_batched(n, ordinal);
+            return;
+        }
         switch (n.kind) {
             case OpKind::GEMV:
             case OpKind::RMS_GEMV:
@@ -407,6 +429,11 @@ class RingLowering {
             size_t tiles_so_far = 0;
             for (size_t ji : per_sm[s]) {
                 RJob r = jobs_[ji];
+                if ((r.j.flags & VDC_JOB_BATCH) && r.j.op == int32_t(Opcode::ATTN_DECODE) && (tiles_so_far & 1)) {
+                    // K tiles on even ring indices: pages map to warp pairs by slot
+                    r.j.lead_pad = 1;
+                    r.tiles.insert(r.tiles.begin(), Tile{pad_t_, {0, 0}});
+                }
                 tiles_so_far += r.tiles.size();
                 const int32_t slot = int32_t(p.jobs.size());
                 p.jobs.push_back(r.j);
@@ -436,6 +463,251 @@ class RingLowering {
             }
             vm.push_back({0, -1, -1});
             cm.push_back({0, -1, -1});
+        }
+    }
+
+    // ---------------------------------------------------------------- batched
+    // Batched programs (decode.hpp LayoutConfig::batch): BGEMM µops on the
+    // tensor cores, split-KV attention per (request, kv head), paged pools.
+    bool batched_ = false;
+    int32_t nb_ = 0, npad_ = 0, maxp_ = 0;
+    std::vector<std::vector<int64_t>> pages_;  // request -> physical page of each logical page
+    uint16_t pad_t_ = 0;
+
+    void plan_batched(const workload::OperatorNode& n, uint32_t ordinal) {
+        batched_ = true;
+        nb_ = int32_t(attr_int(n, "batch", 1));
+        npad_ = decode::batch_npad(nb_);
+        pad_t_ = idx("ring.pad");
+        switch (n.kind) {
+            case OpKind::EMBED_ROW: {
+                RJob r;
+                r.ordinal = ordinal;
+                r.sm = 0;
+                vdc_job& j = r.j;
+                j = blank(Opcode::ELEMWISE);
+                j.flags = VDC_JOB_BATCH;
+                j.r0 = 0;
+                j.r1 = nb_;
+                j.nb = nb_;
+                j.npad = npad_;
+                j.x_t = storage(idx(n.inputs[0]));
+                j.w3_t = storage(idx(n.inputs[1]));
+                j.k = int32_t(desc_[uint16_t(j.x_t)].cols());
+                j.o_t = storage(idx(n.outputs[0]));
+                j.o3_t = storage(idx(n.outputs[1]));
+                r.publishes = {j.o_t, j.o3_t};
+                jobs_.push_back(std::move(r));
+                break;
+            }
+            case OpKind::RMS_GEMV:
+            case OpKind::GEMV_ADD:
+                plan_bgemm(n, ordinal);
+                break;
+            case OpKind::ATTN_DECODE:
+                plan_battention(n, ordinal);
+                break;
+            case OpKind::ATTN_COMBINE: {
+                const int32_t part = storage(idx(n.inputs[0])), out = storage(idx(n.outputs[0]));
+                const int64_t width = desc_[uint16_t(out)].cols();
+                for (auto& r : jobs_)
+                    if (r.j.op == int32_t(Opcode::ATTN_DECODE) && r.j.o_t == part) {
+                        r.j.o2_t = out;
+                        r.j.o2_off = int32_t(r.j.req * width + r.head * r.j.group * r.j.head_dim);
+                    }
+                break;
+            }
+            default:
+                throw GeneratorError("node " + n.id + ": kind has no batched lowering");
+        }
+    }
+
+    // stream-K: the op's (row block, k tile) grid in row-block-major order is
+    // cut into one contiguous range per SM; each maximal run inside a row
+    // block is a piece (one µop). Pieces of a split block write fp32
+    // partials; the last to arrive adds them in piece order and runs the
+    // epilogue, so every SM streams the same number of weight tiles (+-1).
+    void plan_bgemm(const workload::OperatorNode& n, uint32_t ordinal) {
+        const uint16_t w = idx(n.inputs[0]);
+        const TileDescriptor& wd = desc_[w];
+        const int64_t M = wd.rows(), K = wd.cols();
+        if (wd.tile_rows != VDC_RING_BGEMM_ROWS || wd.tile_cols != VDC_RING_BGEMM_KT || wd.tma != VDC_RING_BGEMM_ROWS ||
+            M % VDC_RING_BGEMM_ROWS || K % VDC_RING_BGEMM_KT)
+            throw GeneratorError("node " + n.id + ": batched weights need 128 x 64 TMA tiles");
+        const int64_t rb = M / VDC_RING_BGEMM_ROWS, kts = K / VDC_RING_BGEMM_KT, T = rb * kts;
+        const bool qkv = n.outputs.size() == 3, resid = n.kind == OpKind::GEMV_ADD, swiglu = attr_int(n, "swiglu", 0) != 0;
+        const std::string op = n.id.substr(n.id.find('.') == std::string::npos ? 0 : n.id.find('.') + 1);
+        const uint16_t skt = idx(op + ".sk");
+        if (desc_[skt].elem_count() < (rb + int64_t(sms_)) * npad_ * VDC_RING_BGEMM_ROWS)
+            throw GeneratorError("node " + n.id + ": stream-K partial buffer too small for " + std::to_string(sms_) + " SMs");
+        struct Piece {
+            uint32_t sm;
+            int64_t kt0, kt1;
+        };
+        std::vector<std::vector<Piece>> blocks;
+        blocks.resize(size_t(rb));
+        for (uint32_t s = 0; s < sms_; ++s) {
+            const auto [t0, t1] = share(T, s);
+            for (int64_t t = t0; t < t1;) {
+                const int64_t b = t / kts, e = std::min(t1, (b + 1) * kts);
+                blocks[size_t(b)].push_back({s, t - b * kts, e - b * kts});
+                t = e;
+            }
+        }
+        int32_t slot = 0;
+        for (int64_t b = 0; b < rb; ++b) {
+            const auto& ps = blocks[size_t(b)];
+            const int32_t ctr = ps.size() > 1 ? int32_t(desc_.size()) + n_arrive_++ : -1;
+            for (size_t i = 0; i < ps.size(); ++i) {
+                RJob r;
+                r.ordinal = ordinal;
+                r.sm = ps[i].sm;
+                r.counts = i == 0;  // one publisher per row block (whichever piece arrives last)
+                vdc_job& j = r.j;
+                j = blank(Opcode::BGEMM);
+                j.flags = VDC_JOB_BATCH;
+                j.r0 = int32_t(b * VDC_RING_BGEMM_ROWS);
+                j.r1 = j.r0 + VDC_RING_BGEMM_ROWS;
+                j.k = int32_t(K);
+                j.tile_rows = VDC_RING_BGEMM_ROWS;
+                j.tile_cols = VDC_RING_BGEMM_KT;
+                j.kt0 = int32_t(ps[i].kt0);
+                j.kt1 = int32_t(ps[i].kt1);
+                j.nb = nb_;
+                j.npad = npad_;
+                j.x_t = storage(idx(n.inputs[1]));
+                if (desc_[uint16_t(j.x_t)].tma != uint32_t(npad_) || desc_[uint16_t(j.x_t)].cols() != K)
+                    throw GeneratorError("node " + n.id + ": activations must be an (npad, K) TMA tensor");
+                j.part_t = storage(skt);
+                j.part_off = slot++;
+                j.split = int32_t(i);
+                j.arrive_ctr = ctr;
+                j.arrive_need = int32_t(ps.size());
+                j.o_t = storage(idx(n.outputs[0]));
+                j.cache_rows = int32_t(M);
+                if (n.kind == OpKind::RMS_GEMV) {
+                    j.flags |= VDC_JOB_RMS;
+                    j.x2_t = storage(idx(n.inputs[2]));
+                    j.eps = float(attr_num(n, "eps", 1e-5));
+                }
+                if (resid) {
+                    j.flags |= VDC_JOB_RESID;
+                    j.a_t = storage(idx(n.inputs[2]));
+                    j.w3_t = storage(idx(n.inputs[3]));
+                    j.o3_t = storage(idx(n.outputs[1]));
+                    r.publishes = {j.o_t, j.o3_t};
+                } else if (qkv) {
+                    const TileDescriptor& kc = desc_[idx(n.outputs[1])];
+                    j.flags |= VDC_JOB_QKV;
+                    j.head_dim = int32_t(kc.shape[2]);
+                    j.kvrows = int32_t(kc.shape[1] / 64 * kc.shape[2]);
+                    j.block = int32_t(M - 2 * j.kvrows);
+                    j.cache_rows = j.block;  // q row stride
+                    j.theta = float(attr_num(n, "theta", 10000.0));
+                    j.b_t = storage(idx(n.outputs[1]));
+                    j.o2_t = storage(idx(n.outputs[2]));
+                    j.ptab = 3 * nb_;
+                    r.publishes = {j.o_t, j.b_t, j.o2_t};
+                } else {
+                    if (swiglu) {
+                        j.flags |= VDC_JOB_SWIGLU;
+                        j.cache_rows = int32_t(M / 2);
+                    }
+                    r.publishes = {j.o_t};
+                }
+                for (int64_t kt = ps[i].kt0; kt < ps[i].kt1; ++kt) r.tiles.push_back({w, {uint16_t(b), uint16_t(kt)}});
+                jobs_.push_back(std::move(r));
+            }
+        }
+    }
+
+    // split-KV jobs of (request, kv head, page range), balanced over the SMs
+    // by page count (longest first onto the least loaded SM)
+    void plan_battention(const workload::OperatorNode& n, uint32_t ordinal) {
+        const uint16_t q = idx(n.inputs[0]), kc = idx(n.inputs[1]), vc = idx(n.inputs[2]), part = idx(n.outputs[0]);
+        const TileDescriptor& kd = desc_[kc];
+        const int64_t hd = kd.shape[2], hkv = kd.shape[1] / 64, qrows = desc_[q].cols(), grp = qrows / hd / hkv;
+        if (!(grp == 4 || grp == 8) || hd != 128) throw GeneratorError("node " + n.id + ": batched attention needs hd 128, group 4/8");
+        const int64_t per = attr_int(n, "pages_per_job", 4);
+        if (pages_.empty()) {  // contiguous page allocation in the pool, request-major
+            std::vector<int64_t> rp;
+            std::string s = n.attrs.at("req_pages");
+            for (size_t p0 = 0; p0 < s.size();) {
+                const size_t p1 = s.find(',', p0);
+                rp.push_back(std::stoll(s.substr(p0, p1 == std::string::npos ? std::string::npos : p1 - p0)));
+                p0 = p1 == std::string::npos ? s.size() : p1 + 1;
+            }
+            int64_t next = 0;
+            for (int64_t c : rp) {
+                pages_.emplace_back();
+                for (int64_t i = 0; i < c; ++i) pages_.back().push_back(next++);
+                maxp_ = std::max<int32_t>(maxp_, int32_t(c));
+            }
+            if (int64_t(pages_.size()) != nb_) throw GeneratorError("req_pages does not match the batch");
+        }
+        struct AJ {
+            int64_t b, h, s, p0, p1;
+        };
+        std::vector<AJ> all;
+        for (int64_t b = 0; b < nb_; ++b) {
+            const int64_t np = int64_t(pages_[size_t(b)].size()), splits = ceil_div(np, per);
+            for (int64_t h = 0; h < hkv; ++h)
+                for (int64_t s = 0; s < splits; ++s) all.push_back({b, h, s, s * per, std::min(np, (s + 1) * per)});
+        }
+        // partial slots: (b, h) blocks contiguous in split order (the combiner walks them)
+        std::vector<int64_t> order(all.size());
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t c) {
+            return all[size_t(a)].p1 - all[size_t(a)].p0 > all[size_t(c)].p1 - all[size_t(c)].p0;
+        });
+        std::vector<int64_t> load(sms_, 0);
+        std::vector<uint32_t> sm_of(all.size());
+        for (int64_t i : order) {
+            const uint32_t s = uint32_t(std::min_element(load.begin(), load.end()) - load.begin());
+            sm_of[size_t(i)] = s;
+            load[s] += 2 * (all[size_t(i)].p1 - all[size_t(i)].p0) + 1;
+        }
+        std::map<std::pair<int64_t, int64_t>, int32_t> ctr;
+        for (size_t i = 0; i < all.size(); ++i) {
+            const AJ& a = all[i];
+            if (!ctr.count({a.b, a.h})) ctr[{a.b, a.h}] = int32_t(desc_.size()) + n_arrive_++;
+            RJob r;
+            r.ordinal = ordinal;
+            r.sm = sm_of[i];
+            r.head = int32_t(a.h);
+            vdc_job& j = r.j;
+            j = blank(Opcode::ATTN_DECODE);
+            j.flags = VDC_JOB_BATCH;
+            j.r0 = int32_t(a.p0);
+            j.r1 = int32_t(a.p1);
+            j.k = int32_t(hd);
+            j.head_dim = int32_t(hd);
+            j.group = int32_t(grp);
+            j.tile_rows = 64;
+            j.tile_cols = int32_t(hd);
+            j.cache_rows = int32_t(hkv * 64);
+            j.scale = float(1.0 / std::sqrt(double(hd)));
+            j.nb = nb_;
+            j.npad = npad_;
+            j.req = int32_t(a.b);
+            j.ptab = 3 * nb_;
+            j.x_t = storage(q);
+            j.x_off = int32_t(a.b * qrows + a.h * grp * hd);
+            j.a_t = storage(kc);
+            j.a_off = int32_t(a.h * 64 * hd);
+            j.b_t = storage(vc);
+            j.b_off = j.a_off;
+            j.o_t = storage(part);
+            j.o_off = int32_t(i) * int32_t(grp * (hd + 2));
+            j.split = int32_t(a.s);
+            j.arrive_ctr = ctr[{a.b, a.h}];
+            j.arrive_need = int32_t(ceil_div<int64_t>(int64_t(pages_[size_t(a.b)].size()), per));
+            for (int64_t pg = a.p0; pg < a.p1; ++pg) {
+                const uint16_t phys = uint16_t(pages_[size_t(a.b)][size_t(pg)]);
+                r.tiles.push_back({kc, {phys, uint16_t(a.h), 0}});
+                r.tiles.push_back({vc, {phys, uint16_t(a.h), 0}});
+            }
+            jobs_.push_back(std::move(r));
         }
     }
 
@@ -475,6 +747,7 @@ std::vector<isa::Violation> validate_ring_program(const LoweredProgram& p) {
                 const vdc_job& j = p.jobs.at(size_t(s[i].imm));
                 writer_op[j.o_t] = m[i].op;
                 if (j.flags & VDC_JOB_QKV) writer_op[j.b_t] = writer_op[j.o2_t] = m[i].op;
+                if (j.o3_t >= 0 && (j.flags & VDC_JOB_BATCH)) writer_op[j.o3_t] = m[i].op;
             }
     }
     for (const auto& [core, s] : p.streams) {
@@ -492,7 +765,8 @@ std::vector<isa::Violation> validate_ring_program(const LoweredProgram& p) {
             last_op = m[i].op;
             const vdc_job& j = p.jobs.at(size_t(s[i].imm));
             const int32_t b_in = (j.flags & VDC_JOB_QKV) ? -1 : j.b_t;  // QKV: b_t is an output (K cache)
-            for (int32_t t : {j.x_t, j.a_t, b_in}) {
+            const int32_t x2 = (j.flags & VDC_JOB_BATCH) ? j.x2_t : -1;
+            for (int32_t t : {j.x_t, j.a_t, b_in, x2}) {
                 const auto it = writer_op.find(t);
                 if (it != writer_op.end() && it->second >= m[i].op)
                     v.push_back({i, core.name() + ": waits on an operator that does not precede it"});

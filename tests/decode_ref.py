@@ -32,10 +32,20 @@ def decode_step(T: dict, cfg: dict, token: int, pos: int) -> dict:
     ctx = pos + 1
     grp = hq // hkv
 
+    # batched programs store the normalised operand as bf16(x * w) and apply
+    # the per-request 1/rms to the GEMM output (cfg["norm_scale_after"])
+    scale_after = cfg.get("norm_scale_after", False)
+
     def rmsnorm(x, w):
         ss = np.float32(np.sum(x.astype(np.float64) ** 2))
         inv = f32(1.0) / np.sqrt(ss / f32(x.size) + f32(eps))
-        return rnd(x * inv * w)
+        if scale_after:
+            return rnd(x * w), inv
+        return rnd(x * inv * w), f32(1.0)
+
+    def mv(W, h):
+        hv, s = h
+        return (W.astype(np.float64) @ hv.astype(np.float64)).astype(np.float32) * s
 
     def rope(v, row0):
         out = v.copy()
@@ -52,8 +62,7 @@ def decode_step(T: dict, cfg: dict, token: int, pos: int) -> dict:
     for l in range(layers):
         L = f"L{l}."
         h = rmsnorm(x, T[L + "attn_norm"].reshape(-1))
-        W = T[L + "wqkv"].reshape(-1, d)
-        qkv = (W.astype(np.float64) @ h.astype(np.float64)).astype(np.float32)
+        qkv = mv(T[L + "wqkv"].reshape(-1, d), h)
         q = rnd(rope(qkv[: hq * hd], 0))
         k = rnd(rope(qkv[hq * hd: (hq + hkv) * hd], hq * hd))
         v = rnd(qkv[(hq + hkv) * hd:])
@@ -72,11 +81,11 @@ def decode_step(T: dict, cfg: dict, token: int, pos: int) -> dict:
         att = rnd(att)
         x1 = rnd(x + (T[L + "wo"].reshape(d, -1).astype(np.float64) @ att.astype(np.float64)).astype(np.float32))
         h2 = rmsnorm(x1, T[L + "mlp_norm"].reshape(-1))
-        gu = (T[L + "wgu"].reshape(-1, d).astype(np.float64) @ h2.astype(np.float64)).astype(np.float32)
+        gu = mv(T[L + "wgu"].reshape(-1, d), h2)
         gu = gu.reshape(-1, gu_block)
         gate, up = gu[:, : gu_block // 2].reshape(-1), gu[:, gu_block // 2:].reshape(-1)
         a = rnd(gate / (1.0 + np.exp(-gate)) * up)
         x = rnd(x1 + (T[L + "wd"].reshape(d, -1).astype(np.float64) @ a.astype(np.float64)).astype(np.float32))
     hf = rmsnorm(x, T["final_norm"].reshape(-1))
-    res["logits"] = (T["lm_head"].reshape(-1, d).astype(np.float64) @ hf.astype(np.float64)).astype(np.float32)
+    res["logits"] = mv(T["lm_head"].reshape(-1, d), hf)
     return res
