@@ -107,7 +107,8 @@ typedef struct vdc_job {
     int32_t req;              /* ATTN / ELEMWISE: request index (first request of an embed job) */
     int32_t ptab, maxp;       /* page table: step-block offset and pages per request row */
     int32_t kvrows;           /* BGEMM + QKV: k (= v) rows */
-    int32_t rsv[2];
-} vdc_job;  /* 192 bytes */
+    int32_t rsv[18];          /* pads the block to 256 bytes: the single-request fields stay in
+                                 the first 128-byte line, the batched ones in the second */
+} vdc_job;  /* 256 bytes */
 
 #endif

@@ -1843,6 +1843,7 @@ struct vdc_ctx {
     bool ring = false;
     uint32_t ring_slots = 0;
     vdc_job* d_jobs = nullptr;
+    char* d_jobs_core = nullptr;
     uint32_t n_jobs = 0;
     uint32_t epoch = 0;
     uint32_t ring_prefetch = 0;
@@ -1854,7 +1855,7 @@ struct vdc_ctx {
     unsigned long long* d_tile_trace = nullptr;
     bool ring_attr_set = false;
     // batched ring programs: TMA tensor maps of the descriptors with vdc_desc.tma > 0
-    std::vector<CUtensorMap> tmaps_host;
+    std::vector<CUtensorMap> tmaps_host;  // one per descriptor (only vdc_desc.tma > 0 are encoded)
     CUtensorMap* d_tmaps = nullptr;
     bool tmaps_dirty = false;
     bool batched = false;
@@ -1909,7 +1910,8 @@ int vdc_create(const vdc_profile* p, int device, vdc_ctx** out) {
                                        std::to_string(prop.sharedMemPerBlockOptin));
     }
     if (p->slot_size == VDC_RING_SLOT_BYTES)
-        CU(cudaFuncSetAttribute(ring_kernel_entry(), cudaFuncAttributeMaxDynamicSharedMemorySize, int(ctx->smem_bytes)));
+        for (bool b : {false, true})
+            CU(cudaFuncSetAttribute(ring_kernel_entry(b), cudaFuncAttributeMaxDynamicSharedMemorySize, int(ctx->smem_bytes)));
     else
         CU(cudaFuncSetAttribute(engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ctx->smem_bytes)));
     CU(cudaMalloc(&ctx->d_stats, sizeof(SmStats) * p->sm_count));
@@ -1929,6 +1931,7 @@ int vdc_destroy(vdc_ctx* ctx) {
     dfree(ctx->d_counters);
     dfree(ctx->d_params);
     dfree(ctx->d_jobs);
+    dfree(ctx->d_jobs_core);
     dfree(ctx->d_sym);
     dfree(ctx->d_tmaps);
     dfree(ctx->d_stats);
@@ -2012,16 +2015,15 @@ int vdc_load_program(vdc_ctx* ctx, const uint8_t* words, const uint32_t* words_p
         d.elem = s.dtype == VDC_DTYPE_BF16 ? 2 : s.dtype == VDC_DTYPE_I64 ? 8 : 4;
         d.storage = s.view_of >= 0 ? s.view_of : int32_t(i);
         d.ptr = nullptr;
-        d.tmap = -1;
         if (s.tma) {
             if (s.view_of >= 0 || s.rank != 2 || s.dtype != VDC_DTYPE_BF16 || s.tma > 256 || s.shape[1] % 64)
                 return fail(VDC_ERR_INPUT, "TMA descriptors must be owned rank-2 bf16 tensors with 64-column tiles");
-            d.tmap = int32_t(n_tmaps++);
+            ++n_tmaps;
         }
     }
-    ctx->tmaps_host.assign(n_tmaps, CUtensorMap{});
+    ctx->tmaps_host.assign(n_tmaps ? n_desc : 0, CUtensorMap{});
     dfree(ctx->d_tmaps);
-    if (n_tmaps) CU(cudaMalloc(&ctx->d_tmaps, sizeof(CUtensorMap) * n_tmaps));
+    if (n_tmaps) CU(cudaMalloc(&ctx->d_tmaps, sizeof(CUtensorMap) * n_desc));
     ctx->tmaps_dirty = n_tmaps > 0;
     ctx->max_dep = 0;
     for (uint32_t i = 0; i < n_queues; ++i) ctx->max_dep = std::max<uint32_t>(ctx->max_dep, queues[i].dep_id);
@@ -2063,8 +2065,7 @@ int vdc_load_jobs(vdc_ctx* ctx, const vdc_job* jobs, uint32_t n_jobs, uint32_t r
         }
         if (j.op == 0x2D) {
             for (int32_t t : {j.x_t})
-                if (t < 0 || t >= int32_t(ctx->descs.size()) || ctx->dev_descs[size_t(t)].tmap < 0 ||
-                    ctx->descs[size_t(t)].tma != uint32_t(j.npad))
+                if (t < 0 || t >= int32_t(ctx->descs.size()) || ctx->descs[size_t(t)].tma != uint32_t(j.npad))
                     return fail(VDC_ERR_INPUT, "job " + std::to_string(i) + ": BGEMM activations need an npad-row tensor map");
         }
         for (int32_t t : {j.x_t, j.a_t, j.b_t, j.o_t, j.o2_t, j.x2_t, j.o3_t, j.w3_t, j.part_t})
@@ -2083,6 +2084,11 @@ int vdc_load_jobs(vdc_ctx* ctx, const vdc_job* jobs, uint32_t n_jobs, uint32_t r
     dfree(ctx->d_jobs);
     CU(cudaMalloc(&ctx->d_jobs, sizeof(vdc_job) * std::max<uint32_t>(1, n_jobs)));
     if (n_jobs) CU(cudaMemcpy(ctx->d_jobs, jobs, sizeof(vdc_job) * n_jobs, cudaMemcpyHostToDevice));
+    // single-request µops only read the first 128 bytes of their block: a packed
+    // copy keeps one 128-byte line per µop (one L2 round trip per operand fetch)
+    dfree(ctx->d_jobs_core);
+    CU(cudaMalloc(&ctx->d_jobs_core, size_t(128) * std::max<uint32_t>(1, n_jobs)));
+    if (n_jobs) CU(cudaMemcpy2D(ctx->d_jobs_core, 128, jobs, sizeof(vdc_job), 128, n_jobs, cudaMemcpyHostToDevice));
     ctx->n_jobs = n_jobs;
     ctx->ring = true;
     ctx->batched = batched;
@@ -2107,7 +2113,7 @@ int vdc_bind_tensor(vdc_ctx* ctx, uint16_t tensor, void* dptr, size_t bytes, int
     for (size_t i = 0; i < ctx->dev_descs.size(); ++i)
         if (ctx->dev_descs[i].storage == int32_t(tensor)) ctx->dev_descs[i].ptr = static_cast<char*>(dptr);
     ctx->descs_dirty = true;
-    if (d.tmap >= 0) {
+    if (s.tma) {
         // {64 columns x tma rows} boxes, 128-byte swizzle: the K-major SW128
         // operand layout of tcgen05.mma (ring_engine.cu, bgemm)
         using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -2125,7 +2131,7 @@ int vdc_bind_tensor(vdc_ctx* ctx, uint16_t tensor, void* dptr, size_t bytes, int
         const cuuint64_t strides[1] = {cuuint64_t(d.cols) * 2};
         const cuuint32_t box[2] = {64, s.tma};
         const cuuint32_t es[2] = {1, 1};
-        const CUresult r = enc(&ctx->tmaps_host[size_t(d.tmap)], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dptr, dims, strides, box, es,
+        const CUresult r = enc(&ctx->tmaps_host[tensor], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dptr, dims, strides, box, es,
                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(VDC_ERR_INPUT, "tensor map encode failed for tensor " + std::to_string(tensor));
@@ -2204,6 +2210,7 @@ int vdc_launch(vdc_ctx* ctx, void* stream) {
         R.core_off = ctx->d_core_off;
         R.descs = ctx->d_descs;
         R.jobs = ctx->d_jobs;
+        R.jobs_core = ctx->d_jobs_core;
         R.counters = ctx->d_counters;
         R.step = ctx->d_step;
         R.n_step = int32_t(ctx->d_step ? ctx->n_step : 0);
@@ -2242,7 +2249,7 @@ int vdc_launch(vdc_ctx* ctx, void* stream) {
         }
         void* rargs[] = {&R};
         CU(cudaEventRecord(ctx->ev0, s));
-        CU(cudaLaunchCooperativeKernel(ring_kernel_entry(), dim3(ctx->prof.sm_count), dim3(kRingThreads), rargs,
+        CU(cudaLaunchCooperativeKernel(ring_kernel_entry(ctx->batched), dim3(ctx->prof.sm_count), dim3(kRingThreads), rargs,
                                        ring_smem_bytes(ctx->ring_slots), s));
         CU(cudaEventRecord(ctx->ev1, s));
         ctx->last_stream = s;

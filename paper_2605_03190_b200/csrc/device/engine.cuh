@@ -44,8 +44,6 @@ struct DevDesc {
     int32_t elem;         // bytes per element
     int32_t dtype;        // VDC_DTYPE_*
     int32_t storage;      // counter index (owner descriptor)
-    int32_t tmap;         // index into RingParams::tmaps (batched ring programs), -1 = none
-    int32_t pad_;
 };
 
 struct DepQueue {          // global FIFO per dep id (single producer / consumer site)
@@ -109,6 +107,7 @@ struct RingParams {
     const uint32_t* core_off;
     const DevDesc* descs;
     const ::vdc_job* jobs;
+    const char* jobs_core;     // the first 128 bytes of every operand block, packed (single-request programs)
     uint32_t* counters;        // per storage descriptor, monotonic across launches
     const int64_t* step;
     int32_t n_step;
@@ -126,10 +125,10 @@ struct RingParams {
     unsigned long long* trace;  // optional: per VCC core trace_cap records {core<<32|pc, t_enter, t_ready, t_done}
     uint32_t trace_cap;
     uint32_t batched;           // batched program: TMEM accumulator + X ring for BGEMM µops
-    const void* tmaps;          // CUtensorMap[] (64-byte aligned), indexed by DevDesc::tmap
+    const void* tmaps;          // CUtensorMap[n_desc] (128 bytes each), indexed by descriptor (vdc_desc.tma > 0 only)
 };
 size_t ring_smem_bytes(uint32_t ring_slots);
-const void* ring_kernel_entry();
+const void* ring_kernel_entry(bool batched);
 constexpr uint32_t kRingThreads = 32 * (8 + 1);
 
 // A region of `count` slots, not necessarily contiguous (indices packed 8

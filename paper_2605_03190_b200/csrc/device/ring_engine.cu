@@ -68,12 +68,12 @@ struct alignas(16) Shared {
     float bc[2 * CW];
     float rope_cs[MAX_HD / 2], rope_sn[MAX_HD / 2];  // rotary table of the launch's position
     int32_t flag;
-    // batched programs: activation-chunk ring (in x), MMA completion, TMEM base, rms scales
+    alignas(16) uint4 x[XBUF / 16];  // GEMV input vector (normalised, model dtype), reused across jobs;
+                                       // batched programs: activation-chunk ring (128-byte swizzle, from the first 1 KB boundary)
+    // batched programs: activation-chunk barriers, MMA completion, TMEM base, rms scales
     uint64_t xfull[NXMAX], xempty[NXMAX], mma_bar;
     uint32_t tmem_base;
     float binv[VDC_RING_MAX_BATCH];
-    alignas(1024) uint4 x[XBUF / 16];  // GEMV input vector (normalised, model dtype), reused across jobs;
-                                       // batched programs: activation chunks (128-byte swizzle, 1 KB aligned)
 };
 
 size_t smem_bytes(uint32_t slots) { return size_t(slots) * SLOT + ((sizeof(Shared) + 127) & ~size_t(127)); }
@@ -125,6 +125,10 @@ __device__ __forceinline__ float dot16(uint4 a, uint4 b) {
     }
 }
 
+// BATCHED: the kernel instance for batched programs (BGEMM µops, paged
+// attention); single-request programs run the instance without those paths
+// so their register allocation and scheduling are unaffected
+template <bool BATCHED>
 struct Vcc {
     const RingParams* P;
     Shared* S;
@@ -709,13 +713,13 @@ struct Vcc {
             sync();
         }
         const uint32_t xbytes = uint32_t(npad) * 128u;
-        const uint32_t NX = min(uint32_t(NXMAX), uint32_t(XBUF) / xbytes);
-        const uint32_t xb0 = smem_addr(S->x);
+        const uint32_t xb0 = (smem_addr(S->x) + 1023u) & ~1023u;  // 128-byte swizzle atoms repeat every 1 KB
+        const uint32_t NX = min(uint32_t(NXMAX), (uint32_t(XBUF) - (xb0 - smem_addr(S->x))) / xbytes);
         if (ct == 0) {
             // generic writes (other SMs' epilogues, this CTA's scratch) before async-proxy reads / writes
             fence_proxy_async_global();
             fence_proxy_async_smem();
-            const void* xm = static_cast<const char*>(P->tmaps) + size_t(P->descs[J.x_t].tmap) * 128;
+            const void* xm = static_cast<const char*>(P->tmaps) + size_t(J.x_t) * 128;
             const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(npad >> 3) << 17) | (uint32_t(128 >> 4) << 24);
             auto issue_x = [&](int j) -> bool {
                 const uint32_t i = xq % NX;
@@ -877,7 +881,7 @@ struct Vcc {
                     double ang = double(pos) * invf;
                     ang -= 6.283185307179586 * rint(ang * 0.15915494309189535);
                     float sn, cs;
-                    sincosf(float(ang), &sn, &cs);
+                    __sincosf(float(ang), &sn, &cs);  // |ang| <= pi after the reduction
                     v[c] = even ? v[c] * cs - other * sn : other * sn + v[c] * cs;
                 }
                 if (isq) {
@@ -995,10 +999,10 @@ struct Vcc {
         // pages mapped to warp pairs by ring slot (slot s -> pair (s % 8) / 2,
         // K on even slots: a leading pad tile aligns the job), so every slot
         // keeps a single consumer pair and jobs may span more than the ring
-        const bool batched = J.flags & VDC_JOB_BATCH;
+        const bool batched = BATCHED && (J.flags & VDC_JOB_BATCH);
         const int64_t pos = batched ? P->step[3 * J.req + 1] : P->step[VDC_STEP_POS];
         const int64_t ctx = batched ? P->step[3 * J.req + 2] : P->step[VDC_STEP_CTX];
-        if (J.lead_pad) {
+        if (batched && J.lead_pad) {
             const uint32_t s0 = kt % R;
             if ((s0 & uint32_t(CW - 1)) == w) {
                 if (!wait_full(s0, (kt / R) & 1u)) {
@@ -1349,8 +1353,9 @@ struct Vcc {
     }
 };
 
+template <bool BATCHED>
 __device__ void vcc_role(const RingParams& P, Shared& S, char* ring) {
-    Vcc v;
+    Vcc<BATCHED> v;
     v.P = &P;
     v.S = &S;
     v.ring = smem_addr(ring);
@@ -1368,7 +1373,25 @@ __device__ void vcc_role(const RingParams& P, Shared& S, char* ring) {
         const uint4 raw = __ldg(&P.words[w0 + pc]);
         const uint32_t op = raw.x & 0xff;
         if (op == OP_HALT) break;
-        const vdc_job& J = P.jobs[raw.z];
+        // batched programs read whole 256-byte operand blocks, single-request
+        // programs the packed first halves (the only fields their µops use)
+        const char* jb = BATCHED ? reinterpret_cast<const char*>(P.jobs) : P.jobs_core;
+        const size_t js = BATCHED ? sizeof(vdc_job) : 128;
+        if (pc + 1 < n) {  // the next µop's operand block -> L1 while this one runs
+            const uint4 nx = __ldg(&P.words[w0 + pc + 1]);
+            if ((nx.x & 0xff) != OP_HALT && v.ct * 128u < js)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(jb + size_t(nx.z) * js + 128 * v.ct));
+        }
+        // single-request µops: the 128-byte core of the block by value (all
+        // fields requested in one round trip, kept in registers; measured
+        // ~2% faster per token than field loads through a reference)
+        vdc_job Jv;
+        if constexpr (!BATCHED) {
+            const uint4* src = reinterpret_cast<const uint4*>(jb + size_t(raw.z) * js);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) reinterpret_cast<uint4*>(&Jv)[i] = __ldg(src + i);
+        }
+        const vdc_job& J = BATCHED ? *reinterpret_cast<const vdc_job*>(jb + size_t(raw.z) * js) : Jv;
         const bool bf = J.x_t >= 0 && v.tdtype(J.x_t) == VDC_DTYPE_BF16;
         const unsigned long long t_enter = P.trace ? now_ns() : 0;
         v.t_ready = 0;
@@ -1376,13 +1399,13 @@ __device__ void vcc_role(const RingParams& P, Shared& S, char* ring) {
             case OP_GEMV:
             case OP_RMS_GEMV:
             case OP_GEMV_ADD:
-                if (bf) v.gemv<true>(J); else v.gemv<false>(J);
+                if (bf) v.template gemv<true>(J); else v.template gemv<false>(J);
                 break;
             case OP_ATTN_DECODE: {
                 const bool kbf = v.tdtype(J.a_t) == VDC_DTYPE_BF16;
                 const int dpl = J.head_dim / 32, G = J.group;
 #define VDC_ATTN_CASE(B, D, GG) \
-    if (kbf == B && dpl == D && G == GG) { v.attn<B, D, GG>(J); break; }
+    if (kbf == B && dpl == D && G == GG) { v.template attn<B, D, GG>(J); break; }
                 VDC_ATTN_CASE(true, 4, 4)
                 VDC_ATTN_CASE(true, 4, 8)
                 VDC_ATTN_CASE(false, 2, 1)
@@ -1393,9 +1416,22 @@ __device__ void vcc_role(const RingParams& P, Shared& S, char* ring) {
             }
             case OP_ATTN_COMBINE: v.combine(J); break;
             case OP_ALLREDUCE_ADD: v.allreduce(J); break;
-            case OP_BGEMM: v.bgemm(J); break;
+            case OP_BGEMM:
+                if constexpr (BATCHED) {
+                    v.bgemm(J);
+                    break;
+                }
+                if (v.ct == 0) v.fire(4, (core << 16) | pc);
+                v.ok = false;
+                break;
             case OP_ELEMWISE:
-                if (J.flags & VDC_JOB_BATCH) v.embed_rows(J); else v.copy_row(J);
+                if constexpr (BATCHED) {
+                    if (J.flags & VDC_JOB_BATCH) {
+                        v.embed_rows(J);
+                        break;
+                    }
+                }
+                v.copy_row(J);
                 break;
             default:
                 if (v.ct == 0) v.fire(4, (core << 16) | pc);
@@ -1432,6 +1468,7 @@ struct Tile {
     __device__ uint32_t bytes() const { return copies * run; }
 };
 
+template <bool BATCHED>
 __device__ __forceinline__ Tile resolve_load(const RingParams& P, uint4 raw) {
     Tile t;
     const uint32_t op = raw.x & 0xff;
@@ -1453,13 +1490,13 @@ __device__ __forceinline__ Tile resolve_load(const RingParams& P, uint4 raw) {
         return t;
     }
     const int64_t c0 = int64_t(pl & 0xfff), c1 = int64_t((pl >> 12) & 0xfff), c2 = int64_t((pl >> 24) & 0xfff);
-    if (d.tmap >= 0) {  // one 2-D tensor copy: 64 columns x tile_rows rows, 128-byte swizzle
-        t.tmap = static_cast<const char*>(P.tmaps) + size_t(d.tmap) * 128;
+    if (BATCHED && ((raw.y >> 24) & 1u)) {  // reg1 = 1: one 2-D tensor copy (64 columns x tile_rows rows, 128-byte swizzle)
+        t.tmap = static_cast<const char*>(P.tmaps) + size_t(ti) * 128;
         t.cx = int32_t(c1 * d.tile_cols);
         t.cy = int32_t(c0 * d.tile_rows);
         t.copies = 1;
         t.run = uint32_t(d.tile_rows * d.tile_cols * d.elem);
-        t.bad = t.run > SLOT || rank != 2 || c0 >= d.grid[0] || c1 >= d.grid[1];
+        t.bad = !P.tmaps || t.run > SLOT || rank != 2 || c0 >= d.grid[0] || c1 >= d.grid[1];
         return t;
     }
     const int64_t rt = rank == 3 ? c1 : c0, ctile = rank == 3 ? c2 : c1, plane = rank == 3 ? c0 : 0;
@@ -1497,6 +1534,7 @@ __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
 // barrier (non-blocking test_wait) in one converged loop and issue the bulk
 // copy of their next tile as soon as it is free; optional L2 prefetch of
 // the tile `prefetch` rounds ahead.
+template <bool BATCHED>
 __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t core = 2 * blockIdx.x;
@@ -1523,7 +1561,7 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
             ready = m == 0 || mbar_test(&S.empty[slot], (m - 1u) & 1u);
         }
         if (ready) {
-            const Tile t = resolve_load(P, raw);
+            const Tile t = resolve_load<BATCHED>(P, raw);
             if (t.bad || t.halt) {
                 if (atomicCAS(&P.status->abort, 0, 2) == 0) {
                     P.status->fault_code = 5;
@@ -1534,7 +1572,7 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
                 if (P.tile_trace && blockIdx.x == (P.debug >> 8) && g < P.tile_trace_cap) P.tile_trace[3 * g] = now_ns();
                 mbar_expect_tx(&S.full[slot], t.bytes());
                 char* dst = ring + size_t(slot) * SLOT;
-                if (t.tmap)
+                if (BATCHED && t.tmap)
                     tma_2d(smem_addr(dst), t.tmap, t.cx, t.cy, &S.full[slot]);
                 else
                     for (uint32_t q = 0; q < t.copies; ++q)
@@ -1550,7 +1588,7 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
         if (PF && pending && !ready && pf_g < ntiles && pf_g < g + R * (1 + PF)) {
             // slot busy (the compute core is behind or waiting on a dependency):
             // keep DRAM busy by pulling this lane's upcoming tiles into L2
-            const Tile ta = resolve_load(P, __ldg(&P.words[w0 + pf_g]));
+            const Tile ta = resolve_load<BATCHED>(P, __ldg(&P.words[w0 + pf_g]));
             if (!ta.bad && !ta.halt && !ta.tmap)
                 for (uint32_t q = 0; q < ta.copies; ++q) prefetch_l2(ta.src + size_t(q) * ta.pitch, ta.run);
             pf_g += R;
@@ -1592,6 +1630,7 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
     }
 }
 
+template <bool BATCHED>
 __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(const __grid_constant__ RingParams P) {
     extern __shared__ __align__(1024) char smem[];
     char* ring = smem;
@@ -1601,24 +1640,26 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(const __grid_cons
             mbar_init(&S.full[i], 1);
             mbar_init(&S.empty[i], 1);
         }
-        for (int i = 0; i < NXMAX; ++i) {
-            mbar_init(&S.xfull[i], 1);
-            mbar_init(&S.xempty[i], 1);
+        if (BATCHED) {
+            for (int i = 0; i < NXMAX; ++i) {
+                mbar_init(&S.xfull[i], 1);
+                mbar_init(&S.xempty[i], 1);
+            }
+            mbar_init(&S.mma_bar, 1);
         }
-        mbar_init(&S.mma_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (P.batched && threadIdx.x < 32) {  // TMEM accumulator of the batched GEMM µops (one CTA per SM)
+    if (BATCHED && threadIdx.x < 32) {  // TMEM accumulator of the batched GEMM µops (one CTA per SM)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&S.tmem_base)),
                      "r"(TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    tc_fence_before();
+    if (BATCHED) tc_fence_before();
     __syncthreads();
-    tc_fence_after();
+    if (BATCHED) tc_fence_after();
     if (threadIdx.x < NCT) {
-        vcc_role(P, S, ring);
-        if (P.batched) {
+        vcc_role<BATCHED>(P, S, ring);
+        if (BATCHED) {
             tc_fence_before();
             named_bar(BAR_VCC, NCT);
             tc_fence_after();
@@ -1626,13 +1667,15 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(const __grid_cons
                 asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(S.tmem_base), "r"(TMEM_COLS));
         }
     } else {
-        vmc_role(P, S, ring);
+        vmc_role<BATCHED>(P, S, ring);
     }
 }
 
 }  // namespace ring
 
 size_t ring_smem_bytes(uint32_t ring_slots) { return ring::smem_bytes(ring_slots); }
-const void* ring_kernel_entry() { return reinterpret_cast<const void*>(&ring::ring_kernel); }
+const void* ring_kernel_entry(bool batched) {
+    return batched ? reinterpret_cast<const void*>(&ring::ring_kernel<true>) : reinterpret_cast<const void*>(&ring::ring_kernel<false>);
+}
 
 }  // namespace vdc_dev

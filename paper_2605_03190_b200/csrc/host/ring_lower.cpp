@@ -444,6 +444,7 @@ class RingLowering {
                     u.flow = 1;
                     u.size = 1;
                     u.addr = isa::AddressSpec::tile(t.tensor, t.coord);
+                    u.reg1 = desc_[t.tensor].tma ? 1 : 0;  // TMA tensor tile (batched weights)
                     vs.push_back(u);
                     vm.push_back({r.ordinal, slot, -1});
                 }
