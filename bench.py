@@ -396,6 +396,146 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     return result
 
 
+# ---------------------------------------------------------------------------
+# C3: batched decode (B requests, per-request contexts, paged KV)
+
+MASK64 = (1 << 64) - 1
+
+
+def splitmix64_stream(seed: int):
+    state = seed & MASK64
+    while True:
+        state = (state + 0x9E3779B97F4A7C15) & MASK64
+        z = state
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & MASK64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & MASK64
+        yield z ^ (z >> 31)
+
+
+def c3_contexts(batch: int, lo: int = 128, hi: int = 8192, seed: int = 1) -> list:
+    """ctx_r = splitmix64(seed 1) -> U[128, 8192]"""
+    g = splitmix64_stream(seed)
+    return [lo + next(g) % (hi - lo + 1) for _ in range(batch)]
+
+
+def run_batched(args):
+    import torch
+    from paper_2605_03190_b200 import Program
+    from paper_2605_03190_b200.engine import Engine
+
+    B = args.batch
+    ctxs = c3_contexts(B)
+    pages = [(c + 63) // 64 for c in ctxs]
+    t_build = time.time()
+    req = {"engine": "ring", "model": {"preset": "llama3-8b", "layers": args.layers},
+           "layout": {"batch": B, "req_pages": pages, "pages_per_job": args.pages_per_job, "gu_block": 128, "page_rows": 64},
+           "profile": {"builtin": "b200"}}
+    prog = Program.build(req)
+    build_s = time.time() - t_build
+    eng = Engine(prog, watchdog_ms=20000)
+    tens = init_tensors(eng)
+    info = eng.info
+    bi = info["batch"]
+    st_host = [0] * int(info["step_scalars"])
+    for b in range(B):
+        st_host[3 * b: 3 * b + 3] = [17 + b, ctxs[b] - 1, ctxs[b]]
+    st_host[bi["page_table_off"]: bi["page_table_off"] + len(bi["page_table"])] = bi["page_table"]
+    step = torch.tensor(st_host, dtype=torch.int64, device="cuda")
+    eng.bind_step(step)
+    stream = torch.cuda.Stream()
+    # algorithmic bytes: bf16 weights once + one embedding row per request + each
+    # request's K/V rows over its context + the appended rows
+    w = kvr = kvw = 0
+    layers = args.layers
+    for d in info["descriptors"]:
+        if d["view_of"] >= 0 or not (d["external"] or d["state"]):
+            continue
+        n = 1
+        for x in d["shape"]:
+            n *= x
+        if d["name"] == "embed.table":
+            w += B * d["shape"][-1] * 2
+        elif d["name"].endswith(".kc") or d["name"].endswith(".vc"):
+            hkv, hd = d["shape"][1] // 64, d["shape"][2]
+            kvr += sum(ctxs) * hkv * hd * 2
+            kvw += B * hkv * hd * 2
+        elif d["dtype"] == "bf16" and d["name"] != "ring.pad":
+            w += n * 2
+    nbytes = {"weights": w, "kv_read": kvr, "kv_write": kvw, "total": w + kvr + kvw}
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            eng.launch(stream)
+        rep = eng.wait()
+    if not rep.completed:
+        raise SystemExit(f"engine did not complete: {rep.message} stalled={rep.stalled}")
+    sampler = ClockSampler(0)
+    sampler.start()
+    time.sleep(0.3)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    torch.cuda.synchronize()
+    w0 = time.time()
+    with torch.cuda.stream(stream):
+        ev[0].record(stream)
+        for k in range(args.steps):
+            eng.launch(stream)
+            ev[k + 1].record(stream)
+    stream.synchronize()
+    sampler.mark(w0, time.time())
+    rep = eng.wait()
+    per = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+
+    # e2e: per step the request triples (token, pos, ctx) go H2D from pinned
+    # memory, the engine runs, all B x V fp32 logits come back D2H and the next
+    # tokens are picked on the host (greedy)
+    logits = tens["logits"]
+    h_trip = torch.tensor(st_host[: 3 * B], dtype=torch.int64).pin_memory()
+    h_logits = torch.empty(logits.numel(), dtype=torch.float32).pin_memory()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    w2 = time.time()
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for k in range(args.steps):
+            step[: 3 * B].copy_(h_trip, non_blocking=True)
+            eng.launch(stream)
+            h_logits.copy_(logits, non_blocking=True)
+            stream.synchronize()
+            nxt = torch.argmax(h_logits.view(B, -1), dim=1)
+            h_trip.view(B, 3)[:, 0] = nxt
+        e1.record(stream)
+    stream.synchronize()
+    sampler.mark(w2, time.time())
+    e2e_ms = e0.elapsed_time(e1)
+    clocks = sampler.stop()
+    value = B * args.steps / (total_ms / 1e3)
+    peak, peak_src = measured_peak()
+    achieved = nbytes["total"] / (sum(per) / len(per) / 1e3) / 1e9
+    return {
+        "metric": "Llama-3-8B bf16 batched decode tokens/s (C3: batch %d, paged KV) + HBM GB/s fraction of peak" % B,
+        "value": round(value, 2), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic: random-init Llama-3-8B weights, random bf16 KV pages, contexts splitmix64(seed 1) -> U[128, 8192]",
+        "config": {"workload": f"C3 Llama-3-8B bf16 decode, batch {B}, per-request contexts U[128,8192] (sum {sum(ctxs)}), "
+                               f"paged KV (64-row pages, {sum(pages)} pages), {layers} layers + lm_head",
+                   "model": "llama3-8b", "batch": B, "contexts": ctxs, "parallelism": "1 GPU",
+                   "l2": "inputs larger than L2 (algorithmic %.2f GB per step vs 126 MB L2)" % (nbytes["total"] / 1e9),
+                   "program_uops": info["total_uops"], "build_seconds": round(build_s, 2)},
+        "e2e": {"value": round(B * args.steps / (e2e_ms / 1e3), 2), "unit": "tokens/s", "h2d_bytes_per_step": 3 * B * 8,
+                "d2h_bytes_per_step": logits.numel() * 4},
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                     "bytes_per_step": nbytes, "kernel": "vdc_dev::ring::ring_kernel<true> (persistent, 1 CTA/SM)",
+                     "kernel_ms_median": round(sorted(per)[len(per) // 2], 4)},
+        "clocks": clocks,
+        "engine_report": {"uops_executed": rep.uops_executed, "bytes_loaded": rep.bytes_loaded,
+                          "wait_cycles_sum_over_sms": rep.wait_cycles},
+    }
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -408,6 +548,8 @@ def main():
     ap.add_argument("--engine", default="ring", choices=["ring", "reference"])
     ap.add_argument("--ring-slots", type=int, default=12)
     ap.add_argument("--pages-per-job", type=int, default=4)
+    ap.add_argument("--batch", type=int, default=1,
+                    help="> 1: C3 batched decode (per-request contexts, paged KV, BGEMM on tcgen05); 1 GPU")
     ap.add_argument("--parallel", default="tp", choices=["tp", "replicas"],
                     help="N>1: tensor parallel over the N GPUs (default) or N independent replicas")
     args = ap.parse_args()
@@ -434,6 +576,10 @@ def main():
         print(json.dumps(line))
         return
 
+    if args.batch > 1:
+        if rank == 0:
+            print(json.dumps(run_batched(args)))
+        return
     if world > 1:
         import torch
         import torch.distributed as dist

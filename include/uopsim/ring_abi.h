@@ -65,13 +65,20 @@
 /* Batched programs (BGEMM and friends, layout.batch > 1):
  *  - activations are (npad, K) bf16 row-major, request b = row b; rows
  *    >= nb stay zero. npad in {16, 32, 64} is the tcgen05 MMA N.
- *  - weight tiles are 128 rows x 64 columns moved by TMA tensor copies
- *    with 128-byte swizzle (vdc_desc.tma = 128), the canonical K-major
- *    operand layout of tcgen05.mma; activation chunks (npad x 64) are
- *    loaded by the compute core's MMA issuer after the readiness wait
- *    (vdc_desc.tma = npad).
+ *  - weight tiles are 128 rows x 64 columns, stored packed and
+ *    pre-swizzled (VDC_DESC_PACKED_SW128) and moved by one bulk copy each;
+ *    activation chunks (npad x 64) are loaded by the compute core's MMA
+ *    issuer with TMA tensor copies (128-byte swizzle, vdc_desc.tma = npad)
+ *    after the readiness wait.
  *  - KV caches are page pools (pages, hkv * 64, hd): tile (page, head). */
 #define VDC_RING_BGEMM_ROWS 128  /* output rows per BGEMM job (MMA M) */
+/* vdc_desc.tma value of a weight stored as packed tiles: tile (rb, kt) of
+ * 128 rows x 64 columns is 16 KB contiguous at ((rb * K/64) + kt) * 16 KB,
+ * pre-swizzled (16-byte chunk c of row r at chunk c ^ (r % 8)), i.e. the
+ * K-major 128-byte-swizzle operand layout of tcgen05.mma: one contiguous
+ * bulk copy per ring tile (row-major 128 x 64 boxes would be 128 separate
+ * 128-byte DRAM bursts per tile, ~half the HBM rate). */
+#define VDC_DESC_PACKED_SW128 0x80000000u
 #define VDC_RING_BGEMM_KT 64     /* reduction columns per weight tile (128-byte swizzle atom) */
 #define VDC_RING_MAX_BATCH 64
 

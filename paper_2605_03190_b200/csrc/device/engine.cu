@@ -1910,8 +1910,9 @@ int vdc_create(const vdc_profile* p, int device, vdc_ctx** out) {
                                        std::to_string(prop.sharedMemPerBlockOptin));
     }
     if (p->slot_size == VDC_RING_SLOT_BYTES)
-        for (bool b : {false, true})
-            CU(cudaFuncSetAttribute(ring_kernel_entry(b), cudaFuncAttributeMaxDynamicSharedMemorySize, int(ctx->smem_bytes)));
+        for (bool b : {false, true})  // launch sizes depend on the loaded program (ring slots, batched)
+            CU(cudaFuncSetAttribute(ring_kernel_entry(b), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(prop.sharedMemPerBlockOptin)));
     else
         CU(cudaFuncSetAttribute(engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ctx->smem_bytes)));
     CU(cudaMalloc(&ctx->d_stats, sizeof(SmStats) * p->sm_count));
@@ -2015,7 +2016,11 @@ int vdc_load_program(vdc_ctx* ctx, const uint8_t* words, const uint32_t* words_p
         d.elem = s.dtype == VDC_DTYPE_BF16 ? 2 : s.dtype == VDC_DTYPE_I64 ? 8 : 4;
         d.storage = s.view_of >= 0 ? s.view_of : int32_t(i);
         d.ptr = nullptr;
-        if (s.tma) {
+        if (s.tma == VDC_DESC_PACKED_SW128) {
+            if (s.view_of >= 0 || s.rank != 2 || s.dtype != VDC_DTYPE_BF16 || s.tile_rows != 128 || s.tile_cols != 64 ||
+                s.shape[0] % 128 || s.shape[1] % 64)
+                return fail(VDC_ERR_INPUT, "packed weights must be owned rank-2 bf16 tensors of 128 x 64 tiles");
+        } else if (s.tma) {
             if (s.view_of >= 0 || s.rank != 2 || s.dtype != VDC_DTYPE_BF16 || s.tma > 256 || s.shape[1] % 64)
                 return fail(VDC_ERR_INPUT, "TMA descriptors must be owned rank-2 bf16 tensors with 64-column tiles");
             ++n_tmaps;
@@ -2090,6 +2095,14 @@ int vdc_load_jobs(vdc_ctx* ctx, const vdc_job* jobs, uint32_t n_jobs, uint32_t r
     CU(cudaMalloc(&ctx->d_jobs_core, size_t(128) * std::max<uint32_t>(1, n_jobs)));
     if (n_jobs) CU(cudaMemcpy2D(ctx->d_jobs_core, 128, jobs, sizeof(vdc_job), 128, n_jobs, cudaMemcpyHostToDevice));
     ctx->n_jobs = n_jobs;
+    {
+        int dev = 0, optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        if (ring_smem_bytes(ring_slots, batched) > size_t(optin))
+            return fail(VDC_ERR_INPUT, "ring of " + std::to_string(ring_slots) + " slots needs " +
+                                           std::to_string(ring_smem_bytes(ring_slots, batched)) + " B of shared memory");
+    }
     ctx->ring = true;
     ctx->batched = batched;
     ctx->ring_slots = ring_slots;
@@ -2113,7 +2126,7 @@ int vdc_bind_tensor(vdc_ctx* ctx, uint16_t tensor, void* dptr, size_t bytes, int
     for (size_t i = 0; i < ctx->dev_descs.size(); ++i)
         if (ctx->dev_descs[i].storage == int32_t(tensor)) ctx->dev_descs[i].ptr = static_cast<char*>(dptr);
     ctx->descs_dirty = true;
-    if (s.tma) {
+    if (s.tma && s.tma != VDC_DESC_PACKED_SW128) {
         // {64 columns x tma rows} boxes, 128-byte swizzle: the K-major SW128
         // operand layout of tcgen05.mma (ring_engine.cu, bgemm)
         using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -2178,7 +2191,7 @@ int vdc_bind_trace(vdc_ctx* ctx, void* dptr, uint32_t records_per_core) {
 // debug: copy the tile trace of the last launch (3 x u64 per tile) to host memory
 extern "C" int vdc_debug_tile_trace(vdc_ctx* ctx, void* host, uint32_t n) {
     if (!ctx || !ctx->d_tile_trace) return fail(VDC_ERR_INPUT, "no tile trace (set VDC_RING_DEBUG bit 1)");
-    CU(cudaMemcpy(host, ctx->d_tile_trace, sizeof(unsigned long long) * 3 * std::min<uint32_t>(n, 65536), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(host, ctx->d_tile_trace, sizeof(unsigned long long) * std::min<uint32_t>(n, 4 * 65536), cudaMemcpyDeviceToHost));
     return VDC_OK;
 }
 
@@ -2241,8 +2254,8 @@ int vdc_launch(vdc_ctx* ctx, void* stream) {
         R.batched = ctx->batched ? 1u : 0u;
         if (R.debug & 2u) {
             static unsigned long long* tt = nullptr;
-            if (!tt) cudaMalloc(&tt, sizeof(unsigned long long) * 3 * 65536);
-            cudaMemsetAsync(tt, 0, sizeof(unsigned long long) * 3 * 65536, s);
+            if (!tt) cudaMalloc(&tt, sizeof(unsigned long long) * 4 * 65536);
+            cudaMemsetAsync(tt, 0, sizeof(unsigned long long) * 4 * 65536, s);
             R.tile_trace = tt;
             R.tile_trace_cap = 65536;
             ctx->d_tile_trace = tt;
@@ -2250,7 +2263,7 @@ int vdc_launch(vdc_ctx* ctx, void* stream) {
         void* rargs[] = {&R};
         CU(cudaEventRecord(ctx->ev0, s));
         CU(cudaLaunchCooperativeKernel(ring_kernel_entry(ctx->batched), dim3(ctx->prof.sm_count), dim3(kRingThreads), rargs,
-                                       ring_smem_bytes(ctx->ring_slots), s));
+                                       ring_smem_bytes(ctx->ring_slots, ctx->batched), s));
         CU(cudaEventRecord(ctx->ev1, s));
         ctx->last_stream = s;
         return VDC_OK;

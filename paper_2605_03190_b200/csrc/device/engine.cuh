@@ -127,7 +127,7 @@ struct RingParams {
     uint32_t batched;           // batched program: TMEM accumulator + X ring for BGEMM µops
     const void* tmaps;          // CUtensorMap[n_desc] (128 bytes each), indexed by descriptor (vdc_desc.tma > 0 only)
 };
-size_t ring_smem_bytes(uint32_t ring_slots);
+size_t ring_smem_bytes(uint32_t ring_slots, bool batched = false);
 const void* ring_kernel_entry(bool batched);
 constexpr uint32_t kRingThreads = 32 * (8 + 1);
 

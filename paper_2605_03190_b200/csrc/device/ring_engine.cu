@@ -55,11 +55,16 @@ enum : uint32_t {
     OP_LOAD = 0x01, OP_ELEMWISE = 0x25, OP_GEMV = 0x27, OP_RMS_GEMV = 0x28, OP_GEMV_ADD = 0x29, OP_ATTN_DECODE = 0x2A,
     OP_ATTN_COMBINE = 0x2B, OP_ALLREDUCE_ADD = 0x2C, OP_BGEMM = 0x2D, OP_HALT = 0x45,
 };
-constexpr int NXMAX = 8;            // activation-chunk ring depth of batched GEMMs
-constexpr uint32_t TMEM_COLS = 64;  // fp32 accumulator columns (>= npad)
+constexpr int NXMAX = 16;  // activation-chunk groups of batched GEMMs
+// batched kernel: activation-chunk ring after the control block. Its loads
+// queue behind the in-flight weight tiles of the SM's copy engine, so the
+// MMA issuer keeps more than a ring's worth of chunks in flight.
+constexpr uint32_t XRING_BYTES = 60 * 1024;
+constexpr uint32_t TMEM_COLS = 128;  // two fp32 accumulators of <= 64 columns (npad)
 
 // stat slots (SmStats::wait)
-enum : int { S_VMC_EMPTY = 0, S_VCC_FULL = 1, S_VCC_DEP = 2, S_VCC_EPI = 3, S_VCC_TOTAL = 4, S_VMC_TOTAL = 5, S_NJOBS = 6 };
+enum : int { S_VMC_EMPTY = 0, S_VCC_FULL = 1, S_VCC_DEP = 2, S_VCC_EPI = 3, S_VCC_TOTAL = 4, S_VMC_TOTAL = 5, S_NJOBS = 6,
+             S_X_FULL = 7, S_X_EMPTY = 8, S_MMA_DONE = 9, S_BG_PRO = 10 };
 
 struct alignas(16) Shared {
     uint64_t full[VDC_RING_MAX_SLOTS];
@@ -76,7 +81,10 @@ struct alignas(16) Shared {
     float binv[VDC_RING_MAX_BATCH];
 };
 
-size_t smem_bytes(uint32_t slots) { return size_t(slots) * SLOT + ((sizeof(Shared) + 127) & ~size_t(127)); }
+size_t smem_bytes(uint32_t slots, bool batched) {
+    return size_t(slots) * SLOT + (batched ? ((sizeof(Shared) + 1023) & ~size_t(1023)) + XRING_BYTES
+                                           : ((sizeof(Shared) + 127) & ~size_t(127)));
+}
 
 __device__ __forceinline__ float warp_sum(float x) {
 #pragma unroll
@@ -675,7 +683,16 @@ struct Vcc {
     __device__ uint16_t* u16p(int32_t t) const { return reinterpret_cast<uint16_t*>(tptr(t)); }
     __device__ int64_t req_pos(int b) const { return P->step[3 * b + 1]; }
 
-    __device__ bool spin(uint64_t* bar, uint32_t parity) {
+    unsigned long long st_xf = 0, st_xe = 0, st_mma = 0, st_pro = 0;
+    __device__ bool spin(uint64_t* bar, uint32_t parity, unsigned long long* acc = nullptr) {
+        const long long c0 = clock64();
+        struct Acc {
+            unsigned long long* a;
+            long long c0;
+            __device__ ~Acc() {
+                if (a) *a += clock64() - c0;
+            }
+        } guard{acc, c0};
         if (mbar_try(bar, parity)) return true;
         const unsigned long long t0 = now_ns();
         for (uint32_t n = 1;; ++n) {
@@ -691,6 +708,7 @@ struct Vcc {
     }
 
     __device__ void bgemm(const vdc_job& J) {
+        const long long p0 = clock64();
         const int n = J.kt1 - J.kt0, K = J.k, nb = J.nb, npad = J.npad;
         const bool rms = J.flags & VDC_JOB_RMS;
         if (!wait_ready(J.x_t, J.x_need, rms ? J.x2_t : -1, J.x2_need, (J.flags & VDC_JOB_RESID) ? J.a_t : -1, J.a_need)) {
@@ -713,47 +731,73 @@ struct Vcc {
             sync();
         }
         const uint32_t xbytes = uint32_t(npad) * 128u;
-        const uint32_t xb0 = (smem_addr(S->x) + 1023u) & ~1023u;  // 128-byte swizzle atoms repeat every 1 KB
-        const uint32_t NX = min(uint32_t(NXMAX), (uint32_t(XBUF) - (xb0 - smem_addr(S->x))) / xbytes);
+        // activation-chunk ring after the control block (1 KB aligned: the
+        // 128-byte swizzle atoms repeat every 1 KB)
+        const uint32_t xb0 = (smem_addr(S) + uint32_t(sizeof(Shared)) + 1023u) & ~1023u;
+        // tiles are handled in groups of G (one activation-chunk barrier, one
+        // fence, G W-slot commits per group): the issuer's fixed per-step cost
+        // (barrier round trips, commits) is paid once per G x 16 KB
+        const int G = npad <= 32 ? 4 : 2;
+        const uint32_t NXG = min(uint32_t(NXMAX), XRING_BYTES / (uint32_t(G) * xbytes));
+        if (ct == 0) st_pro += clock64() - p0;
         if (ct == 0) {
             // generic writes (other SMs' epilogues, this CTA's scratch) before async-proxy reads / writes
             fence_proxy_async_global();
             fence_proxy_async_smem();
             const void* xm = static_cast<const char*>(P->tmaps) + size_t(J.x_t) * 128;
             const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(npad >> 3) << 17) | (uint32_t(128 >> 4) << 24);
-            auto issue_x = [&](int j) -> bool {
-                const uint32_t i = xq % NX;
-                if (xq >= NX && !spin(&S->xempty[i], ((xq / NX) - 1u) & 1u)) return false;
-                mbar_expect_tx(&S->xfull[i], xbytes);
-                tma_2d(xb0 + i * xbytes, xm, (J.kt0 + j) * VDC_RING_BGEMM_KT, 0, &S->xfull[i]);
+            const int ngrp = (n + G - 1) / G;
+            auto issue_grp = [&](int j) -> bool {  // activation chunks of tile group j -> buffer xq % NXG
+                const uint32_t i = xq % NXG;
+                if (xq >= NXG && !spin(&S->xempty[i], ((xq / NXG) - 1u) & 1u, &st_xe)) return false;
+                const int cnt = min(G, n - j * G);
+                mbar_expect_tx(&S->xfull[i], uint32_t(cnt) * xbytes);
+                for (int u = 0; u < cnt; ++u)
+                    tma_2d(xb0 + (i * uint32_t(G) + uint32_t(u)) * xbytes, xm, (J.kt0 + j * G + u) * VDC_RING_BGEMM_KT, 0,
+                           &S->xfull[i]);
                 ++xq;
                 return true;
             };
+            // group look-ahead NXG - 1: the refill after group t reuses the
+            // buffer of group t - 1 (its MMAs were issued a group earlier)
             bool good = true;
-            const int pre = min(n, int(NX) - 1);
-            for (int j = 0; j < pre && good; ++j) good = issue_x(j);
+            const int L = max(1, int(NXG) - 1);
+            for (int j = 0; j < min(ngrp, L) && good; ++j) good = issue_grp(j);
             uint32_t g = kt;
-            for (int t = 0; t < n && good; ++t, ++g) {
-                if (t + int(NX) - 1 < n && !issue_x(t + int(NX) - 1)) {
+            for (int t = 0; t < ngrp && good; ++t) {
+                const int cnt = min(G, n - t * G);
+                const uint32_t xi = xd % NXG;
+                if (!spin(&S->xfull[xi], (xd / NXG) & 1u, &st_xf)) {
                     good = false;
                     break;
                 }
-                const uint32_t xi = xd % NX;
-                const uint32_t slot = g % R;
-                if (!spin(&S->xfull[xi], (xd / NX) & 1u) || !wait_full(slot, (g / R) & 1u)) {
-                    good = false;
-                    break;
-                }
+                for (int u = 0; u < cnt && good; ++u) good = wait_full((g + uint32_t(u)) % R, ((g + uint32_t(u)) / R) & 1u);
+                if (!good) break;
                 tc_fence_after();
-                if (!(P->debug & 1u)) {
-                    const uint32_t a0 = ring + slot * SLOT, b0 = xb0 + xi * xbytes;
+                const bool ttr = P->tile_trace && sm == (P->debug >> 8) && g < P->tile_trace_cap;
+                if (ttr) P->tile_trace[3 * g + 1] = now_ns();
+                for (int u = 0; u < cnt; ++u) {
+                    const uint32_t slot = (g + uint32_t(u)) % R;
+                    if (!(P->debug & 1u)) {
+                        const uint32_t a0 = ring + slot * SLOT, b0 = xb0 + (xi * uint32_t(G) + uint32_t(u)) * xbytes;
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)
-                        umma_bf16(tmem, umma_sw128_desc(a0 + kk * 32), umma_sw128_desc(b0 + kk * 32), idesc, (t | kk) ? 1u : 0u);
+                        // tiles alternate between two accumulators (columns 0 and
+                        // 64): consecutive MMAs do not serialise on one accumulator
+                        const int tile = t * G + u;
+                        for (int kk = 0; kk < 4; ++kk)
+                            umma_bf16(tmem + uint32_t(tile & 1) * 64u, umma_sw128_desc(a0 + kk * 32),
+                                      umma_sw128_desc(b0 + kk * 32), idesc, (tile > 1 || kk) ? 1u : 0u);
+                    }
+                    umma_commit(&S->empty[slot]);  // W slot -> memory core when its MMAs are done
                 }
-                umma_commit(&S->empty[slot]);  // W slot -> memory core when the MMAs are done
                 umma_commit(&S->xempty[xi]);
+                if (ttr) P->tile_trace[3 * g + 2] = now_ns();
                 ++xd;
+                g += uint32_t(cnt);
+                if (t + L < ngrp && !issue_grp(t + L)) {
+                    good = false;
+                    break;
+                }
             }
             if (good) umma_commit(&S->mma_bar);
             S->flag = good ? 1 : 0;
@@ -764,7 +808,7 @@ struct Vcc {
             ok = false;
             return;
         }
-        if (!spin(&S->mma_bar, nmma & 1u)) {
+        if (!spin(&S->mma_bar, nmma & 1u, ct == 0 ? &st_mma : nullptr)) {
             ok = false;
             return;
         }
@@ -824,6 +868,12 @@ struct Vcc {
         const int rg = J.r0 + row;           // global W row
         float v[NH];
         tmem_ld<NH>(tmem + (uint32_t(q * 32) << 16) + uint32_t(c0), v);
+        if (J.kt1 - J.kt0 > 1) {  // second accumulator (odd tiles), added in fixed order
+            float v2[NH];
+            tmem_ld<NH>(tmem + (uint32_t(q * 32) << 16) + 64u + uint32_t(c0), v2);
+#pragma unroll
+            for (int c = 0; c < NH; ++c) v[c] += v2[c];
+        }
         tc_fence_before();  // the accumulator may be overwritten after the next barrier
         if (J.arrive_need > 1) {
             // stream-K: this piece's partial -> global; the last piece of the
@@ -1040,6 +1090,8 @@ struct Vcc {
             // page i -> warp pair i mod 4 (balanced over the 8 warps); the
             // job's tiles (<= ring depth) were issued after every earlier
             // tile was released, so any warp may wait on their slots
+            // single-request programs: page i -> pair i % 4; batched programs on
+            // an 8-slot ring: pair (sk % 8) / 2 (one consumer pair per slot)
             const uint32_t pair = batched ? ((sk & uint32_t(CW - 1)) >> 1) : i % uint32_t(CW / 2);
             if ((w >> 1) != pair) continue;
             const int half = int(w & 1u);
@@ -1454,6 +1506,12 @@ __device__ void vcc_role(const RingParams& P, Shared& S, char* ring) {
         st.wait[S_VCC_EPI] = v.st_epi;
         st.wait[S_VCC_TOTAL] = clock64() - t0;
         st.wait[S_NJOBS] = jobs;
+        if constexpr (BATCHED) {
+            st.wait[S_X_FULL] = v.st_xf;
+            st.wait[S_X_EMPTY] = v.st_xe;
+            st.wait[S_MMA_DONE] = v.st_mma;
+            st.wait[S_BG_PRO] = v.st_pro;
+        }
     }
 }
 
@@ -1461,8 +1519,6 @@ __device__ void vcc_role(const RingParams& P, Shared& S, char* ring) {
 // `pitch` apart (whole-row tiles are a single run).
 struct Tile {
     const char* src = nullptr;
-    const void* tmap = nullptr;  // TMA tensor tile (batched weights): box at (cx, cy)
-    int32_t cx = 0, cy = 0;
     uint32_t copies = 0, run = 0, pitch = 0;
     bool bad = false, halt = false;
     __device__ uint32_t bytes() const { return copies * run; }
@@ -1490,13 +1546,12 @@ __device__ __forceinline__ Tile resolve_load(const RingParams& P, uint4 raw) {
         return t;
     }
     const int64_t c0 = int64_t(pl & 0xfff), c1 = int64_t((pl >> 12) & 0xfff), c2 = int64_t((pl >> 24) & 0xfff);
-    if (BATCHED && ((raw.y >> 24) & 1u)) {  // reg1 = 1: one 2-D tensor copy (64 columns x tile_rows rows, 128-byte swizzle)
-        t.tmap = static_cast<const char*>(P.tmaps) + size_t(ti) * 128;
-        t.cx = int32_t(c1 * d.tile_cols);
-        t.cy = int32_t(c0 * d.tile_rows);
+    if (BATCHED && ((raw.y >> 24) & 1u)) {  // reg1 = 1: packed, pre-swizzled 16 KB weight tile (one bulk copy)
+        t.src = d.ptr + (c0 * d.grid[1] + c1) * (d.tile_rows * d.tile_cols * d.elem);
         t.copies = 1;
         t.run = uint32_t(d.tile_rows * d.tile_cols * d.elem);
-        t.bad = !P.tmaps || t.run > SLOT || rank != 2 || c0 >= d.grid[0] || c1 >= d.grid[1];
+        t.pitch = 0;
+        t.bad = t.run != SLOT || rank != 2 || c0 >= d.grid[0] || c1 >= d.grid[1];
         return t;
     }
     const int64_t rt = rank == 3 ? c1 : c0, ctile = rank == 3 ? c2 : c1, plane = rank == 3 ? c0 : 0;
@@ -1572,11 +1627,8 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
                 if (P.tile_trace && blockIdx.x == (P.debug >> 8) && g < P.tile_trace_cap) P.tile_trace[3 * g] = now_ns();
                 mbar_expect_tx(&S.full[slot], t.bytes());
                 char* dst = ring + size_t(slot) * SLOT;
-                if (BATCHED && t.tmap)
-                    tma_2d(smem_addr(dst), t.tmap, t.cx, t.cy, &S.full[slot]);
-                else
-                    for (uint32_t q = 0; q < t.copies; ++q)
-                        bulk_g2s(dst + q * t.run, t.src + size_t(q) * t.pitch, t.run, &S.full[slot]);
+                for (uint32_t q = 0; q < t.copies; ++q)
+                    bulk_g2s(dst + q * t.run, t.src + size_t(q) * t.pitch, t.run, &S.full[slot]);
                 bytes += t.bytes();
                 ++uops;
             }
@@ -1589,7 +1641,7 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
             // slot busy (the compute core is behind or waiting on a dependency):
             // keep DRAM busy by pulling this lane's upcoming tiles into L2
             const Tile ta = resolve_load<BATCHED>(P, __ldg(&P.words[w0 + pf_g]));
-            if (!ta.bad && !ta.halt && !ta.tmap)
+            if (!ta.bad && !ta.halt)
                 for (uint32_t q = 0; q < ta.copies; ++q) prefetch_l2(ta.src + size_t(q) * ta.pitch, ta.run);
             pf_g += R;
             ready = true;  // made progress: skip the back-off
@@ -1673,7 +1725,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(const __grid_cons
 
 }  // namespace ring
 
-size_t ring_smem_bytes(uint32_t ring_slots) { return ring::smem_bytes(ring_slots); }
+size_t ring_smem_bytes(uint32_t ring_slots, bool batched) { return ring::smem_bytes(ring_slots, batched); }
 const void* ring_kernel_entry(bool batched) {
     return batched ? reinterpret_cast<const void*>(&ring::ring_kernel<true>) : reinterpret_cast<const void*>(&ring::ring_kernel<false>);
 }

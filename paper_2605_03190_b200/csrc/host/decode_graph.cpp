@@ -307,7 +307,7 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
     auto wgt = [&](const std::string& name, int64_t rows, int64_t cols, double fan_in) {
         TensorRef& t = b.add(name, {rows, cols}, VDC_RING_BGEMM_ROWS, VDC_RING_BGEMM_KT, winit, e,
                              m.scaled_init ? float(1.0 / std::sqrt(fan_in)) : 1.0f);
-        t.tma = VDC_RING_BGEMM_ROWS;
+        t.tma = VDC_DESC_PACKED_SW128;
         return name;
     };
     auto sk = [&](const std::string& name, int64_t row_blocks) {  // stream-K partials (shared by all layers)

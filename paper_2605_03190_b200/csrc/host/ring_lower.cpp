@@ -444,7 +444,7 @@ class RingLowering {
                     u.flow = 1;
                     u.size = 1;
                     u.addr = isa::AddressSpec::tile(t.tensor, t.coord);
-                    u.reg1 = desc_[t.tensor].tma ? 1 : 0;  // TMA tensor tile (batched weights)
+                    u.reg1 = desc_[t.tensor].tma == VDC_DESC_PACKED_SW128 ? 1 : 0;  // packed 16 KB weight tile
                     vs.push_back(u);
                     vm.push_back({r.ordinal, slot, -1});
                 }
@@ -532,9 +532,9 @@ class RingLowering {
         const uint16_t w = idx(n.inputs[0]);
         const TileDescriptor& wd = desc_[w];
         const int64_t M = wd.rows(), K = wd.cols();
-        if (wd.tile_rows != VDC_RING_BGEMM_ROWS || wd.tile_cols != VDC_RING_BGEMM_KT || wd.tma != VDC_RING_BGEMM_ROWS ||
+        if (wd.tile_rows != VDC_RING_BGEMM_ROWS || wd.tile_cols != VDC_RING_BGEMM_KT || wd.tma != VDC_DESC_PACKED_SW128 ||
             M % VDC_RING_BGEMM_ROWS || K % VDC_RING_BGEMM_KT)
-            throw GeneratorError("node " + n.id + ": batched weights need 128 x 64 TMA tiles");
+            throw GeneratorError("node " + n.id + ": batched weights need packed 128 x 64 tiles");
         const int64_t rb = M / VDC_RING_BGEMM_ROWS, kts = K / VDC_RING_BGEMM_KT, T = rb * kts;
         const bool qkv = n.outputs.size() == 3, resid = n.kind == OpKind::GEMV_ADD, swiglu = attr_int(n, "swiglu", 0) != 0;
         const std::string op = n.id.substr(n.id.find('.') == std::string::npos ? 0 : n.id.find('.') + 1);

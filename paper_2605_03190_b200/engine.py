@@ -44,9 +44,30 @@ WAIT_SITES = ["cfu_alloc", "cfu_m2c", "cfu_unit", "ldu_idle", "ldu_dep", "stu_id
               "vcc_ready", "vcc_barrier", "vcc_c2m", "vcc_compute", "cfu_total", "vcc_total", "ldu_issue", "cfu_resolve",
               "vcc_sync", "vcc_push", "vcc_prologue", "vcc_epilogue", "vcc_pop", "cfu_allocloop", "cfu_synckick", "cfu_dispatch"]
 
-RING_SITES = ["vmc_empty_wait", "vcc_full_wait", "vcc_dep_wait", "vcc_epilogue", "vcc_total", "vmc_total", "jobs"]
+RING_SITES = ["vmc_empty_wait", "vcc_full_wait", "vcc_dep_wait", "vcc_epilogue", "vcc_total", "vmc_total", "jobs",
+              "bgemm_xchunk_wait", "bgemm_xbuffer_wait", "bgemm_mma_wait", "bgemm_prologue"]
 
 TORCH_DTYPE = {"f32": "float32", "bf16": "bfloat16", "i64": "int64"}
+
+
+PACKED_SW128 = 0x80000000  # ring_abi.h VDC_DESC_PACKED_SW128
+
+
+def pack_sw128(a: np.ndarray, rows: int, cols: int) -> np.ndarray:
+    """Row-major (rows, cols) -> packed 128 x 64 tiles, tile (rb, kt) at
+    (rb * cols/64 + kt) * 8192 elements, 16-byte chunk c of tile row r stored
+    at chunk c ^ (r % 8) (the 128-byte swizzle of the tcgen05 K-major operand)."""
+    t = a.reshape(rows // 128, 128, cols // 64, 8, 8).transpose(0, 2, 1, 3, 4)  # rb, kt, r, c, e
+    r = np.arange(128)[:, None]
+    p = np.arange(8)[None, :]
+    return np.ascontiguousarray(t[:, :, r, p ^ (r & 7), :]).reshape(-1)
+
+
+def unpack_sw128(a: np.ndarray, rows: int, cols: int) -> np.ndarray:
+    t = a.reshape(rows // 128, cols // 64, 128, 8, 8)  # rb, kt, r, p, e
+    r = np.arange(128)[:, None]
+    c = np.arange(8)[None, :]
+    return np.ascontiguousarray(t[:, :, r, c ^ (r & 7), :].transpose(0, 2, 1, 3, 4)).reshape(-1)
 
 
 class Engine:
@@ -89,6 +110,8 @@ class Engine:
         del torch
 
     def bind_inputs(self, arrays: dict) -> dict:
+        # weights of batched programs are stored as packed, pre-swizzled tiles
+        # (ring_abi.h VDC_DESC_PACKED_SW128): row-major host arrays are packed here
         """Allocate every storage tensor on the device from host arrays (float32
         values; bf16 tensors are cast); missing names are zero-filled."""
         torch = _torch()
@@ -99,8 +122,10 @@ class Engine:
             n = int(np.prod(d["shape"]))
             dt = getattr(torch, TORCH_DTYPE[d["dtype"]])
             if d["name"] in arrays:
-                t = torch.from_numpy(np.ascontiguousarray(arrays[d["name"]], dtype=np.float32).reshape(-1)).to(
-                    f"cuda:{self.device}").to(dt)
+                a = np.ascontiguousarray(arrays[d["name"]], dtype=np.float32).reshape(-1)
+                if d.get("tma") == PACKED_SW128:
+                    a = pack_sw128(a, *d["shape"])
+                t = torch.from_numpy(a).to(f"cuda:{self.device}").to(dt)
             else:
                 t = torch.zeros(n, dtype=dt, device=f"cuda:{self.device}")
             self.bind(d["name"], t)
@@ -117,8 +142,10 @@ class Engine:
             n = int(np.prod(d["shape"]))
             dt = getattr(torch, TORCH_DTYPE[d["dtype"]])
             if d["name"] in arrays:
-                t = torch.from_numpy(np.ascontiguousarray(arrays[d["name"]], dtype=np.float32).reshape(-1)).to(
-                    f"cuda:{self.device}").to(dt)
+                a = np.ascontiguousarray(arrays[d["name"]], dtype=np.float32).reshape(-1)
+                if d.get("tma") == PACKED_SW128:
+                    a = pack_sw128(a, *d["shape"])
+                t = torch.from_numpy(a).to(f"cuda:{self.device}").to(dt)
             else:
                 t = torch.zeros(n, dtype=dt, device=f"cuda:{self.device}")
             self.bind(d["name"], t)

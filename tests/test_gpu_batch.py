@@ -40,7 +40,7 @@ def run(model, req_pages, steps, sms=None, ppj=4, seed=0):
         st.copy_(torch.from_numpy(bc.step_block(info, tokens, pos)))
         rep = eng.run()
         assert rep.status == 0, rep.message
-        host = {k: v.float().cpu().numpy() for k, v in tens.items()}
+        host = bc.readback(info, tens)
         results.append(bc.check_batch(info, state, host, tokens, pos))
         state = host
     return results
