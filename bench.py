@@ -47,7 +47,8 @@ def model_request(layers: int = 32, ctx: int = CTX, engine: str = "ring", ring_s
         return {
             "engine": "ring", "ring_slots": ring_slots,
             "model": {"preset": "llama3-8b", "layers": layers},
-            "layout": {"ctx_pages": pages, "max_ctx": pages * 64, "pages_per_job": pages_per_job, "gu_block": 4},
+            "layout": {"ctx_pages": pages, "max_ctx": pages * 64, "pages_per_job": pages_per_job, "gu_block": 4,
+                       "argmax": True},
             "profile": {"builtin": "b200"},
         }
     return {
@@ -218,7 +219,9 @@ def init_tensors(eng, seed: int = 0):
             n *= s
         dt = {"f32": torch.float32, "bf16": torch.bfloat16, "i64": torch.int64}[d["dtype"]]
         t = torch.empty(n, dtype=dt, device=f"cuda:{eng.device}")
-        if d["init"] == 2:  # ones
+        if d["dtype"] == "i64":  # indices (sampled token)
+            t.zero_()
+        elif d["init"] == 2:  # ones
             t.fill_(1)
         elif d["external"] or d["state"]:
             s = d["init_scale"] if d["init"] == 4 else 1.0
@@ -313,12 +316,16 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     per = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
     total_ms = ev[0].elapsed_time(ev[-1])
 
-    # ---- e2e: host loop through the public API (H2D step block, D2H logits)
+    # ---- e2e: host loop through the public API (H2D step block; D2H of the
+    # token sampled on the device (greedy argmax fused into lm_head), or of
+    # the logits under TP, where the vocab is split over the ranks)
     logits = tens["logits"]
     h_step = torch.zeros(8, dtype=torch.int64).pin_memory()
     n_logits = logits.numel() * (world if tp else 1)
     h_logits = torch.empty(n_logits, dtype=torch.float32).pin_memory()
     gathered = torch.empty(n_logits, dtype=torch.float32, device=f"cuda:{local_rank}") if tp else None
+    next_tok = tens.get("next_token")
+    h_tok = torch.zeros(1, dtype=torch.int64).pin_memory()
     token = 17
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -333,10 +340,16 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 import torch.distributed as dist
                 dist.all_gather_into_tensor(gathered, logits)
                 h_logits.copy_(gathered, non_blocking=True)
+                stream.synchronize()
+                token = int(torch.argmax(h_logits))
+            elif next_tok is not None:
+                h_tok.copy_(next_tok, non_blocking=True)
+                stream.synchronize()
+                token = int(h_tok[0])
             else:
                 h_logits.copy_(logits, non_blocking=True)
-            stream.synchronize()
-            token = int(torch.argmax(h_logits))
+                stream.synchronize()
+                token = int(torch.argmax(h_logits))
         e1.record(stream)
     stream.synchronize()
     w3 = time.time()
@@ -373,13 +386,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "scaling": "strong" if tp else "weak",
         "vs_baseline": None,
         "dtype": "bf16",
-        "data": "synthetic: random-init Llama-3-8B weights (uniform/sqrt(fan_in)), random bf16 KV cache, greedy token feedback in e2e",
+        "data": "synthetic: random-init Llama-3-8B weights (uniform/sqrt(fan_in)), random bf16 KV cache, greedy token feedback in e2e (device argmax)",
         "config": {"workload": f"C2 Llama-3-8B bf16 decode, batch 1, ctx {args.ctx}, {args.layers} layers + lm_head",
                    "model": "llama3-8b", "batch": 1, "ctx": args.ctx, "parallelism": parallelism,
                    "l2": "inputs larger than L2 (algorithmic %.2f GB per step vs 126 MB L2)" % (nbytes["total"] / 1e9),
                    "program_uops": info["total_uops"], "virtual_cores": prog.cores()[0], "build_seconds": round(build_s, 2)},
         "e2e": {"value": round(e2e_value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 8 * 8,
-                "d2h_bytes_per_step": n_logits * 4},
+                "d2h_bytes_per_step": 8 if (next_tok is not None and not tp) else n_logits * 4,
+                "sampling": "greedy argmax fused into the lm_head epilogue (device)" if (next_tok is not None and not tp)
+                            else "host argmax over D2H logits"},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": committed_traffic() if world == 1 else None,

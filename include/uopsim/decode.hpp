@@ -63,6 +63,7 @@ struct LayoutConfig {
     // addressed through a page table; request b covers req_pages[b] logical
     // pages (its context capacity in this program), allocated contiguously
     // in the pool (the page table is part of the lowered program).
+    bool argmax = false;  // greedy sampling fused into lm_head (single-request, no TP): next_token (int64)
     int batch = 0;
     std::vector<int> req_pages;
 };

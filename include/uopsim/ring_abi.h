@@ -58,6 +58,9 @@
 #define VDC_SYM_HEADER_BYTES 128 /* symmetric buffer = header (u32 readiness counter) + data */
 #define VDC_JOB_QKV 0x80        /* fused q|k|v rows: q -> o_t, k -> cache b_t, v -> cache o2_t;
                                    block = q rows, split = k (= v) rows; rotary on q and k */
+#define VDC_JOB_ARGMAX 0x800     /* lm_head GEMV: greedy sampling fused into the logits epilogue: each
+                                   job posts (max, argmax) of its rows to b_t[split]; the last of
+                                   arrive_need jobs writes the token (int64) to o2_t */
 #define VDC_JOB_BATCH 0x400     /* batched program (nb requests): per-request token / pos / ctx in
                                    the step block (3 int64 each), paged KV pools, page table at
                                    step[ptab + b * maxp + logical page] */

@@ -372,7 +372,61 @@ struct Vcc {
                 for (uint32_t q = 0; q < P->tp_world; ++q)
                     asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(sym_base(J.o_t, q)) : "memory");
         } else {
+            if (J.flags & VDC_JOB_ARGMAX) argmax_rows(J, J.r1 - J.r0);
             publish(J.o_t);
+        }
+    }
+
+    // greedy sampling fused into the lm_head epilogue: (max, first argmax)
+    // of this job's logit rows, merged into the SM's running best; the SM's
+    // last lm_head job posts it to its slot, and the last SM to arrive
+    // reduces the slots (one warp, ties -> lowest vocab index like numpy
+    // argmax) and writes the token
+    float am_v = -INFINITY;
+    int am_i = 0x7fffffff;
+    __device__ static void am_merge(float& bv, int& bi, float ov, int oi) {
+        if (ov > bv || (ov == bv && oi < bi)) {
+            bv = ov;
+            bi = oi;
+        }
+    }
+    __device__ void argmax_rows(const vdc_job& J, int rows) {
+        const int tpr = J.k / J.tile_cols;
+        float bv = -INFINITY;
+        int bi = 0x7fffffff;
+        for (int i = int(ct); i < rows; i += NCT) am_merge(bv, bi, row_sum(i, tpr), J.r0 - J.out_row0 + i);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) am_merge(bv, bi, __shfl_xor_sync(0xffffffffu, bv, o), __shfl_xor_sync(0xffffffffu, bi, o));
+        if (lane == 0) {
+            S->bc[w] = bv;
+            S->bc[CW + w] = __int_as_float(bi);
+        }
+        sync();
+        if (ct == 0) {
+            for (int q = 0; q < CW; ++q) am_merge(am_v, am_i, S->bc[q], __float_as_int(S->bc[CW + q]));
+            S->flag = 0;
+            if (J.block) {  // the SM's last lm_head job: post, arrive
+                float* part = reinterpret_cast<float*>(tptr(J.b_t)) + 2 * J.split;
+                part[0] = am_v;
+                part[1] = __int_as_float(am_i);
+                uint32_t old;
+                asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&P->counters[J.arrive_ctr]) : "memory");
+                S->flag = (old + 1u == uint32_t(J.arrive_need) * P->epoch) ? 1 : 0;
+            }
+        }
+        sync();
+        if (S->flag && w == 0) {
+            const float* all = reinterpret_cast<const float*>(tptr(J.b_t));
+            float v0 = -INFINITY;
+            int i0 = 0x7fffffff;
+            for (int q = int(lane); q < J.arrive_need; q += 32)
+                am_merge(v0, i0, ldcg_f32(all + 2 * q), __float_as_int(ldcg_f32(all + 2 * q + 1)));
+#pragma unroll
+            for (int o = 16; o; o >>= 1) am_merge(v0, i0, __shfl_xor_sync(0xffffffffu, v0, o), __shfl_xor_sync(0xffffffffu, i0, o));
+            if (lane == 0) {
+                *reinterpret_cast<int64_t*>(tptr(J.o2_t)) = int64_t(i0);
+                red_release_add(ctr(J.o2_t), 1u);
+            }
         }
     }
 

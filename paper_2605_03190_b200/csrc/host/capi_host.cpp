@@ -101,6 +101,7 @@ decode::LayoutConfig layout_from(const json& j) {
     l.tp_world = j.value("tp_world", l.tp_world);
     l.tp_rank = j.value("tp_rank", l.tp_rank);
     l.batch = j.value("batch", l.batch);
+    l.argmax = j.value("argmax", l.argmax);
     l.req_pages = j.value("req_pages", l.req_pages);
     return l;
 }

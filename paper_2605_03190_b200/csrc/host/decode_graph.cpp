@@ -250,8 +250,14 @@ OperatorGraph build_decode_graph(const ModelConfig& m, const LayoutConfig& l) {
     b.norm("final_norm", d);
     b.weight("lm_head", vocab, d, l.head_job_rows, float(d));  // vocab-parallel: this rank's logit rows
     b.add("logits", {vocab, 1}, l.head_job_rows, 1, InitKind::zeros, ElemType::f32);
-    b.node("head", OpKind::RMS_GEMV, {"lm_head", b.view(x, ".all", d), "final_norm"}, {"logits"},
-           {{"eps", eps}, {"job_rows", std::to_string(l.head_job_rows)}});
+    std::map<std::string, std::string> head_attrs = {{"eps", eps}, {"job_rows", std::to_string(l.head_job_rows)}};
+    if (l.argmax && !tp) {
+        // per-job (max, argmax) slots and the sampled token
+        b.add("head.amax", {4096, 2}, 4096, 2, InitKind::zeros, ElemType::f32);
+        b.add("next_token", {1, 1}, 1, 1, InitKind::zeros, ElemType::i64);
+        head_attrs["argmax"] = "1";
+    }
+    b.node("head", OpKind::RMS_GEMV, {"lm_head", b.view(x, ".all", d), "final_norm"}, {"logits"}, head_attrs);
     b.g.validate();
     return std::move(b.g);
 }

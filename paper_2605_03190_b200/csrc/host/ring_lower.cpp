@@ -152,9 +152,29 @@ class RingLowering {
         switch (n.kind) {
             case OpKind::GEMV:
             case OpKind::RMS_GEMV:
-            case OpKind::GEMV_ADD:
+            case OpKind::GEMV_ADD: {
+                const size_t first = jobs_.size();
                 plan_gemv(n, ordinal);
+                if (attr_int(n, "argmax", 0)) {  // greedy sampling fused into the lm_head jobs
+                    // one slot per SM: the SM's last job of the node posts (block = 1)
+                    const int32_t ctr = int32_t(desc_.size()) + n_arrive_++;
+                    std::map<uint32_t, size_t> last;
+                    for (size_t i = first; i < jobs_.size(); ++i) last[jobs_[i].sm] = i;
+                    std::map<uint32_t, int32_t> slot;
+                    for (const auto& [sm, i] : last) slot[sm] = int32_t(slot.size());
+                    for (size_t i = first; i < jobs_.size(); ++i) {
+                        vdc_job& j = jobs_[i].j;
+                        j.flags |= VDC_JOB_ARGMAX;
+                        j.b_t = storage(idx("head.amax"));
+                        j.o2_t = storage(idx("next_token"));
+                        j.arrive_ctr = ctr;
+                        j.arrive_need = int32_t(last.size());
+                        j.split = slot[jobs_[i].sm];
+                        j.block = last[jobs_[i].sm] == i ? 1 : 0;
+                    }
+                }
                 break;
+            }
             case OpKind::ATTN_DECODE:
                 plan_attention(n, ordinal);
                 break;

@@ -74,6 +74,17 @@ def test_mid_bf16_matches_dense(cuda, token, pos):
     assert_close(outs[0][0], fp32=False)
 
 
+def test_fused_argmax_matches_logits(cuda):
+    """greedy sampling fused into the lm_head epilogue: next_token equals the
+    argmax of the device logits (first index on ties) and of the reference"""
+    base = {"model": dict(rc.MID["model"]), "layout": dict(rc.MID["layout"], argmax=True)}
+    for token, pos in ((17, 300), (4095, 511)):
+        info, req, ins, outs = run(base, None, ((token, pos),))
+        res, host = outs[0]
+        assert_close(res, fp32=False)
+        assert int(host["next_token"][0]) == int(np.argmax(host["logits"])), (host["next_token"], np.argmax(host["logits"]))
+
+
 def test_llama3_8b_layer_matches_dense(cuda):
     _, _, _, outs = run(LLAMA_1L, None, ((1234, 777),))
     assert_close(outs[0][0], fp32=False)
