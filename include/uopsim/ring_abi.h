@@ -117,7 +117,8 @@ typedef struct vdc_job {
     int32_t req;              /* ATTN / ELEMWISE: request index (first request of an embed job) */
     int32_t ptab, maxp;       /* page table: step-block offset and pages per request row */
     int32_t kvrows;           /* BGEMM + QKV: k (= v) rows */
-    int32_t rsv[18];          /* pads the block to 256 bytes: the single-request fields stay in
+    int32_t am_ctr, am_need;  /* BGEMM + ARGMAX: sampling arrival counter, SMs posting (slot = req) */
+    int32_t rsv[16];          /* pads the block to 256 bytes: the single-request fields stay in
                                  the first 128-byte line, the batched ones in the second */
 } vdc_job;  /* 256 bytes */
 

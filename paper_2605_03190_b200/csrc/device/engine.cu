@@ -2083,6 +2083,9 @@ int vdc_load_jobs(vdc_ctx* ctx, const vdc_job* jobs, uint32_t n_jobs, uint32_t r
     size_t n_ctr = std::max<size_t>(1, ctx->descs.size());
     for (uint32_t i = 0; i < n_jobs; ++i)
         if (jobs[i].arrive_ctr >= 0) n_ctr = std::max<size_t>(n_ctr, size_t(jobs[i].arrive_ctr) + 1);
+    for (uint32_t i = 0; i < n_jobs; ++i)
+        if ((jobs[i].flags & VDC_JOB_ARGMAX) && (jobs[i].flags & VDC_JOB_BATCH))
+            n_ctr = std::max<size_t>(n_ctr, size_t(jobs[i].am_ctr) + 1);
     dfree(ctx->d_counters);
     CU(cudaMalloc(&ctx->d_counters, sizeof(uint32_t) * n_ctr));
     ctx->n_counters = n_ctr;

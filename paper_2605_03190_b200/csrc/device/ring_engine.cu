@@ -79,6 +79,8 @@ struct alignas(16) Shared {
     uint64_t xfull[NXMAX], xempty[NXMAX], mma_bar;
     uint32_t tmem_base;
     float binv[VDC_RING_MAX_BATCH];
+    float am_v[VDC_RING_MAX_BATCH];  // batched greedy sampling: this SM's best logit per request
+    int32_t am_i[VDC_RING_MAX_BATCH];
 };
 
 size_t smem_bytes(uint32_t slots, bool batched) {
@@ -876,6 +878,7 @@ struct Vcc {
             default: fin = bgemm_epilogue<32>(J); break;
         }
         if (ct == 0) st_epi += clock64() - e0;
+        if ((J.flags & VDC_JOB_ARGMAX) && J.block) post_argmax_batched(J);
         if (!fin) return;  // a piece of a split row block that was not the last to arrive
         fence_proxy_async_global();  // consumers read these activations with TMA (async proxy)
         sync();
@@ -1033,9 +1036,67 @@ struct Vcc {
 #pragma unroll
             for (int c = 0; c < NH; ++c)
                 if (c0 + c < nb) store_out(tptr(J.o_t), obf, int64_t(c0 + c) * M + rg, v[c]);
+            if (J.flags & VDC_JOB_ARGMAX) {
+                // per request: (max, first argmax) over this block's 128 rows,
+                // merged into the SM's running best (S->am_*)
+                float* scr = reinterpret_cast<float*>(S->x);  // [4 row quarters][npad] x (value, index)
+#pragma unroll
+                for (int c = 0; c < NH; ++c) {
+                    float bv = v[c];
+                    int bi = rg;
+#pragma unroll
+                    for (int o = 16; o; o >>= 1)
+                        am_merge(bv, bi, __shfl_xor_sync(0xffffffffu, bv, o), __shfl_xor_sync(0xffffffffu, bi, o));
+                    if (lane == 0) {
+                        scr[2 * (q * npad + c0 + c)] = bv;
+                        scr[2 * (q * npad + c0 + c) + 1] = __int_as_float(bi);
+                    }
+                }
+                sync();
+                if (int(ct) < npad) {
+                    float bv = S->am_v[ct];
+                    int bi = S->am_i[ct];
+                    for (int qq = 0; qq < 4; ++qq)
+                        am_merge(bv, bi, scr[2 * (qq * npad + int(ct))], __float_as_int(scr[2 * (qq * npad + int(ct)) + 1]));
+                    S->am_v[ct] = bv;
+                    S->am_i[ct] = bi;
+                }
+            }
         }
         (void)npad;
         return true;
+    }
+
+    // batched greedy sampling: the SM's last lm_head piece posts the SM's
+    // per-request best (slot J.req); the last SM to arrive reduces the slots
+    // per request (warp per request) and writes the tokens
+    __device__ void post_argmax_batched(const vdc_job& J) {
+        const int npad = J.npad, nb = J.nb;
+        float* slot = reinterpret_cast<float*>(tptr(J.b_t)) + size_t(J.req) * npad * 2;
+        sync();
+        if (int(ct) < npad) {
+            slot[2 * ct] = S->am_v[ct];
+            slot[2 * ct + 1] = __int_as_float(S->am_i[ct]);
+        }
+        sync();
+        if (ct == 0) {
+            uint32_t old;
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&P->counters[J.am_ctr]) : "memory");
+            S->flag = (old + 1u == uint32_t(J.am_need) * P->epoch) ? 1 : 0;
+        }
+        sync();
+        if (!S->flag) return;
+        const float* all = reinterpret_cast<const float*>(tptr(J.b_t));
+        for (int b = int(w); b < nb; b += CW) {
+            float bv = -INFINITY;
+            int bi = 0x7fffffff;
+            for (int s2 = int(lane); s2 < J.am_need; s2 += 32)
+                am_merge(bv, bi, ldcg_f32(all + (size_t(s2) * npad + b) * 2), __float_as_int(ldcg_f32(all + (size_t(s2) * npad + b) * 2 + 1)));
+#pragma unroll
+            for (int o = 16; o; o >>= 1) am_merge(bv, bi, __shfl_xor_sync(0xffffffffu, bv, o), __shfl_xor_sync(0xffffffffu, bi, o));
+            if (lane == 0) reinterpret_cast<int64_t*>(tptr(J.o2_t))[b] = int64_t(bi);
+        }
+        publish(J.o2_t);
     }
 
     // ELEMWISE (batched): embedding rows of requests [r0, r1) -> x, and the
@@ -1754,6 +1815,10 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(const __grid_cons
             mbar_init(&S.mma_bar, 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (BATCHED && threadIdx.x < VDC_RING_MAX_BATCH) {
+        S.am_v[threadIdx.x] = -INFINITY;
+        S.am_i[threadIdx.x] = 0x7fffffff;
     }
     if (BATCHED && threadIdx.x < 32) {  // TMEM accumulator of the batched GEMM µops (one CTA per SM)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&S.tmem_base)),

@@ -363,7 +363,13 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
     }
     wgt("lm_head", m.vocab, d, double(d));
     b.add("logits", {B, m.vocab}, 1, m.vocab, InitKind::zeros, ElemType::f32);
-    b.node("head", OpKind::RMS_GEMV, {"lm_head", xn, x}, {"logits"}, {{"eps", eps}, {"batch", bs}});
+    std::map<std::string, std::string> head_attrs = {{"eps", eps}, {"batch", bs}};
+    if (l.argmax) {  // greedy sampling fused into the lm_head GEMM: per-SM slots, tokens per request
+        b.add("head.amax", {256 * N, 2}, N, 2, InitKind::zeros, ElemType::f32);
+        b.add("next_token", {B, 1}, 1, 1, InitKind::zeros, ElemType::i64);
+        head_attrs["argmax"] = "1";
+    }
+    b.node("head", OpKind::RMS_GEMV, {"lm_head", xn, x}, {"logits"}, head_attrs);
     return std::move(b.g);
 }
 

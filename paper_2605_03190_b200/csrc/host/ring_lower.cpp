@@ -576,6 +576,7 @@ class RingLowering {
             }
         }
         int32_t slot = 0;
+        const size_t first_job = jobs_.size();
         for (int64_t b = 0; b < rb; ++b) {
             const auto& ps = blocks[size_t(b)];
             const int32_t ctr = ps.size() > 1 ? int32_t(desc_.size()) + n_arrive_++ : -1;
@@ -638,6 +639,27 @@ class RingLowering {
                 }
                 for (int64_t kt = ps[i].kt0; kt < ps[i].kt1; ++kt) r.tiles.push_back({w, {uint16_t(b), uint16_t(kt)}});
                 jobs_.push_back(std::move(r));
+            }
+        }
+        if (attr_int(n, "argmax", 0)) {
+            // greedy sampling: each SM merges its finished row blocks per request;
+            // its last piece (block = 1) posts slot `req`; arrival counter am_ctr,
+            // am_need SMs; the last SM writes the tokens
+            const int32_t ctr = int32_t(desc_.size()) + n_arrive_++;
+            std::map<uint32_t, size_t> last;
+            for (size_t i = first_job; i < jobs_.size(); ++i) last[jobs_[i].sm] = i;
+            std::map<uint32_t, int32_t> slot_of;
+            for (const auto& [sm, i] : last) slot_of[sm] = int32_t(slot_of.size());
+            if (slot_of.size() > 256) throw GeneratorError("node " + n.id + ": argmax slots exceed 256 SMs");
+            for (size_t i = first_job; i < jobs_.size(); ++i) {
+                vdc_job& j = jobs_[i].j;
+                j.flags |= VDC_JOB_ARGMAX;
+                j.b_t = storage(idx("head.amax"));
+                j.o2_t = storage(idx("next_token"));
+                j.req = slot_of[jobs_[i].sm];
+                j.block = last[jobs_[i].sm] == i ? 1 : 0;
+                j.am_ctr = ctr;
+                j.am_need = int32_t(slot_of.size());
             }
         }
     }

@@ -22,11 +22,12 @@ pytestmark = pytest.mark.gpu
 LLAMA_1L = {"preset": "llama3-8b", "layers": 1, "vocab": 32000}
 
 
-def run(model, req_pages, steps, sms=None, ppj=4, seed=0):
+def run(model, req_pages, steps, sms=None, ppj=4, seed=0, argmax=False):
     import torch
     from paper_2605_03190_b200.engine import Engine
 
     req = bc.request(model, req_pages, ppj, sms)
+    req["layout"]["argmax"] = argmax
     prog = Program.build(req)
     info = prog.info()
     ins = bc.synth_inputs(info, seed)
@@ -41,7 +42,11 @@ def run(model, req_pages, steps, sms=None, ppj=4, seed=0):
         rep = eng.run()
         assert rep.status == 0, rep.message
         host = bc.readback(info, tens)
-        results.append(bc.check_batch(info, state, host, tokens, pos))
+        rs = bc.check_batch(info, state, host, tokens, pos)
+        if argmax:  # fused greedy sampling: the device tokens are the argmax of the device logits
+            lg = host["logits"].reshape(len(req_pages), -1)
+            assert [int(t) for t in host["next_token"]] == [int(i) for i in np.argmax(lg, axis=1)]
+        results.append(rs)
         state = host
     return results
 
@@ -70,7 +75,7 @@ def test_mid_batch20_multistep(cuda):
     steps = []
     for s in range(3):
         steps.append(([int(t) for t in rng.integers(0, 4096, 20)], [p + s for p in pos0]))
-    for rs in run(bc.MID_MODEL, pages, steps):
+    for rs in run(bc.MID_MODEL, pages, steps, argmax=True):
         assert_close(rs)
 
 
@@ -88,4 +93,4 @@ def test_llama3_8b_layer_batch32(cuda):
     pages = [int(p) for p in rng.integers(2, 20, 32)]
     pos = [int(rng.integers(0, 64 * p)) for p in pages]
     tokens = [int(t) for t in rng.integers(0, 32000, 32)]
-    assert_close(run(LLAMA_1L, pages, [(tokens, pos)])[0])
+    assert_close(run(LLAMA_1L, pages, [(tokens, pos)], argmax=True)[0])
