@@ -740,27 +740,39 @@ struct Vcc {
     __device__ int64_t req_pos(int b) const { return P->step[3 * b + 1]; }
 
     unsigned long long st_xf = 0, st_xe = 0, st_mma = 0, st_pro = 0;
-    __device__ bool spin(uint64_t* bar, uint32_t parity, unsigned long long* acc = nullptr) {
+    // wait for an mbarrier phase; returns the cycles waited, or -1 if the
+    // launch aborted (no member addresses escape: the Vcc stays in registers)
+    __device__ long long spin(uint64_t* bar, uint32_t parity) {
         const long long c0 = clock64();
-        struct Acc {
-            unsigned long long* a;
-            long long c0;
-            __device__ ~Acc() {
-                if (a) *a += clock64() - c0;
-            }
-        } guard{acc, c0};
-        if (mbar_try(bar, parity)) return true;
+        if (mbar_try(bar, parity)) return clock64() - c0;
         const unsigned long long t0 = now_ns();
         for (uint32_t n = 1;; ++n) {
-            if (mbar_wait_hint(bar, parity)) return true;
+            if (mbar_wait_hint(bar, parity)) return clock64() - c0;
             if ((n & 15) == 0) {
-                if (aborted()) return false;
+                if (aborted()) return -1;
                 if (P->watchdog_ns && now_ns() - t0 > P->watchdog_ns) {
                     fire(0, 0x40000u);
-                    return false;
+                    return -1;
                 }
             }
         }
+    }
+
+    // activation chunks of tile group j of the running BGEMM -> chunk buffer xq % NXG
+    __device__ __forceinline__ bool issue_grp(const vdc_job& J, int j, int n, int G, uint32_t NXG, uint32_t xbytes, uint32_t xb0,
+                                              const void* xm) {
+        const uint32_t i = xq % NXG;
+        if (xq >= NXG) {
+            const long long c = spin(&S->xempty[i], ((xq / NXG) - 1u) & 1u);
+            if (c < 0) return false;
+            st_xe += c;
+        }
+        const int cnt = min(G, n - j * G);
+        mbar_expect_tx(&S->xfull[i], uint32_t(cnt) * xbytes);
+        for (int u = 0; u < cnt; ++u)
+            tma_2d(xb0 + (i * uint32_t(G) + uint32_t(u)) * xbytes, xm, (J.kt0 + j * G + u) * VDC_RING_BGEMM_KT, 0, &S->xfull[i]);
+        ++xq;
+        return true;
     }
 
     __device__ void bgemm(const vdc_job& J) {
@@ -803,30 +815,21 @@ struct Vcc {
             const void* xm = static_cast<const char*>(P->tmaps) + size_t(J.x_t) * 128;
             const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(npad >> 3) << 17) | (uint32_t(128 >> 4) << 24);
             const int ngrp = (n + G - 1) / G;
-            auto issue_grp = [&](int j) -> bool {  // activation chunks of tile group j -> buffer xq % NXG
-                const uint32_t i = xq % NXG;
-                if (xq >= NXG && !spin(&S->xempty[i], ((xq / NXG) - 1u) & 1u, &st_xe)) return false;
-                const int cnt = min(G, n - j * G);
-                mbar_expect_tx(&S->xfull[i], uint32_t(cnt) * xbytes);
-                for (int u = 0; u < cnt; ++u)
-                    tma_2d(xb0 + (i * uint32_t(G) + uint32_t(u)) * xbytes, xm, (J.kt0 + j * G + u) * VDC_RING_BGEMM_KT, 0,
-                           &S->xfull[i]);
-                ++xq;
-                return true;
-            };
             // group look-ahead NXG - 1: the refill after group t reuses the
             // buffer of group t - 1 (its MMAs were issued a group earlier)
             bool good = true;
             const int L = max(1, int(NXG) - 1);
-            for (int j = 0; j < min(ngrp, L) && good; ++j) good = issue_grp(j);
+            for (int j = 0; j < min(ngrp, L) && good; ++j) good = issue_grp(J, j, n, G, NXG, xbytes, xb0, xm);
             uint32_t g = kt;
             for (int t = 0; t < ngrp && good; ++t) {
                 const int cnt = min(G, n - t * G);
                 const uint32_t xi = xd % NXG;
-                if (!spin(&S->xfull[xi], (xd / NXG) & 1u, &st_xf)) {
+                const long long wc = spin(&S->xfull[xi], (xd / NXG) & 1u);
+                if (wc < 0) {
                     good = false;
                     break;
                 }
+                st_xf += wc;
                 for (int u = 0; u < cnt && good; ++u) good = wait_full((g + uint32_t(u)) % R, ((g + uint32_t(u)) / R) & 1u);
                 if (!good) break;
                 tc_fence_after();
@@ -850,7 +853,7 @@ struct Vcc {
                 if (ttr) P->tile_trace[3 * g + 2] = now_ns();
                 ++xd;
                 g += uint32_t(cnt);
-                if (t + L < ngrp && !issue_grp(t + L)) {
+                if (t + L < ngrp && !issue_grp(J, t + L, n, G, NXG, xbytes, xb0, xm)) {
                     good = false;
                     break;
                 }
@@ -864,10 +867,12 @@ struct Vcc {
             ok = false;
             return;
         }
-        if (!spin(&S->mma_bar, nmma & 1u, ct == 0 ? &st_mma : nullptr)) {
+        const long long wm = spin(&S->mma_bar, nmma & 1u);
+        if (wm < 0) {
             ok = false;
             return;
         }
+        if (ct == 0) st_mma += wm;
         ++nmma;
         tc_fence_after();
         const long long e0 = clock64();
@@ -1187,7 +1192,21 @@ struct Vcc {
         {
             const uint4* qb = reinterpret_cast<const uint4*>(tptr(J.x_t) + size_t(J.x_off) * EB);
             uint4* qd = S->x;
-            for (int i = int(ct); i < G * NCH; i += NCT) qd[i] = ldcg128(qb + i);
+            if constexpr (BF) {
+                // bf16 caches: q staged as fp32 in split halves, [head][half][chunk]
+                // x 4 floats (dims 8c..8c+3 | 8c+4..8c+7), so the score loop's
+                // packed-fp32 FMAs read q without unpacking (conflict-free)
+                for (int i = int(ct); i < G * NCH; i += NCT) {
+                    const uint4 u = ldcg128(qb + i);
+                    const int h = i / NCH, c = i % NCH;
+                    qd[(h * 2) * NCH + c] = make_uint4(__float_as_uint(bf_lo(u.x)), __float_as_uint(bf_hi(u.x)),
+                                                       __float_as_uint(bf_lo(u.y)), __float_as_uint(bf_hi(u.y)));
+                    qd[(h * 2 + 1) * NCH + c] = make_uint4(__float_as_uint(bf_lo(u.z)), __float_as_uint(bf_hi(u.z)),
+                                                           __float_as_uint(bf_lo(u.w)), __float_as_uint(bf_hi(u.w)));
+                }
+            } else {
+                for (int i = int(ct); i < G * NCH; i += NCT) qd[i] = ldcg128(qb + i);
+            }
         }
         sync();
         float m[G], l[G], o[G][DPL];
@@ -1248,14 +1267,38 @@ struct Vcc {
             for (int h = 0; h < G; ++h) s[h] = 0.f;
             if (int(lane) < rows_w) {
                 const uint32_t krow = kb + lane * rowb;
-#pragma unroll 4
-                for (int c = 0; c < NCH; ++c) {
-                    const int cc = (c + int(lane)) & (NCH - 1);
-                    const uint4 kv = lds128(krow + uint32_t(cc) * 16u);
+                if constexpr (BF) {  // packed fp32 FMAs (FFMA2): even / odd dims in the two halves
+                    float2 acc[G];
 #pragma unroll
-                    for (int h = 0; h < G; ++h) {
-                        const uint4 qv = lds128(qs + uint32_t(h * NCH + cc) * 16u);
-                        s[h] += dot16<BF>(qv, kv);
+                    for (int h = 0; h < G; ++h) acc[h] = make_float2(0.f, 0.f);
+#pragma unroll 4
+                    for (int c = 0; c < NCH; ++c) {
+                        const int cc = (c + int(lane)) & (NCH - 1);
+                        const uint4 kv = lds128(krow + uint32_t(cc) * 16u);
+                        const float2 k01 = make_float2(bf_lo(kv.x), bf_hi(kv.x)), k23 = make_float2(bf_lo(kv.y), bf_hi(kv.y));
+                        const float2 k45 = make_float2(bf_lo(kv.z), bf_hi(kv.z)), k67 = make_float2(bf_lo(kv.w), bf_hi(kv.w));
+#pragma unroll
+                        for (int h = 0; h < G; ++h) {
+                            const uint4 qa = lds128(qs + uint32_t((h * 2) * NCH + cc) * 16u);
+                            const uint4 qb2 = lds128(qs + uint32_t((h * 2 + 1) * NCH + cc) * 16u);
+                            acc[h] = __ffma2_rn(k01, make_float2(__uint_as_float(qa.x), __uint_as_float(qa.y)), acc[h]);
+                            acc[h] = __ffma2_rn(k23, make_float2(__uint_as_float(qa.z), __uint_as_float(qa.w)), acc[h]);
+                            acc[h] = __ffma2_rn(k45, make_float2(__uint_as_float(qb2.x), __uint_as_float(qb2.y)), acc[h]);
+                            acc[h] = __ffma2_rn(k67, make_float2(__uint_as_float(qb2.z), __uint_as_float(qb2.w)), acc[h]);
+                        }
+                    }
+#pragma unroll
+                    for (int h = 0; h < G; ++h) s[h] = acc[h].x + acc[h].y;
+                } else {
+#pragma unroll 4
+                    for (int c = 0; c < NCH; ++c) {
+                        const int cc = (c + int(lane)) & (NCH - 1);
+                        const uint4 kv = lds128(krow + uint32_t(cc) * 16u);
+#pragma unroll
+                        for (int h = 0; h < G; ++h) {
+                            const uint4 qv = lds128(qs + uint32_t(h * NCH + cc) * 16u);
+                            s[h] += dot16<BF>(qv, kv);
+                        }
                     }
                 }
             }
@@ -1282,8 +1325,18 @@ struct Vcc {
 #pragma unroll
                 for (int h = 0; h < G; ++h) {
                     const float ph = __shfl_sync(0xffffffffu, p[h], r);
+                    if constexpr (DPL % 2 == 0) {  // packed fp32 FMAs over dim pairs
 #pragma unroll
-                    for (int d = 0; d < DPL; ++d) o[h][d] = fmaf(ph, vv[d], o[h][d]);
+                        for (int d = 0; d < DPL; d += 2) {
+                            const float2 a = __ffma2_rn(make_float2(vv[d], vv[d + 1]), make_float2(ph, ph),
+                                                        make_float2(o[h][d], o[h][d + 1]));
+                            o[h][d] = a.x;
+                            o[h][d + 1] = a.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int d = 0; d < DPL; ++d) o[h][d] = fmaf(ph, vv[d], o[h][d]);
+                    }
                 }
             }
             // both warps of the pair are done with K and V: each returns its slot
