@@ -59,8 +59,8 @@ constexpr int NXMAX = 16;  // activation-chunk groups of batched GEMMs
 // batched kernel: activation-chunk ring after the control block. Its loads
 // queue behind the in-flight weight tiles of the SM's copy engine, so the
 // MMA issuer keeps more than a ring's worth of chunks in flight.
-constexpr uint32_t XRING_BYTES = 60 * 1024;
-constexpr uint32_t TMEM_COLS = 128;  // two fp32 accumulators of <= 64 columns (npad)
+constexpr uint32_t XRING_BYTES = 64 * 1024;
+constexpr uint32_t TMEM_COLS = 512;  // one fp32 accumulator (npad columns) per compute warp
 
 // stat slots (SmStats::wait)
 enum : int { S_VMC_EMPTY = 0, S_VCC_FULL = 1, S_VCC_DEP = 2, S_VCC_EPI = 3, S_VCC_TOTAL = 4, S_VMC_TOTAL = 5, S_NJOBS = 6,
@@ -758,23 +758,6 @@ struct Vcc {
         }
     }
 
-    // activation chunks of tile group j of the running BGEMM -> chunk buffer xq % NXG
-    __device__ __forceinline__ bool issue_grp(const vdc_job& J, int j, int n, int G, uint32_t NXG, uint32_t xbytes, uint32_t xb0,
-                                              const void* xm) {
-        const uint32_t i = xq % NXG;
-        if (xq >= NXG) {
-            const long long c = spin(&S->xempty[i], ((xq / NXG) - 1u) & 1u);
-            if (c < 0) return false;
-            st_xe += c;
-        }
-        const int cnt = min(G, n - j * G);
-        mbar_expect_tx(&S->xfull[i], uint32_t(cnt) * xbytes);
-        for (int u = 0; u < cnt; ++u)
-            tma_2d(xb0 + (i * uint32_t(G) + uint32_t(u)) * xbytes, xm, (J.kt0 + j * G + u) * VDC_RING_BGEMM_KT, 0, &S->xfull[i]);
-        ++xq;
-        return true;
-    }
-
     __device__ void bgemm(const vdc_job& J) {
         const long long p0 = clock64();
         const int n = J.kt1 - J.kt0, K = J.k, nb = J.nb, npad = J.npad;
@@ -799,67 +782,67 @@ struct Vcc {
             sync();
         }
         const uint32_t xbytes = uint32_t(npad) * 128u;
-        // activation-chunk ring after the control block (1 KB aligned: the
-        // 128-byte swizzle atoms repeat every 1 KB)
+        // activation-chunk buffers after the control block (1 KB aligned: the
+        // 128-byte swizzle atoms repeat every 1 KB), NXW per compute warp
         const uint32_t xb0 = (smem_addr(S) + uint32_t(sizeof(Shared)) + 1023u) & ~1023u;
-        // tiles are handled in groups of G (one activation-chunk barrier, one
-        // fence, G W-slot commits per group): the issuer's fixed per-step cost
-        // (barrier round trips, commits) is paid once per G x 16 KB
-        const int G = npad <= 32 ? 4 : 2;
-        const uint32_t NXG = min(uint32_t(NXMAX), XRING_BYTES / (uint32_t(G) * xbytes));
+        const uint32_t NXW = min(2u, XRING_BYTES / xbytes / uint32_t(CW));
         if (ct == 0) st_pro += clock64() - p0;
-        if (ct == 0) {
-            // generic writes (other SMs' epilogues, this CTA's scratch) before async-proxy reads / writes
+        if (ct == 0) S->flag = 1;
+        sync();
+        // Every compute warp is an MMA issuer (lane 0) for the tiles of its own
+        // ring slot (slot w of the 8-slot ring) into its own TMEM accumulator
+        // (columns w * npad): like the single-request GEMV, each slot's
+        // turnaround is independent, so one late tile does not hold the other
+        // slots (head-of-line blocking of a single in-order issuer). The
+        // epilogue adds the 8 accumulators in warp order (deterministic).
+        if (lane == 0) {
             fence_proxy_async_global();
             fence_proxy_async_smem();
             const void* xm = static_cast<const char*>(P->tmaps) + size_t(J.x_t) * 128;
             const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(npad >> 3) << 17) | (uint32_t(128 >> 4) << 24);
-            const int ngrp = (n + G - 1) / G;
-            // group look-ahead NXG - 1: the refill after group t reuses the
-            // buffer of group t - 1 (its MMAs were issued a group earlier)
+            const uint32_t acc = tmem + w * uint32_t(npad);
+            const int t0 = int((w + uint32_t(CW) - kt % uint32_t(CW)) % uint32_t(CW));  // first tile of this warp's slot
             bool good = true;
-            const int L = max(1, int(NXG) - 1);
-            for (int j = 0; j < min(ngrp, L) && good; ++j) good = issue_grp(J, j, n, G, NXG, xbytes, xb0, xm);
-            uint32_t g = kt;
-            for (int t = 0; t < ngrp && good; ++t) {
-                const int cnt = min(G, n - t * G);
-                const uint32_t xi = xd % NXG;
-                const long long wc = spin(&S->xfull[xi], (xd / NXG) & 1u);
-                if (wc < 0) {
+            auto xload = [&](int t) {  // activation chunk of tile t -> this warp's buffer xq % NXW
+                const uint32_t i = w * NXW + xq % NXW;
+                if (xq >= NXW) {
+                    const long long c = spin(&S->xempty[i], ((xq / NXW) - 1u) & 1u);
+                    if (c < 0) return false;
+                    st_xe += c;
+                }
+                mbar_expect_tx(&S->xfull[i], xbytes);
+                tma_2d(xb0 + i * xbytes, xm, (J.kt0 + t) * VDC_RING_BGEMM_KT, 0, &S->xfull[i]);
+                ++xq;
+                return true;
+            };
+            for (int t = t0, u = 0; t < n && u < int(NXW) && good; t += CW, ++u) good = xload(t);
+            for (int t = t0; t < n && good; t += CW) {
+                const uint32_t g = kt + uint32_t(t), slot = g % R;
+                const uint32_t xi = w * NXW + xd % NXW;
+                const long long wc = spin(&S->xfull[xi], (xd / NXW) & 1u);
+                if (wc < 0 || !wait_full(slot, (g / R) & 1u)) {
                     good = false;
                     break;
                 }
                 st_xf += wc;
-                for (int u = 0; u < cnt && good; ++u) good = wait_full((g + uint32_t(u)) % R, ((g + uint32_t(u)) / R) & 1u);
-                if (!good) break;
                 tc_fence_after();
-                const bool ttr = P->tile_trace && sm == (P->debug >> 8) && g < P->tile_trace_cap;
-                if (ttr) P->tile_trace[3 * g + 1] = now_ns();
-                for (int u = 0; u < cnt; ++u) {
-                    const uint32_t slot = (g + uint32_t(u)) % R;
-                    if (!(P->debug & 1u)) {
-                        const uint32_t a0 = ring + slot * SLOT, b0 = xb0 + (xi * uint32_t(G) + uint32_t(u)) * xbytes;
+                if (!(P->debug & 1u)) {
+                    const uint32_t a0 = ring + slot * SLOT, b0 = xb0 + xi * xbytes;
 #pragma unroll
-                        // tiles alternate between two accumulators (columns 0 and
-                        // 64): consecutive MMAs do not serialise on one accumulator
-                        const int tile = t * G + u;
-                        for (int kk = 0; kk < 4; ++kk)
-                            umma_bf16(tmem + uint32_t(tile & 1) * 64u, umma_sw128_desc(a0 + kk * 32),
-                                      umma_sw128_desc(b0 + kk * 32), idesc, (tile > 1 || kk) ? 1u : 0u);
-                    }
-                    umma_commit(&S->empty[slot]);  // W slot -> memory core when its MMAs are done
+                    for (int kk = 0; kk < 4; ++kk)
+                        umma_bf16(acc, umma_sw128_desc(a0 + kk * 32), umma_sw128_desc(b0 + kk * 32), idesc,
+                                  (t == t0 && kk == 0) ? 0u : 1u);
                 }
+                umma_commit(&S->empty[slot]);  // W slot -> memory core when its MMAs are done
                 umma_commit(&S->xempty[xi]);
-                if (ttr) P->tile_trace[3 * g + 2] = now_ns();
                 ++xd;
-                g += uint32_t(cnt);
-                if (t + L < ngrp && !issue_grp(J, t + L, n, G, NXG, xbytes, xb0, xm)) {
+                if (t + int(NXW) * CW < n && !xload(t + int(NXW) * CW)) {
                     good = false;
                     break;
                 }
             }
-            if (good) umma_commit(&S->mma_bar);
-            S->flag = good ? 1 : 0;
+            umma_commit(&S->mma_bar);  // count 8: one per warp issuer (arrives at once if it issued nothing)
+            if (!good) S->flag = 0;
         }
         kt += uint32_t(n);
         sync();
@@ -929,12 +912,16 @@ struct Vcc {
         const int64_t M = J.cache_rows;      // output row stride (elements per request)
         const int rg = J.r0 + row;           // global W row
         float v[NH];
-        tmem_ld<NH>(tmem + (uint32_t(q * 32) << 16) + uint32_t(c0), v);
-        if (J.kt1 - J.kt0 > 1) {  // second accumulator (odd tiles), added in fixed order
-            float v2[NH];
-            tmem_ld<NH>(tmem + (uint32_t(q * 32) << 16) + 64u + uint32_t(c0), v2);
 #pragma unroll
-            for (int c = 0; c < NH; ++c) v[c] += v2[c];
+        for (int c = 0; c < NH; ++c) v[c] = 0.f;
+        const int ntile = J.kt1 - J.kt0;
+        for (int a = 0; a < CW; ++a) {  // per-warp accumulators in warp order; a warp without tiles wrote none
+            const int t0 = int((uint32_t(a) + uint32_t(CW) - (kt - uint32_t(ntile)) % uint32_t(CW)) % uint32_t(CW));
+            if (t0 >= ntile) continue;
+            float va[NH];
+            tmem_ld<NH>(tmem + (uint32_t(q * 32) << 16) + uint32_t(a * npad) + uint32_t(c0), va);
+#pragma unroll
+            for (int c = 0; c < NH; ++c) v[c] += va[c];
         }
         tc_fence_before();  // the accumulator may be overwritten after the next barrier
         if (J.arrive_need > 1) {
@@ -1865,7 +1852,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(const __grid_cons
                 mbar_init(&S.xfull[i], 1);
                 mbar_init(&S.xempty[i], 1);
             }
-            mbar_init(&S.mma_bar, 1);
+            mbar_init(&S.mma_bar, CW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
