@@ -563,7 +563,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--engine", default="ring", choices=["ring", "reference"])
     ap.add_argument("--ring-slots", type=int, default=12)
-    ap.add_argument("--pages-per-job", type=int, default=4)
+    ap.add_argument("--pages-per-job", type=int, default=None,
+                    help="split-KV granularity (default 4 at batch 1, 64 for batched decode)")
     ap.add_argument("--batch", type=int, default=1,
                     help="> 1: C3 batched decode (per-request contexts, paged KV, BGEMM on tcgen05); 1 GPU")
     ap.add_argument("--parallel", default="tp", choices=["tp", "replicas"],
@@ -592,6 +593,8 @@ def main():
         print(json.dumps(line))
         return
 
+    if args.pages_per_job is None:
+        args.pages_per_job = 64 if args.batch > 1 else 4
     if args.batch > 1:
         if rank == 0:
             print(json.dumps(run_batched(args)))
