@@ -38,6 +38,7 @@ struct ModelConfig {
     float theta = 10000.0f;
     workload::ElemType dtype = workload::ElemType::f32;
     bool scaled_init = false;  // (u-1)/2/sqrt(fan_in) weights instead of raw unit_float
+    bool qk_norm = false;      // Qwen3: per-head RMSNorm of q and k (weights L.q_norm / L.k_norm) before the rotary
 };
 
 struct LayoutConfig {

@@ -61,6 +61,10 @@
 #define VDC_JOB_ARGMAX 0x800     /* lm_head GEMV: greedy sampling fused into the logits epilogue: each
                                    job posts (max, argmax) of its rows to b_t[split]; the last of
                                    arrive_need jobs writes the token (int64) to o2_t */
+#define VDC_JOB_QKNORM 0x1000    /* Qwen3 QK-norm. qkv µops store q and k un-rotated; ATTN_DECODE
+                                   normalises q (and the appended k row, written back to the
+                                   cache) per head with weights out_row0 (q) / block (k) and
+                                   eps, then applies the rotary (theta) */
 #define VDC_JOB_BATCH 0x400     /* batched program (nb requests): per-request token / pos / ctx in
                                    the step block (3 int64 each), paged KV pools, page table at
                                    step[ptab + b * maxp + logical page] */

@@ -1859,6 +1859,7 @@ struct vdc_ctx {
     CUtensorMap* d_tmaps = nullptr;
     bool tmaps_dirty = false;
     bool batched = false;
+    bool qknorm = false;  // a Qwen3 QK-norm program: its own kernel instance
 };
 
 namespace {
@@ -1911,8 +1912,9 @@ int vdc_create(const vdc_profile* p, int device, vdc_ctx** out) {
     }
     if (p->slot_size == VDC_RING_SLOT_BYTES)
         for (bool b : {false, true})  // launch sizes depend on the loaded program (ring slots, batched)
-            CU(cudaFuncSetAttribute(ring_kernel_entry(b), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(prop.sharedMemPerBlockOptin)));
+            for (bool q : {false, true})
+                CU(cudaFuncSetAttribute(ring_kernel_entry(b, q), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(prop.sharedMemPerBlockOptin)));
     else
         CU(cudaFuncSetAttribute(engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ctx->smem_bytes)));
     CU(cudaMalloc(&ctx->d_stats, sizeof(SmStats) * p->sm_count));
@@ -2108,6 +2110,8 @@ int vdc_load_jobs(vdc_ctx* ctx, const vdc_job* jobs, uint32_t n_jobs, uint32_t r
     }
     ctx->ring = true;
     ctx->batched = batched;
+    ctx->qknorm = false;
+    for (uint32_t i = 0; i < n_jobs; ++i) ctx->qknorm = ctx->qknorm || (jobs[i].flags & VDC_JOB_QKNORM);
     ctx->ring_slots = ring_slots;
     ctx->epoch = 0;
     CU(cudaMemset(ctx->d_counters, 0, sizeof(uint32_t) * ctx->n_counters));
@@ -2265,7 +2269,7 @@ int vdc_launch(vdc_ctx* ctx, void* stream) {
         }
         void* rargs[] = {&R};
         CU(cudaEventRecord(ctx->ev0, s));
-        CU(cudaLaunchCooperativeKernel(ring_kernel_entry(ctx->batched), dim3(ctx->prof.sm_count), dim3(kRingThreads), rargs,
+        CU(cudaLaunchCooperativeKernel(ring_kernel_entry(ctx->batched, ctx->qknorm), dim3(ctx->prof.sm_count), dim3(kRingThreads), rargs,
                                        ring_smem_bytes(ctx->ring_slots, ctx->batched), s));
         CU(cudaEventRecord(ctx->ev1, s));
         ctx->last_stream = s;

@@ -128,7 +128,7 @@ struct RingParams {
     const void* tmaps;          // CUtensorMap[n_desc] (128 bytes each), indexed by descriptor (vdc_desc.tma > 0 only)
 };
 size_t ring_smem_bytes(uint32_t ring_slots, bool batched = false);
-const void* ring_kernel_entry(bool batched);
+const void* ring_kernel_entry(bool batched, bool qknorm = false);
 constexpr uint32_t kRingThreads = 32 * (8 + 1);
 
 // A region of `count` slots, not necessarily contiguous (indices packed 8

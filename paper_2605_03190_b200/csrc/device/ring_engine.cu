@@ -107,6 +107,11 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
     return v;
 }
+__device__ __forceinline__ uint2 ldcg64(const void* p) {
+    uint2 v;
+    asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
 __device__ __forceinline__ uint2 lds64(uint32_t a) {
     uint2 v;
     asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
@@ -135,10 +140,33 @@ __device__ __forceinline__ float dot16(uint4 a, uint4 b) {
     }
 }
 
+// Qwen3 QK-norm on one 128-dim head held 4 dims per lane (bf16x4 in u):
+// x = bf16(x * rsqrt(mean(x^2) + eps) * w), then the interleaved-pair rotary
+// at `pos` (double-precision angles), rounded to bf16. Not inlined: its
+// double-precision registers stay out of the kernel's allocation.
+__device__ __forceinline__ uint2 qk_norm_rope4(uint2 u, uint2 wv, uint32_t lane, int head_dim, float eps, float theta, int64_t pos) {
+    float x[4] = {bf_lo(u.x), bf_hi(u.x), bf_lo(u.y), bf_hi(u.y)};
+    const float wgt[4] = {bf_lo(wv.x), bf_hi(wv.x), bf_lo(wv.y), bf_hi(wv.y)};
+    const float ss = warp_sum(x[0] * x[0] + x[1] * x[1] + x[2] * x[2] + x[3] * x[3]);
+    const float inv = 1.0f / sqrtf(ss / float(head_dim) + eps);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) x[e] = bf_lo(uint32_t(f2bf(x[e] * inv * wgt[e])));
+    float y[4];
+#pragma unroll
+    for (int p2 = 0; p2 < 2; ++p2) {
+        const int d = int(lane) * 4 + 2 * p2;
+        const double ang = double(pos) * pow(double(theta), -double(d) / double(head_dim));
+        const float cs = float(cos(ang)), sn = float(sin(ang));
+        y[2 * p2] = x[2 * p2] * cs - x[2 * p2 + 1] * sn;
+        y[2 * p2 + 1] = x[2 * p2] * sn + x[2 * p2 + 1] * cs;
+    }
+    return make_uint2(pack2(y[0], y[1]), pack2(y[2], y[3]));
+}
+
 // BATCHED: the kernel instance for batched programs (BGEMM µops, paged
 // attention); single-request programs run the instance without those paths
 // so their register allocation and scheduling are unaffected
-template <bool BATCHED>
+template <bool BATCHED, bool QKNORM = false>
 struct Vcc {
     const RingParams* P;
     Shared* S;
@@ -662,7 +690,7 @@ struct Vcc {
             for (int p = int(ct); p < rows / 2; p += NCT) {
                 const int wr = J.r0 + 2 * p;  // W row (pairs never straddle a region boundary)
                 float a = row_sum(2 * p, tpr), b = row_sum(2 * p + 1, tpr);
-                if (wr < qrows + kvr) {
+                if (wr < qrows + kvr && !(J.flags & VDC_JOB_QKNORM)) {
                     const int d = (wr < qrows ? wr : wr - qrows) % hd;
                     const float cs = S->rope_cs[d / 2], sn = S->rope_sn[d / 2];
                     const float na = a * cs - b * sn, nb = a * sn + b * cs;
@@ -976,7 +1004,7 @@ struct Vcc {
                 const float other = __shfl_xor_sync(0xffffffffu, v[c], 1);
                 if (b >= nb) continue;
                 const int64_t pos = req_pos(b);
-                if (isq || isk) {
+                if ((isq || isk) && !(J.flags & VDC_JOB_QKNORM)) {
                     double ang = double(pos) * invf;
                     ang -= 6.283185307179586 * rint(ang * 0.15915494309189535);
                     float sn, cs;
@@ -1139,7 +1167,9 @@ struct Vcc {
     __device__ void astamp(int ev) {
         if (P->tile_trace && sm == (P->debug >> 8) && ct == 0) P->tile_trace[60000 + 8 * (n_attn & 7) + ev] = now_ns();
     }
-    template <bool BF, int DPL, int G>
+    // QKN: Qwen3 QK-norm instance (separate, so the other instances carry no
+    // call to the double-precision norm/rotary helper)
+    template <bool BF, int DPL, int G, bool QKN = false>
     __device__ void attn(const vdc_job& J) {
         constexpr int EB = BF ? 2 : 4;
         astamp(0);
@@ -1179,7 +1209,17 @@ struct Vcc {
         {
             const uint4* qb = reinterpret_cast<const uint4*>(tptr(J.x_t) + size_t(J.x_off) * EB);
             uint4* qd = S->x;
-            if constexpr (BF) {
+            if constexpr (BF && DPL == 4 && QKN) {  // Qwen3: per-head RMSNorm of q, then the rotary (warp per head)
+                const uint2 wv = *reinterpret_cast<const uint2*>(tptr(J.out_row0) + lane * 8);
+                for (int h = int(w); h < G; h += CW) {
+                    const uint2 u = ldcg64(reinterpret_cast<const char*>(qb) + h * HD * 2 + lane * 8);
+                    const uint2 o = qk_norm_rope4(u, wv, lane, J.head_dim, J.eps, J.theta, pos);
+                    // lane's dims 4 lane .. 4 lane + 3 = chunk lane / 2, half lane % 2
+                    qd[(h * 2 + int(lane & 1u)) * NCH + int(lane >> 1)] =
+                        make_uint4(__float_as_uint(bf_lo(o.x)), __float_as_uint(bf_hi(o.x)), __float_as_uint(bf_lo(o.y)),
+                                   __float_as_uint(bf_hi(o.y)));
+                }
+            } else if constexpr (BF) {
                 // bf16 caches: q staged as fp32 in split halves, [head][half][chunk]
                 // x 4 floats (dims 8c..8c+3 | 8c+4..8c+7), so the score loop's
                 // packed-fp32 FMAs read q without unpacking (conflict-free)
@@ -1237,8 +1277,17 @@ struct Vcc {
                                             : size_t(pos);
                 const char* kn = tptr(J.a_t) + (size_t(J.a_off) + crow * HD) * EB;
                 const char* vn = tptr(J.b_t) + (size_t(J.b_off) + crow * HD) * EB;
+                constexpr bool qkn = BF && DPL == 4 && QKN;
+                if constexpr (qkn) {  // QK-norm + rotary of the appended k row, written back to the cache
+                    const uint2 u = ldcg64(kn + lane * 8);
+                    const uint2 wv = *reinterpret_cast<const uint2*>(tptr(J.block) + lane * 8);
+                    const uint2 o = qk_norm_rope4(u, wv, lane, J.head_dim, J.eps, J.theta, pos);
+                    *reinterpret_cast<uint2*>(const_cast<char*>(kn) + lane * 8) = o;
+                    asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(kb + uint32_t(r) * rowb + lane * 8u), "r"(o.x), "r"(o.y) : "memory");
+                }
                 for (int c = int(lane); c < 2 * NCH; c += 32) {
                     const bool isk = c < NCH;
+                    if (isk && qkn) continue;
                     const int cc = isk ? c : c - NCH;
                     const uint4 v = ldcg128(reinterpret_cast<const uint4*>(isk ? kn : vn) + cc);
                     const uint32_t dst = (isk ? kb : vb) + uint32_t(r) * rowb + uint32_t(cc) * 16u;
@@ -1560,9 +1609,9 @@ struct Vcc {
     }
 };
 
-template <bool BATCHED>
+template <bool BATCHED, bool QKNORM>
 __device__ void vcc_role(const RingParams& P, Shared& S, char* ring) {
-    Vcc<BATCHED> v;
+    Vcc<BATCHED, QKNORM> v;
     v.P = &P;
     v.S = &S;
     v.ring = smem_addr(ring);
@@ -1613,6 +1662,13 @@ __device__ void vcc_role(const RingParams& P, Shared& S, char* ring) {
                 const int dpl = J.head_dim / 32, G = J.group;
 #define VDC_ATTN_CASE(B, D, GG) \
     if (kbf == B && dpl == D && G == GG) { v.template attn<B, D, GG>(J); break; }
+#define VDC_ATTN_QKN_CASE(GG) \
+    if (kbf && dpl == 4 && G == GG && (J.flags & VDC_JOB_QKNORM)) { v.template attn<true, 4, GG, true>(J); break; }
+                if constexpr (QKNORM) {  // Qwen3 programs run their own kernel instance
+                    VDC_ATTN_QKN_CASE(4)
+                    VDC_ATTN_QKN_CASE(8)
+                }
+#undef VDC_ATTN_QKN_CASE
                 VDC_ATTN_CASE(true, 4, 4)
                 VDC_ATTN_CASE(true, 4, 8)
                 VDC_ATTN_CASE(false, 2, 1)
@@ -1837,7 +1893,7 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
     }
 }
 
-template <bool BATCHED>
+template <bool BATCHED, bool QKNORM>
 __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(const __grid_constant__ RingParams P) {
     extern __shared__ __align__(1024) char smem[];
     char* ring = smem;
@@ -1869,7 +1925,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(const __grid_cons
     __syncthreads();
     if (BATCHED) tc_fence_after();
     if (threadIdx.x < NCT) {
-        vcc_role<BATCHED>(P, S, ring);
+        vcc_role<BATCHED, QKNORM>(P, S, ring);
         if (BATCHED) {
             tc_fence_before();
             named_bar(BAR_VCC, NCT);
@@ -1885,8 +1941,14 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(const __grid_cons
 }  // namespace ring
 
 size_t ring_smem_bytes(uint32_t ring_slots, bool batched) { return ring::smem_bytes(ring_slots, batched); }
-const void* ring_kernel_entry(bool batched) {
-    return batched ? reinterpret_cast<const void*>(&ring::ring_kernel<true>) : reinterpret_cast<const void*>(&ring::ring_kernel<false>);
+// four instances: single-request / batched x without / with Qwen3 QK-norm,
+// so each program type keeps its own register allocation
+const void* ring_kernel_entry(bool batched, bool qknorm) {
+    if (batched)
+        return qknorm ? reinterpret_cast<const void*>(&ring::ring_kernel<true, true>)
+                      : reinterpret_cast<const void*>(&ring::ring_kernel<true, false>);
+    return qknorm ? reinterpret_cast<const void*>(&ring::ring_kernel<false, true>)
+                  : reinterpret_cast<const void*>(&ring::ring_kernel<false, false>);
 }
 
 }  // namespace vdc_dev

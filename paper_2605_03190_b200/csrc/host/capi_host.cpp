@@ -79,6 +79,7 @@ decode::ModelConfig model_from(const json& j) {
     m.eps = j.value("eps", m.eps);
     m.theta = j.value("theta", m.theta);
     m.scaled_init = j.value("scaled_init", m.scaled_init);
+    m.qk_norm = j.value("qk_norm", m.qk_norm);
     if (j.contains("dtype")) {
         auto e = workload::elem_from_name(j.at("dtype").get<std::string>());
         if (!e) throw std::invalid_argument("bad dtype");

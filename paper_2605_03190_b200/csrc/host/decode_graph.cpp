@@ -39,6 +39,7 @@ ModelConfig qwen3_8b() {
     m.vocab = 151936;
     m.eps = 1e-6f;
     m.theta = 1000000.0f;
+    m.qk_norm = true;
     return m;
 }
 ModelConfig llama3_70b() {
@@ -210,12 +211,24 @@ OperatorGraph build_decode_graph(const ModelConfig& m, const LayoutConfig& l) {
             t.state = true;
             b.view(L + c, ".seg", 1, R);
         }
+        std::map<std::string, std::string> qkv_attrs = {{"eps", eps}, {"theta", theta}, {"rope", "1"}, {"job_rows", std::to_string(R)}};
+        if (m.qk_norm) {
+            b.norm(L + "q_norm", hd);
+            b.norm(L + "k_norm", hd);
+            qkv_attrs["qk_norm"] = "1";
+        }
         b.node(L + "qkv", OpKind::RMS_GEMV, {L + "wqkv", b.view(x, ".all", d), L + "attn_norm"},
-               {L + "q", L + "kc.seg", L + "vc.seg"},
-               {{"eps", eps}, {"theta", theta}, {"rope", "1"}, {"job_rows", std::to_string(R)}});
+               {L + "q", L + "kc.seg", L + "vc.seg"}, qkv_attrs);
         b.add(L + "part", {hkv * splits * grp, hd + 2}, grp, hd + 2, InitKind::zeros, ElemType::f32);
-        b.node(L + "attn", OpKind::ATTN_DECODE, {b.view(L + "q", ".grp", grp * hd), L + "kc", L + "vc"}, {L + "part"},
-               {{"ctx_pages", std::to_string(l.ctx_pages)}, {"pages_per_job", std::to_string(l.pages_per_job)}});
+        std::map<std::string, std::string> attn_attrs = {{"ctx_pages", std::to_string(l.ctx_pages)},
+                                                         {"pages_per_job", std::to_string(l.pages_per_job)}};
+        if (m.qk_norm) {
+            attn_attrs["q_norm"] = L + "q_norm";
+            attn_attrs["k_norm"] = L + "k_norm";
+            attn_attrs["eps"] = eps;
+            attn_attrs["theta"] = theta;
+        }
+        b.node(L + "attn", OpKind::ATTN_DECODE, {b.view(L + "q", ".grp", grp * hd), L + "kc", L + "vc"}, {L + "part"}, attn_attrs);
         b.vec(L + "attn", qrows, grp * hd, e);
         // the combine reads all partials of one kv head as a single tile
         b.node(L + "comb", OpKind::ATTN_COMBINE, {b.view(L + "part", ".head", splits * grp)}, {L + "attn"});
@@ -338,11 +351,21 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
             TensorRef& t = b.add(L + c, {pool, hkv * l.page_rows, hd}, l.page_rows, hd, winit, e);
             t.state = true;
         }
-        b.node(L + "qkv", OpKind::RMS_GEMV, {L + "wqkv", xn, x}, {L + "q", L + "kc", L + "vc"},
-               {{"eps", eps}, {"theta", theta}, {"rope", "1"}, {"batch", bs}});
+        std::map<std::string, std::string> qkv_attrs = {{"eps", eps}, {"theta", theta}, {"rope", "1"}, {"batch", bs}};
+        std::map<std::string, std::string> attn_attrs = {{"pages_per_job", std::to_string(l.pages_per_job)}, {"batch", bs},
+                                                         {"req_pages", rp}};
+        if (m.qk_norm) {
+            b.norm(L + "q_norm", hd);
+            b.norm(L + "k_norm", hd);
+            qkv_attrs["qk_norm"] = "1";
+            attn_attrs["q_norm"] = L + "q_norm";
+            attn_attrs["k_norm"] = L + "k_norm";
+            attn_attrs["eps"] = eps;
+            attn_attrs["theta"] = theta;
+        }
+        b.node(L + "qkv", OpKind::RMS_GEMV, {L + "wqkv", xn, x}, {L + "q", L + "kc", L + "vc"}, qkv_attrs);
         b.add(L + "part", {jobs * hkv * grp, hd + 2}, grp, hd + 2, InitKind::zeros, ElemType::f32);
-        b.node(L + "attn", OpKind::ATTN_DECODE, {L + "q", L + "kc", L + "vc"}, {L + "part"},
-               {{"pages_per_job", std::to_string(l.pages_per_job)}, {"batch", bs}, {"req_pages", rp}});
+        b.node(L + "attn", OpKind::ATTN_DECODE, {L + "q", L + "kc", L + "vc"}, {L + "part"}, attn_attrs);
         act(L + "attn", qrows, true);
         b.node(L + "comb", OpKind::ATTN_COMBINE, {L + "part"}, {L + "attn"}, {{"batch", bs}});
         wgt(L + "wo", d, qrows, double(qrows));

@@ -289,6 +289,7 @@ class RingLowering {
                     j.head_dim = int32_t(head_dim);
                     if (qkv) {
                         j.flags |= VDC_JOB_QKV;
+                        if (attr_int(n, "qk_norm", 0)) j.flags |= VDC_JOB_QKNORM;  // q / k stored un-rotated
                         j.theta = float(attr_num(n, "theta", 10000.0));
                         j.block = int32_t(qrows);
                         j.split = int32_t(kvrows);
@@ -324,6 +325,17 @@ class RingLowering {
                 }
             }
         }
+    }
+
+    // Qwen3 QK-norm: the attention µop normalises q and the appended k row
+    // (weights in out_row0 / block), then applies the rotary
+    void qk_norm_fields(const workload::OperatorNode& n, vdc_job& j) const {
+        if (!n.attrs.count("q_norm")) return;
+        j.flags |= VDC_JOB_QKNORM;
+        j.out_row0 = storage(idx(n.attrs.at("q_norm")));
+        j.block = storage(idx(n.attrs.at("k_norm")));
+        j.eps = float(attr_num(n, "eps", 1e-6));
+        j.theta = float(attr_num(n, "theta", 10000.0));
     }
 
     void plan_attention(const workload::OperatorNode& n, uint32_t ordinal) {
@@ -374,6 +386,7 @@ class RingLowering {
                 j.split = int32_t(s);
                 j.arrive_ctr = ctr;
                 j.arrive_need = int32_t(splits);
+                qk_norm_fields(n, j);
                 for (int64_t pg = j.r0; pg < j.r1; ++pg) {
                     r.tiles.push_back({kc, {uint16_t(h), uint16_t(pg), 0}});
                     r.tiles.push_back({vc, {uint16_t(h), uint16_t(pg), 0}});
@@ -621,6 +634,7 @@ class RingLowering {
                 } else if (qkv) {
                     const TileDescriptor& kc = desc_[idx(n.outputs[1])];
                     j.flags |= VDC_JOB_QKV;
+                    if (attr_int(n, "qk_norm", 0)) j.flags |= VDC_JOB_QKNORM;
                     j.head_dim = int32_t(kc.shape[2]);
                     j.kvrows = int32_t(kc.shape[1] / 64 * kc.shape[2]);
                     j.block = int32_t(M - 2 * j.kvrows);
@@ -744,6 +758,7 @@ class RingLowering {
             j.o_off = int32_t(i) * int32_t(grp * (hd + 2));
             j.split = int32_t(a.s);
             j.arrive_ctr = ctr[{a.b, a.h}];
+            qk_norm_fields(n, j);
             j.arrive_need = int32_t(ceil_div<int64_t>(int64_t(pages_[size_t(a.b)].size()), per));
             for (int64_t pg = a.p0; pg < a.p1; ++pg) {
                 const uint16_t phys = uint16_t(pages_[size_t(a.b)][size_t(pg)]);

@@ -35,7 +35,7 @@ def model_cfg(info: dict) -> dict:
             "theta": float(nodes["L0.qkv"]["attrs"]["theta"]), "layers": layers, "gu_block": 128, "dtype": "bf16",
             # batched programs store the RMSNorm operand as bf16(x * w) and scale
             # the GEMM output by 1/rms (decode_ref documents both conventions)
-            "norm_scale_after": True}
+            "norm_scale_after": True, "qk_norm": "L0.q_norm" in g}
 
 
 def step_block(info: dict, tokens, pos) -> np.ndarray:

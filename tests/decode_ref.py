@@ -63,8 +63,18 @@ def decode_step(T: dict, cfg: dict, token: int, pos: int) -> dict:
         L = f"L{l}."
         h = rmsnorm(x, T[L + "attn_norm"].reshape(-1))
         qkv = mv(T[L + "wqkv"].reshape(-1, d), h)
-        q = rnd(rope(qkv[: hq * hd], 0))
-        k = rnd(rope(qkv[hq * hd: (hq + hkv) * hd], hq * hd))
+        if cfg.get("qk_norm"):
+            # Qwen3: q / k stored as bf16, per-head RMSNorm (bf16) then the rotary
+            def headnorm(v, w):
+                v = rnd(v).reshape(-1, hd)
+                ss = np.sum(v.astype(np.float32) * v.astype(np.float32), axis=1, dtype=np.float32)
+                inv = (f32(1.0) / np.sqrt(ss / f32(hd) + f32(eps))).astype(np.float32)
+                return rnd(v * inv[:, None] * w.reshape(1, hd)).reshape(-1)
+            q = rnd(rope(headnorm(qkv[: hq * hd], T[L + "q_norm"]), 0))
+            k = rnd(rope(headnorm(qkv[hq * hd: (hq + hkv) * hd], T[L + "k_norm"]), hq * hd))
+        else:
+            q = rnd(rope(qkv[: hq * hd], 0))
+            k = rnd(rope(qkv[hq * hd: (hq + hkv) * hd], hq * hd))
         v = rnd(qkv[(hq + hkv) * hd:])
         Kc = T[L + "kc"].reshape(hkv, -1, hd).copy()
         Vc = T[L + "vc"].reshape(hkv, -1, hd).copy()

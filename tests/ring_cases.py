@@ -34,7 +34,8 @@ def model_cfg(info: dict, req: dict) -> dict:
     layers = sum(1 for n in info["graph"]["operators"] if n["id"].endswith(".qkv"))
     dtype = [x["dtype"] for x in info["descriptors"] if x["name"] == "L0.wqkv"][0]
     return {"hidden": d, "heads": q // hd, "kv_heads": kc[0], "head_dim": hd, "ffn": g["L0.a"]["shape"][0],
-            "eps": eps, "theta": theta, "layers": layers, "gu_block": req["layout"]["gu_block"], "dtype": dtype}
+            "eps": eps, "theta": theta, "layers": layers, "gu_block": req["layout"]["gu_block"], "dtype": dtype,
+            "qk_norm": "L0.q_norm" in g}
 
 
 def synth_inputs(info: dict, seed: int = 0) -> dict:
@@ -53,6 +54,8 @@ def synth_inputs(info: dict, seed: int = 0) -> dict:
             a = (rng.random(n, np.float32) * 2 - 1) / np.float32(np.sqrt(fan))
         else:
             a = np.zeros(n, np.float32)
+        if d["name"].endswith("q_norm") or d["name"].endswith("k_norm"):  # non-trivial QK-norm weights
+            a = (1.0 + 0.25 * (rng.random(n, np.float32) * 2 - 1)).astype(np.float32)
         if d["dtype"] == "bf16":
             a = decode_ref.bf16(a)
         out[d["name"]] = a

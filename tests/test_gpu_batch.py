@@ -88,6 +88,18 @@ def test_mid_batch64_long_jobs(cuda):
     assert_close(run(bc.MID_MODEL, pages, [(tokens, pos)], ppj=16)[0])
 
 
+def test_mid_qwen3_qk_norm_batch8(cuda):
+    """Qwen3 QK-norm in the batched path (C4 model family): q / k normalised
+    per head by the attention µops, appended k rows written back"""
+    model = dict(bc.MID_MODEL, qk_norm=True, eps=1e-6, theta=1e6)
+    rng = np.random.default_rng(5)
+    pages = [int(p) for p in rng.integers(1, 6, 8)]
+    pos0 = [int(rng.integers(0, 64 * p - 2)) for p in pages]
+    steps = [([int(t) for t in rng.integers(0, 4096, 8)], [p + s for p in pos0]) for s in range(2)]
+    for rs in run(model, pages, steps):
+        assert_close(rs)
+
+
 def test_llama3_8b_layer_batch32(cuda):
     rng = np.random.default_rng(4)
     pages = [int(p) for p in rng.integers(2, 20, 32)]

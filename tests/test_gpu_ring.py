@@ -85,6 +85,16 @@ def test_fused_argmax_matches_logits(cuda):
         assert int(host["next_token"][0]) == int(np.argmax(host["logits"])), (host["next_token"], np.argmax(host["logits"]))
 
 
+@pytest.mark.parametrize("token,pos", [(17, 300), (3, 0), (4095, 511)])
+def test_mid_qwen3_qk_norm_matches_dense(cuda, token, pos):
+    """Qwen3 QK-norm (per-head RMSNorm of q and k before the rotary, applied
+    by the attention µop; the appended k row is written back normalised)"""
+    base = {"model": dict(rc.MID["model"], qk_norm=True, eps=1e-6, theta=1e6), "layout": dict(rc.MID["layout"])}
+    _, _, _, outs = run(base, None, ((token, pos), (token + 1, pos + 1)) if pos < 511 else ((token, pos),))
+    for res, _ in outs:
+        assert_close(res, fp32=False)
+
+
 def test_llama3_8b_layer_matches_dense(cuda):
     _, _, _, outs = run(LLAMA_1L, None, ((1234, 777),))
     assert_close(outs[0][0], fp32=False)
