@@ -898,7 +898,10 @@ struct Vcc {
         if (!fin) return;  // a piece of a split row block that was not the last to arrive
         fence_proxy_async_global();  // consumers read these activations with TMA (async proxy)
         sync();
-        if (ct == 0) {
+        if (ct == 0 && (J.flags & VDC_JOB_SYM_OUT)) {  // publish on every rank (system scope)
+            for (uint32_t qr = 0; qr < P->tp_world; ++qr)
+                asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(sym_base(J.o_t, qr)) : "memory");
+        } else if (ct == 0) {
             red_release_add(ctr(J.o_t), 1u);
             if (J.flags & VDC_JOB_QKV) {
                 red_release_add(ctr(J.b_t), 1u);
@@ -1050,6 +1053,14 @@ struct Vcc {
                 const uint16_t xo = f2bf(v[c] + r[c]);
                 u16p(J.o_t)[int64_t(b) * M + rg] = xo;
                 if (J.o3_t >= 0) u16p(J.o3_t)[int64_t(b) * M + rg] = f2bf(bf_lo(xo) * wn);
+            }
+        } else if (J.flags & VDC_JOB_SYM_OUT) {
+            // TP partial sums (fp32) -> slot tp_rank of every rank's exchange buffer (peer stores)
+            for (uint32_t qr = 0; qr < P->tp_world; ++qr) {
+                float* dst = reinterpret_cast<float*>(sym_base(J.o_t, qr) + VDC_SYM_HEADER_BYTES) + J.o_off;
+#pragma unroll
+                for (int c = 0; c < NH; ++c)
+                    if (c0 + c < nb) dst[int64_t(c0 + c) * M + rg] = v[c];
             }
         } else {
             const bool obf = tdtype(J.o_t) == VDC_DTYPE_BF16;
@@ -1571,6 +1582,12 @@ struct Vcc {
     // rows [r0, r1): x_next = residual + sum over the W rank slots of the
     // symmetric partial buffer, in rank order (same result on every rank)
     __device__ void allreduce(const vdc_job& J) {
+        if constexpr (BATCHED) {
+            if (J.flags & VDC_JOB_BATCH) {
+                allreduce_batched(J);
+                return;
+            }
+        }
         if (!wait_ready(J.x_t, J.x_need, J.a_t, J.a_need, -1, 0)) {
             ok = false;
             return;
@@ -1595,6 +1612,35 @@ struct Vcc {
             store_out(ob, obf, r, v);
         }
         publish(J.o_t);
+    }
+
+    // batched (npad, d) hidden states: x = residual + sum of the rank slots
+    // (rank order), and the next RMSNorm's operand bf16(x * w)
+    __device__ void allreduce_batched(const vdc_job& J) {
+        if (!wait_ready(J.x_t, J.x_need, J.a_t, J.a_need, -1, 0)) {
+            ok = false;
+            return;
+        }
+        const float* part = reinterpret_cast<const float*>(tptr(J.x_t));
+        const uint16_t* res = u16p(J.a_t);
+        const uint16_t* wn = u16p(J.w3_t);
+        const int64_t M = J.k, slot = int64_t(J.npad) * M;
+        const int rows = J.r1 - J.r0;
+        for (int i = int(ct); i < J.nb * rows; i += NCT) {
+            const int b = i / rows, r = J.r0 + i % rows;
+            const int64_t e = int64_t(b) * M + r;
+            float v = 0.f;
+            for (int qr = 0; qr < J.group; ++qr) v += ldcg_f32(part + qr * slot + e);
+            const uint16_t xo = f2bf(v + bf_lo(ldcg_u16(res + e)));
+            u16p(J.o_t)[e] = xo;
+            u16p(J.o3_t)[e] = f2bf(bf_lo(xo) * bf_lo(wn[r]));
+        }
+        fence_proxy_async_global();  // the next GEMM reads x * w with TMA
+        sync();
+        if (ct == 0) {
+            red_release_add(ctr(J.o_t), 1u);
+            red_release_add(ctr(J.o3_t), 1u);
+        }
     }
 
     // ------------------------------------------- ELEMWISE copy (embedding row)

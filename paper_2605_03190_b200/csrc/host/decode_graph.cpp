@@ -295,16 +295,31 @@ int batch_npad(int batch) {
 // xn = bf16(x * w_norm) of the next RMSNorm (its per-request 1/rms is
 // applied in the consuming GEMM's epilogue); gate/up rows come in blocks of
 // 128 = [64 gate | 64 up] (gu_block 128: one MMA row block).
+static std::map<std::string, std::string> with_attrs(std::map<std::string, std::string> a, const std::map<std::string, std::string>& extra) {
+    a.insert(extra.begin(), extra.end());
+    return a;
+}
+
 OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfig& l) {
     const int B = l.batch, N = batch_npad(B);
     if (m.dtype != ElemType::bf16 || m.head_dim != 128 || l.page_rows != 64)
         throw workload::WorkloadError("batched decode is built for bf16 models with head_dim 128 and 64-row pages");
     if (int(l.req_pages.size()) != B) throw workload::WorkloadError("layout.req_pages needs one entry per request");
     if (l.gu_block != 128) throw workload::WorkloadError("batched decode uses gu_block 128");
-    const int64_t d = m.hidden, hd = m.head_dim, hq = m.heads, hkv = m.kv_heads, grp = hq / hkv;
-    const int64_t qrows = hq * hd, kvrows = hkv * hd, ffn = m.ffn;
-    if (d % 128 || qrows % 128 || kvrows % 128 || ffn % 64 || m.vocab % 128 || hq % hkv)
+    // tensor parallelism (rank tp_rank of tp_world): column-parallel qkv and
+    // gate/up, row-parallel o / down into symmetric fp32 partial buffers,
+    // in-kernel ALLREDUCE_ADD (+ residual, + the next norm's operand),
+    // vocab-parallel lm_head
+    const bool tp = l.tp_world >= 1;
+    const int64_t W = tp ? l.tp_world : 1;
+    if (tp && (l.tp_rank < 0 || l.tp_rank >= W || m.kv_heads % W || m.ffn % (W * 64) || m.vocab % (W * 128)))
+        throw workload::WorkloadError("tensor parallelism needs kv_heads, ffn / 64 and vocab / 128 divisible by tp_world");
+    const int64_t d = m.hidden, hd = m.head_dim, hq = m.heads / W, hkv = m.kv_heads / W, grp = hq / hkv;
+    const int64_t qrows = hq * hd, kvrows = hkv * hd, ffn = m.ffn / W, vocab = m.vocab / W;
+    if (d % 128 || qrows % 128 || kvrows % 128 || ffn % 64 || vocab % 128 || hq % hkv)
         throw workload::WorkloadError("batched decode needs 128-row aligned projections");
+    const std::map<std::string, std::string> tp_attrs = {{"tp_world", std::to_string(W)}, {"tp_rank", std::to_string(l.tp_rank)}};
+
     int64_t pool = 0, jobs = 0;
     for (int p : l.req_pages) {
         if (p < 1) throw workload::WorkloadError("every request covers at least one page");
@@ -313,6 +328,11 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
     }
     if (pool > 4095) throw workload::WorkloadError("KV pool exceeds 4095 pages (12-bit tile coordinates)");
     Builder b{{}, m, l};
+    auto sym = [&](const std::string& name) {  // exchange buffer: one (npad, d) fp32 slot per rank
+        TensorRef& t = b.add(name, {W * N * d, 1}, N * d, 1, InitKind::zeros, ElemType::f32);
+        t.symmetric = true;
+        return name;
+    };
     const ElemType e = m.dtype;
     const InitKind winit = m.scaled_init ? InitKind::centered : InitKind::random;
     const std::string eps = num(m.eps), theta = num(m.theta), bs = std::to_string(B);
@@ -339,7 +359,7 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
     sk("o.sk", d / 128);
     sk("gu.sk", 2 * ffn / 128);
     sk("down.sk", d / 128);
-    sk("head.sk", m.vocab / 128);
+    sk("head.sk", vocab / 128);
     std::string x = act("embed.x", d, false), xn = act("embed.xn", d, true);
     b.norm("L0.attn_norm", d);
     b.node("embed", OpKind::EMBED_ROW, {"embed.table", "L0.attn_norm"}, {x, xn}, {{"batch", bs}});
@@ -368,26 +388,37 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
         b.node(L + "attn", OpKind::ATTN_DECODE, {L + "q", L + "kc", L + "vc"}, {L + "part"}, attn_attrs);
         act(L + "attn", qrows, true);
         b.node(L + "comb", OpKind::ATTN_COMBINE, {L + "part"}, {L + "attn"}, {{"batch", bs}});
-        wgt(L + "wo", d, qrows, double(qrows));
+        wgt(L + "wo", d, qrows, double(qrows * W));
         b.norm(L + "mlp_norm", d);
         act(L + "x1", d, false);
         act(L + "x1n", d, true);
-        b.node(L + "o", OpKind::GEMV_ADD, {L + "wo", L + "attn", x, L + "mlp_norm"}, {L + "x1", L + "x1n"}, {{"batch", bs}});
+        if (tp) {
+            b.node(L + "o", OpKind::GEMV, {L + "wo", L + "attn"}, {sym(L + "o.part")}, with_attrs({{"batch", bs}}, tp_attrs));
+            b.node(L + "o.ar", OpKind::ALLREDUCE_ADD, {L + "o.part", x, L + "mlp_norm"}, {L + "x1", L + "x1n"},
+                   with_attrs({{"batch", bs}}, tp_attrs));
+        } else {
+            b.node(L + "o", OpKind::GEMV_ADD, {L + "wo", L + "attn", x, L + "mlp_norm"}, {L + "x1", L + "x1n"}, {{"batch", bs}});
+        }
         wgt(L + "wgu", 2 * ffn, d, double(d));
         act(L + "a", ffn, true);
         b.node(L + "gu", OpKind::RMS_GEMV, {L + "wgu", L + "x1n", L + "x1"}, {L + "a"},
                {{"eps", eps}, {"swiglu", "128"}, {"batch", bs}});
-        wgt(L + "wd", d, ffn, double(ffn));
+        wgt(L + "wd", d, ffn, double(ffn * W));
         const std::string next_norm = li + 1 < m.layers ? "L" + std::to_string(li + 1) + ".attn_norm" : "final_norm";
         b.norm(next_norm, d);
         x = act(L + "x2", d, false);
         xn = act(L + "x2n", d, true);
-        b.node(L + "down", OpKind::GEMV_ADD, {L + "wd", L + "a", L + "x1", next_norm}, {x, xn}, {{"batch", bs}});
+        if (tp) {
+            b.node(L + "down", OpKind::GEMV, {L + "wd", L + "a"}, {sym(L + "d.part")}, with_attrs({{"batch", bs}}, tp_attrs));
+            b.node(L + "down.ar", OpKind::ALLREDUCE_ADD, {L + "d.part", L + "x1", next_norm}, {x, xn}, with_attrs({{"batch", bs}}, tp_attrs));
+        } else {
+            b.node(L + "down", OpKind::GEMV_ADD, {L + "wd", L + "a", L + "x1", next_norm}, {x, xn}, {{"batch", bs}});
+        }
     }
-    wgt("lm_head", m.vocab, d, double(d));
-    b.add("logits", {B, m.vocab}, 1, m.vocab, InitKind::zeros, ElemType::f32);
+    wgt("lm_head", vocab, d, double(d));  // vocab-parallel: this rank's logit columns
+    b.add("logits", {B, vocab}, 1, vocab, InitKind::zeros, ElemType::f32);
     std::map<std::string, std::string> head_attrs = {{"eps", eps}, {"batch", bs}};
-    if (l.argmax) {  // greedy sampling fused into the lm_head GEMM: per-SM slots, tokens per request
+    if (l.argmax && !tp) {  // greedy sampling fused into the lm_head GEMM: per-SM slots, tokens per request
         b.add("head.amax", {256 * N, 2}, N, 2, InitKind::zeros, ElemType::f32);
         b.add("next_token", {B, 1}, 1, 1, InitKind::zeros, ElemType::i64);
         head_attrs["argmax"] = "1";

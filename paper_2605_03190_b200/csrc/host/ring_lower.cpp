@@ -536,7 +536,11 @@ class RingLowering {
             }
             case OpKind::RMS_GEMV:
             case OpKind::GEMV_ADD:
+            case OpKind::GEMV:
                 plan_bgemm(n, ordinal);
+                break;
+            case OpKind::ALLREDUCE_ADD:
+                plan_ballreduce(n, ordinal);
                 break;
             case OpKind::ATTN_DECODE:
                 plan_battention(n, ordinal);
@@ -649,6 +653,11 @@ class RingLowering {
                         j.flags |= VDC_JOB_SWIGLU;
                         j.cache_rows = int32_t(M / 2);
                     }
+                    if (desc_[uint16_t(j.o_t)].symmetric) {  // TP partial sums -> slot tp_rank of every rank's buffer
+                        j.flags |= VDC_JOB_SYM_OUT;
+                        j.o_off = int32_t(attr_int(n, "tp_rank", 0) * npad_ * M);
+                        j.group = int32_t(attr_int(n, "tp_world", 1));
+                    }
                     r.publishes = {j.o_t};
                 }
                 for (int64_t kt = ps[i].kt0; kt < ps[i].kt1; ++kt) r.tiles.push_back({w, {uint16_t(b), uint16_t(kt)}});
@@ -675,6 +684,45 @@ class RingLowering {
                 j.am_ctr = ctr;
                 j.am_need = int32_t(slot_of.size());
             }
+        }
+    }
+
+    // batched ALLREDUCE_ADD (TP): rows split over the SMs (8-row units); per
+    // row and request x = residual + sum of the W rank slots (rank order),
+    // plus the next RMSNorm's operand x * w. The partials' readiness target
+    // is W x (row blocks of the producer) on the local header counter.
+    void plan_ballreduce(const workload::OperatorNode& n, uint32_t ordinal) {
+        const int32_t part = storage(idx(n.inputs[0])), res = storage(idx(n.inputs[1])), nw = storage(idx(n.inputs[2]));
+        const int32_t out = storage(idx(n.outputs[0])), outn = storage(idx(n.outputs[1]));
+        const int64_t d = desc_[uint16_t(out)].cols(), W = attr_int(n, "tp_world", 1);
+        int32_t producers = 0;
+        for (const auto& r : jobs_)
+            for (int32_t t : r.publishes)
+                if (t == part) producers += r.counts ? 1 : 0;
+        const int64_t unit = 8, units = ceil_div<int64_t>(d, unit);
+        for (uint32_t s = 0; s < sms_; ++s) {
+            const auto [u0, u1] = share(units, s);
+            if (u0 == u1) continue;
+            RJob r;
+            r.ordinal = ordinal;
+            r.sm = s;
+            vdc_job& j = r.j;
+            j = blank(Opcode::ALLREDUCE_ADD);
+            j.flags = VDC_JOB_SYM_IN | VDC_JOB_RESID | VDC_JOB_BATCH;
+            j.r0 = int32_t(u0 * unit);
+            j.r1 = int32_t(std::min(d, u1 * unit));
+            j.k = int32_t(d);
+            j.group = int32_t(W);
+            j.nb = nb_;
+            j.npad = npad_;
+            j.x_t = part;
+            j.x_need = int32_t(W) * producers;
+            j.a_t = res;
+            j.w3_t = nw;
+            j.o_t = out;
+            j.o3_t = outn;
+            r.publishes = {out, outn};
+            jobs_.push_back(std::move(r));
         }
     }
 
