@@ -51,6 +51,11 @@ TORCH_DTYPE = {"f32": "float32", "bf16": "bfloat16", "i64": "int64"}
 
 
 PACKED_SW128 = 0x80000000  # ring_abi.h VDC_DESC_PACKED_SW128
+def to_logical(d: dict, a: np.ndarray) -> np.ndarray:
+    """device storage order -> row-major (packed weight layouts undone)"""
+    if d.get("tma") == PACKED_SW128:
+        return unpack_sw128(a, *d["shape"])
+    return a
 
 
 def pack_sw128(a: np.ndarray, rows: int, cols: int) -> np.ndarray:
@@ -158,6 +163,10 @@ class Engine:
         arr = (ctypes.c_void_p * len(peer_ptrs))(*peer_ptrs)
         check(lib().vdc_bind_symmetric(self._h, d["index"], arr, world, rank))
 
+    def host_arrays(self, tensors: dict) -> dict:
+        """bound device tensors -> host float32 arrays in logical row-major order"""
+        return {k: to_logical(self.descs[k], v.float().cpu().numpy()) for k, v in tensors.items()}
+
     def bind_step(self, tensor) -> None:
         """Device-resident int64 step block (token, pos, ctx, ...)."""
         check(lib().vdc_bind_step(self._h, ctypes.c_void_p(tensor.data_ptr()), tensor.numel()))
@@ -211,5 +220,5 @@ def simulate(program: Program, inputs: dict, step=None, device: int = 0):
         st = torch.tensor(list(step) + [0] * (8 - len(step)), dtype=torch.int64, device=f"cuda:{device}")
         eng.bind_step(st)
     rep = eng.run()
-    host = {k: v.float().cpu().numpy() for k, v in tens.items()}
+    host = eng.host_arrays(tens)
     return rep, host

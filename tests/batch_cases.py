@@ -112,14 +112,7 @@ synth_inputs = rc.synth_inputs
 def readback(info: dict, tens: dict) -> dict:
     """Device tensors -> host float32 arrays in logical (row-major) order
     (packed weight tiles are unpacked)."""
-    from paper_2605_03190_b200.engine import PACKED_SW128, unpack_sw128
+    from paper_2605_03190_b200.engine import to_logical
 
     shapes = {d["name"]: d for d in info["descriptors"]}
-    out = {}
-    for k, v in tens.items():
-        a = v.float().cpu().numpy()
-        d = shapes[k]
-        if d.get("tma") == PACKED_SW128:
-            a = unpack_sw128(a, *d["shape"])
-        out[k] = a
-    return out
+    return {k: to_logical(shapes[k], v.float().cpu().numpy()) for k, v in tens.items()}

@@ -44,7 +44,7 @@ def run(base, sms=None, steps=((17, 40),), seed=0):
         st[0], st[1], st[2] = token, pos, pos + 1
         rep = eng.run()
         assert rep.status == 0, rep.message
-        host = {k: v.float().cpu().numpy() for k, v in tens.items()}
+        host = eng.host_arrays(tens)
         res = rc.check_against_dense(info, req, state, host, token, pos)
         outs.append((res, host))
         state = {k: v.copy() for k, v in host.items()}  # the device caches feed the next step

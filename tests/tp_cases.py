@@ -98,7 +98,7 @@ def run_emulated(base: dict, world: int, steps=((17, 40),), seed: int = 0):
         reps = [e.wait() for e in engines]
         for rep in reps:
             assert rep.status == 0, rep.message
-        host = [{k: v.float().cpu().numpy() for k, v in t.items()} for t in tens]
+        host = [e.host_arrays(t) for e, t in zip(engines, tens)]
         full_in = assemble_full(infos, state, cfg_full)
         full_dev = {"logits": np.concatenate([h["logits"] for h in host])}
         hd = cfg_full["head_dim"]
