@@ -186,6 +186,45 @@ class Engine:
         a = a[a[:, 1] != 0]
         return [(int(r[0]) >> 32, int(r[0]) & 0xffffffff, int(r[1]), int(r[2]), int(r[3])) for r in a]
 
+    def chrome_trace(self, path: str) -> int:
+        """Write the last launch's per-µop device trace (vdc_bind_trace
+        records) as a Chrome trace (chrome://tracing, Perfetto): one process
+        per SM, one thread per core, a slice per compute µop split into its
+        dependency wait ("wait") and its execution (opcode + operand block),
+        named by the µop's operator. Returns the number of slices."""
+        import json
+
+        ops = {}
+        text = self.program.text(False)
+        for core_name, st in text["streams"].items():
+            if ".vcc" not in core_name:
+                continue
+            sm = int(core_name[2:].split(".")[0])
+            pc = 0
+            for line in st.splitlines():
+                if line.startswith("#"):
+                    continue
+                op = line.rsplit("op=", 1)[1] if "op=" in line else "?"
+                imm = line.split("imm=")[1].split()[0] if "imm=" in line else "0"
+                ops[(2 * sm + 1, pc)] = (line.split()[0], op, imm)
+                pc += 1
+        rows = self.trace()
+        if not rows:
+            return 0
+        t0 = min(r[2] for r in rows)
+        ev = []
+        for core, pc, te, tr, td in rows:
+            name, op, imm = ops.get((core, pc), ("?", "?", "0"))
+            sm = core // 2
+            if tr > te:
+                ev.append({"name": "wait", "cat": "dep", "ph": "X", "pid": sm, "tid": 0, "ts": (te - t0) / 1e3,
+                           "dur": (tr - te) / 1e3, "args": {"op": op}})
+            ev.append({"name": f"{name} op{op}", "cat": "uop", "ph": "X", "pid": sm, "tid": 0, "ts": (tr - t0) / 1e3,
+                       "dur": max(td - tr, 0) / 1e3, "args": {"pc": pc, "job": int(imm), "operator": op}})
+        with open(path, "w") as f:
+            json.dump({"traceEvents": ev, "displayTimeUnit": "ns"}, f)
+        return len(ev)
+
     # -- execution ----------------------------------------------------------
     def launch(self, stream=None) -> None:
         s = ctypes.c_void_p(stream.cuda_stream if stream is not None else _torch().cuda.current_stream(self.device).cuda_stream)
