@@ -65,6 +65,7 @@ struct LayoutConfig {
     // pages (its context capacity in this program), allocated contiguously
     // in the pool (the page table is part of the lowered program).
     bool argmax = false;  // greedy sampling fused into lm_head (single-request, no TP): next_token (int64)
+    bool feedback = false;  // with argmax: token fed back + position advanced in the step block on the device
     int batch = 0;
     std::vector<int> req_pages;
 };

@@ -65,6 +65,9 @@
                                    normalises q (and the appended k row, written back to the
                                    cache) per head with weights out_row0 (q) / block (k) and
                                    eps, then applies the rotary (theta) */
+#define VDC_JOB_FEEDBACK 0x2000  /* with ARGMAX: the sampled token is fed back on the device: the step
+                                   block's token becomes it and pos / ctx advance by one, so the
+                                   next launch decodes the next position without the host */
 #define VDC_JOB_BATCH 0x400     /* batched program (nb requests): per-request token / pos / ctx in
                                    the step block (3 int64 each), paged KV pools, page table at
                                    step[ptab + b * maxp + logical page] */

@@ -455,6 +455,12 @@ struct Vcc {
             for (int o = 16; o; o >>= 1) am_merge(v0, i0, __shfl_xor_sync(0xffffffffu, v0, o), __shfl_xor_sync(0xffffffffu, i0, o));
             if (lane == 0) {
                 *reinterpret_cast<int64_t*>(tptr(J.o2_t)) = int64_t(i0);
+                if (J.flags & VDC_JOB_FEEDBACK) {  // next launch: this token at the next position
+                    int64_t* st = const_cast<int64_t*>(P->step);
+                    st[VDC_STEP_TOKEN] = int64_t(i0);
+                    st[VDC_STEP_POS] += 1;
+                    st[VDC_STEP_CTX] += 1;
+                }
                 red_release_add(ctr(J.o2_t), 1u);
             }
         }
@@ -1125,7 +1131,15 @@ struct Vcc {
                 am_merge(bv, bi, ldcg_f32(all + (size_t(s2) * npad + b) * 2), __float_as_int(ldcg_f32(all + (size_t(s2) * npad + b) * 2 + 1)));
 #pragma unroll
             for (int o = 16; o; o >>= 1) am_merge(bv, bi, __shfl_xor_sync(0xffffffffu, bv, o), __shfl_xor_sync(0xffffffffu, bi, o));
-            if (lane == 0) reinterpret_cast<int64_t*>(tptr(J.o2_t))[b] = int64_t(bi);
+            if (lane == 0) {
+                reinterpret_cast<int64_t*>(tptr(J.o2_t))[b] = int64_t(bi);
+                if (J.flags & VDC_JOB_FEEDBACK) {  // next launch: request b's token at its next position
+                    int64_t* st = const_cast<int64_t*>(P->step);
+                    st[3 * b] = int64_t(bi);
+                    st[3 * b + 1] += 1;
+                    st[3 * b + 2] += 1;
+                }
+            }
         }
         publish(J.o2_t);
     }

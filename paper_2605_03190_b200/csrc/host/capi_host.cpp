@@ -103,6 +103,7 @@ decode::LayoutConfig layout_from(const json& j) {
     l.tp_rank = j.value("tp_rank", l.tp_rank);
     l.batch = j.value("batch", l.batch);
     l.argmax = j.value("argmax", l.argmax);
+    l.feedback = j.value("feedback", l.feedback);
     l.req_pages = j.value("req_pages", l.req_pages);
     return l;
 }

@@ -269,6 +269,7 @@ OperatorGraph build_decode_graph(const ModelConfig& m, const LayoutConfig& l) {
         b.add("head.amax", {4096, 2}, 4096, 2, InitKind::zeros, ElemType::f32);
         b.add("next_token", {1, 1}, 1, 1, InitKind::zeros, ElemType::i64);
         head_attrs["argmax"] = "1";
+        if (l.feedback) head_attrs["feedback"] = "1";
     }
     b.node("head", OpKind::RMS_GEMV, {"lm_head", b.view(x, ".all", d), "final_norm"}, {"logits"}, head_attrs);
     b.g.validate();
@@ -422,6 +423,7 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
         b.add("head.amax", {256 * N, 2}, N, 2, InitKind::zeros, ElemType::f32);
         b.add("next_token", {B, 1}, 1, 1, InitKind::zeros, ElemType::i64);
         head_attrs["argmax"] = "1";
+        if (l.feedback) head_attrs["feedback"] = "1";
     }
     b.node("head", OpKind::RMS_GEMV, {"lm_head", xn, x}, {"logits"}, head_attrs);
     return std::move(b.g);

@@ -164,7 +164,7 @@ class RingLowering {
                     for (const auto& [sm, i] : last) slot[sm] = int32_t(slot.size());
                     for (size_t i = first; i < jobs_.size(); ++i) {
                         vdc_job& j = jobs_[i].j;
-                        j.flags |= VDC_JOB_ARGMAX;
+                        j.flags |= VDC_JOB_ARGMAX | (attr_int(n, "feedback", 0) ? VDC_JOB_FEEDBACK : 0);
                         j.b_t = storage(idx("head.amax"));
                         j.o2_t = storage(idx("next_token"));
                         j.arrive_ctr = ctr;
@@ -676,7 +676,7 @@ class RingLowering {
             if (slot_of.size() > 256) throw GeneratorError("node " + n.id + ": argmax slots exceed 256 SMs");
             for (size_t i = first_job; i < jobs_.size(); ++i) {
                 vdc_job& j = jobs_[i].j;
-                j.flags |= VDC_JOB_ARGMAX;
+                j.flags |= VDC_JOB_ARGMAX | (attr_int(n, "feedback", 0) ? VDC_JOB_FEEDBACK : 0);
                 j.b_t = storage(idx("head.amax"));
                 j.o2_t = storage(idx("next_token"));
                 j.req = slot_of[jobs_[i].sm];
