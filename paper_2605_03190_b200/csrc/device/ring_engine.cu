@@ -163,6 +163,17 @@ __device__ __forceinline__ uint2 qk_norm_rope4(uint2 u, uint2 wv, uint32_t lane,
     return make_uint2(pack2(y[0], y[1]), pack2(y[2], y[3]));
 }
 
+// TP exchange: this thread's output row rg for requests c0 .. c0 + nh - 1
+// into slot `off` of every rank's buffer (batched BGEMM epilogue)
+__device__ __noinline__ void sym_store_rows(char* const* bases, uint32_t world, int64_t off, int64_t M, int rg, int c0, int nb, int nh,
+                                            const float* v) {
+    for (uint32_t qr = 0; qr < world; ++qr) {
+        float* dst = reinterpret_cast<float*>(bases[qr] + VDC_SYM_HEADER_BYTES) + off;
+        for (int c = 0; c < nh; ++c)
+            if (c0 + c < nb) dst[int64_t(c0 + c) * M + rg] = v[c];
+    }
+}
+
 // BATCHED: the kernel instance for batched programs (BGEMM µops, paged
 // attention); single-request programs run the instance without those paths
 // so their register allocation and scheduling are unaffected
@@ -1061,13 +1072,12 @@ struct Vcc {
                 if (J.o3_t >= 0) u16p(J.o3_t)[int64_t(b) * M + rg] = f2bf(bf_lo(xo) * wn);
             }
         } else if (J.flags & VDC_JOB_SYM_OUT) {
-            // TP partial sums (fp32) -> slot tp_rank of every rank's exchange buffer (peer stores)
-            for (uint32_t qr = 0; qr < P->tp_world; ++qr) {
-                float* dst = reinterpret_cast<float*>(sym_base(J.o_t, qr) + VDC_SYM_HEADER_BYTES) + J.o_off;
+            // TP partial sums (fp32) -> slot tp_rank of every rank's exchange buffer
+            // (peer stores; out of line: keeps the other epilogues' registers)
+            float vs[NH];
 #pragma unroll
-                for (int c = 0; c < NH; ++c)
-                    if (c0 + c < nb) dst[int64_t(c0 + c) * M + rg] = v[c];
-            }
+            for (int c = 0; c < NH; ++c) vs[c] = v[c];
+            sym_store_rows(P->sym + size_t(J.o_t) * VDC_RING_MAX_TP, P->tp_world, J.o_off, M, rg, c0, nb, NH, vs);
         } else {
             const bool obf = tdtype(J.o_t) == VDC_DTYPE_BF16;
 #pragma unroll
