@@ -68,6 +68,11 @@ struct LayoutConfig {
     bool feedback = false;  // with argmax: token fed back + position advanced in the step block on the device
     int batch = 0;
     std::vector<int> req_pages;
+    // prefill chunk (ext, §8f rank 3): the `batch` rows are consecutive
+    // positions of ONE sequence (causal: row b attends to ctx_b = pos_b + 1)
+    // sharing one page allocation (req_pages all equal); one launch appends
+    // all their K/V rows and returns every row's logits
+    bool prefill = false;
 };
 
 ModelConfig llama3_8b();

@@ -68,6 +68,9 @@
 #define VDC_JOB_FEEDBACK 0x2000  /* with ARGMAX: the sampled token is fed back on the device: the step
                                    block's token becomes it and pos / ctx advance by one, so the
                                    next launch decodes the next position without the host */
+#define VDC_JOB_PREFILL 0x4000  /* batched ATTN of a prefill chunk: the batch's rows are consecutive
+                                   positions of one sequence sharing its pages; every row appended
+                                   in this launch (from request 0's position on) is patched in */
 #define VDC_JOB_BATCH 0x400     /* batched program (nb requests): per-request token / pos / ctx in
                                    the step block (3 int64 each), paged KV pools, page table at
                                    step[ptab + b * maxp + logical page] */

@@ -1300,7 +1300,29 @@ struct Vcc {
             if (ttr) P->tile_trace[3 * (gk + half) + 1] = now_ns();
             const uint32_t kb = ring + sk * SLOT + uint32_t(my_row0) * rowb, vb = ring + sv * SLOT + uint32_t(my_row0) * rowb;
             const int64_t prow0 = int64_t(J.r0 + int(i)) * PR + my_row0;  // global row of this warp's first row
-            const bool fresh = pos >= prow0 && pos < prow0 + rows_w;
+            if (batched && (J.flags & VDC_JOB_PREFILL)) {
+                // prefill chunk: every row appended in this launch (request 0's
+                // position .. this row's position) comes from global
+                const int64_t lo = max(prow0, P->step[1]), hi = min(prow0 + int64_t(rows_w), ctx);
+                for (int64_t rr = lo; rr < hi; ++rr) {
+                    const size_t crow =
+                        size_t(P->step[J.ptab + int64_t(J.req) * J.maxp + rr / PR]) * size_t(J.cache_rows) + size_t(rr % PR);
+                    const char* kn = tptr(J.a_t) + (size_t(J.a_off) + crow * HD) * EB;
+                    const char* vn = tptr(J.b_t) + (size_t(J.b_off) + crow * HD) * EB;
+                    for (int c = int(lane); c < 2 * NCH; c += 32) {
+                        const bool isk = c < NCH;
+                        const int cc = isk ? c : c - NCH;
+                        const uint4 v = ldcg128(reinterpret_cast<const uint4*>(isk ? kn : vn) + cc);
+                        const uint32_t dst = (isk ? kb : vb) + uint32_t(rr - prow0) * rowb + uint32_t(cc) * 16u;
+                        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(dst), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+                    }
+                }
+                if (lo < hi) {
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                }
+            }
+            const bool fresh = pos >= prow0 && pos < prow0 + rows_w && !(batched && (J.flags & VDC_JOB_PREFILL));
             if (fresh) {
                 // the appended row was produced in this launch (after the page's
                 // bulk copy may have been issued): patch it into the slots

@@ -104,6 +104,7 @@ decode::LayoutConfig layout_from(const json& j) {
     l.batch = j.value("batch", l.batch);
     l.argmax = j.value("argmax", l.argmax);
     l.feedback = j.value("feedback", l.feedback);
+    l.prefill = j.value("prefill", l.prefill);
     l.req_pages = j.value("req_pages", l.req_pages);
     return l;
 }

@@ -327,6 +327,12 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
         pool += p;
         jobs += (p + l.pages_per_job - 1) / l.pages_per_job;
     }
+    if (l.prefill) {  // one sequence: every row shares request 0's pages
+        for (int p : l.req_pages)
+            if (p != l.req_pages[0]) throw workload::WorkloadError("a prefill chunk's rows share one page allocation");
+        if (m.qk_norm) throw workload::WorkloadError("prefill chunks of QK-norm models are not supported");
+        pool = l.req_pages[0];
+    }
     if (pool > 4095) throw workload::WorkloadError("KV pool exceeds 4095 pages (12-bit tile coordinates)");
     Builder b{{}, m, l};
     auto sym = [&](const std::string& name) {  // exchange buffer: one (npad, d) fp32 slot per rank
@@ -375,6 +381,7 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
         std::map<std::string, std::string> qkv_attrs = {{"eps", eps}, {"theta", theta}, {"rope", "1"}, {"batch", bs}};
         std::map<std::string, std::string> attn_attrs = {{"pages_per_job", std::to_string(l.pages_per_job)}, {"batch", bs},
                                                          {"req_pages", rp}};
+        if (l.prefill) attn_attrs["prefill"] = "1";
         if (m.qk_norm) {
             b.norm(L + "q_norm", hd);
             b.norm(L + "k_norm", hd);

@@ -743,8 +743,10 @@ class RingLowering {
                 p0 = p1 == std::string::npos ? s.size() : p1 + 1;
             }
             int64_t next = 0;
+            const bool shared = attr_int(n, "prefill", 0) != 0;  // prefill chunk: one sequence's pages
             for (int64_t c : rp) {
                 pages_.emplace_back();
+                if (shared) next = 0;
                 for (int64_t i = 0; i < c; ++i) pages_.back().push_back(next++);
                 maxp_ = std::max<int32_t>(maxp_, int32_t(c));
             }
@@ -782,7 +784,7 @@ class RingLowering {
             r.head = int32_t(a.h);
             vdc_job& j = r.j;
             j = blank(Opcode::ATTN_DECODE);
-            j.flags = VDC_JOB_BATCH;
+            j.flags = VDC_JOB_BATCH | (attr_int(n, "prefill", 0) ? VDC_JOB_PREFILL : 0);
             j.r0 = int32_t(a.p0);
             j.r1 = int32_t(a.p1);
             j.k = int32_t(hd);

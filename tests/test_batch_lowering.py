@@ -137,3 +137,17 @@ def test_qk_norm_jobs():
     assert att and all(j["flags"] & 0x1000 for j in att)
     qkv = [j for j in info["jobs"] if j["op"] == BGEMM and (j["flags"] & 0x80)]
     assert qkv and all(j["flags"] & 0x1000 for j in qkv)
+
+
+def test_prefill_chunk_shares_pages():
+    info, text = build(bc.MID_MODEL, [3] * 10, 16, prefill=True)
+    assert text["certificate_ok"]
+    b = info["batch"]
+    pt = np.asarray(b["page_table"]).reshape(10, b["maxp"])
+    assert (pt == pt[0]).all() and list(pt[0]) == [0, 1, 2]
+    shapes = {d["name"]: d["shape"] for d in info["descriptors"]}
+    assert shapes["L0.kc"][0] == 3  # one sequence's pages
+    att = [j for j in info["jobs"] if j["op"] == ATTN]
+    assert att and all(j["flags"] & 0x4000 for j in att)
+    with pytest.raises(Exception):
+        build(bc.MID_MODEL, [3, 2], 16, prefill=True)  # rows of a chunk share one allocation
