@@ -22,7 +22,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, batched=False):
     import sys
     from pathlib import Path
     root = Path(__file__).resolve().parents[1]
@@ -33,7 +33,11 @@ def _worker(rank, world, port, q):
     try:
         import bench
         from paper_2605_03190_b200 import Program
-        req = bench.model_request(2)
+        if batched:  # batched decode (C4 / C5 shape), Qwen3 with QK-norm
+            import batch_cases as bc
+            req = bc.request({"preset": "qwen3-8b", "layers": 2, "vocab": 32768}, [3, 5, 2, 4, 1, 6, 2, 2], 4, None)
+        else:
+            req = bench.model_request(2)
         req["layout"]["tp_world"], req["layout"]["tp_rank"] = world, rank
         info = Program.build(req).info()
         sym = sorted((d["name"], tuple(d["shape"])) for d in info["descriptors"] if d.get("symmetric"))
@@ -53,11 +57,12 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_rank_tp_programs_agree():
+@pytest.mark.parametrize("batched", [False, True])
+def test_two_rank_tp_programs_agree(batched):
     world, port = 2, _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, batched)) for r in range(world)]
     for p in procs:
         p.start()
     got = [q.get(timeout=240) for _ in range(world)]
@@ -69,5 +74,9 @@ def test_two_rank_tp_programs_agree():
         r0, r1 = allv
         assert r0["sym"] == r1["sym"] and len(r0["sym"]) == 2 * 2  # o.part, d.part per layer
         assert r0["producers"] == r1["producers"]
-        assert r0["ar_need"] == r1["ar_need"] == [world * r0["producers"][0]]
-        assert r0["slots"] == [0] and r1["slots"] == [4096]  # each rank writes its own slot
+        slot = 4096 * (16 if batched else 1)  # (npad x d) fp32 per rank slot when batched
+        if not batched:
+            assert r0["ar_need"] == r1["ar_need"] == [world * r0["producers"][0]]
+        else:  # one publish per row block: d / 128 = 32 row blocks per producer
+            assert r0["ar_need"] == r1["ar_need"] == [world * 32]
+        assert r0["slots"] == [0] and r1["slots"] == [slot]  # each rank writes its own slot
