@@ -433,32 +433,48 @@ def c3_contexts(batch: int, lo: int = 128, hi: int = 8192, seed: int = 1) -> lis
     return [lo + next(g) % (hi - lo + 1) for _ in range(batch)]
 
 
-def run_batched(args):
+def run_batched(args, rank: int = 0, world: int = 1, local_rank: int = 0):
+    """C3 (1 GPU) / C4-C5 shaped (tensor parallel under torchrun) batched decode"""
     import torch
     from paper_2605_03190_b200 import Program
     from paper_2605_03190_b200.engine import Engine
 
+    torch.cuda.set_device(local_rank)
+    tp = world > 1
     B = args.batch
-    ctxs = c3_contexts(B)
+    if args.ctx_fixed:
+        ctxs = [args.ctx_fixed] * B
+    else:
+        ctxs = c3_contexts(B)
     pages = [(c + 63) // 64 for c in ctxs]
     t_build = time.time()
-    req = {"engine": "ring", "model": {"preset": "llama3-8b", "layers": args.layers},
+    req = {"engine": "ring", "model": {"preset": args.model, "layers": args.layers},
            "layout": {"batch": B, "req_pages": pages, "pages_per_job": args.pages_per_job, "gu_block": 128, "page_rows": 64,
-                      "argmax": True},
+                      "argmax": not tp},
            "profile": {"builtin": "b200"}}
+    if tp:
+        req["layout"]["tp_world"], req["layout"]["tp_rank"] = world, rank
     prog = Program.build(req)
     build_s = time.time() - t_build
-    eng = Engine(prog, watchdog_ms=20000)
+    eng = Engine(prog, device=local_rank, watchdog_ms=20000)
     tens = init_tensors(eng)
+    keep_sym = bind_symmetric_tp(eng, world, rank, local_rank) if tp else None
     info = eng.info
     bi = info["batch"]
     st_host = [0] * int(info["step_scalars"])
     for b in range(B):
         st_host[3 * b: 3 * b + 3] = [17 + b, ctxs[b] - 1, ctxs[b]]
     st_host[bi["page_table_off"]: bi["page_table_off"] + len(bi["page_table"])] = bi["page_table"]
-    step = torch.tensor(st_host, dtype=torch.int64, device="cuda")
+    step = torch.tensor(st_host, dtype=torch.int64, device=f"cuda:{local_rank}")
     eng.bind_step(step)
-    stream = torch.cuda.Stream()
+    stream = torch.cuda.Stream(device=local_rank)
+
+    def barrier():
+        if tp:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
     # algorithmic bytes: bf16 weights once + one embedding row per request + each
     # request's K/V rows over its context + the appended rows
     w = kvr = kvw = 0
@@ -485,11 +501,11 @@ def run_batched(args):
         rep = eng.wait()
     if not rep.completed:
         raise SystemExit(f"engine did not complete: {rep.message} stalled={rep.stalled}")
-    sampler = ClockSampler(0)
+    sampler = ClockSampler(local_rank)
     sampler.start()
     time.sleep(0.3)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    torch.cuda.synchronize()
+    barrier()
     w0 = time.time()
     with torch.cuda.stream(stream):
         ev[0].record(stream)
@@ -504,43 +520,66 @@ def run_batched(args):
 
     # e2e: per step the request triples (token, pos, ctx) go H2D from pinned
     # memory, the engine runs (greedy sampling fused into the lm_head GEMM)
-    # and the B sampled tokens come back D2H
+    # and the B sampled tokens come back D2H; under TP the vocab-parallel
+    # logit shards are gathered and every rank picks the same tokens
     logits = tens["logits"]
-    next_tok = tens["next_token"]
+    next_tok = tens.get("next_token")
     h_trip = torch.tensor(st_host[: 3 * B], dtype=torch.int64).pin_memory()
     h_tok = torch.zeros(B, dtype=torch.int64).pin_memory()
+    gathered = torch.empty(world * logits.numel(), dtype=torch.float32, device=f"cuda:{local_rank}") if tp else None
+    h_logits = torch.empty(world * logits.numel(), dtype=torch.float32).pin_memory() if tp else None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
+    barrier()
     w2 = time.time()
     with torch.cuda.stream(stream):
         e0.record(stream)
         for k in range(args.steps):
             step[: 3 * B].copy_(h_trip, non_blocking=True)
             eng.launch(stream)
-            h_tok.copy_(next_tok.view(-1), non_blocking=True)
-            stream.synchronize()
-            h_trip.view(B, 3)[:, 0] = h_tok
+            if tp:
+                import torch.distributed as dist
+                dist.all_gather_into_tensor(gathered, logits)
+                h_logits.copy_(gathered, non_blocking=True)
+                stream.synchronize()
+                lg = h_logits.view(world, B, -1).permute(1, 0, 2).reshape(B, -1)
+                h_trip.view(B, 3)[:, 0] = torch.argmax(lg, dim=1)
+            else:
+                h_tok.copy_(next_tok.view(-1), non_blocking=True)
+                stream.synchronize()
+                h_trip.view(B, 3)[:, 0] = h_tok
         e1.record(stream)
     stream.synchronize()
     sampler.mark(w2, time.time())
     e2e_ms = e0.elapsed_time(e1)
     clocks = sampler.stop()
+    if tp:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms, e2e_ms], device=f"cuda:{local_rank}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, e2e_ms = float(t[0]), float(t[1])
+    del keep_sym
     value = B * args.steps / (total_ms / 1e3)
     peak, peak_src = measured_peak()
     achieved = nbytes["total"] / (sum(per) / len(per) / 1e3) / 1e9
+    name = {"llama3-8b": "Llama-3-8B", "qwen3-8b": "Qwen3-8B", "llama3-70b": "Llama-3-70B"}.get(args.model, args.model)
+    cfg_name = "C3" if (args.model == "llama3-8b" and not tp) else "C4" if args.model == "qwen3-8b" else "C5" if args.model == "llama3-70b" else "batched"
     return {
-        "metric": "Llama-3-8B bf16 batched decode tokens/s (C3: batch %d, paged KV) + HBM GB/s fraction of peak" % B,
-        "value": round(value, 2), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "metric": f"{name} bf16 batched decode tokens/s ({cfg_name}: batch {B}, paged KV) + HBM GB/s fraction of peak",
+        "value": round(value, 2), "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "strong" if tp else "weak",
+        "vs_baseline": None,
         "dtype": "bf16",
-        "data": "synthetic: random-init Llama-3-8B weights, random bf16 KV pages, contexts splitmix64(seed 1) -> U[128, 8192]",
-        "config": {"workload": f"C3 Llama-3-8B bf16 decode, batch {B}, per-request contexts U[128,8192] (sum {sum(ctxs)}), "
+        "data": f"synthetic: random-init {name} weights, random bf16 KV pages, contexts "
+                + (f"fixed {args.ctx_fixed}" if args.ctx_fixed else "splitmix64(seed 1) -> U[128, 8192]"),
+        "config": {"workload": f"{cfg_name} {name} bf16 decode, batch {B}, per-request contexts (sum {sum(ctxs)}), "
                                f"paged KV (64-row pages, {sum(pages)} pages), {layers} layers + lm_head",
-                   "model": "llama3-8b", "batch": B, "contexts": ctxs, "parallelism": "1 GPU",
+                   "model": args.model, "batch": B, "contexts": ctxs,
+                   "parallelism": f"tp{world} (Megatron split, in-kernel NVLink allreduce)" if tp else "1 GPU",
                    "l2": "inputs larger than L2 (algorithmic %.2f GB per step vs 126 MB L2)" % (nbytes["total"] / 1e9),
                    "program_uops": info["total_uops"], "build_seconds": round(build_s, 2)},
         "e2e": {"value": round(B * args.steps / (e2e_ms / 1e3), 2), "unit": "tokens/s", "h2d_bytes_per_step": 3 * B * 8,
-                "d2h_bytes_per_step": B * 8, "sampling": "greedy argmax fused into the lm_head GEMM (device)"},
+                "d2h_bytes_per_step": world * logits.numel() * 4 if tp else B * 8,
+                "sampling": "host argmax over the gathered vocab shards" if tp else "greedy argmax fused into the lm_head GEMM (device)"},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
@@ -565,6 +604,9 @@ def main():
     ap.add_argument("--ring-slots", type=int, default=12)
     ap.add_argument("--pages-per-job", type=int, default=None,
                     help="split-KV granularity (default 4 at batch 1, 64 for batched decode)")
+    ap.add_argument("--model", default="llama3-8b", choices=["llama3-8b", "qwen3-8b", "llama3-70b"],
+                    help="batched decode: model preset (C3 llama3-8b, C4 qwen3-8b, C5 llama3-70b)")
+    ap.add_argument("--ctx-fixed", type=int, default=0, help="batched decode: every request at this context (C4 4096, C5 8192)")
     ap.add_argument("--batch", type=int, default=1,
                     help="> 1: C3 batched decode (per-request contexts, paged KV, BGEMM on tcgen05); 1 GPU")
     ap.add_argument("--parallel", default="tp", choices=["tp", "replicas"],
@@ -596,8 +638,17 @@ def main():
     if args.pages_per_job is None:
         args.pages_per_job = 64 if args.batch > 1 else 4
     if args.batch > 1:
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        res = run_batched(args, rank, world, local_rank)
         if rank == 0:
-            print(json.dumps(run_batched(args)))
+            print(json.dumps(res))
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
         return
     if world > 1:
         import torch
