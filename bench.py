@@ -448,7 +448,10 @@ def run_batched(args, rank: int = 0, world: int = 1, local_rank: int = 0):
         ctxs = c3_contexts(B)
     pages = [(c + 63) // 64 for c in ctxs]
     t_build = time.time()
-    req = {"engine": "ring", "model": {"preset": args.model, "layers": args.layers},
+    model = {"preset": args.model, "layers": args.layers}
+    if args.no_qk_norm:  # ablation: the same shapes without Qwen3's QK-norm
+        model["qk_norm"] = False
+    req = {"engine": "ring", "model": model,
            "layout": {"batch": B, "req_pages": pages, "pages_per_job": args.pages_per_job, "gu_block": 128, "page_rows": 64,
                       "argmax": not tp},
            "profile": {"builtin": "b200"}}
@@ -606,6 +609,7 @@ def main():
                     help="split-KV granularity (default 4 at batch 1, 64 for batched decode)")
     ap.add_argument("--model", default="llama3-8b", choices=["llama3-8b", "qwen3-8b", "llama3-70b"],
                     help="batched decode: model preset (C3 llama3-8b, C4 qwen3-8b, C5 llama3-70b)")
+    ap.add_argument("--no-qk-norm", action="store_true", help="ablation: Qwen3 shapes without QK-norm")
     ap.add_argument("--ctx-fixed", type=int, default=0, help="batched decode: every request at this context (C4 4096, C5 8192)")
     ap.add_argument("--batch", type=int, default=1,
                     help="> 1: C3 batched decode (per-request contexts, paged KV, BGEMM on tcgen05); 1 GPU")

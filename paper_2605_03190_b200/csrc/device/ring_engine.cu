@@ -142,9 +142,9 @@ __device__ __forceinline__ float dot16(uint4 a, uint4 b) {
 
 // Qwen3 QK-norm on one 128-dim head held 4 dims per lane (bf16x4 in u):
 // x = bf16(x * rsqrt(mean(x^2) + eps) * w), then the interleaved-pair rotary
-// at `pos` (double-precision angles), rounded to bf16. Not inlined: its
+// from the job's rotary table (double-precision angles), rounded to bf16. Not inlined: its
 // double-precision registers stay out of the kernel's allocation.
-__device__ __forceinline__ uint2 qk_norm_rope4(uint2 u, uint2 wv, uint32_t lane, int head_dim, float eps, float theta, int64_t pos) {
+__device__ __forceinline__ uint2 qk_norm_rope4(uint2 u, uint2 wv, int head_dim, float eps, float2 cs0, float2 cs1) {
     float x[4] = {bf_lo(u.x), bf_hi(u.x), bf_lo(u.y), bf_hi(u.y)};
     const float wgt[4] = {bf_lo(wv.x), bf_hi(wv.x), bf_lo(wv.y), bf_hi(wv.y)};
     const float ss = warp_sum(x[0] * x[0] + x[1] * x[1] + x[2] * x[2] + x[3] * x[3]);
@@ -152,14 +152,11 @@ __device__ __forceinline__ uint2 qk_norm_rope4(uint2 u, uint2 wv, uint32_t lane,
 #pragma unroll
     for (int e = 0; e < 4; ++e) x[e] = bf_lo(uint32_t(f2bf(x[e] * inv * wgt[e])));
     float y[4];
-#pragma unroll
-    for (int p2 = 0; p2 < 2; ++p2) {
-        const int d = int(lane) * 4 + 2 * p2;
-        const double ang = double(pos) * pow(double(theta), -double(d) / double(head_dim));
-        const float cs = float(cos(ang)), sn = float(sin(ang));
-        y[2 * p2] = x[2 * p2] * cs - x[2 * p2 + 1] * sn;
-        y[2 * p2 + 1] = x[2 * p2] * sn + x[2 * p2 + 1] * cs;
-    }
+    // rotary table entries (cos, sin) of the lane's two dim pairs
+    y[0] = x[0] * cs0.x - x[1] * cs0.y;
+    y[1] = x[0] * cs0.y + x[1] * cs0.x;
+    y[2] = x[2] * cs1.x - x[3] * cs1.y;
+    y[3] = x[2] * cs1.y + x[3] * cs1.x;
     return make_uint2(pack2(y[0], y[1]), pack2(y[2], y[3]));
 }
 
@@ -1245,10 +1242,20 @@ struct Vcc {
             const uint4* qb = reinterpret_cast<const uint4*>(tptr(J.x_t) + size_t(J.x_off) * EB);
             uint4* qd = S->x;
             if constexpr (BF && DPL == 4 && QKN) {  // Qwen3: per-head RMSNorm of q, then the rotary (warp per head)
+                // rotary table of this job's position (q and the appended k row share it)
+                for (int d2 = int(ct); d2 < HD / 2; d2 += NCT) {
+                    const double ang = double(pos) * pow(double(J.theta), -double(2 * d2) / double(HD));
+                    S->rope_cs[d2] = float(cos(ang));
+                    S->rope_sn[d2] = float(sin(ang));
+                }
+                rope_hd = 0;  // the GEMV's cached table is overwritten
+                sync();
+                const float2 cs0 = make_float2(S->rope_cs[2 * lane], S->rope_sn[2 * lane]);
+                const float2 cs1 = make_float2(S->rope_cs[2 * lane + 1], S->rope_sn[2 * lane + 1]);
                 const uint2 wv = *reinterpret_cast<const uint2*>(tptr(J.out_row0) + lane * 8);
                 for (int h = int(w); h < G; h += CW) {
                     const uint2 u = ldcg64(reinterpret_cast<const char*>(qb) + h * HD * 2 + lane * 8);
-                    const uint2 o = qk_norm_rope4(u, wv, lane, J.head_dim, J.eps, J.theta, pos);
+                    const uint2 o = qk_norm_rope4(u, wv, J.head_dim, J.eps, cs0, cs1);
                     // lane's dims 4 lane .. 4 lane + 3 = chunk lane / 2, half lane % 2
                     qd[(h * 2 + int(lane & 1u)) * NCH + int(lane >> 1)] =
                         make_uint4(__float_as_uint(bf_lo(o.x)), __float_as_uint(bf_hi(o.x)), __float_as_uint(bf_lo(o.y)),
@@ -1338,7 +1345,8 @@ struct Vcc {
                 if constexpr (qkn) {  // QK-norm + rotary of the appended k row, written back to the cache
                     const uint2 u = ldcg64(kn + lane * 8);
                     const uint2 wv = *reinterpret_cast<const uint2*>(tptr(J.block) + lane * 8);
-                    const uint2 o = qk_norm_rope4(u, wv, lane, J.head_dim, J.eps, J.theta, pos);
+                    const uint2 o = qk_norm_rope4(u, wv, J.head_dim, J.eps, make_float2(S->rope_cs[2 * lane], S->rope_sn[2 * lane]),
+                                                  make_float2(S->rope_cs[2 * lane + 1], S->rope_sn[2 * lane + 1]));
                     *reinterpret_cast<uint2*>(const_cast<char*>(kn) + lane * 8) = o;
                     asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(kb + uint32_t(r) * rowb + lane * 8u), "r"(o.x), "r"(o.y) : "memory");
                 }
@@ -1702,7 +1710,7 @@ struct Vcc {
 };
 
 template <bool BATCHED, bool QKNORM>
-__device__ void vcc_role(const RingParams& P, Shared& S, char* ring) {
+__device__ __forceinline__ void vcc_role(const RingParams& P, Shared& S, char* ring) {
     Vcc<BATCHED, QKNORM> v;
     v.P = &P;
     v.S = &S;
@@ -1759,6 +1767,11 @@ __device__ void vcc_role(const RingParams& P, Shared& S, char* ring) {
                 if constexpr (QKNORM) {  // Qwen3 programs run their own kernel instance
                     VDC_ATTN_QKN_CASE(4)
                     VDC_ATTN_QKN_CASE(8)
+                }
+                if (J.flags & VDC_JOB_QKNORM) {  // QK-norm geometry without an instance: fail loudly
+                    if (v.ct == 0) v.fire(6, (core << 16) | pc);
+                    v.ok = false;
+                    break;
                 }
 #undef VDC_ATTN_QKN_CASE
                 VDC_ATTN_CASE(true, 4, 4)
