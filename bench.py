@@ -325,6 +325,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     h_logits = torch.empty(n_logits, dtype=torch.float32).pin_memory()
     gathered = torch.empty(n_logits, dtype=torch.float32, device=f"cuda:{local_rank}") if tp else None
     next_tok = tens.get("next_token")
+    vocab = [d["shape"][0] for d in info["descriptors"] if d["name"] == "embed.table"][0]
     h_tok = torch.zeros(1, dtype=torch.int64).pin_memory()
     token = 17
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -527,6 +528,7 @@ def run_batched(args, rank: int = 0, world: int = 1, local_rank: int = 0):
     # logit shards are gathered and every rank picks the same tokens
     logits = tens["logits"]
     next_tok = tens.get("next_token")
+    vocab = [d["shape"][0] for d in info["descriptors"] if d["name"] == "embed.table"][0]
     h_trip = torch.tensor(st_host[: 3 * B], dtype=torch.int64).pin_memory()
     h_tok = torch.zeros(B, dtype=torch.int64).pin_memory()
     gathered = torch.empty(world * logits.numel(), dtype=torch.float32, device=f"cuda:{local_rank}") if tp else None
@@ -544,7 +546,7 @@ def run_batched(args, rank: int = 0, world: int = 1, local_rank: int = 0):
                 dist.all_gather_into_tensor(gathered, logits)
                 h_logits.copy_(gathered, non_blocking=True)
                 stream.synchronize()
-                lg = h_logits.view(world, B, -1).permute(1, 0, 2).reshape(B, -1)
+                lg = h_logits.view(world, B, -1).permute(1, 0, 2).reshape(B, -1)[:, :vocab]  # drop the shards' padding
                 h_trip.view(B, 3)[:, 0] = torch.argmax(lg, dim=1)
             else:
                 h_tok.copy_(next_tok.view(-1), non_blocking=True)

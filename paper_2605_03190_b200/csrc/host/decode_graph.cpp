@@ -313,11 +313,16 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
     // vocab-parallel lm_head
     const bool tp = l.tp_world >= 1;
     const int64_t W = tp ? l.tp_world : 1;
-    if (tp && (l.tp_rank < 0 || l.tp_rank >= W || m.kv_heads % W || m.ffn % (W * 64) || m.vocab % (W * 128)))
-        throw workload::WorkloadError("tensor parallelism needs kv_heads, ffn / 64 and vocab / 128 divisible by tp_world");
+    if (tp && (l.tp_rank < 0 || l.tp_rank >= W || m.kv_heads % W || m.ffn % (W * 64)))
+        throw workload::WorkloadError("tensor parallelism needs kv_heads and ffn / 64 divisible by tp_world");
     const int64_t d = m.hidden, hd = m.head_dim, hq = m.heads / W, hkv = m.kv_heads / W, grp = hq / hkv;
-    const int64_t qrows = hq * hd, kvrows = hkv * hd, ffn = m.ffn / W, vocab = m.vocab / W;
-    if (d % 128 || qrows % 128 || kvrows % 128 || ffn % 64 || vocab % 128 || hq % hkv)
+    // vocab shard per rank: ceil(vocab / W) rounded up to whole 128-row MMA
+    // blocks; rank r holds vocabulary rows [r * shard, (r + 1) * shard), rows
+    // past the vocabulary are zero padding (their logits are not tokens:
+    // sampling and callers use the first `vocab` columns of the gathered logits)
+    const int64_t vocab = ((m.vocab + W - 1) / W + 127) / 128 * 128;
+    const int64_t qrows = hq * hd, kvrows = hkv * hd, ffn = m.ffn / W;
+    if (d % 128 || qrows % 128 || kvrows % 128 || ffn % 64 || hq % hkv)
         throw workload::WorkloadError("batched decode needs 128-row aligned projections");
     const std::map<std::string, std::string> tp_attrs = {{"tp_world", std::to_string(W)}, {"tp_rank", std::to_string(l.tp_rank)}};
 
@@ -426,6 +431,7 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
     wgt("lm_head", vocab, d, double(d));  // vocab-parallel: this rank's logit columns
     b.add("logits", {B, vocab}, 1, vocab, InitKind::zeros, ElemType::f32);
     std::map<std::string, std::string> head_attrs = {{"eps", eps}, {"batch", bs}};
+    if (!tp && vocab != m.vocab) throw workload::WorkloadError("batched decode needs the vocabulary in whole 128-row blocks");
     if (l.argmax && !tp) {  // greedy sampling fused into the lm_head GEMM: per-SM slots, tokens per request
         b.add("head.amax", {256 * N, 2}, N, 2, InitKind::zeros, ElemType::f32);
         b.add("next_token", {B, 1}, 1, 1, InitKind::zeros, ElemType::i64);

@@ -22,7 +22,10 @@ def assemble(infos, ins, cfg):
     qr, kvr = cfg["heads"] // W * hd, cfg["kv_heads"] // W * hd
     shapes = {x["name"]: x["shape"] for x in infos[0]["descriptors"]}
     full = {k: v for k, v in ins[0].items() if not k.startswith("L") or k.endswith("norm")}
-    full["lm_head"] = np.concatenate([x["lm_head"].reshape(-1, d) for x in ins]).reshape(-1)
+    # vocab shards are padded to whole 128-row blocks: the first `vocab` rows of
+    # the concatenation are the vocabulary (in rank order)
+    vocab = ins[0]["embed.table"].size // d
+    full["lm_head"] = np.concatenate([x["lm_head"].reshape(-1, d) for x in ins])[:vocab].reshape(-1)
     for l in range(cfg["layers"]):
         L = f"L{l}."
         wq = [x[L + "wqkv"].reshape(-1, d) for x in ins]
@@ -91,7 +94,8 @@ def run_tp(model, req_pages, steps, world):
         full_state = assemble(infos, state, cfg)
         full_host = assemble(infos, host, cfg)
         nb = len(req_pages)
-        full_host["logits"] = np.concatenate([h["logits"].reshape(nb, -1) for h in host], axis=1).reshape(-1)
+        vocab = ins[0]["embed.table"].size // cfg["hidden"]
+        full_host["logits"] = np.concatenate([h["logits"].reshape(nb, -1) for h in host], axis=1)[:, :vocab].reshape(-1)
         out.append(bc.check_batch(infos[0], full_state, full_host, tokens, pos, cfg=cfg))
         state = host
     return out
@@ -117,4 +121,17 @@ def test_qwen3_layer_batch8_tp4(cuda):
     pos = [int(rng.integers(0, 64 * p)) for p in pages]
     tokens = [int(t) for t in rng.integers(0, 32768, 8)]
     for rs in run_tp(model, pages, [(tokens, pos)], 4):
+        tb.assert_close(rs)
+
+
+def test_mid_batch4_tp2_padded_vocab(cuda):
+    """a vocabulary that does not split into whole 128-row blocks per rank
+    (4000 / 2 = 2000 -> 2048-row shards, zero-padded): logits past the
+    vocabulary are dropped (Llama-3 128256 / 8 and Qwen3 151936 / 4 shards)"""
+    model = dict(bc.MID_MODEL, vocab=4000)
+    rng = np.random.default_rng(9)
+    pages = [2, 3, 1, 2]
+    pos = [int(rng.integers(0, 64 * p)) for p in pages]
+    tokens = [int(t) for t in rng.integers(0, 4000, 4)]
+    for rs in run_tp(model, pages, [(tokens, pos)], 2):
         tb.assert_close(rs)
