@@ -514,15 +514,16 @@ class RingLowering {
         npad_ = decode::batch_npad(nb_);
         pad_t_ = idx("ring.pad");
         switch (n.kind) {
-            case OpKind::EMBED_ROW: {
+            case OpKind::EMBED_ROW:  // one job per request, spread over the SMs
+                for (int32_t rq = 0; rq < nb_; ++rq) {
                 RJob r;
                 r.ordinal = ordinal;
-                r.sm = 0;
+                r.sm = uint32_t(rq) % sms_;
                 vdc_job& j = r.j;
                 j = blank(Opcode::ELEMWISE);
                 j.flags = VDC_JOB_BATCH;
-                j.r0 = 0;
-                j.r1 = nb_;
+                j.r0 = rq;
+                j.r1 = rq + 1;
                 j.nb = nb_;
                 j.npad = npad_;
                 j.x_t = storage(idx(n.inputs[0]));
@@ -532,8 +533,8 @@ class RingLowering {
                 j.o3_t = storage(idx(n.outputs[1]));
                 r.publishes = {j.o_t, j.o3_t};
                 jobs_.push_back(std::move(r));
+                }
                 break;
-            }
             case OpKind::RMS_GEMV:
             case OpKind::GEMV_ADD:
             case OpKind::GEMV:
