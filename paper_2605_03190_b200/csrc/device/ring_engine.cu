@@ -1032,7 +1032,12 @@ struct Vcc {
                     u16p(J.o_t)[int64_t(b) * qrows + rg] = f2bf(v[c]);
                 } else {
                     const int64_t page = P->step[J.ptab + int64_t(b) * J.maxp + pos / 64];
-                    const int64_t at = ((page * hkv + lr / hd) * 64 + pos % 64) * hd + d;
+                    // K rows are stored pre-swizzled: 16-byte chunk ch of page row r at
+                    // (ch & 8) | ((ch & 7) ^ (r & 7)) (attention reads them
+                    // conflict-free with q broadcast); V rows stay row-major
+                    const int ch = d >> 3, r7 = int(pos & 7);
+                    const int dk = isk ? ((((ch & 8) | ((ch & 7) ^ r7)) << 3) | (d & 7)) : d;
+                    const int64_t at = ((page * hkv + lr / hd) * 64 + pos % 64) * hd + dk;
                     u16p(isk ? J.b_t : J.o2_t)[at] = f2bf(v[c]);
                 }
             }
@@ -1343,10 +1348,14 @@ struct Vcc {
                 const char* vn = tptr(J.b_t) + (size_t(J.b_off) + crow * HD) * EB;
                 constexpr bool qkn = BF && DPL == 4 && QKN;
                 if constexpr (qkn) {  // QK-norm + rotary of the appended k row, written back to the cache
+                    // the lane's 4 stored dims; batched pools hold K rows swizzled
+                    const int pc = int(lane >> 1);
+                    const int lc = batched ? ((pc & 8) | ((pc & 7) ^ int(pos & 7))) : pc;
+                    const int dbase = lc * 8 + int(lane & 1u) * 4;
                     const uint2 u = ldcg64(kn + lane * 8);
-                    const uint2 wv = *reinterpret_cast<const uint2*>(tptr(J.block) + lane * 8);
-                    const uint2 o = qk_norm_rope4(u, wv, J.head_dim, J.eps, make_float2(S->rope_cs[2 * lane], S->rope_sn[2 * lane]),
-                                                  make_float2(S->rope_cs[2 * lane + 1], S->rope_sn[2 * lane + 1]));
+                    const uint2 wv = *reinterpret_cast<const uint2*>(tptr(J.block) + dbase * 2);
+                    const uint2 o = qk_norm_rope4(u, wv, J.head_dim, J.eps, make_float2(S->rope_cs[dbase / 2], S->rope_sn[dbase / 2]),
+                                                  make_float2(S->rope_cs[dbase / 2 + 1], S->rope_sn[dbase / 2 + 1]));
                     *reinterpret_cast<uint2*>(const_cast<char*>(kn) + lane * 8) = o;
                     asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(kb + uint32_t(r) * rowb + lane * 8u), "r"(o.x), "r"(o.y) : "memory");
                 }
@@ -1374,8 +1383,12 @@ struct Vcc {
                     for (int h = 0; h < G; ++h) acc[h] = make_float2(0.f, 0.f);
 #pragma unroll 4
                     for (int c = 0; c < NCH; ++c) {
-                        const int cc = (c + int(lane)) & (NCH - 1);
-                        const uint4 kv = lds128(krow + uint32_t(cc) * 16u);
+                        // single-request caches: chunk order rotated per lane; batched
+                        // pools: K rows pre-swizzled, so every lane reads logical chunk c
+                        // (q loads are broadcasts) from its row's physical chunk
+                        const int cc = batched ? c : (c + int(lane)) & (NCH - 1);
+                        const int kc = batched ? ((c & 8) | ((c & 7) ^ int(lane & 7u))) : cc;
+                        const uint4 kv = lds128(krow + uint32_t(kc) * 16u);
                         const float2 k01 = make_float2(bf_lo(kv.x), bf_hi(kv.x)), k23 = make_float2(bf_lo(kv.y), bf_hi(kv.y));
                         const float2 k45 = make_float2(bf_lo(kv.z), bf_hi(kv.z)), k67 = make_float2(bf_lo(kv.w), bf_hi(kv.w));
 #pragma unroll
