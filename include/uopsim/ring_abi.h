@@ -92,6 +92,13 @@
  * bulk copy per ring tile (row-major 128 x 64 boxes would be 128 separate
  * 128-byte DRAM bursts per tile, ~half the HBM rate). */
 #define VDC_DESC_PACKED_SW128 0x80000000u
+/* vdc_desc.tma value of a batched K page pool (pages, hkv * 64, hd): each
+ * page row's 16-byte chunks are stored swizzled, logical chunk c of page row
+ * r at chunk (c & 8) | ((c & 7) ^ (r & 7)) (written that way by the qkv
+ * epilogue; the attention score loop reads them conflict-free). Hosts that
+ * import or export row-major K caches apply / undo this permutation
+ * (engine.py swizzle_k / unswizzle_k). */
+#define VDC_DESC_KPAGE_SWZ 0x40000000u
 #define VDC_RING_BGEMM_KT 64     /* reduction columns per weight tile (128-byte swizzle atom) */
 #define VDC_RING_MAX_BATCH 64
 

@@ -157,6 +157,15 @@ int vdc_program_cores(const vdc_program* prog, uint32_t* n_cores, uint32_t* sm_c
 int vdc_program_words(const vdc_program* prog, uint32_t core, const uint8_t** words, uint32_t* n_words);
 int vdc_program_load(vdc_ctx* ctx, const vdc_program* prog);
 void vdc_free_string(char* s);
+/* a26 input synthesis on the device (reference workload.cpp:411-435
+ * synthesize_inputs, util.hpp:15-33 splitmix64/unit_float): fills dptr
+ * (`bytes` = the descriptor's element count x its element size) with tensor
+ * `tensor`'s synthetic contents, stream state = seed ^ fnv1a(name), element i
+ * of the logical row-major tensor = the reference stream's draw i, written
+ * in the tensor's device storage order (packed / swizzled layouts applied).
+ * Non-external tensors are zero-filled, like the reference. Asynchronous on
+ * `stream` (a cudaStream_t). */
+int vdc_program_synthesize(const vdc_program* prog, uint16_t tensor, uint64_t seed, void* dptr, size_t bytes, void* stream);
 
 #ifdef __cplusplus
 }

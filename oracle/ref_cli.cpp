@@ -11,6 +11,7 @@
 //                  default = the full generate() pipeline, elaborate.cpp:492-520) }
 // Output (stdout): JSON {ok, error, tilings, streams:{core:text}, sidecar, words:{core:hex},
 //                        makespan_estimate, certificate_ok}
+#include <cstring>
 #include <iostream>
 #include <iterator>
 #include <sstream>
@@ -55,6 +56,29 @@ int main() {
     try {
         auto req = ordered_json::parse(text);
         auto g = workload::parse_workload(req.at("workload").dump());
+        if (req.contains("synthesize")) {
+            // golden vectors of the reference synthesize_inputs (workload.cpp:411-435):
+            // per tensor the first `head` values' fp32 bits and an FNV-1a of all bits
+            const auto& sj = req.at("synthesize");
+            const size_t head = sj.value("head", size_t(16));
+            auto arrays = workload::synthesize_inputs(g, sj.value("seed", 0ull));
+            ordered_json ts = ordered_json::array();
+            for (auto& [name, v] : arrays) {
+                uint64_t h = 0xcbf29ce484222325ULL;
+                ordered_json first = ordered_json::array();
+                for (size_t i = 0; i < v.size(); ++i) {
+                    uint32_t u;
+                    std::memcpy(&u, &v[i], 4);
+                    for (int k = 0; k < 4; ++k) h = (h ^ ((u >> (8 * k)) & 0xff)) * 0x100000001b3ULL;
+                    if (i < head) first.push_back(u);
+                }
+                ts.push_back({{"name", name}, {"n", v.size()}, {"head_bits", first}, {"fnv1a_bits", std::to_string(h)}});
+            }
+            out["synthesized"] = ts;
+            out["ok"] = true;
+            std::cout << out.dump() << "\n";
+            return 0;
+        }
         auto hw = profile_from(req.value("profile", ordered_json{{"builtin", "h100"}}));
         generator::GenOptions opt;
         auto jo = req.value("options", ordered_json::object());

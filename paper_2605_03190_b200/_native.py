@@ -72,7 +72,7 @@ EXPORTS = [
     "vdc_last_error", "vdc_version", "vdc_create", "vdc_destroy", "vdc_load_program", "vdc_load_jobs", "vdc_set_params",
     "vdc_bind_tensor", "vdc_bind_symmetric", "vdc_bind_step", "vdc_bind_trace", "vdc_launch", "vdc_wait", "vdc_set_watchdog", "vdc_set_prefetch", "vdc_program_build",
     "vdc_program_parse", "vdc_program_free", "vdc_program_text", "vdc_program_cores", "vdc_program_words",
-    "vdc_program_load", "vdc_free_string",
+    "vdc_program_load", "vdc_free_string", "vdc_program_synthesize",
 ]
 
 _lib = None
@@ -112,6 +112,7 @@ def lib() -> ctypes.CDLL:
         "vdc_program_words": ([vp, c.c_uint32, c.POINTER(c.c_void_p), c.POINTER(c.c_uint32)], c.c_int),
         "vdc_program_load": ([vp, vp], c.c_int),
         "vdc_free_string": ([c.c_void_p], None),
+        "vdc_program_synthesize": ([vp, c.c_uint16, c.c_uint64, vp, c.c_size_t, vp], c.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -1852,7 +1852,9 @@ struct vdc_ctx {
     char** d_sym = nullptr;
     bool sym_dirty = false;
     uint32_t tp_rank = 0, tp_world = 1;
-    unsigned long long* d_tile_trace = nullptr;
+    unsigned long long* d_tile_trace = nullptr;  // debug tile trace (VDC_RING_DEBUG bit 1), owned
+    uint32_t debug = 0;                          // VDC_RING_DEBUG, read once at vdc_create
+    bool tp_poisoned = false;                    // a TP launch aborted: symmetric headers must be re-bound
     bool ring_attr_set = false;
     // batched ring programs: TMA tensor maps of the descriptors with vdc_desc.tma > 0
     std::vector<CUtensorMap> tmaps_host;  // one per descriptor (only vdc_desc.tma > 0 are encoded)
@@ -1896,6 +1898,7 @@ int vdc_create(const vdc_profile* p, int device, vdc_ctx** out) {
     if (prop.major < 10) return fail(VDC_ERR_INPUT, "device is not sm_100 class (B200 required)");
     auto ctx = new vdc_ctx;
     ctx->prof = *p;
+    if (const char* dbg = getenv("VDC_RING_DEBUG")) ctx->debug = uint32_t(atoi(dbg));
     ctx->device = device;
     ctx->num_sms = prop.multiProcessorCount;
     if (p->sm_count < 1 || int(p->sm_count) > prop.multiProcessorCount) {
@@ -1939,6 +1942,7 @@ int vdc_destroy(vdc_ctx* ctx) {
     dfree(ctx->d_tmaps);
     dfree(ctx->d_stats);
     dfree(ctx->d_status);
+    dfree(ctx->d_tile_trace);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     delete ctx;
@@ -2022,6 +2026,8 @@ int vdc_load_program(vdc_ctx* ctx, const uint8_t* words, const uint32_t* words_p
             if (s.view_of >= 0 || s.rank != 2 || s.dtype != VDC_DTYPE_BF16 || s.tile_rows != 128 || s.tile_cols != 64 ||
                 s.shape[0] % 128 || s.shape[1] % 64)
                 return fail(VDC_ERR_INPUT, "packed weights must be owned rank-2 bf16 tensors of 128 x 64 tiles");
+        } else if (s.tma == VDC_DESC_KPAGE_SWZ) {
+            if (s.dtype != VDC_DTYPE_BF16 || s.rank != 3) return fail(VDC_ERR_INPUT, "swizzled K pools are rank-3 bf16 page pools");
         } else if (s.tma) {
             if (s.view_of >= 0 || s.rank != 2 || s.dtype != VDC_DTYPE_BF16 || s.tma > 256 || s.shape[1] % 64)
                 return fail(VDC_ERR_INPUT, "TMA descriptors must be owned rank-2 bf16 tensors with 64-column tiles");
@@ -2133,7 +2139,7 @@ int vdc_bind_tensor(vdc_ctx* ctx, uint16_t tensor, void* dptr, size_t bytes, int
     for (size_t i = 0; i < ctx->dev_descs.size(); ++i)
         if (ctx->dev_descs[i].storage == int32_t(tensor)) ctx->dev_descs[i].ptr = static_cast<char*>(dptr);
     ctx->descs_dirty = true;
-    if (s.tma && s.tma != VDC_DESC_PACKED_SW128) {
+    if (s.tma && s.tma != VDC_DESC_PACKED_SW128 && s.tma != VDC_DESC_KPAGE_SWZ) {
         // {64 columns x tma rows} boxes, 128-byte swizzle: the K-major SW128
         // operand layout of tcgen05.mma (ring_engine.cu, bgemm)
         using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -2171,6 +2177,11 @@ int vdc_bind_symmetric(vdc_ctx* ctx, uint16_t tensor, void* const* peer_bases, u
     }
     ctx->tp_rank = rank;
     ctx->tp_world = world;
+    // (re-)binding restarts the epochs: the caller hands over zeroed headers
+    // on every rank (after an abort too), so all ranks restart together
+    ctx->tp_poisoned = false;
+    ctx->epoch = 0;
+    if (ctx->d_counters) CU(cudaMemset(ctx->d_counters, 0, sizeof(uint32_t) * ctx->n_counters));
     // the local data view (after the header) backs the descriptor like a bound tensor
     char* local = static_cast<char*>(peer_bases[rank]) + VDC_SYM_HEADER_BYTES;
     ctx->bound[tensor] = local;
@@ -2237,7 +2248,10 @@ int vdc_launch(vdc_ctx* ctx, void* stream) {
         R.epoch = ++ctx->epoch;
         R.ring_slots = ctx->ring_slots;
         R.prefetch = ctx->ring_prefetch;
-        R.debug = getenv("VDC_RING_DEBUG") ? uint32_t(atoi(getenv("VDC_RING_DEBUG"))) : 0u;
+        if (ctx->tp_poisoned)
+            return fail(VDC_ERR_INPUT, "a tensor-parallel launch aborted: the peers' symmetric headers are stale; "
+                                       "zero them on every rank and call vdc_bind_symmetric again before launching");
+        R.debug = ctx->debug;
         R.stats = ctx->d_stats;
         R.status = ctx->d_status;
         R.watchdog_ns = (unsigned long long)ctx->watchdog_ms * 1000000ull;
@@ -2260,12 +2274,10 @@ int vdc_launch(vdc_ctx* ctx, void* stream) {
         R.tmaps = ctx->d_tmaps;
         R.batched = ctx->batched ? 1u : 0u;
         if (R.debug & 2u) {
-            static unsigned long long* tt = nullptr;
-            if (!tt) cudaMalloc(&tt, sizeof(unsigned long long) * 4 * 65536);
-            cudaMemsetAsync(tt, 0, sizeof(unsigned long long) * 4 * 65536, s);
-            R.tile_trace = tt;
+            if (!ctx->d_tile_trace) CU(cudaMalloc(&ctx->d_tile_trace, sizeof(unsigned long long) * 4 * 65536));
+            CU(cudaMemsetAsync(ctx->d_tile_trace, 0, sizeof(unsigned long long) * 4 * 65536, s));
+            R.tile_trace = ctx->d_tile_trace;
             R.tile_trace_cap = 65536;
-            ctx->d_tile_trace = tt;
         }
         void* rargs[] = {&R};
         CU(cudaEventRecord(ctx->ev0, s));
@@ -2358,6 +2370,9 @@ int vdc_wait(vdc_ctx* ctx, vdc_report* r) {
         CU(cudaMemset(ctx->d_counters, 0, sizeof(uint32_t) * ctx->n_counters));
         CU(cudaMemset(ctx->d_status, 0, sizeof(Status)));
         ctx->epoch = 0;
+        // the symmetric (TP) headers live in caller-owned peer memory and were
+        // advanced by every rank: this rank alone cannot restore them
+        if (ctx->tp_world > 1) ctx->tp_poisoned = true;
     }
     if (st.abort == 1) return fail(VDC_ERR_DEADLOCK, "device watchdog: deadlock");
     if (st.abort == 2) return fail(VDC_ERR_INTERNAL, "device fault code " + std::to_string(st.fault_code));

@@ -259,7 +259,10 @@ struct Vcc {
                     const uint32_t v0 = u0 ? (sys ? ld_relaxed_sys(c0p) : ld_relaxed(c0p)) : 0u;
                     const uint32_t v1 = u1 ? (sys ? ld_relaxed_sys(c1p) : ld_relaxed(c1p)) : 0u;
                     const uint32_t v2 = u2 ? (sys ? ld_relaxed_sys(c2p) : ld_relaxed(c2p)) : 0u;
-                    if ((!u0 || v0 >= g0) && (!u1 || v1 >= g1) && (!u2 || v2 >= g2)) break;
+                    // signed distance: counters grow monotonically across launches and
+                    // wrap at 2^32; a target is reached when v - g (mod 2^32) is
+                    // non-negative as a signed value (gaps stay far below 2^31)
+                    if ((!u0 || int32_t(v0 - g0) >= 0) && (!u1 || int32_t(v1 - g1) >= 0) && (!u2 || int32_t(v2 - g2) >= 0)) break;
                     if ((n & 255) == 0) {
                         if (aborted()) {
                             good = false;

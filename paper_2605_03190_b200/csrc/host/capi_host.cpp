@@ -9,7 +9,14 @@
 #include "capi_common.hpp"
 #include "uopsim/decode.hpp"
 #include "uopsim/generator.hpp"
+#include "uopsim/ring_abi.h"
+#include "uopsim/util.hpp"
 #include "vdc.h"
+
+namespace vdc_dev {
+int synthesize_launch(void* out, uint64_t n, int bf16, int init, float scale, uint64_t state0, uint32_t layout, int64_t rows,
+                      int64_t cols, void* stream);
+}
 
 using json = nlohmann::ordered_json;
 using namespace uopsim;
@@ -360,6 +367,30 @@ int vdc_program_words(const vdc_program* prog, uint32_t core, const uint8_t** wo
     if (core >= b->words.size()) return fail(VDC_ERR_INPUT, "core index out of range");
     *words = b->words[core].data();
     *n_words = uint32_t(b->words[core].size() / 16);
+    return VDC_OK;
+}
+
+int vdc_program_synthesize(const vdc_program* prog, uint16_t tensor, uint64_t seed, void* dptr, size_t bytes, void* stream) {
+    if (!prog || !dptr) return fail(VDC_ERR_INPUT, "null argument");
+    const auto* b = reinterpret_cast<const ProgramBox*>(prog);
+    const auto& ds = b->program.descriptors;
+    if (tensor >= ds.size()) return fail(VDC_ERR_INPUT, "tensor index out of range");
+    const auto& d = ds[tensor];
+    if (d.view_of >= 0) return fail(VDC_ERR_INPUT, d.tensor + " is a view: synthesize its storage owner");
+    if (d.elem != workload::ElemType::f32 && d.elem != workload::ElemType::bf16)
+        return fail(VDC_ERR_INPUT, d.tensor + ": only f32 / bf16 tensors are synthesised");
+    const uint64_t n = uint64_t(d.elem_count());
+    const int bf = d.elem == workload::ElemType::bf16 ? 1 : 0;
+    if (bytes != n * (bf ? 2u : 4u)) return fail(VDC_ERR_INPUT, d.tensor + ": buffer size does not match the descriptor");
+    // reference synthesize_inputs: only external tensors (and, ext, KV state) carry contents
+    const int init = (d.external || d.state) && !d.symmetric ? int(d.init) : int(workload::InitKind::zeros);
+    const uint32_t layout = (d.tma == VDC_DESC_PACKED_SW128 || d.tma == VDC_DESC_KPAGE_SWZ) ? d.tma : 0u;
+    if (layout == VDC_DESC_PACKED_SW128 && (d.shape.size() != 2 || d.shape[0] % 128 || d.shape[1] % 64))
+        return fail(VDC_ERR_INPUT, d.tensor + ": packed weights are (rows % 128, cols % 64)");
+    if (layout && n % (bf ? 8u : 4u)) return fail(VDC_ERR_INPUT, d.tensor + ": swizzled layouts need whole 16-byte chunks");
+    const int rc = vdc_dev::synthesize_launch(dptr, n, bf, init, d.init_scale, seed ^ fnv1a(d.tensor), layout, d.rows(), d.cols(),
+                                              stream);
+    if (rc != 0) return fail(VDC_ERR_INTERNAL, "synthesis kernel launch failed (cuda error " + std::to_string(rc) + ")");
     return VDC_OK;
 }
 

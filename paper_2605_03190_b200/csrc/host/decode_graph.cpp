@@ -382,6 +382,7 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
         for (const char* c : {"kc", "vc"}) {
             TensorRef& t = b.add(L + c, {pool, hkv * l.page_rows, hd}, l.page_rows, hd, winit, e);
             t.state = true;
+            if (c[0] == 'k') t.tma = VDC_DESC_KPAGE_SWZ;
         }
         std::map<std::string, std::string> qkv_attrs = {{"eps", eps}, {"theta", theta}, {"rope", "1"}, {"batch", bs}};
         std::map<std::string, std::string> attn_attrs = {{"pages_per_job", std::to_string(l.pages_per_job)}, {"batch", bs},

@@ -51,11 +51,51 @@ TORCH_DTYPE = {"f32": "float32", "bf16": "bfloat16", "i64": "int64"}
 
 
 PACKED_SW128 = 0x80000000  # ring_abi.h VDC_DESC_PACKED_SW128
+KPAGE_SWZ = 0x40000000     # ring_abi.h VDC_DESC_KPAGE_SWZ
+
+
 def to_logical(d: dict, a: np.ndarray) -> np.ndarray:
-    """device storage order -> row-major (packed weight layouts undone)"""
+    """device storage order -> row-major (packed weights and swizzled K pages undone)"""
     if d.get("tma") == PACKED_SW128:
         return unpack_sw128(a, *d["shape"])
+    if d.get("tma") == KPAGE_SWZ:
+        return unswizzle_k(a.reshape(-1, 64, d["shape"][-1])).reshape(a.shape)
     return a
+
+
+def to_storage(d: dict, a: np.ndarray) -> np.ndarray:
+    """row-major host array -> the descriptor's device storage order"""
+    if d.get("tma") == PACKED_SW128:
+        return pack_sw128(a, *d["shape"])
+    if d.get("tma") == KPAGE_SWZ:
+        return swizzle_k(a.reshape(-1, 64, d["shape"][-1])).reshape(a.shape)
+    return a
+
+
+def _k_chunk_map(rows: int, hd: int) -> np.ndarray:
+    """physical 16-byte chunk of logical chunk c in page row r: (c & 8) | ((c & 7) ^ (r & 7))"""
+    r = np.arange(rows)[:, None]
+    c = np.arange(hd // 8)[None, :]
+    return (c & 8) | ((c & 7) ^ (r & 7))
+
+
+def swizzle_k(pool: np.ndarray) -> np.ndarray:
+    """(..., 64, hd) row-major K page rows -> the swizzled storage of batched
+    K pools (ring_abi.h VDC_DESC_KPAGE_SWZ)."""
+    rows, hd = pool.shape[-2], pool.shape[-1]
+    pc = _k_chunk_map(rows, hd)
+    x = pool.reshape(pool.shape[:-1] + (hd // 8, 8))
+    out = np.empty_like(x)
+    out[..., np.arange(rows)[:, None], pc, :] = x
+    return out.reshape(pool.shape)
+
+
+def unswizzle_k(pool: np.ndarray) -> np.ndarray:
+    """inverse of swizzle_k: swizzled K page rows -> logical order"""
+    rows, hd = pool.shape[-2], pool.shape[-1]
+    pc = _k_chunk_map(rows, hd)
+    x = pool.reshape(pool.shape[:-1] + (hd // 8, 8))
+    return np.ascontiguousarray(x[..., np.arange(rows)[:, None], pc, :]).reshape(pool.shape)
 
 
 def pack_sw128(a: np.ndarray, rows: int, cols: int) -> np.ndarray:
@@ -114,23 +154,52 @@ class Engine:
         self.tensors[name] = tensor
         del torch
 
-    def bind_inputs(self, arrays: dict) -> dict:
-        # weights of batched programs are stored as packed, pre-swizzled tiles
-        # (ring_abi.h VDC_DESC_PACKED_SW128): row-major host arrays are packed here
+    def bind_inputs(self, arrays: dict, skip_symmetric: bool = False) -> dict:
         """Allocate every storage tensor on the device from host arrays (float32
-        values; bf16 tensors are cast); missing names are zero-filled."""
+        values in logical row-major order; bf16 tensors are cast); missing names
+        are zero-filled. Weights of batched programs are packed into pre-swizzled
+        tiles (VDC_DESC_PACKED_SW128) and K page pools swizzled
+        (VDC_DESC_KPAGE_SWZ) here, so callers never see the device layouts."""
         torch = _torch()
         out = {}
         for d in self.info["descriptors"]:
-            if d["view_of"] >= 0:
+            if d["view_of"] >= 0 or (skip_symmetric and d.get("symmetric")):
                 continue
             n = int(np.prod(d["shape"]))
             dt = getattr(torch, TORCH_DTYPE[d["dtype"]])
             if d["name"] in arrays:
-                a = np.ascontiguousarray(arrays[d["name"]], dtype=np.float32).reshape(-1)
-                if d.get("tma") == PACKED_SW128:
-                    a = pack_sw128(a, *d["shape"])
-                t = torch.from_numpy(a).to(f"cuda:{self.device}").to(dt)
+                a = to_storage(d, np.ascontiguousarray(arrays[d["name"]], dtype=np.float32).reshape(-1))
+                t = torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{self.device}").to(dt)
+            else:
+                t = torch.zeros(n, dtype=dt, device=f"cuda:{self.device}")
+            self.bind(d["name"], t)
+            out[d["name"]] = t
+        return out
+
+    def synthesize(self, seed: int = 0, skip_symmetric: bool = False, overrides: dict | None = None,
+                   seeds: dict | None = None) -> dict:
+        """Allocate every storage tensor and fill it ON THE DEVICE with the
+        reference synthesize_inputs stream (vdc_program_synthesize: splitmix64 /
+        unit_float keyed by seed ^ fnv1a(name), device storage layouts applied);
+        `overrides` maps names to host arrays bound instead (bind_inputs rules);
+        `seeds` maps names to their own seed (e.g. tensors replicated over TP
+        ranks keep one seed while the shards get per-rank seeds)."""
+        torch = _torch()
+        out = {}
+        stream = torch.cuda.current_stream(self.device)
+        for d in self.info["descriptors"]:
+            if d["view_of"] >= 0 or (skip_symmetric and d.get("symmetric")):
+                continue
+            dt = getattr(torch, TORCH_DTYPE[d["dtype"]])
+            n = int(np.prod(d["shape"]))
+            if overrides and d["name"] in overrides:
+                a = to_storage(d, np.ascontiguousarray(overrides[d["name"]], dtype=np.float32).reshape(-1))
+                t = torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{self.device}").to(dt)
+            elif d["dtype"] in ("f32", "bf16"):
+                t = torch.empty(n, dtype=dt, device=f"cuda:{self.device}")
+                sd = (seeds or {}).get(d["name"], seed)
+                check(lib().vdc_program_synthesize(self.program.handle, d["index"], sd, ctypes.c_void_p(t.data_ptr()),
+                                                   n * t.element_size(), ctypes.c_void_p(stream.cuda_stream)))
             else:
                 t = torch.zeros(n, dtype=dt, device=f"cuda:{self.device}")
             self.bind(d["name"], t)
@@ -139,23 +208,7 @@ class Engine:
 
     def bind_inputs_nonsym(self, arrays: dict) -> dict:
         """bind_inputs for every storage tensor except the symmetric (TP) buffers"""
-        torch = _torch()
-        out = {}
-        for d in self.info["descriptors"]:
-            if d["view_of"] >= 0 or d.get("symmetric"):
-                continue
-            n = int(np.prod(d["shape"]))
-            dt = getattr(torch, TORCH_DTYPE[d["dtype"]])
-            if d["name"] in arrays:
-                a = np.ascontiguousarray(arrays[d["name"]], dtype=np.float32).reshape(-1)
-                if d.get("tma") == PACKED_SW128:
-                    a = pack_sw128(a, *d["shape"])
-                t = torch.from_numpy(a).to(f"cuda:{self.device}").to(dt)
-            else:
-                t = torch.zeros(n, dtype=dt, device=f"cuda:{self.device}")
-            self.bind(d["name"], t)
-            out[d["name"]] = t
-        return out
+        return self.bind_inputs(arrays, skip_symmetric=True)
 
     def bind_symmetric(self, name: str, peer_ptrs: list, world: int, rank: int) -> None:
         """TP exchange buffer: peer_ptrs[q] = rank q's buffer (128-byte header + data)"""

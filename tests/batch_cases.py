@@ -49,18 +49,6 @@ def step_block(info: dict, tokens, pos) -> np.ndarray:
     return st
 
 
-def unswizzle_k(pool: np.ndarray) -> np.ndarray:
-    """K page pools store each row's 16-byte chunks swizzled: logical chunk c of
-    page row r at chunk (c & 8) | ((c & 7) ^ (r & 7)) (ring_engine.cu, BGEMM
-    KV append). pool: (..., 64, hd) -> logical order."""
-    rows, hd = pool.shape[-2], pool.shape[-1]
-    r = np.arange(rows)[:, None]
-    c = np.arange(hd // 8)[None, :]
-    pc = (c & 8) | ((c & 7) ^ (r & 7))  # physical chunk of logical chunk c in row r
-    x = pool.reshape(pool.shape[:-1] + (hd // 8, 8))
-    return np.ascontiguousarray(x[..., r, pc, :]).reshape(pool.shape)
-
-
 def request_view(info: dict, T: dict, b: int, cfg: dict) -> dict:
     """Single-request tensors of request b: shared weights + its cache pages
     gathered into the (hkv, pages*64, hd) layout decode_ref expects."""
@@ -74,8 +62,6 @@ def request_view(info: dict, T: dict, b: int, cfg: dict) -> dict:
     for l in range(cfg["layers"]):
         for c in ("kc", "vc"):
             pool = T[f"L{l}.{c}"].reshape(g[f"L{l}.{c}"]["shape"][0], hkv, 64, hd)
-            if c == "kc":
-                pool = unswizzle_k(pool)
             pages = pool[pt[b, :npages]]                      # (np, hkv, 64, hd)
             out[f"L{l}.{c}"] = np.ascontiguousarray(pages.transpose(1, 0, 2, 3)).reshape(-1)
     return out
@@ -89,8 +75,6 @@ def appended_rows(info: dict, host: dict, b: int, pos: int, cfg: dict, l: int):
     rows = []
     for c in ("kc", "vc"):
         pool = host[f"L{l}.{c}"].reshape(g[f"L{l}.{c}"]["shape"][0], hkv, 64, hd)
-        if c == "kc":
-            pool = unswizzle_k(pool)
         rows.append(pool[pt[b, pos // 64], :, pos % 64, :].reshape(-1))
     return rows
 
