@@ -62,8 +62,15 @@ struct LayoutConfig {
     // request index as the row, 128 x 64 weight tiles for the tcgen05 GEMM
     // µops (BGEMM), KV caches as page pools (pool_pages, kv_heads * 64, hd)
     // addressed through a page table; request b covers req_pages[b] logical
-    // pages (its context capacity in this program), allocated contiguously
-    // in the pool (the page table is part of the lowered program).
+    // pages (its context capacity in this program). KV tiles are addressed
+    // (request, logical page, head) and resolved through the step block's
+    // page table at run time, so pages can be allocated, freed and grown
+    // between launches (vdc_kv_* block allocator) without a rebuild; pages
+    // past a request's context are not loaded. pool_pages = 0: the pool holds
+    // sum(req_pages) pages allocated contiguously (the lowered program's
+    // default page table); > 0: a shared pool of that many pages, every
+    // page-table entry unallocated (-1) until the host allocates it.
+    int pool_pages = 0;
     bool argmax = false;  // greedy sampling fused into lm_head (single-request, no TP): next_token (int64)
     bool feedback = false;  // with argmax: token fed back + position advanced in the step block on the device
     int batch = 0;

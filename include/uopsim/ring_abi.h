@@ -99,6 +99,17 @@
  * import or export row-major K caches apply / undo this permutation
  * (engine.py swizzle_k / unswizzle_k). */
 #define VDC_DESC_KPAGE_SWZ 0x40000000u
+/* LOAD word reg1 (ring programs): how the memory core resolves a tile.
+ *  1 VDC_LOAD_PACKED: packed 16 KB weight tile (VDC_DESC_PACKED_SW128).
+ *  2 VDC_LOAD_PAGED: KV page of a page pool, coords (request b, logical page
+ *    i, kv head h): physical page = step[ptab + b * maxp + i] (the program's
+ *    page table); pages with i * 64 >= ctx_b, or unallocated entries (< 0),
+ *    are not loaded (the slot completes empty; attention masks them).
+ *  3 VDC_LOAD_CTX: KV page of a single-request cache, coords (h, i): not
+ *    loaded when i * 64 >= the step's ctx. */
+#define VDC_LOAD_PACKED 1
+#define VDC_LOAD_PAGED 2
+#define VDC_LOAD_CTX 3
 #define VDC_RING_BGEMM_KT 64     /* reduction columns per weight tile (128-byte swizzle atom) */
 #define VDC_RING_MAX_BATCH 64
 

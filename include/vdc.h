@@ -167,6 +167,29 @@ void vdc_free_string(char* s);
  * `stream` (a cudaStream_t). */
 int vdc_program_synthesize(const vdc_program* prog, uint16_t tensor, uint64_t seed, void* dptr, size_t bytes, void* stream);
 
+/* ---- paged-KV block allocator (batched programs) ---------------------- */
+/* A pool of n_pages 64-row pages shared by the n_requests rows of a batched
+ * program's page table (max_pages = the program's pages per request,
+ * vdc_program_text summary "batch.maxp"). The table is exported in the step
+ * block's layout (int64 request-major, -1 = unallocated): copy it to
+ * step[page_table_off ...] before a launch. KV tiles and appends resolve
+ * through it at run time (ring_abi.h VDC_LOAD_PAGED), so contexts grow by
+ * reserving pages between launches. A launch that appends at a position
+ * without a page fails with fault 7. Replaces the reference's static
+ * TileDescriptor addressing (generator.hpp:50-65, fold.cpp:278-293). */
+typedef struct vdc_kv_pages vdc_kv_pages;
+int vdc_kv_create(uint32_t n_pages, uint32_t n_requests, uint32_t max_pages, vdc_kv_pages** out);
+int vdc_kv_destroy(vdc_kv_pages* kv);
+/* request `req` holds pages for `tokens` positions (grows only; VDC_ERR_INPUT
+ * when the pool is exhausted or the program's capacity is exceeded) */
+int vdc_kv_reserve(vdc_kv_pages* kv, uint32_t req, uint64_t tokens);
+/* return every page of request `req` to the pool */
+int vdc_kv_release(vdc_kv_pages* kv, uint32_t req);
+/* free pages; held_by_req (optional): n_requests page counts */
+int vdc_kv_stats(const vdc_kv_pages* kv, uint32_t* free_pages, uint32_t* held_by_req);
+/* the n_requests x max_pages table (int64, -1 = unallocated) */
+int vdc_kv_table(const vdc_kv_pages* kv, int64_t* table);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,4 +6,4 @@ persistent sm_100a kernel executing µop streams (memory virtual cores feeding
 shared-memory slots with bulk copies, compute virtual cores running the
 handlers, device-side dependency counters/queues).
 """
-from ._native import Program, VdcError, lib  # noqa: F401
+from ._native import KvPages, Program, VdcError, lib  # noqa: F401

@@ -73,6 +73,7 @@ EXPORTS = [
     "vdc_bind_tensor", "vdc_bind_symmetric", "vdc_bind_step", "vdc_bind_trace", "vdc_launch", "vdc_wait", "vdc_set_watchdog", "vdc_set_prefetch", "vdc_program_build",
     "vdc_program_parse", "vdc_program_free", "vdc_program_text", "vdc_program_cores", "vdc_program_words",
     "vdc_program_load", "vdc_free_string", "vdc_program_synthesize",
+    "vdc_kv_create", "vdc_kv_destroy", "vdc_kv_reserve", "vdc_kv_release", "vdc_kv_stats", "vdc_kv_table",
 ]
 
 _lib = None
@@ -113,6 +114,12 @@ def lib() -> ctypes.CDLL:
         "vdc_program_load": ([vp, vp], c.c_int),
         "vdc_free_string": ([c.c_void_p], None),
         "vdc_program_synthesize": ([vp, c.c_uint16, c.c_uint64, vp, c.c_size_t, vp], c.c_int),
+        "vdc_kv_create": ([c.c_uint32, c.c_uint32, c.c_uint32, c.POINTER(vp)], c.c_int),
+        "vdc_kv_destroy": ([vp], c.c_int),
+        "vdc_kv_reserve": ([vp, c.c_uint32, c.c_uint64], c.c_int),
+        "vdc_kv_release": ([vp, c.c_uint32], c.c_int),
+        "vdc_kv_stats": ([vp, c.POINTER(c.c_uint32), c.POINTER(c.c_uint32)], c.c_int),
+        "vdc_kv_table": ([vp, c.POINTER(c.c_int64)], c.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -183,4 +190,37 @@ class Program:
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:
             _lib.vdc_program_free(self._h)
+            self._h = None
+
+
+class KvPages:
+    """Paged-KV block allocator (vdc_kv_*): a pool of 64-row pages shared by
+    the request rows of a batched program's page table."""
+
+    def __init__(self, n_pages: int, n_requests: int, max_pages: int):
+        self._h = ctypes.c_void_p()
+        check(lib().vdc_kv_create(n_pages, n_requests, max_pages, ctypes.byref(self._h)))
+        self.n_requests, self.max_pages = n_requests, max_pages
+
+    def reserve(self, req: int, tokens: int) -> None:
+        check(lib().vdc_kv_reserve(self._h, req, tokens))
+
+    def release(self, req: int) -> None:
+        check(lib().vdc_kv_release(self._h, req))
+
+    def stats(self):
+        free = ctypes.c_uint32()
+        held = (ctypes.c_uint32 * self.n_requests)()
+        check(lib().vdc_kv_stats(self._h, ctypes.byref(free), held))
+        return free.value, list(held)
+
+    def table(self):
+        """n_requests x max_pages int64 (-1 = unallocated), request-major"""
+        t = (ctypes.c_int64 * (self.n_requests * self.max_pages))()
+        check(lib().vdc_kv_table(self._h, t))
+        return list(t)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.vdc_kv_destroy(self._h)
             self._h = None

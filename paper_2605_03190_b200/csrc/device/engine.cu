@@ -1862,6 +1862,7 @@ struct vdc_ctx {
     bool tmaps_dirty = false;
     bool batched = false;
     bool qknorm = false;  // a Qwen3 QK-norm program: its own kernel instance
+    int32_t ptab = 0, maxp = 0;  // page table geometry of batched programs (from the attention jobs)
 };
 
 namespace {
@@ -2069,12 +2070,19 @@ int vdc_load_jobs(vdc_ctx* ctx, const vdc_job* jobs, uint32_t n_jobs, uint32_t r
         ring_slots > VDC_RING_MAX_SLOTS)
         return fail(VDC_ERR_INPUT, "ring_slots must be 8, 10, 11 or 12 (<= slot_budget)");
     bool batched = false;
+    ctx->maxp = ctx->ptab = 0;
     for (uint32_t i = 0; i < n_jobs; ++i) {
         const vdc_job& j = jobs[i];
         if (j.flags & VDC_JOB_BATCH) {
             batched = true;
             if (j.npad != 16 && j.npad != 32 && j.npad != 64) return fail(VDC_ERR_INPUT, "batched jobs need npad 16, 32 or 64");
             if (j.nb < 1 || j.nb > j.npad) return fail(VDC_ERR_INPUT, "batched job request count out of range");
+        }
+        if ((j.flags & VDC_JOB_BATCH) && j.maxp > 0 && j.ptab > 0) {  // jobs that read the page table
+            if ((ctx->maxp && (ctx->maxp != j.maxp || ctx->ptab != j.ptab)))
+                return fail(VDC_ERR_INPUT, "batched jobs disagree on the page table geometry");
+            ctx->maxp = j.maxp;
+            ctx->ptab = j.ptab;
         }
         if (j.op == 0x2D) {
             for (int32_t t : {j.x_t})
@@ -2273,6 +2281,8 @@ int vdc_launch(vdc_ctx* ctx, void* stream) {
         }
         R.tmaps = ctx->d_tmaps;
         R.batched = ctx->batched ? 1u : 0u;
+        R.ptab = ctx->ptab;
+        R.maxp = ctx->maxp;
         if (R.debug & 2u) {
             if (!ctx->d_tile_trace) CU(cudaMalloc(&ctx->d_tile_trace, sizeof(unsigned long long) * 4 * 65536));
             CU(cudaMemsetAsync(ctx->d_tile_trace, 0, sizeof(unsigned long long) * 4 * 65536, s));
@@ -2324,6 +2334,17 @@ int vdc_launch(vdc_ctx* ctx, void* stream) {
     return VDC_OK;
 }
 
+// device fault codes (Status::fault_code)
+static const char* fault_name(uint32_t code) {
+    switch (code) {
+        case 4: return "unknown compute opcode";
+        case 5: return "malformed LOAD word";
+        case 6: return "attention geometry without a kernel instance";
+        case 7: return "no KV page allocated for the position (info: request, or position past the cache)";
+        default: return "engine fault";
+    }
+}
+
 int vdc_wait(vdc_ctx* ctx, vdc_report* r) {
     if (!ctx) return fail(VDC_ERR_INPUT, "null ctx");
     CU(cudaEventSynchronize(ctx->ev1));
@@ -2364,7 +2385,8 @@ int vdc_wait(vdc_ctx* ctx, vdc_report* r) {
             std::snprintf(r->message, sizeof r->message, "deadlock: %d core(s) made no progress for %u ms (core %u, info 0x%x)",
                           st.n_stalled, ctx->watchdog_ms, st.stalled_core[0], st.fault_info);
         else if (st.abort == 2)
-            std::snprintf(r->message, sizeof r->message, "fault code %u info %u", st.fault_code, st.fault_info);
+            std::snprintf(r->message, sizeof r->message, "fault code %u (%s) info %u", st.fault_code, fault_name(st.fault_code),
+                          st.fault_info);
     }
     if (st.abort && ctx->ring) {  // counters are inconsistent after an aborted launch: restart the epochs
         CU(cudaMemset(ctx->d_counters, 0, sizeof(uint32_t) * ctx->n_counters));
@@ -2375,7 +2397,9 @@ int vdc_wait(vdc_ctx* ctx, vdc_report* r) {
         if (ctx->tp_world > 1) ctx->tp_poisoned = true;
     }
     if (st.abort == 1) return fail(VDC_ERR_DEADLOCK, "device watchdog: deadlock");
-    if (st.abort == 2) return fail(VDC_ERR_INTERNAL, "device fault code " + std::to_string(st.fault_code));
+    if (st.abort == 2)
+        return fail(VDC_ERR_INTERNAL, "device fault code " + std::to_string(st.fault_code) + " (" + fault_name(st.fault_code) +
+                                          ") info " + std::to_string(st.fault_info));
     return VDC_OK;
 }
 

@@ -126,6 +126,7 @@ struct RingParams {
     uint32_t trace_cap;
     uint32_t batched;           // batched program: TMEM accumulator + X ring for BGEMM µops
     const void* tmaps;          // CUtensorMap[n_desc] (128 bytes each), indexed by descriptor (vdc_desc.tma > 0 only)
+    int32_t ptab, maxp;         // batched programs: page table at step[ptab + b * maxp + logical page] (VDC_LOAD_PAGED)
 };
 size_t ring_smem_bytes(uint32_t ring_slots, bool batched = false);
 const void* ring_kernel_entry(bool batched, bool qknorm = false);

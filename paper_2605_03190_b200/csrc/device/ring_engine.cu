@@ -394,8 +394,7 @@ struct Vcc {
                 default: tiles<false, 8>(J); break;
             }
         }
-        if (!ok) return;
-        sync();
+        sync();  // (an aborted launch runs on through the epilogue: every warp must reach the same barriers)
         const long long e0 = clock64();
         gemv_epilogue(J, J.r1 - J.r0);
         if (ct == 0) st_epi += clock64() - e0;
@@ -518,8 +517,11 @@ struct Vcc {
             if ((wslot & uint32_t(CW - 1)) != w) continue;
             const int rg = t / tpr, c = t - rg * tpr;
             if (!wait_full(wslot, wphase)) {
+                // aborted launch: keep the VCC's control flow uniform (every
+                // warp reaches the same barriers), skip the arithmetic
                 ok = false;
-                return;
+                release(wslot);
+                continue;
             }
             const bool ttr = P->tile_trace && sm == (P->debug >> 8) && g < P->tile_trace_cap && lane == 0;
             if (ttr) P->tile_trace[3 * g + 1] = now_ns();
@@ -608,9 +610,10 @@ struct Vcc {
             }
             if ((wslot & uint32_t(CW - 1)) != w) continue;
             const int rg = t / tpr, c = t - rg * tpr;
-            if (!wait_full(wslot, wphase)) {
+            if (!wait_full(wslot, wphase)) {  // aborted launch: uniform control flow, no arithmetic
                 ok = false;
-                return;
+                release(wslot);
+                continue;
             }
             const uint32_t base = ring + wslot * SLOT;
             const bool ttr = P->tile_trace && sm == (P->debug >> 8) && g < P->tile_trace_cap && lane == 0;
@@ -704,6 +707,10 @@ struct Vcc {
             const int qrows = J.block, kvr = J.split, hd = J.head_dim;
             char* kb = tptr(J.b_t);
             char* vb = tptr(J.o2_t);
+            if (pos >= J.cache_rows) {  // past the cache capacity (e.g. a device decode loop ran too long)
+                if (ct == 0) fire(7, uint32_t(pos));
+                return;
+            }
             for (int p = int(ct); p < rows / 2; p += NCT) {
                 const int wr = J.r0 + 2 * p;  // W row (pairs never straddle a region boundary)
                 float a = row_sum(2 * p, tpr), b = row_sum(2 * p + 1, tpr);
@@ -895,10 +902,14 @@ struct Vcc {
             ok = false;
             return;
         }
-        const long long wm = spin(&S->mma_bar, nmma & 1u);
-        if (wm < 0) {
-            ok = false;
-            return;
+        // every warp issuer commits mma_bar (also after an abort), so this wait
+        // always completes: never abandoned (no tcgen05 work may outlive the job)
+        long long wm = 0;
+        {
+            const long long c0 = clock64();
+            while (!mbar_wait_hint(&S->mma_bar, nmma & 1u)) {
+            }
+            wm = clock64() - c0;
         }
         if (ct == 0) st_mma += wm;
         ++nmma;
@@ -1034,7 +1045,12 @@ struct Vcc {
                 if (isq) {
                     u16p(J.o_t)[int64_t(b) * qrows + rg] = f2bf(v[c]);
                 } else {
-                    const int64_t page = P->step[J.ptab + int64_t(b) * J.maxp + pos / 64];
+                    const int64_t lp = pos / 64;
+                    const int64_t page = lp < J.maxp ? P->step[J.ptab + int64_t(b) * J.maxp + lp] : -1;
+                    if (page < 0) {  // no KV page allocated for this position: fail loudly, write nothing
+                        fire(7, uint32_t(b));
+                        continue;
+                    }
                     // K rows are stored pre-swizzled: 16-byte chunk ch of page row r at
                     // (ch & 8) | ((ch & 7) ^ (r & 7)) (attention reads them
                     // conflict-free with q broadcast); V rows stay row-major
@@ -1232,10 +1248,7 @@ struct Vcc {
         if (batched && J.lead_pad) {
             const uint32_t s0 = kt % R;
             if ((s0 & uint32_t(CW - 1)) == w) {
-                if (!wait_full(s0, (kt / R) & 1u)) {
-                    ok = false;
-                    return;
-                }
+                if (!wait_full(s0, (kt / R) & 1u)) ok = false;  // aborted: carry on (uniform control flow)
                 release(s0);
             }
             kt += 1;
@@ -1307,10 +1320,7 @@ struct Vcc {
             if ((w >> 1) != pair) continue;
             const int half = int(w & 1u);
             const int my_row0 = half * rows_w;
-            if (!wait_full(sk, pk) || !wait_full(sv, pv)) {
-                ok = false;
-                return;
-            }
+            if (!wait_full(sk, pk) || !wait_full(sv, pv)) ok = false;  // aborted: garbage pages, same barriers
             const bool ttr = P->tile_trace && sm == (P->debug >> 8) && gk < P->tile_trace_cap && lane == 0;
             if (ttr) P->tile_trace[3 * (gk + half) + 1] = now_ns();
             const uint32_t kb = ring + sk * SLOT + uint32_t(my_row0) * rowb, vb = ring + sv * SLOT + uint32_t(my_row0) * rowb;
@@ -1741,7 +1751,11 @@ __device__ __forceinline__ void vcc_role(const RingParams& P, Shared& S, char* r
     const uint32_t w0 = P.core_off[core], n = P.core_off[core + 1] - w0;
     const long long t0 = clock64();
     uint32_t jobs = 0;
-    for (uint32_t pc = 0; pc < n && v.ok; ++pc) {
+    // the stream runs to its end even after an abort (every wait then returns
+    // at once), so all compute warps reach the same barriers; only a
+    // dispatch fault (uniform over the VCC) stops it early
+    bool halt = false;
+    for (uint32_t pc = 0; pc < n && !halt; ++pc) {
         const uint4 raw = __ldg(&P.words[w0 + pc]);
         const uint32_t op = raw.x & 0xff;
         if (op == OP_HALT) break;
@@ -1786,7 +1800,7 @@ __device__ __forceinline__ void vcc_role(const RingParams& P, Shared& S, char* r
                 }
                 if (J.flags & VDC_JOB_QKNORM) {  // QK-norm geometry without an instance: fail loudly
                     if (v.ct == 0) v.fire(6, (core << 16) | pc);
-                    v.ok = false;
+                    halt = true;
                     break;
                 }
 #undef VDC_ATTN_QKN_CASE
@@ -1795,7 +1809,7 @@ __device__ __forceinline__ void vcc_role(const RingParams& P, Shared& S, char* r
                 VDC_ATTN_CASE(false, 2, 1)
 #undef VDC_ATTN_CASE
                 if (v.ct == 0) v.fire(6, (core << 16) | pc);  // unsupported head geometry
-                v.ok = false;
+                halt = true;
                 break;
             }
             case OP_ATTN_COMBINE: v.combine(J); break;
@@ -1806,7 +1820,7 @@ __device__ __forceinline__ void vcc_role(const RingParams& P, Shared& S, char* r
                     break;
                 }
                 if (v.ct == 0) v.fire(4, (core << 16) | pc);
-                v.ok = false;
+                halt = true;
                 break;
             case OP_ELEMWISE:
                 if constexpr (BATCHED) {
@@ -1819,7 +1833,7 @@ __device__ __forceinline__ void vcc_role(const RingParams& P, Shared& S, char* r
                 break;
             default:
                 if (v.ct == 0) v.fire(4, (core << 16) | pc);
-                v.ok = false;
+                halt = true;
                 break;
         }
         if (P.trace && v.ct == 0 && jobs < P.trace_cap) {
@@ -1853,6 +1867,7 @@ struct Tile {
     const char* src = nullptr;
     uint32_t copies = 0, run = 0, pitch = 0;
     bool bad = false, halt = false;
+    bool empty = false;  // a KV page past the context (or unallocated): the slot completes without data
     __device__ uint32_t bytes() const { return copies * run; }
 };
 
@@ -1878,7 +1893,31 @@ __device__ __forceinline__ Tile resolve_load(const RingParams& P, uint4 raw) {
         return t;
     }
     const int64_t c0 = int64_t(pl & 0xfff), c1 = int64_t((pl >> 12) & 0xfff), c2 = int64_t((pl >> 24) & 0xfff);
-    if (BATCHED && ((raw.y >> 24) & 1u)) {  // reg1 = 1: packed, pre-swizzled 16 KB weight tile (one bulk copy)
+    const uint32_t mode = (raw.y >> 24) & 0xfu;  // reg1 (ring_abi.h VDC_LOAD_*)
+    if (mode == VDC_LOAD_PAGED) {
+        // (request, logical page, kv head) -> physical page through the step
+        // block's page table; pages past the request's context are not loaded
+        if (!BATCHED || rank != 3 || c1 >= P.maxp) {
+            t.bad = true;
+            return t;
+        }
+        const int64_t ctx = P.step[3 * c0 + 2];
+        const int64_t page = P.step[P.ptab + c0 * P.maxp + c1];
+        if (c1 * d.tile_rows >= ctx || page < 0) {
+            t.empty = true;
+            return t;
+        }
+        t.src = d.ptr + (page * d.lead_stride[0] + c2 * d.tile_rows * d.cols) * d.elem;
+        t.copies = 1;
+        t.run = uint32_t(d.tile_rows * d.cols * d.elem);
+        t.bad = page >= d.grid[0] || c2 >= d.grid[1] || t.run > SLOT;
+        return t;
+    }
+    if (mode == VDC_LOAD_CTX && c1 * d.tile_rows >= (P.n_step > VDC_STEP_CTX ? P.step[VDC_STEP_CTX] : 0)) {
+        t.empty = true;  // single-request cache page past the step's context
+        return t;
+    }
+    if (BATCHED && mode == VDC_LOAD_PACKED) {  // reg1 = 1: packed, pre-swizzled 16 KB weight tile (one bulk copy)
         t.src = d.ptr + (c0 * d.grid[1] + c1) * (d.tile_rows * d.tile_cols * d.elem);
         t.copies = 1;
         t.run = uint32_t(d.tile_rows * d.tile_cols * d.elem);
@@ -1935,9 +1974,14 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
     unsigned long long st_empty = 0, bytes = 0, uops = 0;
     const long long t_start = clock64();
     uint4 raw = issuer && g < ntiles ? __ldg(&P.words[w0 + g]) : make_uint4(0, 0, 0, 0);
+    // the lane's next tile is resolved as soon as its word arrives (descriptor,
+    // page table and context loads overlap the slot polling), not when the
+    // slot frees up
+    Tile cur = issuer && g < ntiles ? resolve_load<BATCHED>(P, raw) : Tile{};
     uint32_t pf_g = g + R;  // next tile of this lane to prefetch into L2 (beyond its slot)
     long long idle_since = 0;
     unsigned long long t_idle = 0;
+    bool real_last = false;  // this lane's last issue was a bulk copy (bytes may still be landing)
     for (;;) {
         const bool pending = issuer && g < ntiles;
         if (!__any_sync(0xffffffffu, pending)) break;
@@ -1948,14 +1992,19 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
             ready = m == 0 || mbar_test(&S.empty[slot], (m - 1u) & 1u);
         }
         if (ready) {
-            const Tile t = resolve_load<BATCHED>(P, raw);
+            const Tile t = cur;
             if (t.bad || t.halt) {
                 if (atomicCAS(&P.status->abort, 0, 2) == 0) {
                     P.status->fault_code = 5;
                     P.status->fault_info = g;
                     P.status->stalled_core[0] = core;
                 }
+            } else if (t.empty) {
+                mbar_arrive(&S.full[slot]);  // no data: the consumer masks the page
+                ++uops;
+                real_last = false;
             } else {
+                real_last = true;
                 if (P.tile_trace && blockIdx.x == (P.debug >> 8) && g < P.tile_trace_cap) P.tile_trace[3 * g] = now_ns();
                 mbar_expect_tx(&S.full[slot], t.bytes());
                 char* dst = ring + size_t(slot) * SLOT;
@@ -1968,6 +2017,7 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
             if (pf_g < g + R) pf_g = g + R;
             ++m;
             raw = g < ntiles ? __ldg(&P.words[w0 + g]) : make_uint4(0, 0, 0, 0);
+            if (g < ntiles) cur = resolve_load<BATCHED>(P, raw);
         }
         if (PF && pending && !ready && pf_g < ntiles && pf_g < g + R * (1 + PF)) {
             // slot busy (the compute core is behind or waiting on a dependency):
@@ -2000,6 +2050,12 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
         }
     }
     if (idle_since) st_empty += clock64() - idle_since;
+    if (*reinterpret_cast<volatile int32_t*>(&P.status->abort) && issuer && m > 0 && real_last) {
+        // aborted launch: the consumers may not wait for this lane's last
+        // copy; let its bytes land before the CTA can exit (bounded)
+        const unsigned long long t0 = now_ns();
+        while (!mbar_test(&S.full[lane], (m - 1u) & 1u) && now_ns() - t0 < 100000000ull) __nanosleep(64);
+    }
     for (int o = 16; o; o >>= 1) {
         bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
         uops += __shfl_xor_sync(0xffffffffu, uops, o);

@@ -113,6 +113,7 @@ decode::LayoutConfig layout_from(const json& j) {
     l.feedback = j.value("feedback", l.feedback);
     l.prefill = j.value("prefill", l.prefill);
     l.req_pages = j.value("req_pages", l.req_pages);
+    l.pool_pages = j.value("pool_pages", l.pool_pages);
     return l;
 }
 

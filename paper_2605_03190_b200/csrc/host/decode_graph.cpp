@@ -338,7 +338,15 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
         if (m.qk_norm) throw workload::WorkloadError("prefill chunks of QK-norm models are not supported");
         pool = l.req_pages[0];
     }
-    if (pool > 4095) throw workload::WorkloadError("KV pool exceeds 4095 pages (12-bit tile coordinates)");
+    // KV tiles are addressed (request, logical page, head) through the page
+    // table, so the pool size is not bounded by the 12-bit tile coordinates
+    if (l.batch > 4095) throw workload::WorkloadError("at most 4095 requests per batched program (12-bit tile coordinates)");
+    for (int p : l.req_pages)
+        if (p > 4095) throw workload::WorkloadError("at most 4095 pages per request (12-bit tile coordinates)");
+    if (l.pool_pages > 0) {
+        if (l.prefill) throw workload::WorkloadError("prefill chunks use the contiguous default pool");
+        pool = l.pool_pages;
+    }
     Builder b{{}, m, l};
     auto sym = [&](const std::string& name) {  // exchange buffer: one (npad, d) fp32 slot per rank
         TensorRef& t = b.add(name, {W * N * d, 1}, N * d, 1, InitKind::zeros, ElemType::f32);
@@ -388,6 +396,7 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
         std::map<std::string, std::string> attn_attrs = {{"pages_per_job", std::to_string(l.pages_per_job)}, {"batch", bs},
                                                          {"req_pages", rp}};
         if (l.prefill) attn_attrs["prefill"] = "1";
+        if (l.pool_pages > 0) attn_attrs["pool_pages"] = std::to_string(l.pool_pages);
         if (m.qk_norm) {
             b.norm(L + "q_norm", hd);
             b.norm(L + "k_norm", hd);

@@ -49,6 +49,7 @@ double attr_num(const workload::OperatorNode& n, const char* key, double dflt) {
 struct Tile {
     uint16_t tensor;
     std::vector<uint16_t> coord;
+    uint8_t mode = 0;  // LOAD reg1: 0 plain, VDC_LOAD_PAGED (request, logical page, head), VDC_LOAD_CTX (ctx-bounded page)
 };
 
 struct RJob {
@@ -110,9 +111,13 @@ class RingLowering {
             p.npad = npad_;
             p.maxp = maxp_;
             p.page_table_off = 3 * nb_;
-            p.page_table.assign(size_t(nb_) * size_t(maxp_), 0);
-            for (size_t b = 0; b < pages_.size(); ++b)
-                for (size_t i = 0; i < pages_[b].size(); ++i) p.page_table[b * size_t(maxp_) + i] = pages_[b][i];
+            // default page table: the contiguous allocation (shared pools:
+            // every entry unallocated, -1, until the host's block allocator
+            // fills it); entries past a request's capacity stay -1
+            p.page_table.assign(size_t(nb_) * size_t(maxp_), -1);
+            if (!shared_pool_)
+                for (size_t b = 0; b < pages_.size(); ++b)
+                    for (size_t i = 0; i < pages_[b].size(); ++i) p.page_table[b * size_t(maxp_) + i] = pages_[b][i];
             p.step_scalars = uint16_t(3 * nb_ + nb_ * maxp_);
         }
         emit(p);
@@ -387,9 +392,10 @@ class RingLowering {
                 j.arrive_ctr = ctr;
                 j.arrive_need = int32_t(splits);
                 qk_norm_fields(n, j);
+                // ctx-bounded: pages past the step's context are not loaded
                 for (int64_t pg = j.r0; pg < j.r1; ++pg) {
-                    r.tiles.push_back({kc, {uint16_t(h), uint16_t(pg), 0}});
-                    r.tiles.push_back({vc, {uint16_t(h), uint16_t(pg), 0}});
+                    r.tiles.push_back({kc, {uint16_t(h), uint16_t(pg), 0}, VDC_LOAD_CTX});
+                    r.tiles.push_back({vc, {uint16_t(h), uint16_t(pg), 0}, VDC_LOAD_CTX});
                 }
                 jobs_.push_back(std::move(r));
             }
@@ -477,7 +483,7 @@ class RingLowering {
                     u.flow = 1;
                     u.size = 1;
                     u.addr = isa::AddressSpec::tile(t.tensor, t.coord);
-                    u.reg1 = desc_[t.tensor].tma == VDC_DESC_PACKED_SW128 ? 1 : 0;  // packed 16 KB weight tile
+                    u.reg1 = desc_[t.tensor].tma == VDC_DESC_PACKED_SW128 ? 1 : t.mode;  // packed 16 KB weight tile / KV page mode
                     vs.push_back(u);
                     vm.push_back({r.ordinal, slot, -1});
                 }
@@ -505,6 +511,7 @@ class RingLowering {
     // tensor cores, split-KV attention per (request, kv head), paged pools.
     bool batched_ = false;
     int32_t nb_ = 0, npad_ = 0, maxp_ = 0;
+    bool shared_pool_ = false;  // layout.pool_pages > 0: the host allocates pages (page table starts unallocated)
     std::vector<std::vector<int64_t>> pages_;  // request -> physical page of each logical page
     uint16_t pad_t_ = 0;
 
@@ -752,6 +759,7 @@ class RingLowering {
                 maxp_ = std::max<int32_t>(maxp_, int32_t(c));
             }
             if (int64_t(pages_.size()) != nb_) throw GeneratorError("req_pages does not match the batch");
+            shared_pool_ = attr_int(n, "pool_pages", 0) > 0;
         }
         struct AJ {
             int64_t b, h, s, p0, p1;
@@ -811,10 +819,12 @@ class RingLowering {
             j.arrive_ctr = ctr[{a.b, a.h}];
             qk_norm_fields(n, j);
             j.arrive_need = int32_t(ceil_div<int64_t>(int64_t(pages_[size_t(a.b)].size()), per));
+            // (request, logical page, head): the memory core resolves the
+            // physical page through the step block's page table at run time
+            // and skips pages past the request's context (no DRAM traffic)
             for (int64_t pg = a.p0; pg < a.p1; ++pg) {
-                const uint16_t phys = uint16_t(pages_[size_t(a.b)][size_t(pg)]);
-                r.tiles.push_back({kc, {phys, uint16_t(a.h), 0}});
-                r.tiles.push_back({vc, {phys, uint16_t(a.h), 0}});
+                r.tiles.push_back({kc, {uint16_t(a.b), uint16_t(pg), uint16_t(a.h)}, VDC_LOAD_PAGED});
+                r.tiles.push_back({vc, {uint16_t(a.b), uint16_t(pg), uint16_t(a.h)}, VDC_LOAD_PAGED});
             }
             jobs_.push_back(std::move(r));
         }
