@@ -203,34 +203,18 @@ def _cpu_name():
 
 # ---------------------------------------------------------------------------
 
-def init_tensors(eng, seed: int = 0):
-    """Random-init weights / KV caches on the device (synthetic), ones for
-    norms, zeros for activations. bf16 weights uniform in [-1,1)/sqrt(fan_in)."""
-    import torch
-
-    g = torch.Generator(device=f"cuda:{eng.device}")
-    g.manual_seed(seed)
-    out = {}
-    for d in eng.info["descriptors"]:
-        if d["view_of"] >= 0:
-            continue
-        n = 1
-        for s in d["shape"]:
-            n *= s
-        dt = {"f32": torch.float32, "bf16": torch.bfloat16, "i64": torch.int64}[d["dtype"]]
-        t = torch.empty(n, dtype=dt, device=f"cuda:{eng.device}")
-        if d["dtype"] == "i64":  # indices (sampled token)
-            t.zero_()
-        elif d["init"] == 2:  # ones
-            t.fill_(1)
-        elif d["external"] or d["state"]:
-            s = d["init_scale"] if d["init"] == 4 else 1.0
-            t.uniform_(-s, s, generator=g)
-        else:
-            t.zero_()
-        eng.bind(d["name"], t)
-        out[d["name"]] = t
-    return out
+def init_tensors(eng, rank: int = 0, tp: bool = False):
+    """Synthetic inputs on the device from the reference synthesize_inputs
+    stream (BASELINE §4: splitmix64 / unit_float keyed by seed ^ fnv1a(name),
+    Engine.synthesize -> vdc_program_synthesize): weights scaled by
+    1/sqrt(fan_in), norms ones, KV caches random, activations zero. Under TP
+    the weight shards take per-rank seeds and the replicated tensors
+    (embedding, norms) one seed; the symmetric exchange buffers are bound
+    separately (bind_symmetric_tp)."""
+    if not tp:
+        return eng.synthesize(seed=0)
+    rep = {d["name"]: 99 for d in eng.info["descriptors"] if d["name"] == "embed.table" or d["name"].endswith("norm")}
+    return eng.synthesize(seed=100 + rank, skip_symmetric=True, seeds=rep)
 
 
 def bind_symmetric_tp(eng, world: int, rank: int, local_rank: int):
@@ -274,7 +258,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     prog = Program.build(req)
     build_s = time.time() - t_build
     eng = Engine(prog, device=local_rank, watchdog_ms=10000)
-    tens = init_tensors(eng)
+    tens = init_tensors(eng, rank, tp)
     keep_sym = bind_symmetric_tp(eng, world, rank, local_rank) if tp else None
     info = eng.info
     nbytes = algorithmic_bytes(info, args.ctx)
@@ -387,7 +371,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "scaling": "strong" if tp else "weak",
         "vs_baseline": None,
         "dtype": "bf16",
-        "data": "synthetic: random-init Llama-3-8B weights (uniform/sqrt(fan_in)), random bf16 KV cache, greedy token feedback in e2e (device argmax)",
+        "data": "synthetic: reference synthesize_inputs stream (splitmix64/unit_float, generated on the device) for the Llama-3-8B weights (scaled 1/sqrt(fan_in)) and the bf16 KV cache, greedy token feedback in e2e",
         "config": {"workload": f"C2 Llama-3-8B bf16 decode, batch 1, ctx {args.ctx}, {args.layers} layers + lm_head",
                    "model": "llama3-8b", "batch": 1, "ctx": args.ctx, "parallelism": parallelism,
                    "l2": "inputs larger than L2 (algorithmic %.2f GB per step vs 126 MB L2)" % (nbytes["total"] / 1e9),
@@ -461,7 +445,7 @@ def run_batched(args, rank: int = 0, world: int = 1, local_rank: int = 0):
     prog = Program.build(req)
     build_s = time.time() - t_build
     eng = Engine(prog, device=local_rank, watchdog_ms=20000)
-    tens = init_tensors(eng)
+    tens = init_tensors(eng, rank, tp)
     keep_sym = bind_symmetric_tp(eng, world, rank, local_rank) if tp else None
     info = eng.info
     bi = info["batch"]
@@ -574,7 +558,7 @@ def run_batched(args, rank: int = 0, world: int = 1, local_rank: int = 0):
         "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "strong" if tp else "weak",
         "vs_baseline": None,
         "dtype": "bf16",
-        "data": f"synthetic: random-init {name} weights, random bf16 KV pages, contexts "
+        "data": f"synthetic: reference synthesize_inputs stream (splitmix64/unit_float, on the device) for the {name} weights and bf16 KV pages, contexts "
                 + (f"fixed {args.ctx_fixed}" if args.ctx_fixed else "splitmix64(seed 1) -> U[128, 8192]"),
         "config": {"workload": f"{cfg_name} {name} bf16 decode, batch {B}, per-request contexts (sum {sum(ctxs)}), "
                                f"paged KV (64-row pages, {sum(pages)} pages), {layers} layers + lm_head",
@@ -594,6 +578,27 @@ def run_batched(args, rank: int = 0, world: int = 1, local_rank: int = 0):
         "engine_report": {"uops_executed": rep.uops_executed, "bytes_loaded": rep.bytes_loaded,
                           "wait_cycles_sum_over_sms": rep.wait_cycles},
     }
+
+
+def self_launch(n: int, impl: str) -> int:
+    """Re-exec this command under torch.distributed.run with N ranks on this
+    node (127.0.0.1 rendezvous, a free port); returns the launcher's exit code."""
+    import socket
+
+    if impl == "ours":  # (the reference arm: rank 0 works on the host, the others exit at once)
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < n:
+            print(json.dumps({"metric": METRIC, "error": f"--gpus {n} requested, {have} GPUs visible"}))
+            return 1
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    print(f"bench.py: launching {n} ranks: {' '.join(cmd)}", file=sys.stderr)
+    return subprocess.call(cmd)
 
 
 def main():
@@ -619,8 +624,14 @@ def main():
                     help="N>1: tensor parallel over the N GPUs (default) or N independent replicas")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` outside torchrun: re-launch as N ranks (one
+        # process per GPU) exactly the way the driver does; rank 0 prints the line
+        raise SystemExit(self_launch(args.gpus, args.impl))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
+    if args.impl == "ours" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
 
     if args.impl == "reference":
