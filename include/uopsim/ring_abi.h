@@ -71,6 +71,9 @@
 #define VDC_JOB_PREFILL 0x4000  /* batched ATTN of a prefill chunk: the batch's rows are consecutive
                                    positions of one sequence sharing its pages; every row appended
                                    in this launch (from request 0's position on) is patched in */
+#define VDC_JOB_KVSWZ 0x8000   /* single-request KV caches with swizzled page rows (VDC_DESC_KPAGE_SWZ):
+                                   the qkv epilogue appends k / v rows swizzled, ATTN_DECODE reads
+                                   them on the tensor cores (batched pools are always swizzled) */
 #define VDC_JOB_BATCH 0x400     /* batched program (nb requests): per-request token / pos / ctx in
                                    the step block (3 int64 each), paged KV pools, page table at
                                    step[ptab + b * maxp + logical page] */
@@ -92,12 +95,13 @@
  * bulk copy per ring tile (row-major 128 x 64 boxes would be 128 separate
  * 128-byte DRAM bursts per tile, ~half the HBM rate). */
 #define VDC_DESC_PACKED_SW128 0x80000000u
-/* vdc_desc.tma value of a batched K page pool (pages, hkv * 64, hd): each
- * page row's 16-byte chunks are stored swizzled, logical chunk c of page row
- * r at chunk (c & 8) | ((c & 7) ^ (r & 7)) (written that way by the qkv
- * epilogue; the attention score loop reads them conflict-free). Hosts that
- * import or export row-major K caches apply / undo this permutation
- * (engine.py swizzle_k / unswizzle_k). */
+/* vdc_desc.tma value of a batched K or V page pool (pages, hkv * 64, hd):
+ * each page row's 16-byte chunks are stored swizzled, logical chunk c of page
+ * row r at chunk (c & 8) | ((c & 7) ^ (r & 7)) (written that way by the qkv
+ * epilogue; attention's ldmatrix reads of 8 consecutive rows, K for Q.K^T and
+ * V transposed for P.V, are bank-conflict free). Hosts that import or export
+ * row-major KV caches apply / undo this permutation (engine.py swizzle_k /
+ * unswizzle_k). */
 #define VDC_DESC_KPAGE_SWZ 0x40000000u
 /* LOAD word reg1 (ring programs): how the memory core resolves a tile.
  *  1 VDC_LOAD_PACKED: packed 16 KB weight tile (VDC_DESC_PACKED_SW128).

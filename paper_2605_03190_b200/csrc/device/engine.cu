@@ -2028,7 +2028,7 @@ int vdc_load_program(vdc_ctx* ctx, const uint8_t* words, const uint32_t* words_p
                 s.shape[0] % 128 || s.shape[1] % 64)
                 return fail(VDC_ERR_INPUT, "packed weights must be owned rank-2 bf16 tensors of 128 x 64 tiles");
         } else if (s.tma == VDC_DESC_KPAGE_SWZ) {
-            if (s.dtype != VDC_DTYPE_BF16 || s.rank != 3) return fail(VDC_ERR_INPUT, "swizzled K pools are rank-3 bf16 page pools");
+            if (s.dtype != VDC_DTYPE_BF16 || s.rank != 3) return fail(VDC_ERR_INPUT, "swizzled KV pools are rank-3 bf16 page pools");
         } else if (s.tma) {
             if (s.view_of >= 0 || s.rank != 2 || s.dtype != VDC_DTYPE_BF16 || s.tma > 256 || s.shape[1] % 64)
                 return fail(VDC_ERR_INPUT, "TMA descriptors must be owned rank-2 bf16 tensors with 64-column tiles");

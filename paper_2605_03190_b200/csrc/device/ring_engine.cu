@@ -160,6 +160,24 @@ __device__ __forceinline__ uint2 qk_norm_rope4(uint2 u, uint2 wv, int head_dim, 
     return make_uint2(pack2(y[0], y[1]), pack2(y[2], y[3]));
 }
 
+// tensor-core attention helpers (mma.sync m16n8k16 bf16 -> fp32; ldmatrix
+// from swizzled KV page rows)
+__device__ __forceinline__ void ldsm_x4(uint32_t a, uint32_t (&r)[4]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(a));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t a, uint32_t (&r)[4]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(a));
+}
+__device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// 16-byte chunk c of KV page row r (r & 7 = r7) in the swizzled page layout
+__device__ __forceinline__ uint32_t kv_swz(uint32_t c, uint32_t r7) { return (c & 8u) | ((c & 7u) ^ r7); }
+
 // TP exchange: this thread's output row rg for requests c0 .. c0 + nh - 1
 // into slot `off` of every rank's buffer (batched BGEMM epilogue)
 __device__ __noinline__ void sym_store_rows(char* const* bases, uint32_t world, int64_t off, int64_t M, int rg, int c0, int nb, int nh,
@@ -696,9 +714,14 @@ struct Vcc {
         const bool obf = tdtype(J.o_t) == VDC_DTYPE_BF16;
         const int lr0 = J.r0 - J.out_row0;  // first output row (region-local)
         const int64_t pos = P->n_step > VDC_STEP_POS ? P->step[VDC_STEP_POS] : 0;
+        const bool swz = J.flags & VDC_JOB_KVSWZ;  // swizzled cache page rows
+        // element d of a cache row at position pos, in storage order
+        auto cache_col = [&](int d) -> int {
+            return swz ? int((kv_swz(uint32_t(d) >> 3, uint32_t(pos & 7)) << 3) | uint32_t(d & 7)) : d;
+        };
         auto out_index = [&](int lr) -> int64_t {
             if (J.flags & VDC_JOB_KV_APPEND)
-                return (int64_t(lr / J.head_dim) * J.cache_rows + pos) * J.head_dim + lr % J.head_dim;
+                return (int64_t(lr / J.head_dim) * J.cache_rows + pos) * J.head_dim + cache_col(lr % J.head_dim);
             return int64_t(J.o_off) + lr;
         };
         if (J.flags & VDC_JOB_QKV) {
@@ -727,7 +750,8 @@ struct Vcc {
                 } else {
                     const bool isk = wr < qrows + kvr;
                     const int lr = isk ? wr - qrows : wr - qrows - kvr;
-                    const int64_t at = (int64_t(lr / hd) * J.cache_rows + pos) * hd + lr % hd;
+                    // (a pair of dims never straddles a 16-byte chunk)
+                    const int64_t at = (int64_t(lr / hd) * J.cache_rows + pos) * hd + cache_col(lr % hd);
                     store_out(isk ? kb : vb, obf, at, a);
                     store_out(isk ? kb : vb, obf, at + 1, b);
                 }
@@ -1051,11 +1075,11 @@ struct Vcc {
                         fire(7, uint32_t(b));
                         continue;
                     }
-                    // K rows are stored pre-swizzled: 16-byte chunk ch of page row r at
-                    // (ch & 8) | ((ch & 7) ^ (r & 7)) (attention reads them
-                    // conflict-free with q broadcast); V rows stay row-major
+                    // K and V rows are stored pre-swizzled: 16-byte chunk ch of page
+                    // row r at (ch & 8) | ((ch & 7) ^ (r & 7)), so attention's
+                    // ldmatrix reads of 8 consecutive rows are bank-conflict free
                     const int ch = d >> 3, r7 = int(pos & 7);
-                    const int dk = isk ? ((((ch & 8) | ((ch & 7) ^ r7)) << 3) | (d & 7)) : d;
+                    const int dk = (((ch & 8) | ((ch & 7) ^ r7)) << 3) | (d & 7);
                     const int64_t at = ((page * hkv + lr / hd) * 64 + pos % 64) * hd + dk;
                     u16p(isk ? J.b_t : J.o2_t)[at] = f2bf(v[c]);
                 }
@@ -1220,6 +1244,118 @@ struct Vcc {
     //    (per-head arrival counter) merges all partials in split order and
     //    publishes the head's attention output (reference finalize,
     //    handlers.cpp:155-168).
+    // One warp's 32 rows of a KV page on the tensor cores (mma.sync m16n8k16,
+    // bf16 -> fp32), K and V rows swizzled (kv_swz): conflict-free ldmatrix.
+    //  S = Q K^T: M = 16 q heads (rows >= G zero), N = 8 keys per n-tile, K = 16 dims;
+    //    K rows are the B operand as stored (ldmatrix).
+    //  online softmax in the log2 domain on the S fragments (lane (g, t) holds
+    //    head g, keys 8 nt + 2t, +1); masked keys (past the context) get p = 0.
+    //  O^T += V^T P^T: M = 16 dims, N = 8 heads, K = 16 keys; V rows through
+    //    ldmatrix.trans, P^T straight from the S fragments (same lane layout),
+    //    P split hi + lo into two bf16 MMAs (P carries ~16 mantissa bits, so the
+    //    products match fp32 P x bf16 V to fp32 accumulation order).
+    template <int G>
+    __device__ __forceinline__ void attn_page_mma(uint32_t kb, uint32_t vb, int nvalid, float sl2, const uint32_t (&qf)[8][2],
+                                                  float (&mo)[8][4], float& mm, float& ml) const {
+        const uint32_t i7 = lane & 7u, mi = lane >> 3;
+        const int g = int(lane >> 2), t = int(lane & 3u);
+        float sc[4][4];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) sc[nt][e] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < 8; ks += 2) {
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+                uint32_t b[4];  // dims 16 ks .. 16 ks + 31 of keys 8 nt .. 8 nt + 7
+                ldsm_x4(kb + (uint32_t(8 * nt) + i7) * 256u + kv_swz(uint32_t(2 * ks) + mi, i7) * 16u, b);
+                mma_bf16(sc[nt], qf[ks][0], 0u, qf[ks][1], 0u, b[0], b[1]);
+                mma_bf16(sc[nt], qf[ks + 1][0], 0u, qf[ks + 1][1], 0u, b[2], b[3]);
+            }
+        }
+        float mx = -INFINITY;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int key = 8 * nt + 2 * t + e;
+                const float v = (g < G && key < nvalid) ? sc[nt][e] * sl2 : -INFINITY;
+                sc[nt][e] = v;
+                mx = fmaxf(mx, v);
+            }
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float mn = fmaxf(mm, mx);
+        const float corr = mn == -INFINITY ? 1.f : exp2f(mm - mn);
+        float ls = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const float p = sc[nt][e] == -INFINITY ? 0.f : exp2f(sc[nt][e] - mn);
+                sc[nt][e] = p;
+                ls += p;
+            }
+        ml = ml * corr + ls;
+        mm = mn;
+        // O^T columns of this lane are heads 2t, 2t + 1: their corrections sit on lanes 8t, 8t + 4
+        const float ca = __shfl_sync(0xffffffffu, corr, 8 * t), cb = __shfl_sync(0xffffffffu, corr, 8 * t + 4);
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+            mo[mt][0] *= ca;
+            mo[mt][1] *= cb;
+            mo[mt][2] *= ca;
+            mo[mt][3] *= cb;
+        }
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+            const uint32_t h0 = pack2(sc[2 * kk][0], sc[2 * kk][1]), h1 = pack2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
+            const uint32_t l0 = pack2(sc[2 * kk][0] - bf_lo(h0), sc[2 * kk][1] - bf_hi(h0));
+            const uint32_t l1 = pack2(sc[2 * kk + 1][0] - bf_lo(h1), sc[2 * kk + 1][1] - bf_hi(h1));
+            const uint32_t row = uint32_t(16 * kk) + (mi >> 1) * 8u + i7;
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+                uint32_t a[4];  // V^T: dims 16 mt .. 16 mt + 15 x keys 16 kk .. 16 kk + 15
+                ldsm_x4_t(vb + row * 256u + kv_swz(uint32_t(2 * mt) + (mi & 1u), i7) * 16u, a);
+                mma_bf16(mo[mt], a[0], a[1], a[2], a[3], h0, h1);
+                mma_bf16(mo[mt], a[0], a[1], a[2], a[3], l0, l1);
+            }
+        }
+    }
+
+    // merge round of the split-KV attention: warp hh < HPR merges the 8 warp
+    // states of head h0 + hh from the scratch (warp order) into the split's
+    // partial (o[HD], m, l)
+    template <int DPL, int HD, int HPR>
+    __device__ void merge_round(float* part, const float* scr, int h0) const {
+        constexpr int SST = HD + 2;
+        if (int(w) < HPR) {
+            const int h = h0 + int(w);
+            const float* base = scr + size_t(w) * CW * SST;
+            float M = -INFINITY;
+            for (int q2 = 0; q2 < CW; ++q2) M = fmaxf(M, base[q2 * SST]);
+            float L = 0.f, O[DPL];
+#pragma unroll
+            for (int d = 0; d < DPL; ++d) O[d] = 0.f;
+            for (int q2 = 0; q2 < CW; ++q2) {
+                const float* t = base + q2 * SST;
+                if (t[0] == -INFINITY) continue;
+                const float f = expf(t[0] - M);
+                L = fmaf(t[1], f, L);
+#pragma unroll
+                for (int d = 0; d < DPL; ++d) O[d] = fmaf(t[2 + lane * DPL + d], f, O[d]);
+            }
+            float* out = part + h * (HD + 2);
+#pragma unroll
+            for (int d = 0; d < DPL; ++d) out[lane * DPL + d] = O[d];
+            if (lane == 0) {
+                out[HD] = M;
+                out[HD + 1] = L;
+            }
+        }
+    }
+
     __device__ void astamp(int ev) {
         if (P->tile_trace && sm == (P->debug >> 8) && ct == 0) P->tile_trace[60000 + 8 * (n_attn & 7) + ev] = now_ns();
     }
@@ -1254,6 +1390,15 @@ struct Vcc {
             kt += 1;
         }
         const int rows_w = PR / 2;  // rows per warp (<= 32: one per lane)
+        // bf16 head-dim-128 caches (K and V page rows swizzled: batched pools and
+        // VDC_JOB_KVSWZ caches): scores and P.V on the tensor cores
+        // (attn_page_mma); the fp32 geometry: CUDA-core path
+        constexpr bool MMA = BF && DPL == 4;
+        const bool swz = batched || (J.flags & VDC_JOB_KVSWZ);
+        if (MMA && !swz) {  // bf16 head-dim-128 caches are always swizzled (decode_graph.cpp)
+            if (ct == 0) fire(6, 0x2A00u | uint32_t(sm));
+            ok = false;
+        }
         // q of the group -> shared memory in the cache dtype, same 16-byte chunk
         // layout as a K row: the rotated chunk reads of the score loop hit 8
         // consecutive chunks per phase (bank-conflict free)
@@ -1277,11 +1422,17 @@ struct Vcc {
                 for (int h = int(w); h < G; h += CW) {
                     const uint2 u = ldcg64(reinterpret_cast<const char*>(qb) + h * HD * 2 + lane * 8);
                     const uint2 o = qk_norm_rope4(u, wv, J.head_dim, J.eps, cs0, cs1);
-                    // lane's dims 4 lane .. 4 lane + 3 = chunk lane / 2, half lane % 2
-                    qd[(h * 2 + int(lane & 1u)) * NCH + int(lane >> 1)] =
-                        make_uint4(__float_as_uint(bf_lo(o.x)), __float_as_uint(bf_hi(o.x)), __float_as_uint(bf_lo(o.y)),
-                                   __float_as_uint(bf_hi(o.y)));
+                    if constexpr (MMA) {  // bf16 rows [head][dim] (MMA A fragments)
+                        *reinterpret_cast<uint2*>(reinterpret_cast<char*>(qd) + h * HD * 2 + lane * 8) = o;
+                    } else {
+                        // lane's dims 4 lane .. 4 lane + 3 = chunk lane / 2, half lane % 2
+                        qd[(h * 2 + int(lane & 1u)) * NCH + int(lane >> 1)] =
+                            make_uint4(__float_as_uint(bf_lo(o.x)), __float_as_uint(bf_hi(o.x)), __float_as_uint(bf_lo(o.y)),
+                                       __float_as_uint(bf_hi(o.y)));
+                    }
                 }
+            } else if constexpr (MMA) {  // bf16 rows [head][dim] (MMA A fragments)
+                for (int i = int(ct); i < G * NCH; i += NCT) qd[i] = ldcg128(qb + i);
             } else if constexpr (BF) {
                 // bf16 caches: q staged as fp32 in split halves, [head][half][chunk]
                 // x 4 floats (dims 8c..8c+3 | 8c+4..8c+7), so the score loop's
@@ -1306,6 +1457,25 @@ struct Vcc {
             l[h] = 0.f;
 #pragma unroll
             for (int d = 0; d < DPL; ++d) o[h][d] = 0.f;
+        }
+        // tensor-core state: q A fragments (head lane / 4), O^T accumulators
+        // (dims x heads), running max (log2 domain) and per-lane partial sum
+        constexpr int NMT = HD / 16;
+        uint32_t qf[NMT][2];
+        float mo[NMT][4], mm = -INFINITY, ml = 0.f;
+        if constexpr (MMA) {
+            const uint32_t g = lane >> 2, t = lane & 3u;
+#pragma unroll
+            for (int ks = 0; ks < NMT; ++ks) {
+                const uint32_t a = qs + g * uint32_t(HD * 2) + uint32_t(16 * ks) * 2u + t * 4u;
+                qf[ks][0] = qf[ks][1] = 0u;
+                if (int(g) < G) {
+                    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(qf[ks][0]) : "r"(a));
+                    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(qf[ks][1]) : "r"(a + 16u));
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) mo[ks][e] = 0.f;
+            }
         }
         const uint32_t npages = uint32_t(J.r1 - J.r0), ntiles = 2u * npages;
         for (uint32_t i = 0; i < npages; ++i) {
@@ -1363,7 +1533,7 @@ struct Vcc {
                 if constexpr (qkn) {  // QK-norm + rotary of the appended k row, written back to the cache
                     // the lane's 4 stored dims; batched pools hold K rows swizzled
                     const int pc = int(lane >> 1);
-                    const int lc = batched ? ((pc & 8) | ((pc & 7) ^ int(pos & 7))) : pc;
+                    const int lc = swz ? ((pc & 8) | ((pc & 7) ^ int(pos & 7))) : pc;
                     const int dbase = lc * 8 + int(lane & 1u) * 4;
                     const uint2 u = ldcg64(kn + lane * 8);
                     const uint2 wv = *reinterpret_cast<const uint2*>(tptr(J.block) + dbase * 2);
@@ -1383,86 +1553,102 @@ struct Vcc {
                 fence_proxy_async_smem();  // these generic writes precede the slot's next bulk refill
                 __syncwarp();
             }
-            // ---- scores: lane = row; chunks rotated by lane (conflict-free K reads)
-            const bool valid = int(lane) < rows_w && prow0 + int(lane) < ctx;
-            float s[G];
-#pragma unroll
-            for (int h = 0; h < G; ++h) s[h] = 0.f;
-            if (int(lane) < rows_w) {
-                const uint32_t krow = kb + lane * rowb;
-                if constexpr (BF) {  // packed fp32 FMAs (FFMA2): even / odd dims in the two halves
-                    float2 acc[G];
-#pragma unroll
-                    for (int h = 0; h < G; ++h) acc[h] = make_float2(0.f, 0.f);
-#pragma unroll 4
-                    for (int c = 0; c < NCH; ++c) {
-                        // single-request caches: chunk order rotated per lane; batched
-                        // pools: K rows pre-swizzled, so every lane reads logical chunk c
-                        // (q loads are broadcasts) from its row's physical chunk
-                        const int cc = batched ? c : (c + int(lane)) & (NCH - 1);
-                        const int kc = batched ? ((c & 8) | ((c & 7) ^ int(lane & 7u))) : cc;
-                        const uint4 kv = lds128(krow + uint32_t(kc) * 16u);
-                        const float2 k01 = make_float2(bf_lo(kv.x), bf_hi(kv.x)), k23 = make_float2(bf_lo(kv.y), bf_hi(kv.y));
-                        const float2 k45 = make_float2(bf_lo(kv.z), bf_hi(kv.z)), k67 = make_float2(bf_lo(kv.w), bf_hi(kv.w));
-#pragma unroll
-                        for (int h = 0; h < G; ++h) {
-                            const uint4 qa = lds128(qs + uint32_t((h * 2) * NCH + cc) * 16u);
-                            const uint4 qb2 = lds128(qs + uint32_t((h * 2 + 1) * NCH + cc) * 16u);
-                            acc[h] = __ffma2_rn(k01, make_float2(__uint_as_float(qa.x), __uint_as_float(qa.y)), acc[h]);
-                            acc[h] = __ffma2_rn(k23, make_float2(__uint_as_float(qa.z), __uint_as_float(qa.w)), acc[h]);
-                            acc[h] = __ffma2_rn(k45, make_float2(__uint_as_float(qb2.x), __uint_as_float(qb2.y)), acc[h]);
-                            acc[h] = __ffma2_rn(k67, make_float2(__uint_as_float(qb2.z), __uint_as_float(qb2.w)), acc[h]);
+            if constexpr (MMA) {
+                const int nvalid = int(ctx - prow0 < 0 ? 0 : (ctx - prow0 < int64_t(rows_w) ? ctx - prow0 : int64_t(rows_w)));
+                if (nvalid > 0) {
+                    if (nvalid < 32) {
+                        // rows past the context: zero V (P is 0 there, 0 x NaN is not), scores masked
+                        for (int idx = int(lane); idx < (32 - nvalid) * NCH; idx += 32) {
+                            const uint32_t dst = vb + uint32_t(nvalid + idx / NCH) * rowb + uint32_t(idx % NCH) * 16u;
+                            asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(dst), "r"(0u) : "memory");
                         }
+                        fence_proxy_async_smem();
+                        __syncwarp();
                     }
-#pragma unroll
-                    for (int h = 0; h < G; ++h) s[h] = acc[h].x + acc[h].y;
-                } else {
-#pragma unroll 4
-                    for (int c = 0; c < NCH; ++c) {
-                        const int cc = (c + int(lane)) & (NCH - 1);
-                        const uint4 kv = lds128(krow + uint32_t(cc) * 16u);
-#pragma unroll
-                        for (int h = 0; h < G; ++h) {
-                            const uint4 qv = lds128(qs + uint32_t(h * NCH + cc) * 16u);
-                            s[h] += dot16<BF>(qv, kv);
+                    attn_page_mma<G>(kb, vb, nvalid, J.scale * 1.4426950408889634f, qf, mo, mm, ml);
+                }
+            } else {
+                // ---- scores: lane = row; chunks rotated by lane (conflict-free K reads)
+                const bool valid = int(lane) < rows_w && prow0 + int(lane) < ctx;
+                float s[G];
+    #pragma unroll
+                for (int h = 0; h < G; ++h) s[h] = 0.f;
+                if (int(lane) < rows_w) {
+                    const uint32_t krow = kb + lane * rowb;
+                    if constexpr (BF) {  // packed fp32 FMAs (FFMA2): even / odd dims in the two halves
+                        float2 acc[G];
+    #pragma unroll
+                        for (int h = 0; h < G; ++h) acc[h] = make_float2(0.f, 0.f);
+    #pragma unroll 4
+                        for (int c = 0; c < NCH; ++c) {
+                            // single-request caches: chunk order rotated per lane; batched
+                            // pools: K rows pre-swizzled, so every lane reads logical chunk c
+                            // (q loads are broadcasts) from its row's physical chunk
+                            const int cc = batched ? c : (c + int(lane)) & (NCH - 1);
+                            const int kc = batched ? ((c & 8) | ((c & 7) ^ int(lane & 7u))) : cc;
+                            const uint4 kv = lds128(krow + uint32_t(kc) * 16u);
+                            const float2 k01 = make_float2(bf_lo(kv.x), bf_hi(kv.x)), k23 = make_float2(bf_lo(kv.y), bf_hi(kv.y));
+                            const float2 k45 = make_float2(bf_lo(kv.z), bf_hi(kv.z)), k67 = make_float2(bf_lo(kv.w), bf_hi(kv.w));
+    #pragma unroll
+                            for (int h = 0; h < G; ++h) {
+                                const uint4 qa = lds128(qs + uint32_t((h * 2) * NCH + cc) * 16u);
+                                const uint4 qb2 = lds128(qs + uint32_t((h * 2 + 1) * NCH + cc) * 16u);
+                                acc[h] = __ffma2_rn(k01, make_float2(__uint_as_float(qa.x), __uint_as_float(qa.y)), acc[h]);
+                                acc[h] = __ffma2_rn(k23, make_float2(__uint_as_float(qa.z), __uint_as_float(qa.w)), acc[h]);
+                                acc[h] = __ffma2_rn(k45, make_float2(__uint_as_float(qb2.x), __uint_as_float(qb2.y)), acc[h]);
+                                acc[h] = __ffma2_rn(k67, make_float2(__uint_as_float(qb2.z), __uint_as_float(qb2.w)), acc[h]);
+                            }
+                        }
+    #pragma unroll
+                        for (int h = 0; h < G; ++h) s[h] = acc[h].x + acc[h].y;
+                    } else {
+    #pragma unroll 4
+                        for (int c = 0; c < NCH; ++c) {
+                            const int cc = (c + int(lane)) & (NCH - 1);
+                            const uint4 kv = lds128(krow + uint32_t(cc) * 16u);
+    #pragma unroll
+                            for (int h = 0; h < G; ++h) {
+                                const uint4 qv = lds128(qs + uint32_t(h * NCH + cc) * 16u);
+                                s[h] += dot16<BF>(qv, kv);
+                            }
                         }
                     }
                 }
-            }
-            // ---- online softmax per head over the warp's rows
-            float p[G];
-#pragma unroll
-            for (int h = 0; h < G; ++h) {
-                const float sc = valid ? s[h] * J.scale : -INFINITY;
-                const float mx = warp_max(sc);
-                const float mn = fmaxf(m[h], mx);
-                const float corr = (mn == -INFINITY) ? 1.f : (m[h] == -INFINITY ? 0.f : expf(m[h] - mn));
-                p[h] = valid ? expf(sc - mn) : 0.f;
-                l[h] = l[h] * corr + warp_sum(p[h]);
-                m[h] = mn;
-#pragma unroll
-                for (int d = 0; d < DPL; ++d) o[h][d] *= corr;
-            }
-            // ---- o += p V (lanes own DPL dims)
-            const int nrow = int(ctx - prow0 < int64_t(rows_w) ? ctx - prow0 : int64_t(rows_w));
-#pragma unroll 4
-            for (int r = 0; r < nrow; ++r) {
-                float vv[DPL];
-                load_row<BF, DPL>(vb + uint32_t(r) * rowb + lane * uint32_t(DPL * EB), vv);
-#pragma unroll
+                // ---- online softmax per head over the warp's rows
+                float p[G];
+    #pragma unroll
                 for (int h = 0; h < G; ++h) {
-                    const float ph = __shfl_sync(0xffffffffu, p[h], r);
-                    if constexpr (DPL % 2 == 0) {  // packed fp32 FMAs over dim pairs
-#pragma unroll
-                        for (int d = 0; d < DPL; d += 2) {
-                            const float2 a = __ffma2_rn(make_float2(vv[d], vv[d + 1]), make_float2(ph, ph),
-                                                        make_float2(o[h][d], o[h][d + 1]));
-                            o[h][d] = a.x;
-                            o[h][d + 1] = a.y;
+                    const float sc = valid ? s[h] * J.scale : -INFINITY;
+                    const float mx = warp_max(sc);
+                    const float mn = fmaxf(m[h], mx);
+                    const float corr = (mn == -INFINITY) ? 1.f : (m[h] == -INFINITY ? 0.f : expf(m[h] - mn));
+                    p[h] = valid ? expf(sc - mn) : 0.f;
+                    l[h] = l[h] * corr + warp_sum(p[h]);
+                    m[h] = mn;
+    #pragma unroll
+                    for (int d = 0; d < DPL; ++d) o[h][d] *= corr;
+                }
+                // ---- o += p V (lanes own DPL dims)
+                const int nrow = int(ctx - prow0 < int64_t(rows_w) ? ctx - prow0 : int64_t(rows_w));
+    #pragma unroll 4
+                for (int r = 0; r < nrow; ++r) {
+                    float vv[DPL];
+                    load_row<BF, DPL>(vb + uint32_t(r) * rowb + lane * uint32_t(DPL * EB), vv);
+    #pragma unroll
+                    for (int h = 0; h < G; ++h) {
+                        const float ph = __shfl_sync(0xffffffffu, p[h], r);
+                        if constexpr (DPL % 2 == 0) {  // packed fp32 FMAs over dim pairs
+    #pragma unroll
+                            for (int d = 0; d < DPL; d += 2) {
+                                const float2 a = __ffma2_rn(make_float2(vv[d], vv[d + 1]), make_float2(ph, ph),
+                                                            make_float2(o[h][d], o[h][d + 1]));
+                                o[h][d] = a.x;
+                                o[h][d + 1] = a.y;
+                            }
+                        } else {
+    #pragma unroll
+                            for (int d = 0; d < DPL; ++d) o[h][d] = fmaf(ph, vv[d], o[h][d]);
                         }
-                    } else {
-#pragma unroll
-                        for (int d = 0; d < DPL; ++d) o[h][d] = fmaf(ph, vv[d], o[h][d]);
                     }
                 }
             }
@@ -1480,6 +1666,35 @@ struct Vcc {
         float* scr = reinterpret_cast<float*>(S->x) + G * HD;  // after the staged q
         constexpr int HPR = G < 4 ? G : 4;
         constexpr int SST = HD + 2;
+        if constexpr (MMA) {
+            // lane (g, t): m, l of head g; O^T of heads 2t, 2t + 1 at dims 16 mt + g (+ 8)
+            ml += __shfl_xor_sync(0xffffffffu, ml, 1);
+            ml += __shfl_xor_sync(0xffffffffu, ml, 2);
+            const int g = int(lane >> 2), t = int(lane & 3u);
+#pragma unroll
+            for (int h0 = 0; h0 < G; h0 += HPR) {
+                if (t == 0 && g >= h0 && g < h0 + HPR) {
+                    float* st = scr + (size_t(g - h0) * CW + w) * SST;
+                    st[0] = mm == -INFINITY ? -INFINITY : mm * 0.69314718055994531f;  // natural-log domain
+                    st[1] = ml;
+                }
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int h = 2 * t + e;
+                    if (h >= h0 && h < h0 + HPR && h < G) {
+                        float* st = scr + (size_t(h - h0) * CW + w) * SST + 2;
+#pragma unroll
+                        for (int mt = 0; mt < NMT; ++mt) {
+                            st[16 * mt + g] = mo[mt][e];
+                            st[16 * mt + 8 + g] = mo[mt][2 + e];
+                        }
+                    }
+                }
+                sync();
+                merge_round<DPL, HD, HPR>(part, scr, h0);
+                sync();
+            }
+        } else {
 #pragma unroll
         for (int h0 = 0; h0 < G; h0 += HPR) {
 #pragma unroll
@@ -1493,31 +1708,9 @@ struct Vcc {
                 for (int d = 0; d < DPL; ++d) st[2 + lane * DPL + d] = o[h0 + hh][d];
             }
             sync();
-            if (int(w) < HPR) {
-                const int h = h0 + int(w);
-                const float* base = scr + size_t(w) * CW * SST;
-                float M = -INFINITY;
-                for (int q2 = 0; q2 < CW; ++q2) M = fmaxf(M, base[q2 * SST]);
-                float L = 0.f, O[DPL];
-#pragma unroll
-                for (int d = 0; d < DPL; ++d) O[d] = 0.f;
-                for (int q2 = 0; q2 < CW; ++q2) {
-                    const float* t = base + q2 * SST;
-                    if (t[0] == -INFINITY) continue;
-                    const float f = expf(t[0] - M);
-                    L = fmaf(t[1], f, L);
-#pragma unroll
-                    for (int d = 0; d < DPL; ++d) O[d] = fmaf(t[2 + lane * DPL + d], f, O[d]);
-                }
-                float* out = part + h * (HD + 2);
-#pragma unroll
-                for (int d = 0; d < DPL; ++d) out[lane * DPL + d] = O[d];
-                if (lane == 0) {
-                    out[HD] = M;
-                    out[HD + 1] = L;
-                }
-            }
+            merge_round<DPL, HD, HPR>(part, scr, h0);
             sync();
+        }
         }
         astamp(4);
         // ---- arrival: the last split of this kv head combines (the

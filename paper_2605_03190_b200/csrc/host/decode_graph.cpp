@@ -209,6 +209,10 @@ OperatorGraph build_decode_graph(const ModelConfig& m, const LayoutConfig& l) {
             TensorRef& t = b.add(L + c, {hkv, l.max_ctx, hd}, l.page_rows, hd,
                                  m.scaled_init ? InitKind::centered : InitKind::random, e);
             t.state = true;
+            // ring programs: bf16 head-dim-128 caches keep their page rows swizzled
+            // for the tensor-core attention (ring_abi.h VDC_DESC_KPAGE_SWZ)
+            if (l.ring && e == ElemType::bf16 && hd == 128 && l.page_rows == 64 && l.max_ctx % 64 == 0)
+                t.tma = VDC_DESC_KPAGE_SWZ;
             b.view(L + c, ".seg", 1, R);
         }
         std::map<std::string, std::string> qkv_attrs = {{"eps", eps}, {"theta", theta}, {"rope", "1"}, {"job_rows", std::to_string(R)}};
@@ -390,7 +394,7 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
         for (const char* c : {"kc", "vc"}) {
             TensorRef& t = b.add(L + c, {pool, hkv * l.page_rows, hd}, l.page_rows, hd, winit, e);
             t.state = true;
-            if (c[0] == 'k') t.tma = VDC_DESC_KPAGE_SWZ;
+            t.tma = VDC_DESC_KPAGE_SWZ;  // K and V page rows swizzled (tensor-core attention)
         }
         std::map<std::string, std::string> qkv_attrs = {{"eps", eps}, {"theta", theta}, {"rope", "1"}, {"batch", bs}};
         std::map<std::string, std::string> attn_attrs = {{"pages_per_job", std::to_string(l.pages_per_job)}, {"batch", bs},

@@ -55,7 +55,7 @@ KPAGE_SWZ = 0x40000000     # ring_abi.h VDC_DESC_KPAGE_SWZ
 
 
 def to_logical(d: dict, a: np.ndarray) -> np.ndarray:
-    """device storage order -> row-major (packed weights and swizzled K pages undone)"""
+    """device storage order -> row-major (packed weights and swizzled KV pages undone)"""
     if d.get("tma") == PACKED_SW128:
         return unpack_sw128(a, *d["shape"])
     if d.get("tma") == KPAGE_SWZ:
@@ -80,8 +80,8 @@ def _k_chunk_map(rows: int, hd: int) -> np.ndarray:
 
 
 def swizzle_k(pool: np.ndarray) -> np.ndarray:
-    """(..., 64, hd) row-major K page rows -> the swizzled storage of batched
-    K pools (ring_abi.h VDC_DESC_KPAGE_SWZ)."""
+    """(..., 64, hd) row-major K/V page rows -> the swizzled storage of batched
+    KV pools (ring_abi.h VDC_DESC_KPAGE_SWZ)."""
     rows, hd = pool.shape[-2], pool.shape[-1]
     pc = _k_chunk_map(rows, hd)
     x = pool.reshape(pool.shape[:-1] + (hd // 8, 8))
@@ -91,7 +91,7 @@ def swizzle_k(pool: np.ndarray) -> np.ndarray:
 
 
 def unswizzle_k(pool: np.ndarray) -> np.ndarray:
-    """inverse of swizzle_k: swizzled K page rows -> logical order"""
+    """inverse of swizzle_k: swizzled K/V page rows -> logical order"""
     rows, hd = pool.shape[-2], pool.shape[-1]
     pc = _k_chunk_map(rows, hd)
     x = pool.reshape(pool.shape[:-1] + (hd // 8, 8))
@@ -158,7 +158,7 @@ class Engine:
         """Allocate every storage tensor on the device from host arrays (float32
         values in logical row-major order; bf16 tensors are cast); missing names
         are zero-filled. Weights of batched programs are packed into pre-swizzled
-        tiles (VDC_DESC_PACKED_SW128) and K page pools swizzled
+        tiles (VDC_DESC_PACKED_SW128) and K/V page pools swizzled
         (VDC_DESC_KPAGE_SWZ) here, so callers never see the device layouts."""
         torch = _torch()
         out = {}

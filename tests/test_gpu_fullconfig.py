@@ -184,7 +184,8 @@ def _batched_run(model: dict, ctxs: list, steps: int, sms=None, ppj: int = 64):
                 page, row = int(pt[b, pos[b] // 64]), pos[b] % 64
                 kl = tr.unswizzle_k(kp[page].contiguous(), hd)[:, row, :].reshape(-1)
                 tally.kv(l, kl, r["k"][l][b], r32["k"][l][b])
-                tally.kv(l, vp[page][:, row, :].reshape(-1), r["v"][l][b], r32["v"][l][b])
+                vl = tr.unswizzle_k(vp[page].contiguous(), hd)[:, row, :].reshape(-1)
+                tally.kv(l, vl, r["v"][l][b], r32["v"][l][b])
         toks, pos = nxt, [p + 1 for p in pos]
     return tally.done()
 

@@ -52,8 +52,11 @@ def unpack_sw128(t, rows: int, cols: int):
     return x.permute(0, 2, 1, 3, 4).reshape(rows, cols)
 
 
+KPAGE_SWZ = 0x40000000  # ring_abi.h VDC_DESC_KPAGE_SWZ
+
+
 def unswizzle_k(t, hd: int):
-    """swizzled K page rows (VDC_DESC_KPAGE_SWZ) -> logical (..., 64, hd)"""
+    """swizzled K/V page rows (VDC_DESC_KPAGE_SWZ) -> logical (..., 64, hd)"""
     torch = _torch()
     x = t.view(-1, 64, hd // 8, 8)
     r = torch.arange(64, device=t.device)[:, None]
@@ -214,7 +217,7 @@ def caches_batched(info: dict, tens: dict, cfg: dict, page_table: np.ndarray, re
             pair = []
             for c in ("kc", "vc"):
                 pool = tens[f"L{l}.{c}"].view(_shape(descs[f"L{l}.{c}"])[0], hkv, 64, hd)
-                if c == "kc":
+                if descs[f"L{l}.{c}"].get("tma") == KPAGE_SWZ:  # swizzled page rows (K and V)
                     pool = unswizzle_k(pool, hd)
                 g = pool[pages].permute(1, 0, 2, 3).reshape(hkv, npg * 64, hd)
                 npad = max(cap_pages - npg, 0) if cap_pages else extra_pages
