@@ -181,7 +181,13 @@ def caches_single(info: dict, tens: dict, cfg: dict, extra: int = 0) -> list:
     out = []
     for l in range(cfg["layers"]):
         T = _shape(descs[f"L{l}.kc"])[1]
-        out.append(tuple(tens[f"L{l}.{c}"].view(hkv, T, hd).clone() for c in ("kc", "vc")))
+        pair = []
+        for c in ("kc", "vc"):
+            t = tens[f"L{l}.{c}"].view(hkv, T, hd)
+            if descs[f"L{l}.{c}"].get("tma") == KPAGE_SWZ:  # swizzled page rows -> logical
+                t = unswizzle_k(t.contiguous(), hd)
+            pair.append(t.clone())
+        out.append(tuple(pair))
     return [out]
 
 
