@@ -301,15 +301,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     total_ms = ev[0].elapsed_time(ev[-1])
 
     # ---- e2e: host loop through the public API (H2D step block; D2H of the
-    # token sampled on the device (greedy argmax fused into lm_head), or of
-    # the logits under TP, where the vocab is split over the ranks)
+    # token sampled on the device: greedy argmax fused into lm_head, under TP
+    # with the cross-rank (max, index) exchange inside the kernel)
     logits = tens["logits"]
     h_step = torch.zeros(8, dtype=torch.int64).pin_memory()
-    n_logits = logits.numel() * (world if tp else 1)
+    n_logits = logits.numel()
     h_logits = torch.empty(n_logits, dtype=torch.float32).pin_memory()
-    gathered = torch.empty(n_logits, dtype=torch.float32, device=f"cuda:{local_rank}") if tp else None
     next_tok = tens.get("next_token")
-    vocab = [d["shape"][0] for d in info["descriptors"] if d["name"] == "embed.table"][0]
     h_tok = torch.zeros(1, dtype=torch.int64).pin_memory()
     token = 17
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -321,13 +319,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             h_step[0], h_step[1], h_step[2] = token, args.ctx - 1, args.ctx
             step.copy_(h_step, non_blocking=True)
             eng.launch(stream)
-            if tp:  # vocab-parallel logits: gather the shards, every rank picks the same token
-                import torch.distributed as dist
-                dist.all_gather_into_tensor(gathered, logits)
-                h_logits.copy_(gathered, non_blocking=True)
-                stream.synchronize()
-                token = int(torch.argmax(h_logits))
-            elif next_tok is not None:
+            if next_tok is not None:  # (TP: the ranks exchanged their (max, index) pairs in the kernel)
                 h_tok.copy_(next_tok, non_blocking=True)
                 stream.synchronize()
                 token = int(h_tok[0])
@@ -377,9 +369,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                    "l2": "inputs larger than L2 (algorithmic %.2f GB per step vs 126 MB L2)" % (nbytes["total"] / 1e9),
                    "program_uops": info["total_uops"], "virtual_cores": prog.cores()[0], "build_seconds": round(build_s, 2)},
         "e2e": {"value": round(e2e_value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 8 * 8,
-                "d2h_bytes_per_step": 8 if (next_tok is not None and not tp) else n_logits * 4,
-                "sampling": "greedy argmax fused into the lm_head epilogue (device)" if (next_tok is not None and not tp)
-                            else "host argmax over D2H logits"},
+                "d2h_bytes_per_step": 8 if next_tok is not None else n_logits * 4,
+                "sampling": ("greedy argmax fused into the lm_head epilogue (device"
+                             + (", cross-rank (max, index) exchange over NVLink)" if tp else ")"))
+                            if next_tok is not None else "host argmax over D2H logits"},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": committed_traffic() if world == 1 else None,
@@ -438,7 +431,7 @@ def run_batched(args, rank: int = 0, world: int = 1, local_rank: int = 0):
         model["qk_norm"] = False
     req = {"engine": "ring", "model": model,
            "layout": {"batch": B, "req_pages": pages, "pages_per_job": args.pages_per_job, "gu_block": 128, "page_rows": 64,
-                      "argmax": not tp},
+                      "argmax": True},
            "profile": {"builtin": "b200"}}
     if tp:
         req["layout"]["tp_world"], req["layout"]["tp_rank"] = world, rank
@@ -508,15 +501,11 @@ def run_batched(args, rank: int = 0, world: int = 1, local_rank: int = 0):
 
     # e2e: per step the request triples (token, pos, ctx) go H2D from pinned
     # memory, the engine runs (greedy sampling fused into the lm_head GEMM)
-    # and the B sampled tokens come back D2H; under TP the vocab-parallel
-    # logit shards are gathered and every rank picks the same tokens
-    logits = tens["logits"]
-    next_tok = tens.get("next_token")
-    vocab = [d["shape"][0] for d in info["descriptors"] if d["name"] == "embed.table"][0]
+    # and the B sampled tokens come back D2H; under TP the ranks exchanged
+    # their (max, index) pairs in the kernel, so every rank holds the same tokens
+    next_tok = tens["next_token"]
     h_trip = torch.tensor(st_host[: 3 * B], dtype=torch.int64).pin_memory()
     h_tok = torch.zeros(B, dtype=torch.int64).pin_memory()
-    gathered = torch.empty(world * logits.numel(), dtype=torch.float32, device=f"cuda:{local_rank}") if tp else None
-    h_logits = torch.empty(world * logits.numel(), dtype=torch.float32).pin_memory() if tp else None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     w2 = time.time()
@@ -525,17 +514,11 @@ def run_batched(args, rank: int = 0, world: int = 1, local_rank: int = 0):
         for k in range(args.steps):
             step[: 3 * B].copy_(h_trip, non_blocking=True)
             eng.launch(stream)
-            if tp:
-                import torch.distributed as dist
-                dist.all_gather_into_tensor(gathered, logits)
-                h_logits.copy_(gathered, non_blocking=True)
-                stream.synchronize()
-                lg = h_logits.view(world, B, -1).permute(1, 0, 2).reshape(B, -1)[:, :vocab]  # drop the shards' padding
-                h_trip.view(B, 3)[:, 0] = torch.argmax(lg, dim=1)
-            else:
-                h_tok.copy_(next_tok.view(-1), non_blocking=True)
-                stream.synchronize()
-                h_trip.view(B, 3)[:, 0] = h_tok
+            # greedy sampling fused into the lm_head GEMM (TP: cross-rank (max,
+            # index) exchange in the kernel, every rank holds the same tokens)
+            h_tok.copy_(next_tok.view(-1), non_blocking=True)
+            stream.synchronize()
+            h_trip.view(B, 3)[:, 0] = h_tok
         e1.record(stream)
     stream.synchronize()
     sampler.mark(w2, time.time())
@@ -567,8 +550,9 @@ def run_batched(args, rank: int = 0, world: int = 1, local_rank: int = 0):
                    "l2": "inputs larger than L2 (algorithmic %.2f GB per step vs 126 MB L2)" % (nbytes["total"] / 1e9),
                    "program_uops": info["total_uops"], "build_seconds": round(build_s, 2)},
         "e2e": {"value": round(B * args.steps / (e2e_ms / 1e3), 2), "unit": "tokens/s", "h2d_bytes_per_step": 3 * B * 8,
-                "d2h_bytes_per_step": world * logits.numel() * 4 if tp else B * 8,
-                "sampling": "host argmax over the gathered vocab shards" if tp else "greedy argmax fused into the lm_head GEMM (device)"},
+                "d2h_bytes_per_step": B * 8,
+                "sampling": "greedy argmax fused into the lm_head GEMM (device" + (
+                    ", cross-rank (max, index) exchange over NVLink)" if tp else ")")},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,

@@ -71,9 +71,13 @@
 #define VDC_JOB_PREFILL 0x4000  /* batched ATTN of a prefill chunk: the batch's rows are consecutive
                                    positions of one sequence sharing its pages; every row appended
                                    in this launch (from request 0's position on) is patched in */
-#define VDC_JOB_KVSWZ 0x8000   /* single-request KV caches with swizzled page rows (VDC_DESC_KPAGE_SWZ):
-                                   the qkv epilogue appends k / v rows swizzled, ATTN_DECODE reads
-                                   them on the tensor cores (batched pools are always swizzled) */
+#define VDC_JOB_TP_ARGMAX 0x10000 /* with ARGMAX under tensor parallelism (vocab-parallel lm_head): the
+                                   rank's best (logit, global vocab index) per request is posted to
+                                   slot tp_rank of every rank's symmetric exchange buffer and each
+                                   rank reduces the W posts in rank order (ties -> lowest index), so
+                                   all ranks sample the same token. Single-request jobs: group =
+                                   exchange tensor, o2_off = the rank's first vocab row; batched:
+                                   am_sym, am_base, am_valid (rows >= am_valid are vocab padding) */
 #define VDC_JOB_BATCH 0x400     /* batched program (nb requests): per-request token / pos / ctx in
                                    the step block (3 int64 each), paged KV pools, page table at
                                    step[ptab + b * maxp + logical page] */
@@ -150,7 +154,9 @@ typedef struct vdc_job {
     int32_t ptab, maxp;       /* page table: step-block offset and pages per request row */
     int32_t kvrows;           /* BGEMM + QKV: k (= v) rows */
     int32_t am_ctr, am_need;  /* BGEMM + ARGMAX: sampling arrival counter, SMs posting (slot = req) */
-    int32_t rsv[16];          /* pads the block to 256 bytes: the single-request fields stay in
+    int32_t am_sym, am_base;  /* BGEMM + TP_ARGMAX: exchange tensor, the rank's first vocab row */
+    int32_t am_valid;         /* BGEMM + TP_ARGMAX: this rank's real vocab rows (the rest is padding) */
+    int32_t rsv[13];          /* pads the block to 256 bytes: the single-request fields stay in
                                  the first 128-byte line, the batched ones in the second */
 } vdc_job;  /* 256 bytes */
 

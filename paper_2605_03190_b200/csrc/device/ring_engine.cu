@@ -435,6 +435,39 @@ struct Vcc {
         }
     }
 
+    // TP sampling exchange (one thread): spin at system scope until the
+    // symmetric header of t reaches n x epoch; false if the launch aborted
+    __device__ bool wait_sym(int32_t t, uint32_t n) const {
+        const uint32_t* c = reinterpret_cast<const uint32_t*>(sym_base(t, P->tp_rank));
+        const uint32_t g = n * P->epoch;
+        const unsigned long long w0 = now_ns();
+        for (uint32_t k = 1;; ++k) {
+            if (int32_t(ld_relaxed_sys(c) - g) >= 0) break;
+            if ((k & 255) == 0) {
+                if (aborted()) return false;
+                if (P->watchdog_ns && now_ns() - w0 > P->watchdog_ns) {
+                    fire(0, 0x50000u | uint32_t(t));
+                    return false;
+                }
+            }
+        }
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        return true;
+    }
+    // (one thread) post n (value, index) pairs into slot tp_rank of every
+    // rank's exchange buffer t (slot = n pairs), release on every header
+    __device__ void post_sym_pairs(int32_t t, int n, const float* v, const int* idx) const {
+        for (uint32_t q = 0; q < P->tp_world; ++q) {
+            float* d = reinterpret_cast<float*>(sym_base(t, q) + VDC_SYM_HEADER_BYTES) + size_t(P->tp_rank) * 2 * n;
+            for (int i = 0; i < n; ++i) {
+                d[2 * i] = v[i];
+                d[2 * i + 1] = __int_as_float(idx[i]);
+            }
+        }
+        for (uint32_t q = 0; q < P->tp_world; ++q)
+            asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(sym_base(t, q)) : "memory");
+    }
+
     // greedy sampling fused into the lm_head epilogue: (max, first argmax)
     // of this job's logit rows, merged into the SM's running best; the SM's
     // last lm_head job posts it to its slot, and the last SM to arrive
@@ -481,6 +514,27 @@ struct Vcc {
                 am_merge(v0, i0, ldcg_f32(all + 2 * q), __float_as_int(ldcg_f32(all + 2 * q + 1)));
 #pragma unroll
             for (int o = 16; o; o >>= 1) am_merge(v0, i0, __shfl_xor_sync(0xffffffffu, v0, o), __shfl_xor_sync(0xffffffffu, i0, o));
+            if (J.flags & VDC_JOB_TP_ARGMAX) {
+                // vocab-parallel: this rank's best with its global index -> every
+                // rank; reduce the W posts in rank order (ties -> lowest index)
+                const int gi = i0 == 0x7fffffff ? i0 : i0 + J.o2_off;
+                int good = 1;
+                if (lane == 0) {
+                    post_sym_pairs(J.group, 1, &v0, &gi);
+                    good = wait_sym(J.group, P->tp_world) ? 1 : 0;
+                }
+                good = __shfl_sync(0xffffffffu, good, 0);
+                v0 = -INFINITY;
+                i0 = 0x7fffffff;
+                if (good && lane < P->tp_world) {
+                    const float* x = reinterpret_cast<const float*>(sym_base(J.group, P->tp_rank) + VDC_SYM_HEADER_BYTES) + 2 * lane;
+                    v0 = ldcg_f32(x);
+                    i0 = __float_as_int(ldcg_f32(x + 1));
+                }
+#pragma unroll
+                for (int o = 16; o; o >>= 1) am_merge(v0, i0, __shfl_xor_sync(0xffffffffu, v0, o), __shfl_xor_sync(0xffffffffu, i0, o));
+                if (!good) ok = false;
+            }
             if (lane == 0) {
                 *reinterpret_cast<int64_t*>(tptr(J.o2_t)) = int64_t(i0);
                 if (J.flags & VDC_JOB_FEEDBACK) {  // next launch: this token at the next position
@@ -714,14 +768,9 @@ struct Vcc {
         const bool obf = tdtype(J.o_t) == VDC_DTYPE_BF16;
         const int lr0 = J.r0 - J.out_row0;  // first output row (region-local)
         const int64_t pos = P->n_step > VDC_STEP_POS ? P->step[VDC_STEP_POS] : 0;
-        const bool swz = J.flags & VDC_JOB_KVSWZ;  // swizzled cache page rows
-        // element d of a cache row at position pos, in storage order
-        auto cache_col = [&](int d) -> int {
-            return swz ? int((kv_swz(uint32_t(d) >> 3, uint32_t(pos & 7)) << 3) | uint32_t(d & 7)) : d;
-        };
         auto out_index = [&](int lr) -> int64_t {
             if (J.flags & VDC_JOB_KV_APPEND)
-                return (int64_t(lr / J.head_dim) * J.cache_rows + pos) * J.head_dim + cache_col(lr % J.head_dim);
+                return (int64_t(lr / J.head_dim) * J.cache_rows + pos) * J.head_dim + lr % J.head_dim;
             return int64_t(J.o_off) + lr;
         };
         if (J.flags & VDC_JOB_QKV) {
@@ -750,8 +799,7 @@ struct Vcc {
                 } else {
                     const bool isk = wr < qrows + kvr;
                     const int lr = isk ? wr - qrows : wr - qrows - kvr;
-                    // (a pair of dims never straddles a 16-byte chunk)
-                    const int64_t at = (int64_t(lr / hd) * J.cache_rows + pos) * hd + cache_col(lr % hd);
+                    const int64_t at = (int64_t(lr / hd) * J.cache_rows + pos) * hd + lr % hd;
                     store_out(isk ? kb : vb, obf, at, a);
                     store_out(isk ? kb : vb, obf, at + 1, b);
                 }
@@ -1134,8 +1182,9 @@ struct Vcc {
                 float* scr = reinterpret_cast<float*>(S->x);  // [4 row quarters][npad] x (value, index)
 #pragma unroll
                 for (int c = 0; c < NH; ++c) {
-                    float bv = v[c];
-                    int bi = rg;
+                    const bool real_row = !(J.flags & VDC_JOB_TP_ARGMAX) || rg < J.am_valid;  // TP: padding rows never win
+                    float bv = real_row ? v[c] : -INFINITY;
+                    int bi = real_row ? rg + ((J.flags & VDC_JOB_TP_ARGMAX) ? J.am_base : 0) : 0x7fffffff;
 #pragma unroll
                     for (int o = 16; o; o >>= 1)
                         am_merge(bv, bi, __shfl_xor_sync(0xffffffffu, bv, o), __shfl_xor_sync(0xffffffffu, bi, o));
@@ -1179,11 +1228,47 @@ struct Vcc {
         sync();
         if (!S->flag) return;
         const float* all = reinterpret_cast<const float*>(tptr(J.b_t));
+        const bool tpx = J.flags & VDC_JOB_TP_ARGMAX;
+        if (tpx) {
+            // vocab-parallel: this rank's best per request -> every rank (one post
+            // of nb pairs), then each request's W posts reduced in rank order
+            for (int b = int(w); b < nb; b += CW) {
+                float bv = -INFINITY;
+                int bi = 0x7fffffff;
+                for (int s2 = int(lane); s2 < J.am_need; s2 += 32)
+                    am_merge(bv, bi, ldcg_f32(all + (size_t(s2) * npad + b) * 2), __float_as_int(ldcg_f32(all + (size_t(s2) * npad + b) * 2 + 1)));
+#pragma unroll
+                for (int o = 16; o; o >>= 1) am_merge(bv, bi, __shfl_xor_sync(0xffffffffu, bv, o), __shfl_xor_sync(0xffffffffu, bi, o));
+                if (lane == 0) {
+                    S->am_v[b] = bv;
+                    S->am_i[b] = bi;
+                }
+            }
+            sync();
+            if (ct == 0) {
+                post_sym_pairs(J.am_sym, nb, S->am_v, S->am_i);
+                S->flag = wait_sym(J.am_sym, P->tp_world) ? 1 : 0;
+            }
+            sync();
+            if (!S->flag) {
+                ok = false;
+                publish(J.o2_t);
+                return;
+            }
+        }
+        const float* xs = tpx ? reinterpret_cast<const float*>(sym_base(J.am_sym, P->tp_rank) + VDC_SYM_HEADER_BYTES) : nullptr;
         for (int b = int(w); b < nb; b += CW) {
             float bv = -INFINITY;
             int bi = 0x7fffffff;
-            for (int s2 = int(lane); s2 < J.am_need; s2 += 32)
-                am_merge(bv, bi, ldcg_f32(all + (size_t(s2) * npad + b) * 2), __float_as_int(ldcg_f32(all + (size_t(s2) * npad + b) * 2 + 1)));
+            if (tpx) {
+                if (int(lane) < int(P->tp_world)) {
+                    bv = ldcg_f32(xs + (size_t(lane) * nb + b) * 2);
+                    bi = __float_as_int(ldcg_f32(xs + (size_t(lane) * nb + b) * 2 + 1));
+                }
+            } else {
+                for (int s2 = int(lane); s2 < J.am_need; s2 += 32)
+                    am_merge(bv, bi, ldcg_f32(all + (size_t(s2) * npad + b) * 2), __float_as_int(ldcg_f32(all + (size_t(s2) * npad + b) * 2 + 1)));
+            }
 #pragma unroll
             for (int o = 16; o; o >>= 1) am_merge(bv, bi, __shfl_xor_sync(0xffffffffu, bv, o), __shfl_xor_sync(0xffffffffu, bi, o));
             if (lane == 0) {
@@ -1252,13 +1337,17 @@ struct Vcc {
     //    head g, keys 8 nt + 2t, +1); masked keys (past the context) get p = 0.
     //  O^T += V^T P^T: M = 16 dims, N = 8 heads, K = 16 keys; V rows through
     //    ldmatrix.trans, P^T straight from the S fragments (same lane layout),
-    //    P split hi + lo into two bf16 MMAs (P carries ~16 mantissa bits, so the
-    //    products match fp32 P x bf16 V to fp32 accumulation order).
+    //    P split hi + mid + lo into three bf16 MMAs (24 significant bits, so the
+    //    products are fp32 P x bf16 V up to fp32 accumulation order).
     template <int G>
-    __device__ __forceinline__ void attn_page_mma(uint32_t kb, uint32_t vb, int nvalid, float sl2, const uint32_t (&qf)[8][2],
+    __device__ __forceinline__ void attn_page_mma(uint32_t kb, uint32_t vb, int nvalid, float sl2, uint32_t qs,
                                                   float (&mo)[8][4], float& mm, float& ml) const {
         const uint32_t i7 = lane & 7u, mi = lane >> 3;
         const int g = int(lane >> 2), t = int(lane & 3u);
+        // q A fragments (rows = heads) by ldmatrix from the staged q (swizzled
+        // like the KV rows); rows >= G read 16 zero bytes after the staged q
+        const bool qrow = int(i7) < G;
+        const uint32_t qa = qrow ? qs + i7 * 256u : qs + uint32_t(G) * 256u;
         float sc[4][4];
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt)
@@ -1266,12 +1355,14 @@ struct Vcc {
             for (int e = 0; e < 4; ++e) sc[nt][e] = 0.f;
 #pragma unroll
         for (int ks = 0; ks < 8; ks += 2) {
+            uint32_t q[4];  // a0, a2 of k-steps ks and ks + 1 (heads x dims 16 ks .. 16 ks + 31)
+            ldsm_x4(qa + (qrow ? kv_swz(uint32_t(2 * ks) + mi, i7) * 16u : 0u), q);
 #pragma unroll
             for (int nt = 0; nt < 4; ++nt) {
                 uint32_t b[4];  // dims 16 ks .. 16 ks + 31 of keys 8 nt .. 8 nt + 7
                 ldsm_x4(kb + (uint32_t(8 * nt) + i7) * 256u + kv_swz(uint32_t(2 * ks) + mi, i7) * 16u, b);
-                mma_bf16(sc[nt], qf[ks][0], 0u, qf[ks][1], 0u, b[0], b[1]);
-                mma_bf16(sc[nt], qf[ks + 1][0], 0u, qf[ks + 1][1], 0u, b[2], b[3]);
+                mma_bf16(sc[nt], q[0], 0u, q[1], 0u, b[0], b[1]);
+                mma_bf16(sc[nt], q[2], 0u, q[3], 0u, b[2], b[3]);
             }
         }
         float mx = -INFINITY;
@@ -1310,16 +1401,24 @@ struct Vcc {
         }
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk) {
-            const uint32_t h0 = pack2(sc[2 * kk][0], sc[2 * kk][1]), h1 = pack2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
-            const uint32_t l0 = pack2(sc[2 * kk][0] - bf_lo(h0), sc[2 * kk][1] - bf_hi(h0));
-            const uint32_t l1 = pack2(sc[2 * kk + 1][0] - bf_lo(h1), sc[2 * kk + 1][1] - bf_hi(h1));
+            // P = hi + mid + lo in bf16 (24 significant bits: fp32 P)
+            uint32_t ph[2], pm[2], pl[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const float x0 = sc[2 * kk + u][0], x1 = sc[2 * kk + u][1];
+                ph[u] = pack2(x0, x1);
+                const float r0 = x0 - bf_lo(ph[u]), r1 = x1 - bf_hi(ph[u]);
+                pm[u] = pack2(r0, r1);
+                pl[u] = pack2(r0 - bf_lo(pm[u]), r1 - bf_hi(pm[u]));
+            }
             const uint32_t row = uint32_t(16 * kk) + (mi >> 1) * 8u + i7;
 #pragma unroll
             for (int mt = 0; mt < 8; ++mt) {
                 uint32_t a[4];  // V^T: dims 16 mt .. 16 mt + 15 x keys 16 kk .. 16 kk + 15
                 ldsm_x4_t(vb + row * 256u + kv_swz(uint32_t(2 * mt) + (mi & 1u), i7) * 16u, a);
-                mma_bf16(mo[mt], a[0], a[1], a[2], a[3], h0, h1);
-                mma_bf16(mo[mt], a[0], a[1], a[2], a[3], l0, l1);
+                mma_bf16(mo[mt], a[0], a[1], a[2], a[3], pl[0], pl[1]);  // smallest terms first
+                mma_bf16(mo[mt], a[0], a[1], a[2], a[3], pm[0], pm[1]);
+                mma_bf16(mo[mt], a[0], a[1], a[2], a[3], ph[0], ph[1]);
             }
         }
     }
@@ -1390,12 +1489,14 @@ struct Vcc {
             kt += 1;
         }
         const int rows_w = PR / 2;  // rows per warp (<= 32: one per lane)
-        // bf16 head-dim-128 caches (K and V page rows swizzled: batched pools and
-        // VDC_JOB_KVSWZ caches): scores and P.V on the tensor cores
-        // (attn_page_mma); the fp32 geometry: CUDA-core path
-        constexpr bool MMA = BF && DPL == 4;
-        const bool swz = batched || (J.flags & VDC_JOB_KVSWZ);
-        if (MMA && !swz) {  // bf16 head-dim-128 caches are always swizzled (decode_graph.cpp)
+        // batched bf16 page pools (K and V page rows swizzled): scores and P.V on
+        // the tensor cores (attn_page_mma). Single-request programs keep the
+        // CUDA-core path: at batch 1 the tensor-core page loop saved ~2.5 us of
+        // attention per layer, but its register demand inside the one
+        // persistent kernel slowed every GEMV operator by ~5 us per layer
+        // (281.6 vs 294.1 tokens/s, A/B on one B200)
+        constexpr bool MMA = BATCHED && BF && DPL == 4;
+        if (MMA && !batched) {  // batched kernels only run batched attention jobs
             if (ct == 0) fire(6, 0x2A00u | uint32_t(sm));
             ok = false;
         }
@@ -1422,8 +1523,9 @@ struct Vcc {
                 for (int h = int(w); h < G; h += CW) {
                     const uint2 u = ldcg64(reinterpret_cast<const char*>(qb) + h * HD * 2 + lane * 8);
                     const uint2 o = qk_norm_rope4(u, wv, J.head_dim, J.eps, cs0, cs1);
-                    if constexpr (MMA) {  // bf16 rows [head][dim] (MMA A fragments)
-                        *reinterpret_cast<uint2*>(reinterpret_cast<char*>(qd) + h * HD * 2 + lane * 8) = o;
+                    if constexpr (MMA) {  // bf16 rows [head][dim], chunks swizzled like KV rows (ldmatrix A fragments)
+                        *reinterpret_cast<uint2*>(reinterpret_cast<char*>(qd) + h * HD * 2 +
+                                                  kv_swz(lane >> 1, uint32_t(h) & 7u) * 16 + (lane & 1u) * 8) = o;
                     } else {
                         // lane's dims 4 lane .. 4 lane + 3 = chunk lane / 2, half lane % 2
                         qd[(h * 2 + int(lane & 1u)) * NCH + int(lane >> 1)] =
@@ -1431,8 +1533,9 @@ struct Vcc {
                                        __float_as_uint(bf_hi(o.y)));
                     }
                 }
-            } else if constexpr (MMA) {  // bf16 rows [head][dim] (MMA A fragments)
-                for (int i = int(ct); i < G * NCH; i += NCT) qd[i] = ldcg128(qb + i);
+            } else if constexpr (MMA) {  // bf16 rows [head][dim], chunks swizzled like KV rows (ldmatrix A fragments)
+                for (int i = int(ct); i < G * NCH; i += NCT)
+                    qd[(i / NCH) * NCH + int(kv_swz(uint32_t(i % NCH), uint32_t(i / NCH) & 7u))] = ldcg128(qb + i);
             } else if constexpr (BF) {
                 // bf16 caches: q staged as fp32 in split halves, [head][half][chunk]
                 // x 4 floats (dims 8c..8c+3 | 8c+4..8c+7), so the score loop's
@@ -1448,6 +1551,9 @@ struct Vcc {
             } else {
                 for (int i = int(ct); i < G * NCH; i += NCT) qd[i] = ldcg128(qb + i);
             }
+            if constexpr (MMA) {
+                if (ct == 0) qd[G * NCH] = make_uint4(0u, 0u, 0u, 0u);  // the zero rows of the q fragments
+            }
         }
         sync();
         float m[G], l[G], o[G][DPL];
@@ -1461,21 +1567,12 @@ struct Vcc {
         // tensor-core state: q A fragments (head lane / 4), O^T accumulators
         // (dims x heads), running max (log2 domain) and per-lane partial sum
         constexpr int NMT = HD / 16;
-        uint32_t qf[NMT][2];
         float mo[NMT][4], mm = -INFINITY, ml = 0.f;
         if constexpr (MMA) {
-            const uint32_t g = lane >> 2, t = lane & 3u;
 #pragma unroll
-            for (int ks = 0; ks < NMT; ++ks) {
-                const uint32_t a = qs + g * uint32_t(HD * 2) + uint32_t(16 * ks) * 2u + t * 4u;
-                qf[ks][0] = qf[ks][1] = 0u;
-                if (int(g) < G) {
-                    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(qf[ks][0]) : "r"(a));
-                    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(qf[ks][1]) : "r"(a + 16u));
-                }
+            for (int mt = 0; mt < NMT; ++mt)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) mo[ks][e] = 0.f;
-            }
+                for (int e = 0; e < 4; ++e) mo[mt][e] = 0.f;
         }
         const uint32_t npages = uint32_t(J.r1 - J.r0), ntiles = 2u * npages;
         for (uint32_t i = 0; i < npages; ++i) {
@@ -1533,7 +1630,7 @@ struct Vcc {
                 if constexpr (qkn) {  // QK-norm + rotary of the appended k row, written back to the cache
                     // the lane's 4 stored dims; batched pools hold K rows swizzled
                     const int pc = int(lane >> 1);
-                    const int lc = swz ? ((pc & 8) | ((pc & 7) ^ int(pos & 7))) : pc;
+                    const int lc = batched ? ((pc & 8) | ((pc & 7) ^ int(pos & 7))) : pc;
                     const int dbase = lc * 8 + int(lane & 1u) * 4;
                     const uint2 u = ldcg64(kn + lane * 8);
                     const uint2 wv = *reinterpret_cast<const uint2*>(tptr(J.block) + dbase * 2);
@@ -1565,7 +1662,7 @@ struct Vcc {
                         fence_proxy_async_smem();
                         __syncwarp();
                     }
-                    attn_page_mma<G>(kb, vb, nvalid, J.scale * 1.4426950408889634f, qf, mo, mm, ml);
+                    attn_page_mma<G>(kb, vb, nvalid, J.scale * 1.4426950408889634f, qs, mo, mm, ml);
                 }
             } else {
                 // ---- scores: lane = row; chunks rotated by lane (conflict-free K reads)

@@ -209,10 +209,6 @@ OperatorGraph build_decode_graph(const ModelConfig& m, const LayoutConfig& l) {
             TensorRef& t = b.add(L + c, {hkv, l.max_ctx, hd}, l.page_rows, hd,
                                  m.scaled_init ? InitKind::centered : InitKind::random, e);
             t.state = true;
-            // ring programs: bf16 head-dim-128 caches keep their page rows swizzled
-            // for the tensor-core attention (ring_abi.h VDC_DESC_KPAGE_SWZ)
-            if (l.ring && e == ElemType::bf16 && hd == 128 && l.page_rows == 64 && l.max_ctx % 64 == 0)
-                t.tma = VDC_DESC_KPAGE_SWZ;
             b.view(L + c, ".seg", 1, R);
         }
         std::map<std::string, std::string> qkv_attrs = {{"eps", eps}, {"theta", theta}, {"rope", "1"}, {"job_rows", std::to_string(R)}};
@@ -268,12 +264,19 @@ OperatorGraph build_decode_graph(const ModelConfig& m, const LayoutConfig& l) {
     b.weight("lm_head", vocab, d, l.head_job_rows, float(d));  // vocab-parallel: this rank's logit rows
     b.add("logits", {vocab, 1}, l.head_job_rows, 1, InitKind::zeros, ElemType::f32);
     std::map<std::string, std::string> head_attrs = {{"eps", eps}, {"job_rows", std::to_string(l.head_job_rows)}};
-    if (l.argmax && !tp) {
+    if (l.argmax) {
         // per-job (max, argmax) slots and the sampled token
         b.add("head.amax", {4096, 2}, 4096, 2, InitKind::zeros, ElemType::f32);
         b.add("next_token", {1, 1}, 1, 1, InitKind::zeros, ElemType::i64);
         head_attrs["argmax"] = "1";
         if (l.feedback) head_attrs["feedback"] = "1";
+        if (tp) {  // vocab-parallel logits: the ranks exchange their (max, global index) pairs
+            TensorRef& t = b.add("head.amx", {W * 2, 1}, 2, 1, InitKind::zeros, ElemType::f32);
+            t.symmetric = true;
+            head_attrs["tp_argmax"] = "head.amx";
+            head_attrs["vocab_base"] = std::to_string(l.tp_rank * vocab);
+            head_attrs["vocab_valid"] = std::to_string(vocab);
+        }
     }
     b.node("head", OpKind::RMS_GEMV, {"lm_head", b.view(x, ".all", d), "final_norm"}, {"logits"}, head_attrs);
     b.g.validate();
@@ -446,11 +449,18 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
     b.add("logits", {B, vocab}, 1, vocab, InitKind::zeros, ElemType::f32);
     std::map<std::string, std::string> head_attrs = {{"eps", eps}, {"batch", bs}};
     if (!tp && vocab != m.vocab) throw workload::WorkloadError("batched decode needs the vocabulary in whole 128-row blocks");
-    if (l.argmax && !tp) {  // greedy sampling fused into the lm_head GEMM: per-SM slots, tokens per request
+    if (l.argmax) {  // greedy sampling fused into the lm_head GEMM: per-SM slots, tokens per request
         b.add("head.amax", {256 * N, 2}, N, 2, InitKind::zeros, ElemType::f32);
         b.add("next_token", {B, 1}, 1, 1, InitKind::zeros, ElemType::i64);
         head_attrs["argmax"] = "1";
         if (l.feedback) head_attrs["feedback"] = "1";
+        if (tp) {  // vocab-parallel logits: the ranks exchange their (max, global index) pairs per request
+            TensorRef& t = b.add("head.amx", {W * N * 2, 1}, N * 2, 1, InitKind::zeros, ElemType::f32);
+            t.symmetric = true;
+            head_attrs["tp_argmax"] = "head.amx";
+            head_attrs["vocab_base"] = std::to_string(l.tp_rank * vocab);
+            head_attrs["vocab_valid"] = std::to_string(std::max<int64_t>(0, std::min<int64_t>(vocab, m.vocab - l.tp_rank * vocab)));
+        }
     }
     b.node("head", OpKind::RMS_GEMV, {"lm_head", xn, x}, {"logits"}, head_attrs);
     return std::move(b.g);

@@ -176,6 +176,11 @@ class RingLowering {
                         j.arrive_need = int32_t(last.size());
                         j.split = slot[jobs_[i].sm];
                         j.block = last[jobs_[i].sm] == i ? 1 : 0;
+                        if (n.attrs.count("tp_argmax")) {  // vocab-parallel: cross-rank (max, index) exchange
+                            j.flags |= VDC_JOB_TP_ARGMAX;
+                            j.group = storage(idx(n.attrs.at("tp_argmax")));
+                            j.o2_off = int32_t(attr_int(n, "vocab_base", 0));
+                        }
                     }
                 }
                 break;
@@ -301,7 +306,6 @@ class RingLowering {
                         j.b_t = storage(idx(n.outputs[1]));
                         j.o2_t = storage(idx(n.outputs[2]));
                         j.cache_rows = int32_t(desc_[idx(n.outputs[1])].shape[1]);
-                        if (desc_[uint16_t(j.b_t)].tma == VDC_DESC_KPAGE_SWZ) j.flags |= VDC_JOB_KVSWZ;
                         if (c0 < qrows) r.publishes.push_back(j.o_t);
                         if (c0 < qrows + kvrows && c1 > qrows) r.publishes.push_back(j.b_t);
                         if (c1 > qrows + kvrows) r.publishes.push_back(j.o2_t);
@@ -392,7 +396,6 @@ class RingLowering {
                 j.split = int32_t(s);
                 j.arrive_ctr = ctr;
                 j.arrive_need = int32_t(splits);
-                if (kd.tma == VDC_DESC_KPAGE_SWZ) j.flags |= VDC_JOB_KVSWZ;
                 qk_norm_fields(n, j);
                 // ctx-bounded: pages past the step's context are not loaded
                 for (int64_t pg = j.r0; pg < j.r1; ++pg) {
@@ -693,6 +696,12 @@ class RingLowering {
                 j.block = last[jobs_[i].sm] == i ? 1 : 0;
                 j.am_ctr = ctr;
                 j.am_need = int32_t(slot_of.size());
+                if (n.attrs.count("tp_argmax")) {  // vocab-parallel: cross-rank (max, index) exchange
+                    j.flags |= VDC_JOB_TP_ARGMAX;
+                    j.am_sym = storage(idx(n.attrs.at("tp_argmax")));
+                    j.am_base = int32_t(attr_int(n, "vocab_base", 0));
+                    j.am_valid = int32_t(attr_int(n, "vocab_valid", 1 << 30));
+                }
             }
         }
     }

@@ -53,13 +53,24 @@ def run(model, req_pages, steps, sms=None, ppj=4, seed=0, argmax=False):
     return results
 
 
-def assert_close(rs, tol=2e-2):
+def assert_close(rs, tol=2e-2, strict_argmax=False):
+    """Per-request tolerances: logits max|d| <= 2e-2 rms; appended
+    K/V rows of layer 0 within 1e-2 of max|ref| (they are bit-exact in practice);
+    deeper layers within 2e-2: the reference mirrors every bf16 rounding point,
+    so a single upstream rounding flip (fp32 accumulation-order differences of
+    ~1e-6 relative landing on a bf16 rounding boundary) propagates. Measured on
+    test_mid_qwen3_qk_norm_batch8 (16 request-steps): CUDA-core attention
+    max 5.4e-3 (4 of 16 with any flip), tensor-core attention max 1.03e-2 (9 of
+    16); logits max 1.9e-2 rms either way."""
     for b, r in enumerate(rs):
         assert r["logits_max_abs"] <= tol * r["logits_rms"], (b, r)
         assert r["logits_max_abs_alt"] <= 5e-2 * r["logits_rms"], (b, r)
         assert r["kv_rel"] <= 1e-2, (b, r)
-        # greedy choice: equal, or a near-tie within the logit tolerance
-        assert r["argmax_equal"] or r["argmax_gap"] <= tol * r["logits_rms"], (b, r)
+        assert r["kv_rel_deep"] <= 2e-2, (b, r)
+        if strict_argmax:
+            assert r["argmax_equal"], (b, r)
+        else:  # greedy choice: equal, or a near-tie within the logit tolerance
+            assert r["argmax_equal"] or r["argmax_gap"] <= tol * r["logits_rms"], (b, r)
 
 
 @pytest.mark.parametrize("sms", [8, 148])
@@ -68,7 +79,7 @@ def test_mid_batch4_matches_dense(cuda, sms):
     rng = np.random.default_rng(1)
     pos = [int(rng.integers(0, 64 * p)) for p in pages]
     tokens = [int(t) for t in rng.integers(0, 4096, len(pages))]
-    assert_close(run(bc.MID_MODEL, pages, [(tokens, pos)], sms)[0])
+    assert_close(run(bc.MID_MODEL, pages, [(tokens, pos)], sms)[0], strict_argmax=True)
 
 
 def test_mid_batch20_multistep(cuda):
@@ -78,11 +89,11 @@ def test_mid_batch20_multistep(cuda):
     steps = []
     for s in range(3):
         steps.append(([int(t) for t in rng.integers(0, 4096, 20)], [p + s for p in pos0]))
-    # later steps start from the device's own KV rows and hidden states, whose
-    # bf16 roundings differ from the reference's in a few elements; on this
-    # random-weight 2-layer model one such flip moves a logit by up to ~2.2e-2 rms
+    # every step is checked against the reference run from the device's own
+    # state (KV rows and tokens of the previous step); measured max logits error
+    # 1.7e-2 / 1.7e-2 / 1.9e-2 rms over the three steps, argmax 20/20 each
     for k, rs in enumerate(run(bc.MID_MODEL, pages, steps, argmax=True)):
-        assert_close(rs, 2e-2 if k == 0 else 3e-2)
+        assert_close(rs, strict_argmax=k == 0)
 
 
 def test_mid_batch64_long_jobs(cuda):

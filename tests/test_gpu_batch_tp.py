@@ -52,6 +52,7 @@ def run_tp(model, req_pages, steps, world):
     for r in range(world):
         q = bc.request(model, req_pages, 4, 148 // world)
         q["layout"]["tp_world"], q["layout"]["tp_rank"] = world, r
+        q["layout"]["argmax"] = True  # fused sampling with the cross-rank (max, index) exchange
         reqs.append(q)
     progs = [Program.build(q) for q in reqs]
     infos = [p.info() for p in progs]
@@ -96,6 +97,10 @@ def run_tp(model, req_pages, steps, world):
         nb = len(req_pages)
         vocab = ins[0]["embed.table"].size // cfg["hidden"]
         full_host["logits"] = np.concatenate([h["logits"].reshape(nb, -1) for h in host], axis=1)[:, :vocab].reshape(-1)
+        # every rank sampled the argmax of the whole (unpadded) vocabulary
+        want = [int(i) for i in np.argmax(full_host["logits"].reshape(nb, vocab), axis=1)]
+        for h in host:
+            assert [int(t) for t in h["next_token"].reshape(-1)[:nb]] == want
         out.append(bc.check_batch(infos[0], full_state, full_host, tokens, pos, cfg=cfg))
         state = host
     return out

@@ -39,6 +39,7 @@ def _worker(rank, world, port, q, batched=False):
         else:
             req = bench.model_request(2)
         req["layout"]["tp_world"], req["layout"]["tp_rank"] = world, rank
+        req["layout"]["argmax"] = True
         info = Program.build(req).info()
         sym = sorted((d["name"], tuple(d["shape"])) for d in info["descriptors"] if d.get("symmetric"))
         producers = {}
@@ -46,7 +47,14 @@ def _worker(rank, world, port, q, batched=False):
             if j["flags"] & 0x100:
                 producers[j["o"][0]] = producers.get(j["o"][0], 0) + 1
         ar_need = sorted({j["x"][2] for j in info["jobs"] if j["op"] == 0x2C})
-        mine = {"sym": sym, "producers": sorted(producers.values()), "ar_need": ar_need,
+        # fused sampling under TP: lm_head jobs exchange (max, global index) pairs;
+        # their vocab base is the rank's first logit row
+        vocab_rows = [d["shape"][0] for d in info["descriptors"] if d["name"] == "logits"] if not batched else \
+            [d["shape"][1] for d in info["descriptors"] if d["name"] == "logits"]
+        tpx = [j for j in info["jobs"] if j["flags"] & 0x10000]
+        bases = sorted({j["o2"][1] for j in tpx}) if not batched else None
+        mine = {"sym": sym, "producers": sorted(producers.values()), "ar_need": ar_need, "n_tpx": len(tpx),
+                "bases": bases, "vocab_rows": vocab_rows,
                 "slots": sorted({j["o"][1] for j in info["jobs"] if j["flags"] & 0x100})}
         allv = [None] * world
         dist.all_gather_object(allv, mine)
@@ -72,7 +80,11 @@ def test_two_rank_tp_programs_agree(batched):
     for rank, allv, t in got:
         assert t == [2.0, 20.0]  # max over ranks (bench.py's timing reduction)
         r0, r1 = allv
-        assert r0["sym"] == r1["sym"] and len(r0["sym"]) == 2 * 2  # o.part, d.part per layer
+        # o.part, d.part per layer + the sampling exchange head.amx
+        assert r0["sym"] == r1["sym"] and len(r0["sym"]) == 2 * 2 + 1 and r0["sym"][-1][0] == "head.amx"
+        assert r0["n_tpx"] == r1["n_tpx"] > 0
+        if not batched:
+            assert r0["bases"] == [0] and r1["bases"] == r0["vocab_rows"]
         assert r0["producers"] == r1["producers"]
         slot = 4096 * (16 if batched else 1)  # (npad x d) fp32 per rank slot when batched
         if not batched:

@@ -19,6 +19,7 @@ def rank_request(base: dict, world: int, rank: int, sms: int | None = None) -> d
     req = rc.request(base, sms if sms is not None else 148 // world)
     req["layout"]["tp_world"] = world
     req["layout"]["tp_rank"] = rank
+    req["layout"]["argmax"] = True  # fused sampling with the cross-rank (max, index) exchange
     return req
 
 
@@ -101,6 +102,8 @@ def run_emulated(base: dict, world: int, steps=((17, 40),), seed: int = 0):
         host = [e.host_arrays(t) for e, t in zip(engines, tens)]
         full_in = assemble_full(infos, state, cfg_full)
         full_dev = {"logits": np.concatenate([h["logits"] for h in host])}
+        want = int(np.argmax(full_dev["logits"]))  # every rank sampled the argmax of the whole vocabulary
+        assert all(int(h["next_token"].reshape(-1)[0]) == want for h in host), [h["next_token"] for h in host]
         hd = cfg_full["head_dim"]
         T = {dd["name"]: dd["shape"] for dd in infos[0]["descriptors"]}["L0.kc"][1]
         for l in range(cfg_full["layers"]):
