@@ -30,6 +30,49 @@ int main() {
                 rep.status == machine::Termination::completed ? "completed" : "deadlock",
                 (unsigned long long)rep.uops_executed, (long long)rep.makespan, cs);
 
+    // the report's serialisations (reference machine.hpp:84-87): JSON round
+    // trip, key=value text, Chrome trace; conservation measured on the device
+    const std::string js = rep.to_json();
+    const auto back = machine::ExecutionReport::from_json(js);
+    const std::string kv = rep.to_kv_text(), ct = rep.chrome_trace();
+    size_t kv_lines = 0;
+    for (char ch : kv) kv_lines += ch == '\n';
+    std::printf("fig4 report: json_roundtrip=%s trace_events=%zu busy_resources=%zu kv_lines=%zu chrome_bytes=%zu "
+                "queues_drained=%d slots_all_free=%d\n",
+                back.to_json() == js ? "exact" : "MISMATCH", rep.trace.size(), rep.busy.size(), kv_lines, ct.size(),
+                int(rep.queues_drained), int(rep.slots_all_free));
+
+    // a wait that can never be satisfied: sm0.vmc first waits on dep queue 9,
+    // whose declared producer (sm1.vmc) never stores to it -> the device
+    // watchdog reports a deadlock and wait_for_edges() names the wait
+    auto stuck = p;
+    generator::QueueInfo q9;
+    q9.dep_id = 9;
+    q9.producer = generator::CoreId::vmc(1);
+    q9.consumer = generator::CoreId::vmc(0);
+    q9.depth = 2;
+    stuck.queues.push_back(q9);
+    isa::UopWord w;
+    w.opcode = isa::Opcode::LOAD_DEP;
+    w.dep_id = 9;
+    w.flow = 1;
+    auto& s0 = stuck.streams.at(generator::CoreId::vmc(0));
+    s0.insert(s0.begin(), w);
+    auto& m0 = stuck.meta.at(generator::CoreId::vmc(0));
+    m0.insert(m0.begin(), generator::UopMeta{});
+    machine::MachineOptions so;
+    so.watchdog_ms = 200;
+    machine::Machine sm(stuck, hw, machine::synthesize_program_inputs(stuck), so);
+    const auto dr = sm.run();
+    const auto edges = sm.wait_for_edges();
+    bool named = false;
+    for (const auto& e : edges) {
+        std::printf("wait edge: %s -> %s (%s)\n", e.from.name().c_str(), e.to.name().c_str(), e.reason.c_str());
+        named = named || (e.from == generator::CoreId::vmc(0) && e.to == generator::CoreId::vmc(1) && e.reason == "dep 9 empty");
+    }
+    std::printf("stuck program: status=%s edges=%zu named=%s\n",
+                dr.status == machine::Termination::deadlock ? "deadlock" : "completed", edges.size(), named ? "yes" : "no");
+
     decode::LayoutConfig lay;
     lay.ring = true;
     lay.gu_block = 16;
@@ -44,5 +87,9 @@ int main() {
     std::printf("tiny decode (ring): status=%s tile_loads=%llu makespan_ns=%lld checksum(logits)=%.6f\n",
                 r2.status == machine::Termination::completed ? "completed" : "deadlock",
                 (unsigned long long)r2.uops_executed, (long long)r2.makespan, lg);
-    return rep.status == machine::Termination::completed && r2.status == machine::Termination::completed ? 0 : 1;
+    return rep.status == machine::Termination::completed && r2.status == machine::Termination::completed &&
+                   back.to_json() == js && rep.queues_drained && rep.slots_all_free &&
+                   dr.status == machine::Termination::deadlock && named
+               ? 0
+               : 1;
 }

@@ -13,11 +13,19 @@
 //   MachineError                                any other C-ABI failure
 //
 // Deviations (documented, not hidden): the device runs the whole program in
-// one launch, so step() executes to completion and returns no events;
-// makespan is measured device time in ns, not a modelled clock; busy
-// intervals and the event trace are not recorded (see vdc_bind_trace).
+// one launch, so step() executes it to completion and returns every traced
+// event at once; makespan is measured device time in ns, not a modelled
+// clock; the event trace and busy intervals are the device trace of the
+// compute µops (vdc_bind_trace: per µop its dependency-ready and done times;
+// memory-core µops are not individually timed on the device);
+// queues_drained / slots_all_free are the device's own end-of-launch counts;
+// wait_for_edges() after a deadlock names, for every core the watchdog found
+// blocked, the core it waits on and why (the reference's stall reasons,
+// elaborate.cpp:193-214). ExecutionReport's to_json / from_json / to_kv_text /
+// chrome_trace live in libvdc.so (csrc/host/report.cpp).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -113,12 +121,18 @@ struct ExecutionReport {
     std::string profile_name;
     double dram_bw = 0;
     int64_t dram_busy_ns = 0;
+
+    std::string to_json() const;
+    static ExecutionReport from_json(const std::string& text);
+    std::string to_kv_text() const;
+    std::string chrome_trace() const;  // Chrome Trace Event JSON array
 };
 
 struct MachineOptions {
-    bool record_trace = true;  // accepted for source compatibility (no event trace on device)
+    bool record_trace = true;       // device trace of every compute µop (vdc_bind_trace)
     int device = 0;
     uint32_t watchdog_ms = 2000;
+    uint32_t trace_records = 4096;  // per compute core
 };
 
 namespace detail {
@@ -218,15 +232,25 @@ class Machine {
             upload(d, dptr, host);
             detail::check(vdc_bind_tensor(ctx_, uint16_t(i), dptr, n * eb, int(d.elem)));
         }
-        if (p.step_scalars) {
-            cudaMalloc(&step_, sizeof(int64_t) * 8);
-            cudaMemset(step_, 0, sizeof(int64_t) * 8);
-            detail::check(vdc_bind_step(ctx_, static_cast<int64_t*>(step_), 8));
+        if (p.step_scalars) {  // per-launch scalars (decode: token / pos / ctx, batched: + page table)
+            n_step_ = std::max<uint32_t>(8u, p.step_scalars);
+            cudaMalloc(&step_, sizeof(int64_t) * n_step_);
+            cudaMemset(step_, 0, sizeof(int64_t) * n_step_);
+            detail::check(vdc_bind_step(ctx_, static_cast<int64_t*>(step_), n_step_));
+        }
+        n_cores_ = prof.sm_count * (1u + prof.vcc_per_sm);
+        per_sm_ = 1u + prof.vcc_per_sm;
+        if (opt.record_trace && opt.trace_records) {
+            const size_t n = size_t(n_cores_) * opt.trace_records * 4;
+            if (cudaMalloc(&trace_, n * sizeof(uint64_t)) != cudaSuccess) throw MachineError("cudaMalloc failed for the trace");
+            cudaMemset(trace_, 0, n * sizeof(uint64_t));
+            detail::check(vdc_bind_trace(ctx_, trace_, opt.trace_records));
         }
     }
     ~Machine() {
         for (auto& b : bufs_) cudaFree(b.ptr);
         if (step_) cudaFree(step_);
+        if (trace_) cudaFree(trace_);
         if (ctx_) vdc_destroy(ctx_);
     }
     Machine(Machine&& o) noexcept { swap(o); }
@@ -237,18 +261,27 @@ class Machine {
     Machine(const Machine&) = delete;
     Machine& operator=(const Machine&) = delete;
 
-    // ext: per-launch scalars of decode programs (token, position, context)
+    // ext: per-launch scalars of decode programs, sized by the program
+    // (LoweredProgram::step_scalars): single request (token, position, context);
+    // batched: (token, position, context) per request, then the page table
     void set_step(const std::vector<int64_t>& s) {
-        std::vector<int64_t> v(8, 0);
-        for (size_t i = 0; i < s.size() && i < 8; ++i) v[i] = s[i];
-        if (step_) cudaMemcpy(step_, v.data(), sizeof(int64_t) * 8, cudaMemcpyHostToDevice);
+        if (!step_) throw MachineError("program has no step scalars");
+        if (s.size() > n_step_) throw MachineError("set_step: " + std::to_string(s.size()) + " scalars, the program reads " +
+                                                   std::to_string(n_step_));
+        std::vector<int64_t> v(n_step_, 0);
+        std::copy(s.begin(), s.end(), v.begin());
+        cudaMemcpy(step_, v.data(), sizeof(int64_t) * n_step_, cudaMemcpyHostToDevice);
     }
+    uint32_t step_scalars() const { return n_step_; }
 
     bool done() const { return done_; }
     int64_t now() const { return now_; }
+    // the device runs the whole program per launch: the first step() runs it
+    // and returns every traced event; later calls return nothing
     std::vector<TraceEvent> step() {
-        if (!done_) last_ = run();
-        return {};
+        if (done_) return {};
+        last_ = run();
+        return last_.trace;
     }
 
     ExecutionReport run(uint64_t watchdog = 1000) {
@@ -271,12 +304,20 @@ class Machine {
                                                        : generator::CoreId::vcc_id(uint16_t(core / per), uint8_t(core % per - 1)));
         }
         for (const auto& b : bufs_) r.tensors.emplace(p_.descriptors[b.desc].tensor, download(p_.descriptors[b.desc], b.ptr, b.n));
+        r.queues_drained = rep.queues_drained != 0;
+        r.slots_all_free = rep.slots_all_free != 0;
+        if (trace_) read_trace(r);
+        edges_.clear();
+        if (r.status == Termination::deadlock)
+            for (uint32_t i = 0; i < rep.n_stalled && i < 16; ++i) edges_.push_back(edge_of(r.deadlock_cycle[i], rep.stalled_pc[i]));
+        r.wait_edges = edges_;
         done_ = true;
         now_ = r.makespan;
         return r;
     }
 
-    std::vector<WaitEdge> wait_for_edges() const { return {}; }
+    // wait-for edges of the last run's blocked cores (empty unless it deadlocked)
+    std::vector<WaitEdge> wait_for_edges() const { return edges_; }
     const SlotAllocator& allocator(uint16_t) const { return alloc_; }
 
   private:
@@ -285,11 +326,95 @@ class Machine {
         void* ptr;
         size_t n;
     };
+    generator::CoreId core_of(uint32_t idx) const {
+        const uint32_t sm = idx / per_sm_, k = idx % per_sm_;
+        return k == 0 ? generator::CoreId::vmc(uint16_t(sm)) : generator::CoreId::vcc_id(uint16_t(sm), uint8_t(k - 1));
+    }
+    // device trace -> events (ts = dependency-ready time, dur = execution) and
+    // per-core busy intervals, relative to the first traced µop
+    void read_trace(ExecutionReport& r) const {
+        std::vector<uint64_t> rec(size_t(n_cores_) * opt_.trace_records * 4);
+        cudaMemcpy(rec.data(), trace_, rec.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost);
+        int64_t t0 = INT64_MAX;
+        for (size_t i = 0; i < rec.size(); i += 4)
+            if (rec[i + 1]) t0 = std::min<int64_t>(t0, int64_t(rec[i + 1]));
+        std::map<generator::CoreId, uint64_t> inst;
+        for (size_t i = 0; i < rec.size(); i += 4) {
+            if (!rec[i + 1]) continue;
+            const auto core = core_of(uint32_t(rec[i] >> 32));
+            const uint32_t pc = uint32_t(rec[i] & 0xffffffffu);
+            TraceEvent e;
+            e.core = core;
+            e.resource = core.name();
+            e.stream_index = pc;
+            e.instance = inst[core]++;
+            e.ts = int64_t(rec[i + 2]) - t0;
+            e.dur = std::max<int64_t>(0, int64_t(rec[i + 3]) - int64_t(rec[i + 2]));
+            if (const auto it = p_.streams.find(core); it != p_.streams.end() && pc < it->second.size()) {
+                e.name = std::string(isa::opcode_name(it->second[pc].opcode));
+                e.flow = it->second[pc].flow;
+            }
+            r.busy[e.resource].push_back({e.ts, e.ts + e.dur});
+            r.trace.push_back(std::move(e));
+        }
+    }
+    // what a blocked core waits for, from the µop it is stuck at (the
+    // reference elaboration's stall reasons, elaborate.cpp:193-214, 318-340)
+    WaitEdge edge_of(const generator::CoreId& core, uint32_t pc) const {
+        WaitEdge e{core, core, "blocked"};
+        const auto it = p_.streams.find(core);
+        if (it == p_.streams.end() || pc >= it->second.size()) return e;
+        const auto& u = it->second[pc];
+        const auto vcc = generator::CoreId::vcc_id(core.sm, uint8_t(u.reg1));
+        if (isa::is_dep_consumer(u.opcode) || isa::is_dep_producer(u.opcode)) {
+            for (const auto& q : p_.queues)
+                if (q.dep_id == u.dep_id) {
+                    const bool cons = isa::is_dep_consumer(u.opcode);
+                    e.to = cons ? q.producer : q.consumer;
+                    e.reason = "dep " + std::to_string(u.dep_id) + (cons ? " empty" : " full");
+                    return e;
+                }
+        }
+        if (core.kind == isa::CoreKind::vcc) {
+            e.to = generator::CoreId::vmc(core.sm);
+            e.reason = "m2c empty";
+        } else if (u.recv()) {
+            e.to = vcc;
+            e.reason = "c2m short";
+        } else if (u.send()) {
+            e.to = vcc;
+            e.reason = "m2c full / slot budget";
+        }
+        return e;
+    }
+    // device storage position of logical (row-major) element i: batched ring
+    // programs keep weights as pre-swizzled 128 x 64 tiles and KV page rows
+    // swizzled (ring_abi.h VDC_DESC_PACKED_SW128 / VDC_DESC_KPAGE_SWZ)
+    static size_t storage_index(const generator::TileDescriptor& d, size_t i) {
+        const size_t cols = size_t(d.shape.back());
+        const size_t r = i / cols, c = i % cols;
+        if (d.tma == VDC_DESC_PACKED_SW128) {
+            const size_t kt = cols / 64, rb = r / 128, rr = r % 128, t = c / 64, ch = (c % 64) / 8;
+            return ((rb * kt + t) * 128 + rr) * 64 + ((ch ^ (rr % 8)) * 8) + c % 8;
+        }
+        if (d.tma == VDC_DESC_KPAGE_SWZ) {
+            const size_t ch = c / 8;
+            return r * cols + (((ch & 8) | ((ch & 7) ^ (r & 7))) * 8) + c % 8;
+        }
+        return i;
+    }
+    static bool permuted(const generator::TileDescriptor& d) {
+        return d.tma == VDC_DESC_PACKED_SW128 || d.tma == VDC_DESC_KPAGE_SWZ;
+    }
     static void upload(const generator::TileDescriptor& d, void* dptr, const std::vector<float>& host) {
         if (d.elem == workload::ElemType::bf16) {
             std::vector<uint16_t> b(host.size());
-            for (size_t i = 0; i < host.size(); ++i) b[i] = detail::to_bf16(host[i]);
+            for (size_t i = 0; i < host.size(); ++i) b[permuted(d) ? storage_index(d, i) : i] = detail::to_bf16(host[i]);
             cudaMemcpy(dptr, b.data(), b.size() * 2, cudaMemcpyHostToDevice);
+        } else if (d.elem == workload::ElemType::i64) {
+            std::vector<int64_t> b(host.size());
+            for (size_t i = 0; i < host.size(); ++i) b[i] = int64_t(host[i]);
+            cudaMemcpy(dptr, b.data(), b.size() * 8, cudaMemcpyHostToDevice);
         } else {
             cudaMemcpy(dptr, host.data(), host.size() * 4, cudaMemcpyHostToDevice);
         }
@@ -299,7 +424,11 @@ class Machine {
         if (d.elem == workload::ElemType::bf16) {
             std::vector<uint16_t> b(n);
             cudaMemcpy(b.data(), dptr, n * 2, cudaMemcpyDeviceToHost);
-            for (size_t i = 0; i < n; ++i) out[i] = detail::from_bf16(b[i]);
+            for (size_t i = 0; i < n; ++i) out[i] = detail::from_bf16(b[permuted(d) ? storage_index(d, i) : i]);
+        } else if (d.elem == workload::ElemType::i64) {
+            std::vector<int64_t> b(n);
+            cudaMemcpy(b.data(), dptr, n * 8, cudaMemcpyDeviceToHost);
+            for (size_t i = 0; i < n; ++i) out[i] = float(b[i]);
         } else {
             cudaMemcpy(out.data(), dptr, n * 4, cudaMemcpyDeviceToHost);
         }
@@ -314,6 +443,12 @@ class Machine {
         std::swap(done_, o.done_);
         std::swap(now_, o.now_);
         std::swap(alloc_, o.alloc_);
+        std::swap(trace_, o.trace_);
+        std::swap(n_step_, o.n_step_);
+        std::swap(n_cores_, o.n_cores_);
+        std::swap(per_sm_, o.per_sm_);
+        std::swap(edges_, o.edges_);
+        std::swap(last_, o.last_);
     }
 
     generator::LoweredProgram p_;
@@ -325,6 +460,9 @@ class Machine {
     int64_t now_ = 0;
     SlotAllocator alloc_;
     ExecutionReport last_;
+    void* trace_ = nullptr;
+    uint32_t n_step_ = 0, n_cores_ = 0, per_sm_ = 1;
+    std::vector<WaitEdge> edges_;
 };
 
 inline ExecutionReport simulate(const generator::LoweredProgram& p, const costmodel::HardwareProfile& hw,

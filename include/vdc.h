@@ -92,6 +92,12 @@ typedef struct vdc_report {
      * vcc ready/barrier/c2m, vcc compute, cfu total, vcc total, ldu issue) */
     uint64_t wait_cycles[24];
     char message[256];
+    /* end-of-launch conservation (reference SPEC.md:402, machine.hpp
+     * ExecutionReport): every m2c / c2m / unit / dep queue empty (ring engine:
+     * every issued tile consumed), every slot free (ring engine: every ring
+     * slot handed back). Measured on the device, not assumed. */
+    uint32_t queues_drained;
+    uint32_t slots_all_free;
 } vdc_report;
 
 typedef struct vdc_ctx vdc_ctx;

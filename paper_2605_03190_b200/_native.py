@@ -64,6 +64,8 @@ class vdc_report(ctypes.Structure):
         ("stalled_pc", ctypes.c_uint32 * 16),
         ("wait_cycles", ctypes.c_uint64 * 24),
         ("message", ctypes.c_char * 256),
+        ("queues_drained", ctypes.c_uint32),
+        ("slots_all_free", ctypes.c_uint32),
     ]
 
 

@@ -284,10 +284,11 @@ struct UnitWords {
 __device__ __forceinline__ UnitWords pack_unit(uint32_t op, uint32_t flags, uint32_t reg1, uint32_t dtype, uint32_t dep,
                                                uint32_t size, const SlotList& l, uint32_t m2c, int32_t storage,
                                                uint32_t bytes, int32_t rows_at, int32_t cols_at, int32_t elem,
-                                               int32_t tile_cols, uint32_t core_pc, const char* gptr, int64_t gpitch) {
+                                               int32_t tile_cols, uint32_t core_pc, const char* gptr, int64_t gpitch,
+                                               uint32_t raw = 0) {
     UnitWords u;
     u.a = make_uint4(op | (flags << 8) | (reg1 << 16) | (dtype << 24), dep | (size << 16), l.lo, l.hi);
-    u.b = make_uint4(l.count | (uint32_t(elem) << 8), m2c, uint32_t(storage), bytes);
+    u.b = make_uint4(l.count | (uint32_t(elem) << 8) | (raw << 16), m2c, uint32_t(storage), bytes);
     u.c = make_uint4(uint32_t(rows_at), uint32_t(cols_at), uint32_t(tile_cols), core_pc);
     const unsigned long long p = reinterpret_cast<unsigned long long>(gptr);
     u.d = make_uint4(uint32_t(p), uint32_t(p >> 32), uint32_t(uint64_t(gpitch)), uint32_t(uint64_t(gpitch) >> 32));
@@ -303,6 +304,7 @@ __device__ __forceinline__ UnitOp unpack_unit(const UnitWords& u) {
     q.size = uint16_t(u.a.y >> 16);
     q.slots = SlotList{u.a.z, u.a.w, u.b.x & 0xff};
     q.elem = int32_t((u.b.x >> 8) & 0xff);
+    q.raw = u.b.x >> 16;
     q.m2c = u.b.y;
     q.storage = int32_t(u.b.z);
     q.bytes = u.b.w;
@@ -537,6 +539,22 @@ __device__ __noinline__ void cfu_role(Cta& c) {
             const uint32_t my_m2c = (v ? mh1 : mh0) + __popc((v ? s1 : s0) & lt);
             mh0 += __popc(s0);
             mh1 += __popc(s1);
+            // same-SM store -> load ordering: data stores dispatched before each
+            // load of the same tensor bucket (stream order = lane order)
+            uint32_t raw = 0;
+            {
+                const bool gst = act && (w.op == OP_STORE || w.op == OP_STORE_DEP) && (w.flags & F_RECV) && w.size > 0 &&
+                                 t.bytes > 0 && t.storage >= 0;
+                const bool gld = act && (w.op == OP_LOAD || w.op == OP_LOAD_DEP || w.op == OP_LOAD_WAIT) && t.bytes > 0 &&
+                                 t.storage >= 0;
+                const uint32_t bkt = uint32_t(t.storage) % kRawBuckets;
+                const uint32_t grp = __match_any_sync(0xffffffffu, (gst || gld) ? bkt : kRawBuckets + lane);
+                const uint32_t sm_ = __ballot_sync(0xffffffffu, gst);
+                if (gld) raw = (C.raw_disp[bkt] + __popc(grp & sm_ & lt)) & 0xffffu;
+                __syncwarp();
+                if (gst && (grp & sm_ & lt) == 0) C.raw_disp[bkt] += __popc(grp & sm_);  // first store lane of the group
+                __syncwarp();
+            }
             uint32_t my_pos = 0;
             {
                 const uint32_t b0 = __ballot_sync(0xffffffffu, act && unit == 0);
@@ -576,7 +594,7 @@ __device__ __noinline__ void cfu_role(Cta& c) {
                     const uint32_t nbytes = (w.size == 0 && w.op != OP_LOAD_LOCAL) ? 0u : t.bytes;
                     const UnitWords uw = pack_unit(w.op, w.flags, w.reg1, uint32_t(t.dtype), w.dep, w.size, l, my_m2c,
                                                    t.storage, nbytes, t.rows_at, t.cols_at, t.elem, t.tile_cols, pc + lane,
-                                                   t.gptr, t.gpitch);
+                                                   t.gptr, t.gpitch, raw);
                     store_unit(unit < 2 ? &C.ldu_q[unit][my_pos % kUnitDepth] : &C.stu_q[unit - 2][my_pos % kUnitDepth], uw);
                 }
                 const long long f0 = clock64();
@@ -605,6 +623,10 @@ __device__ __noinline__ void cfu_role(Cta& c) {
             if (wait[i]) atomicAdd(&c.P->stats[c.sm].wait[i], (unsigned long long)wait[i] << 6);
         atomicAdd(&c.P->stats[c.sm].uops, uops);
         for (int i = 0; i < 4; ++i) atomicAdd(&c.P->stats[c.sm].cfu_phase[i], phase[i]);
+        // the m2c heads live in the CFU's registers (consumers poll entry.ready):
+        // publish the final counts for the end-of-launch conservation check
+        C.m2c_ring[0].head = mh0;
+        C.m2c_ring[1].head = mh1;
         __threadfence_block();
         atomicAdd(const_cast<int32_t*>(&C.done_roles), 1);  // CFU finished dispatching
     }
@@ -672,6 +694,10 @@ __device__ __noinline__ void copy_in(Cta& c, const UnitOp& q, uint32_t lane) {
 // LDU: entries whose dependency is already satisfied and whose tile is one
 // bulk region are issued in parallel, one lane each; the first entry that
 // must wait (or needs a cooperative copy / a dep-queue token) is handled alone.
+__device__ __forceinline__ bool raw_ready(const Control& C, const UnitOp& q) {
+    return int16_t(uint16_t(C.raw_done[uint32_t(q.storage) % kRawBuckets] - q.raw)) >= 0;
+}
+
 __device__ __noinline__ void ldu_role(Cta& c, uint32_t u) {
     const EngineParams& P = *c.P;
     Control& C = *c.C;
@@ -703,12 +729,13 @@ __device__ __noinline__ void ldu_role(Cta& c, uint32_t u) {
         if (lane < nb) q = unpack_unit(load_unit(&C.ldu_q[u][(tail + lane) % kUnitDepth]));
         bool go = lane < nb && (q.op == OP_LOAD || q.op == OP_LOAD_WAIT) && (q.bytes == 0 || bulk_geometry(q));
         if (go && q.op == OP_LOAD_WAIT && q.dep_id) go = ld_relaxed(&P.counters[q.storage]) >= q.dep_id;
+        if (go && q.raw) go = raw_ready(C, q);
         const uint32_t stopm = __ballot_sync(0xffffffffu, !go) | (nb < 32 ? (0xffffffffu << nb) : 0u);
         const uint32_t pre = stopm ? uint32_t(__ffs(stopm) - 1) : 32u;
         if (pre > 0) {
             const long long i0 = clock64();
             if (lane < pre) {
-                if (q.op == OP_LOAD_WAIT && q.dep_id) {
+                if ((q.op == OP_LOAD_WAIT && q.dep_id) || q.raw) {  // data written by generic stores: into the async proxy
                     fence_acquire_gpu();
                     fence_proxy_async();
                 }
@@ -763,6 +790,15 @@ __device__ __noinline__ void ldu_role(Cta& c, uint32_t u) {
             if (lane == 0) {
                 const uint32_t* ctr = &P.counters[h.storage];
                 ok = spin_until(c, [&] { return ld_relaxed(ctr) >= h.dep_id; }, core, h.core_pc, &wait[W_LDU_DEP]);
+                fence_acquire_gpu();
+                fence_proxy_async();
+            }
+            ok = __shfl_sync(0xffffffffu, ok, 0);
+            if (!ok) break;
+        }
+        if (h.raw) {  // this SM's earlier stores to the tile's bucket must be written first
+            if (lane == 0) {
+                ok = spin_until(c, [&] { return raw_ready(C, h); }, core, h.core_pc, &wait[W_LDU_DEP]);
                 fence_acquire_gpu();
                 fence_proxy_async();
             }
@@ -888,7 +924,10 @@ __device__ __noinline__ void stu_role(Cta& c, uint32_t u) {
             if (lane == 0) {
                 if (data) {
                     __threadfence();
-                    if (q.storage >= 0) red_release_add(&P.counters[q.storage], 1u);
+                    if (q.storage >= 0) {
+                        red_release_add(&P.counters[q.storage], 1u);
+                        atomicAdd(const_cast<uint32_t*>(&C.raw_done[uint32_t(q.storage) % kRawBuckets]), 1u);
+                    }
                 }
                 if (q.op == OP_STORE_DEP || q.op == OP_STORE_LOCAL) {
                     DepQueue* dq = &P.deps[q.dep_id];
@@ -1790,6 +1829,16 @@ __global__ void __launch_bounds__(32 * (1 + kMaxLdu + kMaxStu + kMaxVcc * kVccWa
     } else {
         cfu_role(c);
     }
+    // every role has returned: record what is left in the SM's queues and slots
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t pending = 0;
+        for (int i = 0; i < kMaxVcc; ++i) pending += (C.m2c_ring[i].head != C.m2c_ring[i].tail) + (C.c2m_ring[i].head != C.c2m_ring[i].tail);
+        for (int i = 0; i < kMaxLdu; ++i) pending += C.ldu_ring[i].head != C.ldu_ring[i].tail;
+        for (int i = 0; i < kMaxStu; ++i) pending += C.stu_ring[i].head != C.stu_ring[i].tail;
+        P.stats[blockIdx.x].rings_pending = pending;
+        P.stats[blockIdx.x].slot_mask = C.alloc_mask;
+    }
 }
 
 }  // namespace vdc_dev
@@ -2380,6 +2429,24 @@ int vdc_wait(vdc_ctx* ctx, vdc_report* r) {
         if (ctx->ring) {
             std::snprintf(r->message, sizeof r->message, "ring engine: %u slots x 16 KB, epoch %u", ctx->ring_slots, ctx->epoch);
         }
+        // conservation at termination: the device's own end-of-launch counts
+        bool drained = true, free_ = true;
+        for (const auto& s : stats) {
+            if (ctx->ring) {
+                drained = drained && s.tiles_issued == s.tiles_consumed;
+                free_ = free_ && s.tiles_issued == s.tiles_consumed;
+            } else {
+                drained = drained && s.rings_pending == 0;
+                free_ = free_ && s.slot_mask == 0;
+            }
+        }
+        if (!ctx->ring && !ctx->dep_init.empty()) {  // global dep queues: every token produced was consumed
+            std::vector<DepQueue> dq(ctx->dep_init.size());
+            CU(cudaMemcpy(dq.data(), ctx->d_deps, sizeof(DepQueue) * dq.size(), cudaMemcpyDeviceToHost));
+            for (const auto& q : dq) drained = drained && q.produced == q.consumed;
+        }
+        r->queues_drained = drained ? 1u : 0u;
+        r->slots_all_free = free_ ? 1u : 0u;
         r->status = st.abort == 0 ? VDC_OK : st.abort == 1 ? VDC_ERR_DEADLOCK : VDC_ERR_INTERNAL;
         if (st.abort == 1)
             std::snprintf(r->message, sizeof r->message, "deadlock: %d core(s) made no progress for %u ms (core %u, info 0x%x)",

@@ -68,6 +68,10 @@ struct SmStats {
     unsigned long long cfu_stall_cycles;
     unsigned long long wait[24];
     unsigned long long cfu_phase[4];  // refill, resolve, m2c, unit push
+    // end-of-launch conservation: reference-form engine: rings
+    // (m2c / c2m / unit queues) still holding entries and the slot mask; ring
+    // engine: tiles issued by the memory core and consumed by the compute core
+    unsigned long long rings_pending, slot_mask, tiles_issued, tiles_consumed;
 };
 
 struct Status {
@@ -173,7 +177,16 @@ struct alignas(16) UnitOp {
     char* gptr;           // first element of the tile in global memory
     int64_t gpitch;       // global row pitch in bytes
     uint32_t core_pc;
+    uint32_t raw;         // loads: data stores of this SM to the tile's bucket that must complete first (mod 2^16)
 };
+
+// Same-SM store -> load ordering (reference elaborate.cpp:175-279: a memory
+// core executes its µops one at a time in stream order, so a LOAD sees every
+// earlier STORE of its stream): data stores are counted per tensor bucket
+// (storage % kRawBuckets) when the CFU dispatches them and when the STU has
+// written them; a LOAD of that bucket issues once the written count reaches
+// the dispatched count it saw (loads and stores run on different units).
+constexpr int kRawBuckets = 64;
 
 struct Ring {
     volatile uint32_t head;
@@ -209,6 +222,8 @@ struct alignas(16) Control {
     float acc[kMaxVcc][kAccRows];
     float red[kMaxVcc][32];
     volatile int32_t done_roles;
+    uint32_t raw_disp[kRawBuckets];           // CFU: data stores dispatched per bucket
+    volatile uint32_t raw_done[kRawBuckets];  // STU: data stores written per bucket
 };
 
 }  // namespace vdc_dev

@@ -2142,6 +2142,7 @@ __device__ __forceinline__ void vcc_role(const RingParams& P, Shared& S, char* r
         st.wait[S_VCC_EPI] = v.st_epi;
         st.wait[S_VCC_TOTAL] = clock64() - t0;
         st.wait[S_NJOBS] = jobs;
+        st.tiles_consumed = v.kt;  // ring tiles taken from (and handed back to) the memory core
         if constexpr (BATCHED) {
             st.wait[S_X_FULL] = v.st_xf;
             st.wait[S_X_EMPTY] = v.st_xe;
@@ -2357,6 +2358,7 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
         st.bytes_loaded = bytes;
         st.uops = uops;
         st.bytes_stored = 0;
+        st.tiles_issued = uops;
     }
 }
 

@@ -28,6 +28,8 @@ class Report:
     message: str
     stalled: list = field(default_factory=list)
     wait_cycles: dict = field(default_factory=dict)
+    queues_drained: bool = True   # measured on the device at the end of the launch
+    slots_all_free: bool = True
 
     @property
     def completed(self) -> bool:
@@ -291,7 +293,8 @@ class Engine:
         names = RING_SITES if self.info.get("ring_slots") else WAIT_SITES
         return Report(r.status, r.uops_executed, r.bytes_loaded, r.bytes_stored, r.elapsed_ms, r.message.decode(),
                       [(r.stalled_core[i], r.stalled_pc[i]) for i in range(min(16, r.n_stalled))],
-                      {name: int(r.wait_cycles[i]) for i, name in enumerate(names)})
+                      {name: int(r.wait_cycles[i]) for i, name in enumerate(names)},
+                      bool(r.queues_drained), bool(r.slots_all_free))
 
     def run(self, stream=None) -> Report:
         self.launch(stream)

@@ -20,7 +20,7 @@ from paper_2605_03190_b200 import Program, VdcError
 pytestmark = pytest.mark.gpu
 
 CASES = [(n, r) for n, r in corpus.cases() if not n.startswith("err_")]
-KNOWN_DEVIATIONS = {"fig4_nofusion"}  # see DESIGN.md "open issues": STORE_DEP re-read ordering without fusion
+KNOWN_DEVIATIONS: set = set()
 
 
 def run_case(name, req, step=None):
@@ -40,6 +40,8 @@ def run_case(name, req, step=None):
         raise
     assert rep.status == 0, rep.message
     assert rep.uops_executed == idx["uops"]
+    # SPEC.md:402 conservation, measured on the device: all queues empty, all slots free
+    assert rep.queues_drained and rep.slots_all_free, (rep.queues_drained, rep.slots_all_free)
     return harness.compare(host, outs, 1e-4)
 
 

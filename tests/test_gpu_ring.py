@@ -137,7 +137,16 @@ def test_cpp_machine_dropin_runs(cuda):
     import subprocess
     from pathlib import Path
     root = Path(__file__).resolve().parents[1]
-    subprocess.run(["make", "-C", str(root / "examples"), "machine_demo"], check=True, capture_output=True)
+    subprocess.run(["make", "-C", str(root / "examples"), "all"], check=True, capture_output=True)
     r = subprocess.run([str(root / "examples" / "machine_demo")], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "fig4: status=completed" in r.stdout and "tiny decode (ring): status=completed" in r.stdout
+    # ExecutionReport serialisations + device conservation counts, and the
+    # wait-for edge of a program stuck on a dep queue nobody produces
+    assert "json_roundtrip=exact" in r.stdout and "queues_drained=1 slots_all_free=1" in r.stdout, r.stdout
+    assert "stuck program: status=deadlock" in r.stdout and "named=yes" in r.stdout, r.stdout
+    # a batched program driven from C++: step block sized by the program,
+    # page table from the vdc_kv_* block allocator, fused sampling
+    b = subprocess.run([str(root / "examples" / "batched_demo")], capture_output=True, text=True, timeout=120)
+    assert b.returncode == 0, b.stdout + b.stderr
+    assert b.stdout.count("status=completed") == 4, b.stdout
