@@ -940,14 +940,21 @@ struct Vcc {
                 return true;
             };
             for (int t = t0, u = 0; t < n && u < int(NXW) && good; t += CW, ++u) good = xload(t);
+            // debug tile trace (VDC_RING_DEBUG): loop top / activation chunk landed,
+            // weight tile landed / MMAs committed
+            unsigned long long* tt = (P->tile_trace && sm == (P->debug >> 8)) ? P->tile_trace : nullptr;
             for (int t = t0; t < n && good; t += CW) {
                 const uint32_t g = kt + uint32_t(t), slot = g % R;
+                const bool ttr = tt && g < 30000u;
+                if (ttr) tt[100000 + 2 * g] = now_ns();
                 const uint32_t xi = w * NXW + xd % NXW;
                 const long long wc = spin(&S->xfull[xi], (xd / NXW) & 1u);
+                if (ttr) tt[100000 + 2 * g + 1] = now_ns();
                 if (wc < 0 || !wait_full(slot, (g / R) & 1u)) {
                     good = false;
                     break;
                 }
+                if (ttr) tt[3 * g + 1] = now_ns();
                 st_xf += wc;
                 tc_fence_after();
                 if (!(P->debug & 1u)) {
@@ -959,6 +966,7 @@ struct Vcc {
                 }
                 umma_commit(&S->empty[slot]);  // W slot -> memory core when its MMAs are done
                 umma_commit(&S->xempty[xi]);
+                if (ttr) tt[3 * g + 2] = now_ns();
                 ++xd;
                 if (t + int(NXW) * CW < n && !xload(t + int(NXW) * CW)) {
                     good = false;

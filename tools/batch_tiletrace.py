@@ -44,16 +44,19 @@ g = np.diff(iss)
 print("issue gaps (ns): p50 %d p90 %d p99 %d" % tuple(np.percentile(g, [50, 90, 99])))
 seen = np.sort(b[:, 1]); gs = np.diff(seen)
 print("issuer tile-to-tile gaps (ns): p10 %d p50 %d p90 %d" % tuple(np.percentile(gs, [10, 50, 90])))
-# BGEMM tiles: the issuer holds them < 1 us (attention pages take several)
+# BGEMM tiles: those with activation-chunk stamps (tile_trace[100000 + 2g])
 A = a - t0
-bg = ok & ((a[:, 2] - a[:, 1]) < 1000)
+xt = XT[:len(A)]
+bg = ok & (xt[:, 1] > 0)
 ib = np.where(bg)[0]
-lat = A[ib, 1] - A[ib, 0]
-print("BGEMM tiles", len(ib), "issue->seen p10/p50/p90", np.percentile(lat, [10, 50, 90]).astype(int))
-cons = [(A[j, 1] - A[i, 1]) for i, j in zip(ib[:-1], ib[1:]) if j == i + 1]
-print("BGEMM consecutive seen gaps p10/p50/p90", np.percentile(cons, [10, 50, 90]).astype(int))
-# slot turnaround: commit of tile g -> issue of tile g + 8 (same slot)
-turn = [A[g + 8, 0] - A[g, 2] for g in ib if g + 8 < len(A) and A[g + 8, 0] > 0]
-print("commit -> next issue in the slot p10/p50/p90", np.percentile(turn, [10, 50, 90]).astype(int))
-for g in ib[100:140]:
-    print(g, "issue", A[g, 0] % 10**7, "loop top", (XT[g, 0] - t0) % 10**7, "xchunk ok", (XT[g, 1] - t0) % 10**7, "W seen", A[g, 1] % 10**7, "commit", A[g, 2] % 10**7)
+print("BGEMM tiles", len(ib))
+if len(ib):
+    X = xt[ib] - t0
+    print("  W issue -> W landed/seen      p10/p50/p90", np.percentile(A[ib, 1] - A[ib, 0], [10, 50, 90]).astype(int))
+    print("  loop top -> X chunk ready     p10/p50/p90", np.percentile(X[:, 1] - X[:, 0], [10, 50, 90]).astype(int))
+    print("  X ready -> W seen             p10/p50/p90", np.percentile(A[ib, 1] - X[:, 1], [10, 50, 90]).astype(int))
+    print("  W seen -> MMAs committed      p10/p50/p90", np.percentile(A[ib, 2] - A[ib, 1], [10, 50, 90]).astype(int))
+    turn = [A[g + 8, 0] - A[g, 2] for g in ib if g + 8 < len(A) and A[g + 8, 0] > 0]
+    print("  commit -> next issue in slot  p10/p50/p90", np.percentile(turn, [10, 50, 90]).astype(int))
+    for g in ib[:: max(1, len(ib) // 40)]:
+        print(g, "issue", A[g, 0], "loop top", xt[g, 0] - t0, "x ready", xt[g, 1] - t0, "W seen", A[g, 1], "commit", A[g, 2])
