@@ -79,6 +79,11 @@ struct alignas(16) Shared {
     uint64_t xfull[NXMAX], xempty[NXMAX], mma_bar;
     uint32_t tmem_base;
     float binv[VDC_RING_MAX_BATCH];
+    // compute-core wait-site cycles and the trace's readiness stamp, updated by
+    // thread 0 only: in shared memory, not in registers that every compute
+    // thread would carry through the whole µop loop
+    unsigned long long vstat[8];
+    unsigned long long t_ready;
     float am_v[VDC_RING_MAX_BATCH];  // batched greedy sampling: this SM's best logit per request
     int32_t am_i[VDC_RING_MAX_BATCH];
 };
@@ -202,8 +207,9 @@ struct Vcc {
     uint32_t kt = 0;  // ring tiles consumed so far (program order, uniform over the VCC)
     uint32_t R;
     bool ok = true;
-    unsigned long long st_full = 0, st_dep = 0, st_epi = 0;
-    unsigned long long t_ready = 0;  // trace: when the last readiness wait of the running µop completed
+    // wait-site cycle counters (thread 0, shared memory): VS_* slots of S->vstat
+    enum : int { VS_FULL = 0, VS_DEP, VS_EPI, VS_XF, VS_XE, VS_MMA, VS_PRO };
+    __device__ void stat_add(int k, long long c) const { S->vstat[k] += (unsigned long long)c; }
     uint32_t n_attn = 0;             // debug stamps
     float resid = 0.f;               // GEMV_ADD: this thread's residual element, loaded before the tile sweep
     int32_t rope_hd = 0;             // head dim of the cached rotary table (0 = none)
@@ -235,7 +241,7 @@ struct Vcc {
     __device__ bool wait_full(uint32_t slot, uint32_t parity) {
         const long long c0 = clock64();
         if (mbar_try(&S->full[slot], parity)) {
-            if (ct == 0) st_full += clock64() - c0;
+            if (ct == 0) stat_add(VS_FULL, clock64() - c0);
             return true;
         }
         const unsigned long long t0 = now_ns();
@@ -249,7 +255,7 @@ struct Vcc {
                 }
             }
         }
-        if (ct == 0) st_full += clock64() - c0;
+        if (ct == 0) stat_add(VS_FULL, clock64() - c0);
         return true;
     }
     __device__ void release(uint32_t slot) {
@@ -299,8 +305,8 @@ struct Vcc {
                     fence_acquire_gpu();
             }
             S->flag = good ? 1 : 0;
-            st_dep += clock64() - c0;
-            if (P->trace) t_ready = now_ns();
+            stat_add(VS_DEP, clock64() - c0);
+            if (P->trace) S->t_ready = now_ns();
         }
         sync();
         return S->flag != 0;
@@ -415,7 +421,7 @@ struct Vcc {
         sync();  // (an aborted launch runs on through the epilogue: every warp must reach the same barriers)
         const long long e0 = clock64();
         gemv_epilogue(J, J.r1 - J.r0);
-        if (ct == 0) st_epi += clock64() - e0;
+        if (ct == 0) stat_add(VS_EPI, clock64() - e0);
         if (J.flags & VDC_JOB_QKV) {
             const int qrows = J.block, kvr = J.split;
             sync();
@@ -863,7 +869,6 @@ struct Vcc {
     __device__ uint16_t* u16p(int32_t t) const { return reinterpret_cast<uint16_t*>(tptr(t)); }
     __device__ int64_t req_pos(int b) const { return P->step[3 * b + 1]; }
 
-    unsigned long long st_xf = 0, st_xe = 0, st_mma = 0, st_pro = 0;
     // wait for an mbarrier phase; returns the cycles waited, or -1 if the
     // launch aborted (no member addresses escape: the Vcc stays in registers)
     __device__ long long spin(uint64_t* bar, uint32_t parity) {
@@ -910,7 +915,7 @@ struct Vcc {
         // 128-byte swizzle atoms repeat every 1 KB), NXW per compute warp
         const uint32_t xb0 = (smem_addr(S) + uint32_t(sizeof(Shared)) + 1023u) & ~1023u;
         const uint32_t NXW = min(2u, XRING_BYTES / xbytes / uint32_t(CW));
-        if (ct == 0) st_pro += clock64() - p0;
+        if (ct == 0) stat_add(VS_PRO, clock64() - p0);
         if (ct == 0) S->flag = 1;
         sync();
         // Every compute warp is an MMA issuer (lane 0) for the tiles of its own
@@ -932,7 +937,7 @@ struct Vcc {
                 if (xq >= NXW) {
                     const long long c = spin(&S->xempty[i], ((xq / NXW) - 1u) & 1u);
                     if (c < 0) return false;
-                    st_xe += c;
+                    if (ct == 0) stat_add(VS_XE, c);
                 }
                 mbar_expect_tx(&S->xfull[i], xbytes);
                 tma_2d(xb0 + i * xbytes, xm, (J.kt0 + t) * VDC_RING_BGEMM_KT, 0, &S->xfull[i]);
@@ -955,7 +960,7 @@ struct Vcc {
                     break;
                 }
                 if (ttr) tt[3 * g + 1] = now_ns();
-                st_xf += wc;
+                if (ct == 0) stat_add(VS_XF, wc);
                 tc_fence_after();
                 if (!(P->debug & 1u)) {
                     const uint32_t a0 = ring + slot * SLOT, b0 = xb0 + xi * xbytes;
@@ -991,7 +996,7 @@ struct Vcc {
             }
             wm = clock64() - c0;
         }
-        if (ct == 0) st_mma += wm;
+        if (ct == 0) stat_add(VS_MMA, wm);
         ++nmma;
         tc_fence_after();
         const long long e0 = clock64();
@@ -1001,7 +1006,7 @@ struct Vcc {
             case 32: fin = bgemm_epilogue<16>(J); break;
             default: fin = bgemm_epilogue<32>(J); break;
         }
-        if (ct == 0) st_epi += clock64() - e0;
+        if (ct == 0) stat_add(VS_EPI, clock64() - e0);
         if ((J.flags & VDC_JOB_ARGMAX) && J.block) post_argmax_batched(J);
         if (!fin) return;  // a piece of a split row block that was not the last to arrive
         fence_proxy_async_global();  // consumers read these activations with TMA (async proxy)
@@ -1499,10 +1504,10 @@ struct Vcc {
         const int rows_w = PR / 2;  // rows per warp (<= 32: one per lane)
         // batched bf16 page pools (K and V page rows swizzled): scores and P.V on
         // the tensor cores (attn_page_mma). Single-request programs keep the
-        // CUDA-core path: at batch 1 the tensor-core page loop saved ~2.5 us of
-        // attention per layer, but its register demand inside the one
-        // persistent kernel slowed every GEMV operator by ~5 us per layer
-        // (281.6 vs 294.1 tokens/s, A/B on one B200)
+        // CUDA-core path: at batch 1 the tensor-core page loop shortens the
+        // attention phase by ~2.9 us per layer, but inside the one persistent
+        // kernel its register demand costs the GEMV operators more
+        // (A/B on one B200: 290.9 vs 293.9 tokens/s)
         constexpr bool MMA = BATCHED && BF && DPL == 4;
         if (MMA && !batched) {  // batched kernels only run batched attention jobs
             if (ct == 0) fire(6, 0x2A00u | uint32_t(sm));
@@ -1564,6 +1569,7 @@ struct Vcc {
             }
         }
         sync();
+        astamp(2);
         float m[G], l[G], o[G][DPL];
 #pragma unroll
         for (int h = 0; h < G; ++h) {
@@ -1826,10 +1832,13 @@ struct Vcc {
             S->flag = (old + 1u == uint32_t(J.arrive_need) * P->epoch) ? 1 : 0;
         }
         sync();
+        astamp(5);
+        if (S->flag) {
+            if (int(w) < G) combine_head<DPL, HD>(J, int(w));
+            publish(J.o2_t);
+        }
+        astamp(6);
         ++n_attn;
-        if (!S->flag) return;
-        if (int(w) < G) combine_head<DPL, HD>(J, int(w));
-        publish(J.o2_t);
     }
 
     // ATTN_COMBINE as a separate µop (waits for all splits of a kv head on its
@@ -2078,7 +2087,7 @@ __device__ __forceinline__ void vcc_role(const RingParams& P, Shared& S, char* r
         const vdc_job& J = BATCHED ? *reinterpret_cast<const vdc_job*>(jb + size_t(raw.z) * js) : Jv;
         const bool bf = J.x_t >= 0 && v.tdtype(J.x_t) == VDC_DTYPE_BF16;
         const unsigned long long t_enter = P.trace ? now_ns() : 0;
-        v.t_ready = 0;
+        if (v.ct == 0) S.t_ready = 0;
         switch (op) {
             case OP_GEMV:
             case OP_RMS_GEMV:
@@ -2138,24 +2147,24 @@ __device__ __forceinline__ void vcc_role(const RingParams& P, Shared& S, char* r
             unsigned long long* rec = P.trace + (size_t(core) * P.trace_cap + jobs) * 4;
             rec[0] = (static_cast<unsigned long long>(core) << 32) | pc;
             rec[1] = t_enter;
-            rec[2] = v.t_ready ? v.t_ready : t_enter;
+            rec[2] = S.t_ready ? S.t_ready : t_enter;
             rec[3] = now_ns();
         }
         ++jobs;
     }
     if (v.ct == 0) {
         SmStats& st = P.stats[blockIdx.x];
-        st.wait[S_VCC_FULL] = v.st_full;
-        st.wait[S_VCC_DEP] = v.st_dep;
-        st.wait[S_VCC_EPI] = v.st_epi;
+        st.wait[S_VCC_FULL] = S.vstat[v.VS_FULL];
+        st.wait[S_VCC_DEP] = S.vstat[v.VS_DEP];
+        st.wait[S_VCC_EPI] = S.vstat[v.VS_EPI];
         st.wait[S_VCC_TOTAL] = clock64() - t0;
         st.wait[S_NJOBS] = jobs;
         st.tiles_consumed = v.kt;  // ring tiles taken from (and handed back to) the memory core
         if constexpr (BATCHED) {
-            st.wait[S_X_FULL] = v.st_xf;
-            st.wait[S_X_EMPTY] = v.st_xe;
-            st.wait[S_MMA_DONE] = v.st_mma;
-            st.wait[S_BG_PRO] = v.st_pro;
+            st.wait[S_X_FULL] = S.vstat[v.VS_XF];
+            st.wait[S_X_EMPTY] = S.vstat[v.VS_XE];
+            st.wait[S_MMA_DONE] = S.vstat[v.VS_MMA];
+            st.wait[S_BG_PRO] = S.vstat[v.VS_PRO];
         }
     }
 }
@@ -2389,6 +2398,8 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(const __grid_cons
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (threadIdx.x < 8) S.vstat[threadIdx.x] = 0;
+    if (threadIdx.x == 0) S.t_ready = 0;
     if (BATCHED && threadIdx.x < VDC_RING_MAX_BATCH) {
         S.am_v[threadIdx.x] = -INFINITY;
         S.am_i[threadIdx.x] = 0x7fffffff;

@@ -42,7 +42,8 @@ for k in range(8):
     if S[k, 0] == 0:
         continue
     e = (S[k] - t0) / 1e3
-    print(f"attn job {k}: entry {e[0]:8.2f} ready {e[1]:8.2f} pages done {e[3]:8.2f} merged {e[4]:8.2f} us")
+    print(f"attn job {k}: entry {e[0]:8.2f} ready {e[1]:8.2f} q staged {e[2]:8.2f} pages done {e[3]:8.2f} merged {e[4]:8.2f} "
+          f"arrived {e[5]:8.2f} end {e[6]:8.2f} us")
 # tiles: issue, landed (seen by the consumer), released
 R = (T[:n] - t0) / 1e3
 lat = R[:, 1] - R[:, 0]

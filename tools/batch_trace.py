@@ -58,3 +58,13 @@ for op in sorted(rows):
     wait = (trd - te).sum() / 148 / 1e3
     print(f"op {op:3d} {r[0][1]:13s} jobs={len(r):5d} start[min {te.min()/1e3:8.1f}] ready[med {np.median(trd)/1e3:8.1f}] "
           f"done[min {td.min()/1e3:8.1f} med {np.median(td)/1e3:8.1f} max {td.max()/1e3:8.1f}] us  busy/SM {busy:6.1f} (dep wait {wait:5.1f})")
+# the latest SMs of each operator: their jobs (ready -> done, us)
+if len(sys.argv) > 5 and sys.argv[5] == "late":
+    for op in sorted(rows):
+        r = rows[op]
+        fin = {}
+        for sm, name, te, trd, td in r:
+            fin.setdefault(sm, []).append((te / 1e3, trd / 1e3, td / 1e3))
+        late = sorted(fin, key=lambda s: max(x[2] for x in fin[s]))[-3:]
+        print(f"op {op:3d} {r[0][1]:12s} latest SMs: " + "; ".join(
+            f"sm{sm}: " + ", ".join(f"{a:.1f}/{b:.1f}->{c:.1f}" for a, b, c in fin[sm]) for sm in late))
