@@ -132,6 +132,17 @@ int vdc_bind_tensor(vdc_ctx* ctx, uint16_t tensor, void* dptr, size_t bytes, int
  * Replaces the reference-side `vdc_tp_init` + host allreduce: the partial
  * sums move by peer stores inside the persistent kernel. */
 int vdc_bind_symmetric(vdc_ctx* ctx, uint16_t tensor, void* const* peer_bases, uint32_t world, uint32_t rank);
+/* Tensor-parallel setup without torch (the reference-side `vdc_tp_init` of
+ * SURVEY §8b): vdc_tp_alloc allocates and zeroes this rank's exchange buffer
+ * for every symmetric tensor of `prog` and writes an IPC handle blob to `out`
+ * (out = NULL: *len = the blob size); the host exchanges the W blobs between
+ * its rank processes (any channel: MPI, sockets, files) and vdc_tp_bind maps
+ * the peers' buffers (CUDA IPC over NVLink) and binds them
+ * (vdc_bind_symmetric). Contexts of several ranks in one process (single-GPU
+ * emulation) bind each other's buffers directly. The context owns the
+ * buffers and mappings (released by vdc_destroy). */
+int vdc_tp_alloc(vdc_ctx* ctx, const vdc_program* prog, void* out, size_t cap, size_t* len);
+int vdc_tp_bind(vdc_ctx* ctx, const void* const* blobs, uint32_t world, uint32_t rank);
 /* step block: device-resident int64 scalars read by SET_ACC_MEM */
 int vdc_bind_step(vdc_ctx* ctx, int64_t* dptr, uint32_t n);
 /* one execution of the loaded program on `stream` (a cudaStream_t, NULL =

@@ -72,7 +72,7 @@ class vdc_report(ctypes.Structure):
 # every symbol include/vdc.h declares (the CPU suite checks they are exported)
 EXPORTS = [
     "vdc_last_error", "vdc_version", "vdc_create", "vdc_destroy", "vdc_load_program", "vdc_load_jobs", "vdc_set_params",
-    "vdc_bind_tensor", "vdc_bind_symmetric", "vdc_bind_step", "vdc_bind_trace", "vdc_launch", "vdc_wait", "vdc_set_watchdog", "vdc_set_prefetch", "vdc_program_build",
+    "vdc_bind_tensor", "vdc_bind_symmetric", "vdc_tp_alloc", "vdc_tp_bind", "vdc_bind_step", "vdc_bind_trace", "vdc_launch", "vdc_wait", "vdc_set_watchdog", "vdc_set_prefetch", "vdc_program_build",
     "vdc_program_parse", "vdc_program_free", "vdc_program_text", "vdc_program_cores", "vdc_program_words",
     "vdc_program_load", "vdc_free_string", "vdc_program_synthesize",
     "vdc_kv_create", "vdc_kv_destroy", "vdc_kv_reserve", "vdc_kv_release", "vdc_kv_stats", "vdc_kv_table",
@@ -105,6 +105,8 @@ def lib() -> ctypes.CDLL:
         "vdc_bind_trace": ([vp, vp, c.c_uint32], c.c_int),
         "vdc_launch": ([vp, vp], c.c_int),
         "vdc_wait": ([vp, c.POINTER(vdc_report)], c.c_int),
+        "vdc_tp_alloc": ([vp, vp, vp, c.c_size_t, c.POINTER(c.c_size_t)], c.c_int),
+        "vdc_tp_bind": ([vp, c.POINTER(c.c_void_p), c.c_uint32, c.c_uint32], c.c_int),
         "vdc_set_watchdog": ([vp, c.c_uint32], c.c_int),
         "vdc_set_prefetch": ([vp, c.c_uint32], c.c_int),
         "vdc_program_build": ([c.c_char_p, c.POINTER(vp)], c.c_int),

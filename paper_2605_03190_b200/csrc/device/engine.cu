@@ -1848,6 +1848,8 @@ __global__ void __launch_bounds__(32 * (1 + kMaxLdu + kMaxStu + kMaxVcc * kVccWa
 
 #include <cstring>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -1857,6 +1859,8 @@ using namespace vdc_dev;
 using vdc_impl::fail;
 
 struct vdc_ctx {
+    // vdc_tp_alloc / vdc_tp_bind: this rank's exchange buffers and the peers' mappings
+    std::vector<void*> tp_owned, tp_opened;
     vdc_profile prof{};
     int device = 0;
     int num_sms = 0;
@@ -1980,6 +1984,8 @@ int vdc_create(const vdc_profile* p, int device, vdc_ctx** out) {
 
 int vdc_destroy(vdc_ctx* ctx) {
     if (!ctx) return VDC_OK;
+    for (void* p : ctx->tp_opened) cudaIpcCloseMemHandle(p);
+    for (void* p : ctx->tp_owned) cudaFree(p);
     dfree(ctx->d_words);
     dfree(ctx->d_core_off);
     dfree(ctx->d_descs);
@@ -2246,6 +2252,95 @@ int vdc_bind_symmetric(vdc_ctx* ctx, uint16_t tensor, void* const* peer_bases, u
         if (ctx->dev_descs[i].storage == int32_t(tensor)) ctx->dev_descs[i].ptr = local;
     ctx->descs_dirty = true;
     ctx->sym_dirty = true;
+    return VDC_OK;
+}
+
+// ---- tensor-parallel setup without torch (CUDA IPC) ----------------------
+// One record per symmetric tensor of the program: {u16 tensor, u16 pad, u32
+// pad, u64 bytes, cudaIpcMemHandle_t}. Handles created by this process are
+// remembered, so ranks emulated as several contexts in ONE process (tests on
+// a single GPU) bind each other's buffers by pointer (CUDA refuses to open
+// an IPC handle in the process that exported it).
+namespace {
+struct TpRecord {
+    uint16_t tensor;
+    uint16_t pad0;
+    uint32_t pad1;
+    uint64_t bytes;
+    cudaIpcMemHandle_t handle;
+};
+std::mutex g_tp_mu;
+std::map<std::string, void*> g_tp_local;  // exported handle bytes -> pointer (this process)
+std::string handle_key(const cudaIpcMemHandle_t& h) { return std::string(reinterpret_cast<const char*>(&h), sizeof h); }
+}  // namespace
+
+extern "C" int vdc_tp_alloc(vdc_ctx* ctx, const vdc_program* prog, void* out, size_t cap, size_t* len) {
+    if (!ctx || !prog || !len) return fail(VDC_ERR_INPUT, "null argument");
+    const auto& P = reinterpret_cast<const vdc_impl::ProgramBox*>(prog)->program;
+    std::vector<TpRecord> recs;
+    for (size_t i = 0; i < P.descriptors.size(); ++i) {
+        const auto& d = P.descriptors[i];
+        if (!d.symmetric) continue;
+        TpRecord r{};
+        r.tensor = uint16_t(i);
+        r.bytes = VDC_SYM_HEADER_BYTES + uint64_t(d.elem_count()) * uopsim::workload::elem_bytes(d.elem);
+        recs.push_back(r);
+    }
+    const size_t need = sizeof(uint32_t) + recs.size() * sizeof(TpRecord);
+    *len = need;
+    if (!out) return VDC_OK;  // size query
+    if (cap < need) return fail(VDC_ERR_INPUT, "handle buffer too small");
+    CU(cudaSetDevice(ctx->device));
+    for (auto& r : recs) {
+        void* p = nullptr;
+        CU(cudaMalloc(&p, r.bytes));
+        CU(cudaMemset(p, 0, r.bytes));  // zeroed headers: every rank starts at epoch 0
+        ctx->tp_owned.push_back(p);
+        CU(cudaIpcGetMemHandle(&r.handle, p));
+        std::lock_guard<std::mutex> lk(g_tp_mu);
+        g_tp_local[handle_key(r.handle)] = p;
+    }
+    CU(cudaDeviceSynchronize());
+    const uint32_t n = uint32_t(recs.size());
+    std::memcpy(out, &n, sizeof n);
+    if (n) std::memcpy(static_cast<char*>(out) + sizeof n, recs.data(), recs.size() * sizeof(TpRecord));
+    return VDC_OK;
+}
+
+extern "C" int vdc_tp_bind(vdc_ctx* ctx, const void* const* blobs, uint32_t world, uint32_t rank) {
+    if (!ctx || !blobs || world < 1 || world > VDC_RING_MAX_TP || rank >= world) return fail(VDC_ERR_INPUT, "bad world/rank");
+    uint32_t n = 0;
+    std::memcpy(&n, blobs[rank], sizeof n);
+    auto rec = [&](uint32_t q, uint32_t i) {
+        TpRecord r;
+        std::memcpy(&r, static_cast<const char*>(blobs[q]) + sizeof(uint32_t) + size_t(i) * sizeof(TpRecord), sizeof r);
+        return r;
+    };
+    for (uint32_t q = 0; q < world; ++q) {
+        uint32_t nq = 0;
+        std::memcpy(&nq, blobs[q], sizeof nq);
+        if (nq != n) return fail(VDC_ERR_INPUT, "ranks disagree on the symmetric tensors");
+    }
+    CU(cudaSetDevice(ctx->device));
+    for (uint32_t i = 0; i < n; ++i) {
+        const TpRecord mine = rec(rank, i);
+        void* peers[VDC_RING_MAX_TP] = {};
+        for (uint32_t q = 0; q < world; ++q) {
+            const TpRecord r = rec(q, i);
+            if (r.tensor != mine.tensor || r.bytes != mine.bytes) return fail(VDC_ERR_INPUT, "ranks disagree on the symmetric tensors");
+            {
+                std::lock_guard<std::mutex> lk(g_tp_mu);
+                const auto it = g_tp_local.find(handle_key(r.handle));
+                if (it != g_tp_local.end()) peers[q] = it->second;  // exported by this process
+            }
+            if (!peers[q]) {
+                CU(cudaIpcOpenMemHandle(&peers[q], r.handle, cudaIpcMemLazyEnablePeerAccess));
+                ctx->tp_opened.push_back(peers[q]);
+            }
+        }
+        const int rc = vdc_bind_symmetric(ctx, mine.tensor, peers, world, rank);
+        if (rc != VDC_OK) return rc;
+    }
     return VDC_OK;
 }
 

@@ -218,6 +218,22 @@ class Engine:
         arr = (ctypes.c_void_p * len(peer_ptrs))(*peer_ptrs)
         check(lib().vdc_bind_symmetric(self._h, d["index"], arr, world, rank))
 
+    def tp_alloc(self) -> bytes:
+        """This rank's exchange buffers (vdc_tp_alloc): allocated and zeroed by
+        the library; returns the IPC handle blob to hand to every rank."""
+        n = ctypes.c_size_t(0)
+        check(lib().vdc_tp_alloc(self._h, self.program.handle, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value)
+        check(lib().vdc_tp_alloc(self._h, self.program.handle, buf, n.value, ctypes.byref(n)))
+        return buf.raw[: n.value]
+
+    def tp_bind(self, blobs: list, rank: int) -> None:
+        """Map and bind every rank's exchange buffers from their vdc_tp_alloc
+        blobs (vdc_tp_bind: CUDA IPC across processes)."""
+        keep = [ctypes.create_string_buffer(b, len(b)) for b in blobs]
+        arr = (ctypes.c_void_p * len(keep))(*[ctypes.cast(k, ctypes.c_void_p) for k in keep])
+        check(lib().vdc_tp_bind(self._h, arr, len(blobs), rank))
+
     def host_arrays(self, tensors: dict) -> dict:
         """bound device tensors -> host float32 arrays in logical row-major order"""
         return {k: to_logical(self.descs[k], v.float().cpu().numpy()) for k, v in tensors.items()}

@@ -57,7 +57,7 @@ def assemble_full(infos: list, ins: list, cfg_full: dict) -> dict:
     return full
 
 
-def run_emulated(base: dict, world: int, steps=((17, 40),), seed: int = 0):
+def run_emulated(base: dict, world: int, steps=((17, 40),), seed: int = 0, capi_tp: bool = False):
     """returns (per-step dense-reference errors, full cfg)"""
     import torch
     from paper_2605_03190_b200 import Program
@@ -72,15 +72,18 @@ def run_emulated(base: dict, world: int, steps=((17, 40),), seed: int = 0):
         e = Engine(p, watchdog_ms=5000)
         tens.append(e.bind_inputs_nonsym(x))
         engines.append(e)
-    # symmetric buffers: one per rank per symmetric tensor, shared by pointer
-    syms = [d for d in infos[0]["descriptors"] if d.get("symmetric")]
     keep = []
-    for d in syms:
-        nbytes = 128 + int(np.prod(d["shape"])) * 4
-        bufs = [torch.zeros(nbytes // 4, dtype=torch.float32, device="cuda") for _ in range(world)]
-        keep.append(bufs)
+    if capi_tp:  # the library allocates, exports and binds (vdc_tp_alloc / vdc_tp_bind), no torch buffers
+        blobs = [e.tp_alloc() for e in engines]
         for r, e in enumerate(engines):
-            e.bind_symmetric(d["name"], [b.data_ptr() for b in bufs], world, r)
+            e.tp_bind(blobs, r)
+    else:  # symmetric buffers: one per rank per symmetric tensor, shared by pointer
+        for d in [d for d in infos[0]["descriptors"] if d.get("symmetric")]:
+            nbytes = 128 + int(np.prod(d["shape"])) * 4
+            bufs = [torch.zeros(nbytes // 4, dtype=torch.float32, device="cuda") for _ in range(world)]
+            keep.append(bufs)
+            for r, e in enumerate(engines):
+                e.bind_symmetric(d["name"], [b.data_ptr() for b in bufs], world, r)
     step_t = [torch.zeros(8, dtype=torch.int64, device="cuda") for _ in range(world)]
     for e, st in zip(engines, step_t):
         e.bind_step(st)
