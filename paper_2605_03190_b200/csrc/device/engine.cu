@@ -97,14 +97,17 @@ struct Cta {
 // Returns false when the engine aborts. The fast check is inlined; the wait
 // loop (backoff, watchdog, accounting) is out of line so the hot paths of the
 // roles stay compact in the instruction cache.
-__device__ __noinline__ void watchdog_fire(const Cta& c, uint32_t core, uint32_t pc) {
+__device__ __noinline__ void record_stalled(const Cta& c, uint32_t core, uint32_t pc) {
     Status* st = c.P->status;
     const int k = atomicAdd(&st->n_stalled, 1);
     if (k < 16) {
         st->stalled_core[k] = core;
         st->stalled_pc[k] = pc;
     }
-    atomicExch(&st->abort, 1);
+}
+__device__ __noinline__ void watchdog_fire(const Cta& c, uint32_t core, uint32_t pc) {
+    record_stalled(c, core, pc);
+    atomicExch(&c.P->status->abort, 1);
 }
 
 template <typename F>
@@ -117,7 +120,12 @@ __device__ __noinline__ bool spin_slow(const Cta& c, F cond, uint32_t core, uint
             return true;
         }
         if ((n & 63) == 63) {
-            if (c.aborted()) return false;
+            if (c.aborted()) {
+                // another core's watchdog declared a deadlock while this one was
+                // blocked too: it belongs to the wait-for picture (report.stalled)
+                if (*reinterpret_cast<volatile int32_t*>(&c.P->status->abort) == 1) record_stalled(c, core, pc);
+                return false;
+            }
             if (c.P->watchdog_ns && now_ns() - t0 > c.P->watchdog_ns) {
                 watchdog_fire(c, core, pc);
                 return false;

@@ -58,5 +58,6 @@ if len(ib):
     print("  W seen -> MMAs committed      p10/p50/p90", np.percentile(A[ib, 2] - A[ib, 1], [10, 50, 90]).astype(int))
     turn = [A[g + 8, 0] - A[g, 2] for g in ib if g + 8 < len(A) and A[g + 8, 0] > 0]
     print("  commit -> next issue in slot  p10/p50/p90", np.percentile(turn, [10, 50, 90]).astype(int))
-    for g in ib[:: max(1, len(ib) // 40)]:
+    step = int(os.environ.get("TT_STEP", max(1, len(ib) // 40)))
+    for g in ib[: int(os.environ.get("TT_FIRST", len(ib)))][::step]:
         print(g, "issue", A[g, 0], "loop top", xt[g, 0] - t0, "x ready", xt[g, 1] - t0, "W seen", A[g, 1], "commit", A[g, 2])
