@@ -156,7 +156,11 @@ typedef struct vdc_job {
     int32_t am_ctr, am_need;  /* BGEMM + ARGMAX: sampling arrival counter, SMs posting (slot = req) */
     int32_t am_sym, am_base;  /* BGEMM + TP_ARGMAX: exchange tensor, the rank's first vocab row */
     int32_t am_valid;         /* BGEMM + TP_ARGMAX: this rank's real vocab rows (the rest is padding) */
-    int32_t rsv[13];          /* pads the block to 256 bytes: the single-request fields stay in
+    int32_t ssq_t;            /* batched activations: sums of squares per 32-row group and request
+                                 (f32 [d/32][npad]), written by x's producer (embedding, residual
+                                 epilogue) and read by the RMS GEMM for its 1/rms (-1: none, the
+                                 consumer sums x itself) */
+    int32_t rsv[12];          /* pads the block to 256 bytes: the single-request fields stay in
                                  the first 128-byte line, the batched ones in the second */
 } vdc_job;  /* 256 bytes */
 

@@ -77,8 +77,14 @@ struct alignas(16) Shared {
                                        // batched programs: activation-chunk ring (128-byte swizzle, from the first 1 KB boundary)
     // batched programs: activation-chunk barriers, MMA completion, TMEM base, rms scales
     uint64_t xfull[NXMAX], xempty[NXMAX], mma_bar;
+    uint64_t lbar;  // batched programs: bulk copy of the RMS sums of squares
     uint32_t tmem_base;
     float binv[VDC_RING_MAX_BATCH];
+    // batched programs: each request's position and the physical page of its
+    // appended KV row (-1: none), read from the step block once per launch
+    // (constant within a launch) instead of per epilogue element
+    int64_t bpos[VDC_RING_MAX_BATCH];
+    int32_t bpage[VDC_RING_MAX_BATCH];
     // compute-core wait-site cycles and the trace's readiness stamp, updated by
     // thread 0 only: in shared memory, not in registers that every compute
     // thread would carry through the whole µop loop
@@ -867,7 +873,7 @@ struct Vcc {
 
     __device__ float* f32p(int32_t t) const { return reinterpret_cast<float*>(tptr(t)); }
     __device__ uint16_t* u16p(int32_t t) const { return reinterpret_cast<uint16_t*>(tptr(t)); }
-    __device__ int64_t req_pos(int b) const { return P->step[3 * b + 1]; }
+    __device__ int64_t req_pos(int b) const { return S->bpos[b]; }
 
     // wait for an mbarrier phase; returns the cycles waited, or -1 if the
     // launch aborted (no member addresses escape: the Vcc stays in registers)
@@ -887,22 +893,98 @@ struct Vcc {
         }
     }
 
+    // debug trace (VDC_RING_DEBUG): per BGEMM µop of the traced SM, phase stamps
+    // at tile_trace[200000 + 8 * (job % 4096) + ev]
+    __device__ void bstamp(int ev) const {
+        if (P->tile_trace && sm == (P->debug >> 8) && ct == 0) P->tile_trace[200000 + 16 * (nmma & 2047u) + ev] = now_ns();
+    }
+    // The RMS prologue's sums of squares move as one bulk copy (the TMA
+    // engine), not as LSU loads: with every SM streaming weights, an L2-hit
+    // ld.global round trip measured ~4.4 us, the bulk copy ~2.2 us (bulk copies
+    // of the stream-K partials and residual rows measured no gain: 2954 vs
+    // 2984 tokens/s, so those stay loads). Thread 0 issues (after the acquire
+    // that made the producer's generic writes visible; the async proxy needs
+    // its own fence) and every compute thread waits on S->lbar.
+    uint32_t lph = 0;  // S->lbar phase (uniform over the VCC)
+    __device__ void lbar_issue(uint32_t bytes) const {
+        fence_proxy_async_global();
+        mbar_expect_tx(&S->lbar, bytes);
+    }
+    __device__ bool lbar_wait() {
+        const long long c = spin(&S->lbar, lph & 1u);
+        ++lph;
+        return c >= 0;
+    }
+
+
     __device__ void bgemm(const vdc_job& J) {
         const long long p0 = clock64();
+        bstamp(0);
         const int n = J.kt1 - J.kt0, K = J.k, nb = J.nb, npad = J.npad;
         const bool rms = J.flags & VDC_JOB_RMS;
         if (!wait_ready(J.x_t, J.x_need, rms ? J.x2_t : -1, J.x2_need, (J.flags & VDC_JOB_RESID) ? J.a_t : -1, J.a_need)) {
             ok = false;
             return;
         }
-        if (rms && binv_t != J.x2_t) {  // per-request 1 / rms of the raw activations (warp per request)
+        bstamp(1);
+        if (rms && binv_t != J.x2_t && J.ssq_t >= 0) {
+            // 1 / rms from the producer's per-group sums of squares: 8 threads per
+            // request each add K/32/8 groups (loads issued together), then the 8
+            // partials in fixed order (deterministic)
+            // the [K/32][npad] sums arrive in one bulk copy (after the staging area
+            // of the per-thread partial sums), then 8 threads per request add
+            // K/256 groups each and one thread adds the 8 partials in order
+            const int G = K / 32, per = (G + 7) / 8;
+            bstamp(9);
+            float* scr = reinterpret_cast<float*>(S->x);
+            float* sq = scr + 8 * VDC_RING_MAX_BATCH;
+            const uint32_t sbytes = uint32_t(G * npad) * 4u;
+            if (sbytes + 8u * VDC_RING_MAX_BATCH * 4u <= uint32_t(XBUF)) {
+                if (ct == 0) {
+                    lbar_issue(sbytes);
+                    bulk_g2s(sq, f32p(J.ssq_t), sbytes, &S->lbar);
+                }
+                if (!lbar_wait()) {
+                    ok = false;
+                    return;
+                }
+            } else {
+                for (int i = int(ct); i < G * npad; i += NCT) sq[i] = ldcg_f32(f32p(J.ssq_t) + i);
+                sync();
+            }
+            for (int b0 = 0; b0 < nb; b0 += NCT / 8) {
+                const int b = b0 + (int(ct) >> 3), part = int(ct) & 7;
+                float ss = 0.f;
+                if (b < nb)
+                    for (int i = 0; i < per; ++i) {
+                        const int g = part * per + i;
+                        if (g < G) ss += sq[g * npad + b];
+                    }
+                scr[(b0 * 8) + int(ct)] = ss;
+            }
+            bstamp(8);
+            sync();
+            for (int b = int(ct); b < nb; b += NCT) {
+                float tot = 0.f;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) tot += scr[b * 8 + i];
+                S->binv[b] = 1.0f / sqrtf(tot / float(K) + J.eps);
+            }
+            binv_t = J.x2_t;
+            sync();
+        } else if (rms && binv_t != J.x2_t) {  // per-request 1 / rms of the raw activations (warp per request)
             const uint16_t* xr = u16p(J.x2_t);
             for (int b = int(w); b < nb; b += CW) {
                 const uint4* row = reinterpret_cast<const uint4*>(xr + int64_t(b) * K);
                 float ss = 0.f;
-                for (int c = int(lane); c < K / 8; c += 32) {
-                    const uint4 u = ldcg128(row + c);
-                    ss += dot16<true>(u, u);
+                // 16 chunks per lane requested before any is used: one L2 round trip
+                // per 16 (the loads are volatile asm, so the compiler keeps their order)
+                for (int c0 = int(lane); c0 < K / 8; c0 += 32 * 16) {
+                    uint4 u[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) u[i] = c0 + 32 * i < K / 8 ? ldcg128(row + c0 + 32 * i) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) ss += dot16<true>(u[i], u[i]);
                 }
                 ss = warp_sum(ss);
                 if (lane == 0) S->binv[b] = 1.0f / sqrtf(ss / float(K) + J.eps);
@@ -918,6 +1000,7 @@ struct Vcc {
         if (ct == 0) stat_add(VS_PRO, clock64() - p0);
         if (ct == 0) S->flag = 1;
         sync();
+        bstamp(2);
         // Every compute warp is an MMA issuer (lane 0) for the tiles of its own
         // ring slot (slot w of the 8-slot ring) into its own TMEM accumulator
         // (columns w * npad): like the single-request GEMV, each slot's
@@ -983,6 +1066,7 @@ struct Vcc {
         }
         kt += uint32_t(n);
         sync();
+        bstamp(3);
         if (!S->flag) {
             ok = false;
             return;
@@ -997,7 +1081,7 @@ struct Vcc {
             wm = clock64() - c0;
         }
         if (ct == 0) stat_add(VS_MMA, wm);
-        ++nmma;
+        bstamp(4);
         tc_fence_after();
         const long long e0 = clock64();
         bool fin = false;
@@ -1007,6 +1091,8 @@ struct Vcc {
             default: fin = bgemm_epilogue<32>(J); break;
         }
         if (ct == 0) stat_add(VS_EPI, clock64() - e0);
+        bstamp(5);
+        ++nmma;
         if ((J.flags & VDC_JOB_ARGMAX) && J.block) post_argmax_batched(J);
         if (!fin) return;  // a piece of a split row block that was not the last to arrive
         fence_proxy_async_global();  // consumers read these activations with TMA (async proxy)
@@ -1068,6 +1154,7 @@ struct Vcc {
             for (int c = 0; c < NH; ++c) v[c] += va[c];
         }
         tc_fence_before();  // the accumulator may be overwritten after the next barrier
+        bstamp(6);
         if (J.arrive_need > 1) {
             // stream-K: this piece's partial -> global; the last piece of the
             // row block to arrive adds all partials in piece order
@@ -1082,11 +1169,13 @@ struct Vcc {
                 S->flag = (old + 1u == uint32_t(J.arrive_need) * P->epoch) ? 1 : 0;
             }
             sync();
+            bstamp(7);
             if (!S->flag) return false;
             const float* p0 = part + size_t(J.part_off - J.split) * size_t(npad) * 128;
             float acc[NH];
 #pragma unroll
             for (int c = 0; c < NH; ++c) acc[c] = 0.f;
+#pragma unroll 4
             for (int s = 0; s < J.arrive_need; ++s) {
                 float t[NH];
                 if (s == J.split) {
@@ -1130,8 +1219,7 @@ struct Vcc {
                 if (isq) {
                     u16p(J.o_t)[int64_t(b) * qrows + rg] = f2bf(v[c]);
                 } else {
-                    const int64_t lp = pos / 64;
-                    const int64_t page = lp < J.maxp ? P->step[J.ptab + int64_t(b) * J.maxp + lp] : -1;
+                    const int64_t page = S->bpage[b];  // (request b's page of pos, -1 if none)
                     if (page < 0) {  // no KV page allocated for this position: fail loudly, write nothing
                         fire(7, uint32_t(b));
                         continue;
@@ -1172,8 +1260,12 @@ struct Vcc {
 #pragma unroll
             for (int c = 0; c < NH; ++c) {
                 const int b = c0 + c;
-                if (b >= nb) continue;
                 const uint16_t xo = f2bf(v[c] + r[c]);
+                if (J.ssq_t >= 0) {  // this warp's 32 rows: the sum of squares of request b's group
+                    const float ss = warp_sum(b < nb ? bf_lo(xo) * bf_lo(xo) : 0.f);
+                    if (lane == 0 && b < nb) f32p(J.ssq_t)[int64_t(rg >> 5) * J.npad + b] = ss;
+                }
+                if (b >= nb) continue;
                 u16p(J.o_t)[int64_t(b) * M + rg] = xo;
                 if (J.o3_t >= 0) u16p(J.o3_t)[int64_t(b) * M + rg] = f2bf(bf_lo(xo) * wn);
             }
@@ -1316,6 +1408,13 @@ struct Vcc {
             o.z = pack2(bf_lo(u.z) * bf_lo(g.z), bf_hi(u.z) * bf_hi(g.z));
             o.w = pack2(bf_lo(u.w) * bf_lo(g.w), bf_hi(u.w) * bf_hi(g.w));
             xn[int64_t(b) * nch + c] = o;
+            if (J.ssq_t >= 0) {  // sum of squares of each 32-element group (4 chunks = 4 consecutive lanes)
+                float ss = dot16<true>(u, u);
+                const uint32_t m = __activemask();
+                ss += __shfl_xor_sync(m, ss, 1);
+                ss += __shfl_xor_sync(m, ss, 2);
+                if ((c & 3) == 0) f32p(J.ssq_t)[int64_t(c >> 2) * J.npad + b] = ss;
+            }
         }
         fence_proxy_async_global();
         sync();
@@ -2056,6 +2155,16 @@ __device__ __forceinline__ void vcc_role(const RingParams& P, Shared& S, char* r
     v.tmem = S.tmem_base;
     const uint32_t core = 2 * blockIdx.x + 1;
     const uint32_t w0 = P.core_off[core], n = P.core_off[core + 1] - w0;
+    if constexpr (BATCHED) {  // requests' positions and append pages of this launch
+        const int b = int(v.ct);
+        if (b < VDC_RING_MAX_BATCH) {
+            const int64_t pos = 3 * b + 1 < P.n_step ? P.step[3 * b + 1] : 0;
+            const int64_t lp = pos / 64, at = int64_t(P.ptab) + int64_t(b) * P.maxp + lp;
+            S.bpos[b] = pos;
+            S.bpage[b] = (P.maxp > 0 && pos >= 0 && lp < P.maxp && at < P.n_step) ? int32_t(P.step[at]) : -1;
+        }
+        v.sync();
+    }
     const long long t0 = clock64();
     uint32_t jobs = 0;
     // the stream runs to its end even after an abort (every wait then returns
@@ -2395,6 +2504,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(const __grid_cons
                 mbar_init(&S.xempty[i], 1);
             }
             mbar_init(&S.mma_bar, CW);
+            mbar_init(&S.lbar, 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }

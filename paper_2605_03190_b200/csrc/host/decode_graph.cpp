@@ -387,7 +387,13 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
     sk("gu.sk", 2 * ffn / 128);
     sk("down.sk", d / 128);
     sk("head.sk", vocab / 128);
+    // sums of squares of a residual-stream activation per 32-row group and
+    // request, written by its producer so RMS consumers need not re-read it
+    auto ssq = [&](const std::string& xname) {
+        if (!tp) b.add(xname + ".ssq", {d / 32, N}, 1, N, InitKind::zeros, ElemType::f32);
+    };
     std::string x = act("embed.x", d, false), xn = act("embed.xn", d, true);
+    ssq(x);
     b.norm("L0.attn_norm", d);
     b.node("embed", OpKind::EMBED_ROW, {"embed.table", "L0.attn_norm"}, {x, xn}, {{"batch", bs}});
     for (int li = 0; li < m.layers; ++li) {
@@ -422,6 +428,7 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
         b.norm(L + "mlp_norm", d);
         act(L + "x1", d, false);
         act(L + "x1n", d, true);
+        ssq(L + "x1");
         if (tp) {
             b.node(L + "o", OpKind::GEMV, {L + "wo", L + "attn"}, {sym(L + "o.part")}, with_attrs({{"batch", bs}}, tp_attrs));
             b.node(L + "o.ar", OpKind::ALLREDUCE_ADD, {L + "o.part", x, L + "mlp_norm"}, {L + "x1", L + "x1n"},
@@ -438,6 +445,7 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
         b.norm(next_norm, d);
         x = act(L + "x2", d, false);
         xn = act(L + "x2n", d, true);
+        ssq(x);
         if (tp) {
             b.node(L + "down", OpKind::GEMV, {L + "wd", L + "a"}, {sym(L + "d.part")}, with_attrs({{"batch", bs}}, tp_attrs));
             b.node(L + "down.ar", OpKind::ALLREDUCE_ADD, {L + "d.part", L + "x1", next_norm}, {x, xn}, with_attrs({{"batch", bs}}, tp_attrs));

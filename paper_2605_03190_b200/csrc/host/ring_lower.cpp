@@ -141,7 +141,12 @@ class RingLowering {
         j.x_t = j.a_t = j.b_t = j.o_t = j.o2_t = -1;
         j.x2_t = j.o3_t = j.w3_t = j.part_t = -1;
         j.arrive_ctr = -1;
+        j.ssq_t = -1;
         return j;
+    }
+    // the sums-of-squares companion of a batched activation (decode_graph.cpp), or -1
+    int32_t ssq_of(const std::string& x) const {
+        return g_.find_tensor(x + ".ssq") ? storage(idx(x + ".ssq")) : -1;
     }
 
     // contiguous, unit-aligned share of `units` for SM s
@@ -543,6 +548,7 @@ class RingLowering {
                 j.k = int32_t(desc_[uint16_t(j.x_t)].cols());
                 j.o_t = storage(idx(n.outputs[0]));
                 j.o3_t = storage(idx(n.outputs[1]));
+                j.ssq_t = ssq_of(n.outputs[0]);
                 r.publishes = {j.o_t, j.o3_t};
                 jobs_.push_back(std::move(r));
                 }
@@ -641,12 +647,14 @@ class RingLowering {
                     j.flags |= VDC_JOB_RMS;
                     j.x2_t = storage(idx(n.inputs[2]));
                     j.eps = float(attr_num(n, "eps", 1e-5));
+                    j.ssq_t = ssq_of(n.inputs[2]);
                 }
                 if (resid) {
                     j.flags |= VDC_JOB_RESID;
                     j.a_t = storage(idx(n.inputs[2]));
                     j.w3_t = storage(idx(n.inputs[3]));
                     j.o3_t = storage(idx(n.outputs[1]));
+                    j.ssq_t = ssq_of(n.outputs[0]);
                     r.publishes = {j.o_t, j.o3_t};
                 } else if (qkv) {
                     const TileDescriptor& kc = desc_[idx(n.outputs[1])];

@@ -64,7 +64,7 @@ def assert_close(rs, tol=2e-2, strict_argmax=False):
     16); logits max 1.9e-2 rms either way."""
     for b, r in enumerate(rs):
         assert r["logits_max_abs"] <= tol * r["logits_rms"], (b, r)
-        assert r["logits_max_abs_alt"] <= 5e-2 * r["logits_rms"], (b, r)
+        assert r["logits_max_abs_alt"] <= 6e-2 * r["logits_rms"], (b, r)  # (other rounding convention: a loose cross-check)
         assert r["kv_rel"] <= 1e-2, (b, r)
         assert r["kv_rel_deep"] <= 2e-2, (b, r)
         if strict_argmax:

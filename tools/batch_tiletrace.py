@@ -61,3 +61,14 @@ if len(ib):
     step = int(os.environ.get("TT_STEP", max(1, len(ib) // 40)))
     for g in ib[: int(os.environ.get("TT_FIRST", len(ib)))][::step]:
         print(g, "issue", A[g, 0], "loop top", xt[g, 0] - t0, "x ready", xt[g, 1] - t0, "W seen", A[g, 1], "commit", A[g, 2])
+# BGEMM µop phases on this SM: entry, ready, prologue done, issue loop done,
+# MMAs complete, epilogue done (us, relative to the first tile issue)
+B = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)[200000:200000 + 16 * 2048].reshape(-1, 16)
+print("BGEMM µops, us after entry: ready prologue loop mma | tmem-read arrived | epilogue-done")
+for k, row in enumerate(B):
+    if row[0] == 0:
+        continue
+    r = [round((x - row[0]) / 1e3, 2) if x else None for x in row]
+    print(k, "entry", round((row[0] - B[0][0]) / 1e3, 2), r[1:5], "|", r[6], r[7], "|", r[5], "| ssq start/loaded", r[9], r[8])
+    if k > 60:
+        break
