@@ -253,6 +253,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     tp = world > 1 and args.parallel == "tp"
     t_build = time.time()
     req = model_request(args.layers, args.ctx, args.engine, args.ring_slots, args.pages_per_job)
+    R = max(1, args.resident)
+    if R > 1:
+        # resident decode: R steps per launch, the sampled token fed back on the
+        # device; positions advance from ctx - 1 through warm-up and timed steps
+        if args.steps % R:
+            raise SystemExit("--steps must be a multiple of --resident")
+        advance = args.warmup * R + args.steps
+        pages = (args.ctx + advance + 63) // 64
+        req["layout"].update(feedback=True, ctx_pages=pages, max_ctx=pages * 64)
     if tp:
         req["layout"]["tp_world"], req["layout"]["tp_rank"] = world, rank
     prog = Program.build(req)
@@ -261,10 +270,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     tens = init_tensors(eng, rank, tp)
     keep_sym = bind_symmetric_tp(eng, world, rank, local_rank) if tp else None
     info = eng.info
-    nbytes = algorithmic_bytes(info, args.ctx)
+    # KV bytes at the mean context of the timed steps (resident decode advances it)
+    ctx_mean = args.ctx + (args.warmup * R + (args.steps - 1) / 2.0 if R > 1 else 0)
+    nbytes = algorithmic_bytes(info, int(round(ctx_mean)))
     step = torch.tensor([17, args.ctx - 1, args.ctx, 0, 0, 0, 0, 0], dtype=torch.int64, device=f"cuda:{local_rank}")
     eng.bind_step(step)
     stream = torch.cuda.Stream(device=local_rank)
+    if R > 1:
+        eng.set_steps(R)
 
     def barrier():
         if world > 1:
@@ -283,13 +296,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     sampler.start()
     time.sleep(0.3)
 
-    # ---- value: device-resident inputs, K back-to-back steps
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    # ---- value: device-resident inputs, K back-to-back steps (resident: K / R
+    # launches of R steps each)
+    launches = args.steps // R
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(launches + 1)]
     barrier()
     w0 = time.time()
     with torch.cuda.stream(stream):
         ev[0].record(stream)
-        for k in range(args.steps):
+        for k in range(launches):
             eng.launch(stream)
             ev[k + 1].record(stream)
     stream.synchronize()
@@ -297,7 +312,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     barrier()
     sampler.mark(w0, w1)
     rep = eng.wait()
-    per = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    per = [ev[k].elapsed_time(ev[k + 1]) / R for k in range(launches)]  # per decode step
+    if R > 1:
+        eng.set_steps(1)  # e2e: one step per launch, the host supplies every token
     total_ms = ev[0].elapsed_time(ev[-1])
 
     # ---- e2e: host loop through the public API (H2D step block; D2H of the
@@ -367,13 +384,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "config": {"workload": f"C2 Llama-3-8B bf16 decode, batch 1, ctx {args.ctx}, {args.layers} layers + lm_head",
                    "model": "llama3-8b", "batch": 1, "ctx": args.ctx, "parallelism": parallelism,
                    "l2": "inputs larger than L2 (algorithmic %.2f GB per step vs 126 MB L2)" % (nbytes["total"] / 1e9),
-                   "program_uops": info["total_uops"], "virtual_cores": prog.cores()[0], "build_seconds": round(build_s, 2)},
+                   "program_uops": info["total_uops"], "virtual_cores": prog.cores()[0], "build_seconds": round(build_s, 2),
+                   "resident_steps_per_launch": R,
+                   **({"ctx_mean_timed": round(ctx_mean, 1)} if R > 1 else {})},
         "e2e": {"value": round(e2e_value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 8 * 8,
                 "d2h_bytes_per_step": 8 if next_tok is not None else n_logits * 4,
                 "sampling": ("greedy argmax fused into the lm_head epilogue (device"
                              + (", cross-rank (max, index) exchange over NVLink)" if tp else ")"))
                             if next_tok is not None else "host argmax over D2H logits"},
-        "gpu_launches": args.steps,
+        "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": committed_traffic() if world == 1 else None,
                      "peak_source": peak_src, "frac_of_8TBps_spec": round(achieved / 8000.0, 4),
@@ -604,6 +623,9 @@ def main():
     ap.add_argument("--ctx-fixed", type=int, default=0, help="batched decode: every request at this context (C4 4096, C5 8192)")
     ap.add_argument("--batch", type=int, default=1,
                     help="> 1: C3 batched decode (per-request contexts, paged KV, BGEMM on tcgen05); 1 GPU")
+    ap.add_argument("--resident", type=int, default=1,
+                    help="batch-1 decode: decode steps per launch of the persistent kernel (device-side "
+                         "token feedback, vdc_set_steps); --steps must be a multiple")
     ap.add_argument("--parallel", default="tp", choices=["tp", "replicas"],
                     help="N>1: tensor parallel over the N GPUs (default) or N independent replicas")
     args = ap.parse_args()

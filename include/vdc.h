@@ -157,6 +157,13 @@ int vdc_bind_trace(vdc_ctx* ctx, void* dptr, uint32_t records_per_core);
 /* ring engine: L2 prefetch look-ahead of the memory core, in rounds of 8
  * tiles (default 0 = off, <= 31) */
 int vdc_set_prefetch(vdc_ctx* ctx, uint32_t tiles);
+/* resident decode: every following launch runs `steps`
+ * decode steps inside the persistent kernel. Needs a program that samples on
+ * the device and feeds the token back (layout.argmax + layout.feedback): step
+ * e + 1 starts on each SM once step e's token is in the step block, while the
+ * memory cores keep streaming the next step's weights across the boundary
+ * (KV pages wait for the token, they may hold step e's appended rows). */
+int vdc_set_steps(vdc_ctx* ctx, uint32_t steps);
 /* watchdog: abort a launch whose cores make no progress for `ms` (0 = off) */
 int vdc_set_watchdog(vdc_ctx* ctx, uint32_t ms);
 

@@ -1869,6 +1869,8 @@ using vdc_impl::fail;
 struct vdc_ctx {
     // vdc_tp_alloc / vdc_tp_bind: this rank's exchange buffers and the peers' mappings
     std::vector<void*> tp_owned, tp_opened;
+    uint32_t n_epochs = 1;  // decode steps per launch (vdc_set_steps)
+    int32_t fb_ctr = -1;    // counter of the fed-back token
     vdc_profile prof{};
     int device = 0;
     int num_sms = 0;
@@ -2185,6 +2187,10 @@ int vdc_load_jobs(vdc_ctx* ctx, const vdc_job* jobs, uint32_t n_jobs, uint32_t r
             return fail(VDC_ERR_INPUT, "ring of " + std::to_string(ring_slots) + " slots needs " +
                                            std::to_string(ring_smem_bytes(ring_slots, batched)) + " B of shared memory");
     }
+    ctx->fb_ctr = -1;  // the counter of the token the device feeds back (resident decode)
+    for (uint32_t i = 0; i < n_jobs; ++i)
+        if ((jobs[i].flags & VDC_JOB_FEEDBACK) && jobs[i].o2_t >= 0) ctx->fb_ctr = jobs[i].o2_t;
+    ctx->n_epochs = 1;
     ctx->ring = true;
     ctx->batched = batched;
     ctx->qknorm = false;
@@ -2380,6 +2386,15 @@ int vdc_set_prefetch(vdc_ctx* ctx, uint32_t tiles) {
     return VDC_OK;
 }
 
+int vdc_set_steps(vdc_ctx* ctx, uint32_t steps) {
+    if (!ctx || !ctx->loaded || !ctx->ring) return fail(VDC_ERR_INPUT, "load a ring program first");
+    if (steps < 1) return fail(VDC_ERR_INPUT, "steps must be >= 1");
+    if (steps > 1 && ctx->fb_ctr < 0)
+        return fail(VDC_ERR_INPUT, "resident decode needs a program that feeds its sampled token back (layout.feedback)");
+    ctx->n_epochs = steps;
+    return VDC_OK;
+}
+
 int vdc_set_watchdog(vdc_ctx* ctx, uint32_t ms) {
     if (!ctx) return fail(VDC_ERR_INPUT, "null ctx");
     ctx->watchdog_ms = ms;
@@ -2405,7 +2420,10 @@ int vdc_launch(vdc_ctx* ctx, void* stream) {
         R.counters = ctx->d_counters;
         R.step = ctx->d_step;
         R.n_step = int32_t(ctx->d_step ? ctx->n_step : 0);
-        R.epoch = ++ctx->epoch;
+        R.epoch = ctx->epoch + 1;
+        R.n_epochs = ctx->n_epochs;
+        R.fb_ctr = ctx->fb_ctr;
+        ctx->epoch += ctx->n_epochs;
         R.ring_slots = ctx->ring_slots;
         R.prefetch = ctx->ring_prefetch;
         if (ctx->tp_poisoned)

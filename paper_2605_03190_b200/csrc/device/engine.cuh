@@ -131,6 +131,11 @@ struct RingParams {
     uint32_t batched;           // batched program: TMEM accumulator + X ring for BGEMM µops
     const void* tmaps;          // CUtensorMap[n_desc] (128 bytes each), indexed by descriptor (vdc_desc.tma > 0 only)
     int32_t ptab, maxp;         // batched programs: page table at step[ptab + b * maxp + logical page] (VDC_LOAD_PAGED)
+    // resident decode: the launch runs n_epochs decode steps back to back
+    // (epochs epoch .. epoch + n_epochs - 1); step e > 0 starts once the
+    // sampled-token counter fb_ctr shows step e - 1 fed its token back
+    uint32_t n_epochs;
+    int32_t fb_ctr;
 };
 size_t ring_smem_bytes(uint32_t ring_slots, bool batched = false);
 const void* ring_kernel_entry(bool batched, bool qknorm = false);

@@ -118,6 +118,14 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
     return v;
 }
+// step-block scalar: an L2 (coherent) load. The device writes the step block
+// during a launch (fed-back token, positions) and resident decode reads the
+// new values in the next step, so no L1 / non-coherent copy may be used.
+__device__ __forceinline__ int64_t ldstep(const int64_t* p) {
+    int64_t v;
+    asm volatile("ld.global.cg.s64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
 __device__ __forceinline__ uint2 ldcg64(const void* p) {
     uint2 v;
     asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
@@ -212,6 +220,7 @@ struct Vcc {
     uint32_t ct, lane, w;
     uint32_t kt = 0;  // ring tiles consumed so far (program order, uniform over the VCC)
     uint32_t R;
+    uint32_t ep = 0;  // epoch of the running decode step (readiness targets are producers x epoch)
     bool ok = true;
     // wait-site cycle counters (thread 0, shared memory): VS_* slots of S->vstat
     enum : int { VS_FULL = 0, VS_DEP, VS_EPI, VS_XF, VS_XE, VS_MMA, VS_PRO };
@@ -240,7 +249,7 @@ struct Vcc {
         char* b = t >= 0 ? sym_base(t, P->tp_rank) : nullptr;
         return b ? reinterpret_cast<uint32_t*>(b) : &P->counters[t < 0 ? 0 : t];
     }
-    __device__ int64_t token() const { return P->n_step > VDC_STEP_TOKEN ? P->step[VDC_STEP_TOKEN] : 0; }
+    __device__ int64_t token() const { return P->n_step > VDC_STEP_TOKEN ? ldstep(P->step + (VDC_STEP_TOKEN)) : 0; }
     __device__ int32_t tdtype(int32_t t) const { return P->descs[t].dtype; }
 
     // all compute threads: wait for ring tile k (slot full)
@@ -277,7 +286,7 @@ struct Vcc {
             // trip per poll, not one per counter; one acquire fence at the end
             const long long c0 = clock64();
             const bool u0 = t0 >= 0 && n0 > 0, u1 = t1 >= 0 && n1 > 0, u2 = t2 >= 0 && n2 > 0;
-            const uint32_t g0 = uint32_t(n0) * P->epoch, g1 = uint32_t(n1) * P->epoch, g2 = uint32_t(n2) * P->epoch;
+            const uint32_t g0 = uint32_t(n0) * ep, g1 = uint32_t(n1) * ep, g2 = uint32_t(n2) * ep;
             const uint32_t* c0p = ctr(u0 ? t0 : -1);
             const uint32_t* c1p = ctr(u1 ? t1 : -1);
             const uint32_t* c2p = ctr(u2 ? t2 : -1);
@@ -400,7 +409,7 @@ struct Vcc {
         }
         if ((J.flags & (VDC_JOB_ROPE | VDC_JOB_QKV)) && (rope_hd != J.head_dim || rope_theta != J.theta)) {
             // rotary table of this launch's position: cos/sin per dim pair, angles in double precision
-            const int64_t pos = P->n_step > VDC_STEP_POS ? P->step[VDC_STEP_POS] : 0;
+            const int64_t pos = P->n_step > VDC_STEP_POS ? ldstep(P->step + (VDC_STEP_POS)) : 0;
             for (int d2 = int(ct); d2 < J.head_dim / 2; d2 += NCT) {
                 const double ang = double(pos) * pow(double(J.theta), -double(2 * d2) / double(J.head_dim));
                 S->rope_cs[d2] = float(cos(ang));
@@ -451,7 +460,7 @@ struct Vcc {
     // symmetric header of t reaches n x epoch; false if the launch aborted
     __device__ bool wait_sym(int32_t t, uint32_t n) const {
         const uint32_t* c = reinterpret_cast<const uint32_t*>(sym_base(t, P->tp_rank));
-        const uint32_t g = n * P->epoch;
+        const uint32_t g = n * ep;
         const unsigned long long w0 = now_ns();
         for (uint32_t k = 1;; ++k) {
             if (int32_t(ld_relaxed_sys(c) - g) >= 0) break;
@@ -514,7 +523,7 @@ struct Vcc {
                 part[1] = __int_as_float(am_i);
                 uint32_t old;
                 asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&P->counters[J.arrive_ctr]) : "memory");
-                S->flag = (old + 1u == uint32_t(J.arrive_need) * P->epoch) ? 1 : 0;
+                S->flag = (old + 1u == uint32_t(J.arrive_need) * ep) ? 1 : 0;
             }
         }
         sync();
@@ -779,7 +788,7 @@ struct Vcc {
         char* ob = tptr(J.o_t);
         const bool obf = tdtype(J.o_t) == VDC_DTYPE_BF16;
         const int lr0 = J.r0 - J.out_row0;  // first output row (region-local)
-        const int64_t pos = P->n_step > VDC_STEP_POS ? P->step[VDC_STEP_POS] : 0;
+        const int64_t pos = P->n_step > VDC_STEP_POS ? ldstep(P->step + (VDC_STEP_POS)) : 0;
         auto out_index = [&](int lr) -> int64_t {
             if (J.flags & VDC_JOB_KV_APPEND)
                 return (int64_t(lr / J.head_dim) * J.cache_rows + pos) * J.head_dim + lr % J.head_dim;
@@ -1145,9 +1154,12 @@ struct Vcc {
 #pragma unroll
         for (int c = 0; c < NH; ++c) v[c] = 0.f;
         const int ntile = J.kt1 - J.kt0;
-        for (int a = 0; a < CW; ++a) {  // per-warp accumulators in warp order; a warp without tiles wrote none
-            const int t0 = int((uint32_t(a) + uint32_t(CW) - (kt - uint32_t(ntile)) % uint32_t(CW)) % uint32_t(CW));
-            if (t0 >= ntile) continue;
+        // the per-warp accumulators in the order of their first tile (warp a took
+        // tiles t = a - k0 mod 8), so the association of the sum does not depend
+        // on where the job started in the ring; a warp without tiles wrote none
+        const uint32_t k0 = (kt - uint32_t(ntile)) % uint32_t(CW);
+        for (int tt = 0; tt < CW && tt < ntile; ++tt) {
+            const int a = int((uint32_t(tt) + k0) % uint32_t(CW));
             float va[NH];
             tmem_ld<NH>(tmem + (uint32_t(q * 32) << 16) + uint32_t(a * npad) + uint32_t(c0), va);
 #pragma unroll
@@ -1166,7 +1178,7 @@ struct Vcc {
             if (ct == 0) {
                 uint32_t old;
                 asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&P->counters[J.arrive_ctr]) : "memory");
-                S->flag = (old + 1u == uint32_t(J.arrive_need) * P->epoch) ? 1 : 0;
+                S->flag = (old + 1u == uint32_t(J.arrive_need) * ep) ? 1 : 0;
             }
             sync();
             bstamp(7);
@@ -1328,7 +1340,7 @@ struct Vcc {
         if (ct == 0) {
             uint32_t old;
             asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&P->counters[J.am_ctr]) : "memory");
-            S->flag = (old + 1u == uint32_t(J.am_need) * P->epoch) ? 1 : 0;
+            S->flag = (old + 1u == uint32_t(J.am_need) * ep) ? 1 : 0;
         }
         sync();
         if (!S->flag) return;
@@ -1399,7 +1411,7 @@ struct Vcc {
         uint4* xn = reinterpret_cast<uint4*>(tptr(J.o3_t));
         for (int i = int(ct); i < (J.r1 - J.r0) * nch; i += NCT) {
             const int b = J.r0 + i / nch, c = i % nch;
-            const int64_t tok = P->step[3 * b];
+            const int64_t tok = ldstep(P->step + (3 * b));
             const uint4 u = __ldg(tab + tok * nch + c), g = __ldg(wv + c);
             xo[int64_t(b) * nch + c] = u;
             uint4 o;
@@ -1590,8 +1602,8 @@ struct Vcc {
         // K on even slots: a leading pad tile aligns the job), so every slot
         // keeps a single consumer pair and jobs may span more than the ring
         const bool batched = BATCHED && (J.flags & VDC_JOB_BATCH);
-        const int64_t pos = batched ? P->step[3 * J.req + 1] : P->step[VDC_STEP_POS];
-        const int64_t ctx = batched ? P->step[3 * J.req + 2] : P->step[VDC_STEP_CTX];
+        const int64_t pos = batched ? ldstep(P->step + (3 * J.req + 1)) : ldstep(P->step + (VDC_STEP_POS));
+        const int64_t ctx = batched ? ldstep(P->step + (3 * J.req + 2)) : ldstep(P->step + (VDC_STEP_CTX));
         if (batched && J.lead_pad) {
             const uint32_t s0 = kt % R;
             if ((s0 & uint32_t(CW - 1)) == w) {
@@ -1708,10 +1720,10 @@ struct Vcc {
             if (batched && (J.flags & VDC_JOB_PREFILL)) {
                 // prefill chunk: every row appended in this launch (request 0's
                 // position .. this row's position) comes from global
-                const int64_t lo = max(prow0, P->step[1]), hi = min(prow0 + int64_t(rows_w), ctx);
+                const int64_t lo = max(prow0, ldstep(P->step + (1))), hi = min(prow0 + int64_t(rows_w), ctx);
                 for (int64_t rr = lo; rr < hi; ++rr) {
                     const size_t crow =
-                        size_t(P->step[J.ptab + int64_t(J.req) * J.maxp + rr / PR]) * size_t(J.cache_rows) + size_t(rr % PR);
+                        size_t(ldstep(P->step + (J.ptab + int64_t(J.req) * J.maxp + rr / PR))) * size_t(J.cache_rows) + size_t(rr % PR);
                     const char* kn = tptr(J.a_t) + (size_t(J.a_off) + crow * HD) * EB;
                     const char* vn = tptr(J.b_t) + (size_t(J.b_off) + crow * HD) * EB;
                     for (int c = int(lane); c < 2 * NCH; c += 32) {
@@ -1734,7 +1746,7 @@ struct Vcc {
                 const int r = int(pos - prow0);
                 // cache row of the appended position: (hkv, T, hd) cache, or
                 // page pool (pages, hkv * 64, hd) through the page table
-                const size_t crow = batched ? size_t(P->step[J.ptab + int64_t(J.req) * J.maxp + pos / PR]) * size_t(J.cache_rows) +
+                const size_t crow = batched ? size_t(ldstep(P->step + (J.ptab + int64_t(J.req) * J.maxp + pos / PR))) * size_t(J.cache_rows) +
                                                   size_t(pos % PR)
                                             : size_t(pos);
                 const char* kn = tptr(J.a_t) + (size_t(J.a_off) + crow * HD) * EB;
@@ -1928,7 +1940,7 @@ struct Vcc {
         if (ct == 0) {
             uint32_t old;
             asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&P->counters[J.arrive_ctr]) : "memory");
-            S->flag = (old + 1u == uint32_t(J.arrive_need) * P->epoch) ? 1 : 0;
+            S->flag = (old + 1u == uint32_t(J.arrive_need) * ep) ? 1 : 0;
         }
         sync();
         astamp(5);
@@ -2133,7 +2145,7 @@ struct Vcc {
     __device__ void copy_row(const vdc_job& J) {
         const int32_t eb = P->descs[J.x_t].elem;
         int64_t off = J.x_off;
-        if (J.flags & VDC_JOB_TOKEN_ROW) off += (P->n_step > VDC_STEP_TOKEN ? P->step[VDC_STEP_TOKEN] : 0) * J.k;
+        if (J.flags & VDC_JOB_TOKEN_ROW) off += (P->n_step > VDC_STEP_TOKEN ? ldstep(P->step + (VDC_STEP_TOKEN)) : 0) * J.k;
         const uint4* src = reinterpret_cast<const uint4*>(tptr(J.x_t) + off * eb);
         uint4* dst = reinterpret_cast<uint4*>(tptr(J.o_t) + int64_t(J.o_off) * eb);
         for (int c = int(ct); c < J.k * eb / 16; c += NCT) dst[c] = __ldg(src + c);
@@ -2155,18 +2167,55 @@ __device__ __forceinline__ void vcc_role(const RingParams& P, Shared& S, char* r
     v.tmem = S.tmem_base;
     const uint32_t core = 2 * blockIdx.x + 1;
     const uint32_t w0 = P.core_off[core], n = P.core_off[core + 1] - w0;
+    const long long t0 = clock64();
+    uint32_t jobs = 0;
+    // resident decode: n_epochs decode steps in this launch. Step e > 0 waits
+    // (thread 0) until step e - 1 fed its token back (every SM has finished
+    // step e - 1 by then: its lm_head jobs are each SM's last µops), then the
+    // per-step caches are refreshed (rotary table, staged x, rms scales,
+    // request positions / append pages)
+    for (uint32_t e = 0; e < P.n_epochs; ++e) {
+    v.ep = P.epoch + e;
+    if (e > 0) {
+        if (v.ct == 0) {
+            const uint32_t* fb = &P.counters[P.fb_ctr];
+            const uint32_t want = v.ep - 1u;
+            const unsigned long long w0t = now_ns();
+            for (uint32_t k = 1; int32_t(ld_relaxed(fb) - want) < 0; ++k) {
+                if ((k & 255) == 0) {
+                    if (v.aborted()) break;
+                    if (P.watchdog_ns && now_ns() - w0t > P.watchdog_ns) {
+                        v.fire(0, 0x60000u | e);
+                        break;
+                    }
+                }
+                __nanosleep(64);
+            }
+            fence_acquire_gpu();
+        }
+        // the sampler's running bests start over (single-request: per thread;
+        // batched: the SM's per-request slots)
+        v.am_v = -INFINITY;
+        v.am_i = 0x7fffffff;
+        if (BATCHED && v.ct < VDC_RING_MAX_BATCH) {
+            S.am_v[v.ct] = -INFINITY;
+            S.am_i[v.ct] = 0x7fffffff;
+        }
+        v.sync();
+        v.xk_t = -2;
+        v.rope_hd = 0;
+        v.binv_t = -2;
+    }
     if constexpr (BATCHED) {  // requests' positions and append pages of this launch
         const int b = int(v.ct);
         if (b < VDC_RING_MAX_BATCH) {
-            const int64_t pos = 3 * b + 1 < P.n_step ? P.step[3 * b + 1] : 0;
+            const int64_t pos = 3 * b + 1 < P.n_step ? ldstep(P.step + (3 * b + 1)) : 0;
             const int64_t lp = pos / 64, at = int64_t(P.ptab) + int64_t(b) * P.maxp + lp;
             S.bpos[b] = pos;
-            S.bpage[b] = (P.maxp > 0 && pos >= 0 && lp < P.maxp && at < P.n_step) ? int32_t(P.step[at]) : -1;
+            S.bpage[b] = (P.maxp > 0 && pos >= 0 && lp < P.maxp && at < P.n_step) ? int32_t(ldstep(P.step + (at))) : -1;
         }
         v.sync();
     }
-    const long long t0 = clock64();
-    uint32_t jobs = 0;
     // the stream runs to its end even after an abort (every wait then returns
     // at once), so all compute warps reach the same barriers; only a
     // dispatch fault (uniform over the VCC) stops it early
@@ -2261,6 +2310,21 @@ __device__ __forceinline__ void vcc_role(const RingParams& P, Shared& S, char* r
         }
         ++jobs;
     }
+    if constexpr (BATCHED) {  // resident steps of odd tile count end with the memory core's pad tile
+        if (P.n_epochs > 1) {
+            const uint32_t vw0 = P.core_off[core - 1], vn = P.core_off[core] - vw0;
+            const uint32_t vt = vn && ((__ldg(&P.words[vw0 + vn - 1]).x & 0xff) == OP_HALT) ? vn - 1 : vn;
+            if (vt & 1u) {
+                const uint32_t s0 = v.kt % v.R;
+                if ((s0 & uint32_t(CW - 1)) == v.w) {
+                    if (!v.wait_full(s0, (v.kt / v.R) & 1u)) v.ok = false;
+                    v.release(s0);
+                }
+                v.kt += 1;
+            }
+        }
+    }
+    }
     if (v.ct == 0) {
         SmStats& st = P.stats[blockIdx.x];
         st.wait[S_VCC_FULL] = S.vstat[v.VS_FULL];
@@ -2318,8 +2382,8 @@ __device__ __forceinline__ Tile resolve_load(const RingParams& P, uint4 raw) {
             t.bad = true;
             return t;
         }
-        const int64_t ctx = P.step[3 * c0 + 2];
-        const int64_t page = P.step[P.ptab + c0 * P.maxp + c1];
+        const int64_t ctx = ldstep(P.step + (3 * c0 + 2));
+        const int64_t page = ldstep(P.step + (P.ptab + c0 * P.maxp + c1));
         if (c1 * d.tile_rows >= ctx || page < 0) {
             t.empty = true;
             return t;
@@ -2330,7 +2394,7 @@ __device__ __forceinline__ Tile resolve_load(const RingParams& P, uint4 raw) {
         t.bad = page >= d.grid[0] || c2 >= d.grid[1] || t.run > SLOT;
         return t;
     }
-    if (mode == VDC_LOAD_CTX && c1 * d.tile_rows >= (P.n_step > VDC_STEP_CTX ? P.step[VDC_STEP_CTX] : 0)) {
+    if (mode == VDC_LOAD_CTX && c1 * d.tile_rows >= (P.n_step > VDC_STEP_CTX ? ldstep(P.step + (VDC_STEP_CTX)) : 0)) {
         t.empty = true;  // single-request cache page past the step's context
         return t;
     }
@@ -2386,27 +2450,64 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
     const uint32_t PF = P.prefetch;
     // the stream is LOAD words followed by one HALT
     const uint32_t ntiles = n && ((__ldg(&P.words[w0 + n - 1]).x & 0xff) == OP_HALT) ? n - 1 : n;
+    // resident decode: the stream is walked once per step; tile g is word
+    // g % ntiles of step g / ntiles. Weight tiles stream across the step
+    // boundary; a KV page of step e > 0 is resolved (context, page table) and
+    // loaded only after step e - 1 fed its token back: by then every append of
+    // step e - 1 is in memory and the step block holds step e's positions.
+    // batched programs place every attention page's K tile on an even ring
+    // index (lead pads); a step of odd length would flip that parity for the
+    // next step, so resident steps are padded to even length with one
+    // data-less tile (the compute core consumes it at the step's end)
+    const uint32_t ept = ntiles + ((BATCHED && P.n_epochs > 1) ? (ntiles & 1u) : 0u);
+    const uint32_t total = ept * P.n_epochs;
+    auto kv_gated = [&](uint4 r, uint32_t gg) {
+        const uint32_t mode = (r.y >> 24) & 0xfu;
+        return ntiles && gg >= ept && (mode == VDC_LOAD_CTX || mode == VDC_LOAD_PAGED);
+    };
+    auto word = [&](uint32_t gg) {  // the LOAD word of tile gg (the step pad: a data-less tile)
+        return gg % ept < ntiles ? __ldg(&P.words[w0 + gg % ept]) : make_uint4(0, 0, 0, 0);
+    };
+    auto resolve = [&](uint4 r, uint32_t gg) {
+        if (gg % ept >= ntiles) {
+            Tile t;
+            t.empty = true;
+            return t;
+        }
+        return resolve_load<BATCHED>(P, r);
+    };
     const bool issuer = lane < R;
     uint32_t g = lane, m = 0;  // lane s issues tiles s, s + R, s + 2R, ... into slot s
     unsigned long long st_empty = 0, bytes = 0, uops = 0;
     const long long t_start = clock64();
-    uint4 raw = issuer && g < ntiles ? __ldg(&P.words[w0 + g]) : make_uint4(0, 0, 0, 0);
+    uint4 raw = issuer && g < total ? word(g) : make_uint4(0, 0, 0, 0);
     // the lane's next tile is resolved as soon as its word arrives (descriptor,
     // page table and context loads overlap the slot polling), not when the
     // slot frees up
-    Tile cur = issuer && g < ntiles ? resolve_load<BATCHED>(P, raw) : Tile{};
+    bool deferred = issuer && g < total && kv_gated(raw, g);
+    Tile cur = issuer && g < total && !deferred ? resolve(raw, g) : Tile{};
     uint32_t pf_g = g + R;  // next tile of this lane to prefetch into L2 (beyond its slot)
     long long idle_since = 0;
     unsigned long long t_idle = 0;
     bool real_last = false;  // this lane's last issue was a bulk copy (bytes may still be landing)
     for (;;) {
-        const bool pending = issuer && g < ntiles;
+        const bool pending = issuer && g < total;
         if (!__any_sync(0xffffffffu, pending)) break;
         bool ready = false;
         uint32_t slot = 0;
         if (pending) {
             slot = lane;
             ready = m == 0 || mbar_test(&S.empty[slot], (m - 1u) & 1u);
+            if (ready && deferred) {  // KV page of a later step: wait for the previous step's token
+                if (int32_t(ld_relaxed(&P.counters[P.fb_ctr]) - (P.epoch + g / ept - 1u)) >= 0) {
+                    fence_acquire_gpu();
+                    fence_proxy_async_global();  // the appends were generic stores; the copy is async-proxy
+                    cur = resolve(raw, g);
+                    deferred = false;
+                } else {
+                    ready = false;
+                }
+            }
         }
         if (ready) {
             const Tile t = cur;
@@ -2433,8 +2534,9 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
             g += R;
             if (pf_g < g + R) pf_g = g + R;
             ++m;
-            raw = g < ntiles ? __ldg(&P.words[w0 + g]) : make_uint4(0, 0, 0, 0);
-            if (g < ntiles) cur = resolve_load<BATCHED>(P, raw);
+            raw = g < total ? word(g) : make_uint4(0, 0, 0, 0);
+            deferred = g < total && kv_gated(raw, g);
+            if (g < total && !deferred) cur = resolve(raw, g);
         }
         if (PF && pending && !ready && pf_g < ntiles && pf_g < g + R * (1 + PF)) {
             // slot busy (the compute core is behind or waiting on a dependency):

@@ -137,6 +137,11 @@ class Engine:
         self.descs = {d["name"]: d for d in info["descriptors"]}
 
     # -- memory -------------------------------------------------------------
+    def set_steps(self, steps: int) -> None:
+        """Resident decode (vdc_set_steps): every following launch runs `steps`
+        decode steps inside the persistent kernel (feedback programs only)."""
+        check(lib().vdc_set_steps(self._h, steps))
+
     def set_prefetch(self, tiles: int) -> None:
         """Ring engine: L2 prefetch look-ahead of the memory core (tiles)."""
         check(lib().vdc_set_prefetch(self._h, tiles))
