@@ -83,8 +83,11 @@ struct alignas(16) Shared {
     // batched programs: each request's position and the physical page of its
     // appended KV row (-1: none), read from the step block once per launch
     // (constant within a launch) instead of per epilogue element
-    int64_t bpos[VDC_RING_MAX_BATCH];
+    int32_t bpos[VDC_RING_MAX_BATCH];
     int32_t bpage[VDC_RING_MAX_BATCH];
+    int32_t btok[VDC_RING_MAX_BATCH], bctx[VDC_RING_MAX_BATCH];
+    // single-request programs: token, position, context of the running step
+    int64_t sstep[3];
     // compute-core wait-site cycles and the trace's readiness stamp, updated by
     // thread 0 only: in shared memory, not in registers that every compute
     // thread would carry through the whole µop loop
@@ -94,6 +97,11 @@ struct alignas(16) Shared {
     int32_t am_i[VDC_RING_MAX_BATCH];
 };
 
+// both kernel instances must fit one B200 CTA (227 KB of dynamic shared memory)
+static_assert(VDC_RING_MAX_SLOTS * SLOT + ((sizeof(Shared) + 127) & ~size_t(127)) <= 232448,
+              "single-request ring + control block exceed the B200 shared memory per CTA");
+static_assert(8 * SLOT + ((sizeof(Shared) + 1023) & ~size_t(1023)) + XRING_BYTES <= 232448,
+              "batched ring + control block + activation ring exceed the B200 shared memory per CTA");
 size_t smem_bytes(uint32_t slots, bool batched) {
     return size_t(slots) * SLOT + (batched ? ((sizeof(Shared) + 1023) & ~size_t(1023)) + XRING_BYTES
                                            : ((sizeof(Shared) + 127) & ~size_t(127)));
@@ -249,7 +257,7 @@ struct Vcc {
         char* b = t >= 0 ? sym_base(t, P->tp_rank) : nullptr;
         return b ? reinterpret_cast<uint32_t*>(b) : &P->counters[t < 0 ? 0 : t];
     }
-    __device__ int64_t token() const { return P->n_step > VDC_STEP_TOKEN ? ldstep(P->step + (VDC_STEP_TOKEN)) : 0; }
+    __device__ int64_t token() const { return S->sstep[0]; }
     __device__ int32_t tdtype(int32_t t) const { return P->descs[t].dtype; }
 
     // all compute threads: wait for ring tile k (slot full)
@@ -409,7 +417,7 @@ struct Vcc {
         }
         if ((J.flags & (VDC_JOB_ROPE | VDC_JOB_QKV)) && (rope_hd != J.head_dim || rope_theta != J.theta)) {
             // rotary table of this launch's position: cos/sin per dim pair, angles in double precision
-            const int64_t pos = P->n_step > VDC_STEP_POS ? ldstep(P->step + (VDC_STEP_POS)) : 0;
+            const int64_t pos = S->sstep[1];
             for (int d2 = int(ct); d2 < J.head_dim / 2; d2 += NCT) {
                 const double ang = double(pos) * pow(double(J.theta), -double(2 * d2) / double(J.head_dim));
                 S->rope_cs[d2] = float(cos(ang));
@@ -788,7 +796,7 @@ struct Vcc {
         char* ob = tptr(J.o_t);
         const bool obf = tdtype(J.o_t) == VDC_DTYPE_BF16;
         const int lr0 = J.r0 - J.out_row0;  // first output row (region-local)
-        const int64_t pos = P->n_step > VDC_STEP_POS ? ldstep(P->step + (VDC_STEP_POS)) : 0;
+        const int64_t pos = S->sstep[1];
         auto out_index = [&](int lr) -> int64_t {
             if (J.flags & VDC_JOB_KV_APPEND)
                 return (int64_t(lr / J.head_dim) * J.cache_rows + pos) * J.head_dim + lr % J.head_dim;
@@ -1411,7 +1419,7 @@ struct Vcc {
         uint4* xn = reinterpret_cast<uint4*>(tptr(J.o3_t));
         for (int i = int(ct); i < (J.r1 - J.r0) * nch; i += NCT) {
             const int b = J.r0 + i / nch, c = i % nch;
-            const int64_t tok = ldstep(P->step + (3 * b));
+            const int64_t tok = S->btok[b];
             const uint4 u = __ldg(tab + tok * nch + c), g = __ldg(wv + c);
             xo[int64_t(b) * nch + c] = u;
             uint4 o;
@@ -1602,8 +1610,8 @@ struct Vcc {
         // K on even slots: a leading pad tile aligns the job), so every slot
         // keeps a single consumer pair and jobs may span more than the ring
         const bool batched = BATCHED && (J.flags & VDC_JOB_BATCH);
-        const int64_t pos = batched ? ldstep(P->step + (3 * J.req + 1)) : ldstep(P->step + (VDC_STEP_POS));
-        const int64_t ctx = batched ? ldstep(P->step + (3 * J.req + 2)) : ldstep(P->step + (VDC_STEP_CTX));
+        const int64_t pos = batched ? S->bpos[J.req] : S->sstep[1];
+        const int64_t ctx = batched ? S->bctx[J.req] : S->sstep[2];
         if (batched && J.lead_pad) {
             const uint32_t s0 = kt % R;
             if ((s0 & uint32_t(CW - 1)) == w) {
@@ -1720,7 +1728,7 @@ struct Vcc {
             if (batched && (J.flags & VDC_JOB_PREFILL)) {
                 // prefill chunk: every row appended in this launch (request 0's
                 // position .. this row's position) comes from global
-                const int64_t lo = max(prow0, ldstep(P->step + (1))), hi = min(prow0 + int64_t(rows_w), ctx);
+                const int64_t lo = max(prow0, int64_t(S->bpos[0])), hi = min(prow0 + int64_t(rows_w), ctx);
                 for (int64_t rr = lo; rr < hi; ++rr) {
                     const size_t crow =
                         size_t(ldstep(P->step + (J.ptab + int64_t(J.req) * J.maxp + rr / PR))) * size_t(J.cache_rows) + size_t(rr % PR);
@@ -2145,7 +2153,7 @@ struct Vcc {
     __device__ void copy_row(const vdc_job& J) {
         const int32_t eb = P->descs[J.x_t].elem;
         int64_t off = J.x_off;
-        if (J.flags & VDC_JOB_TOKEN_ROW) off += (P->n_step > VDC_STEP_TOKEN ? ldstep(P->step + (VDC_STEP_TOKEN)) : 0) * J.k;
+        if (J.flags & VDC_JOB_TOKEN_ROW) off += token() * J.k;
         const uint4* src = reinterpret_cast<const uint4*>(tptr(J.x_t) + off * eb);
         uint4* dst = reinterpret_cast<uint4*>(tptr(J.o_t) + int64_t(J.o_off) * eb);
         for (int c = int(ct); c < J.k * eb / 16; c += NCT) dst[c] = __ldg(src + c);
@@ -2206,16 +2214,21 @@ __device__ __forceinline__ void vcc_role(const RingParams& P, Shared& S, char* r
         v.rope_hd = 0;
         v.binv_t = -2;
     }
-    if constexpr (BATCHED) {  // requests' positions and append pages of this launch
+    // the step's scalars (constant within a step) -> shared memory, read once
+    // here instead of an L2 round trip in every µop that needs them
+    if constexpr (BATCHED) {  // per request: token, position, context, append page
         const int b = int(v.ct);
         if (b < VDC_RING_MAX_BATCH) {
             const int64_t pos = 3 * b + 1 < P.n_step ? ldstep(P.step + (3 * b + 1)) : 0;
             const int64_t lp = pos / 64, at = int64_t(P.ptab) + int64_t(b) * P.maxp + lp;
-            S.bpos[b] = pos;
+            S.bpos[b] = int32_t(pos);
+            S.btok[b] = 3 * b < P.n_step ? int32_t(ldstep(P.step + 3 * b)) : 0;
+            S.bctx[b] = 3 * b + 2 < P.n_step ? int32_t(ldstep(P.step + (3 * b + 2))) : 0;
             S.bpage[b] = (P.maxp > 0 && pos >= 0 && lp < P.maxp && at < P.n_step) ? int32_t(ldstep(P.step + (at))) : -1;
         }
-        v.sync();
     }
+    if (v.ct < 3) S.sstep[v.ct] = int32_t(v.ct) < P.n_step ? ldstep(P.step + v.ct) : 0;
+    v.sync();
     // the stream runs to its end even after an abort (every wait then returns
     // at once), so all compute warps reach the same barriers; only a
     // dispatch fault (uniform over the VCC) stops it early
@@ -2382,8 +2395,11 @@ __device__ __forceinline__ Tile resolve_load(const RingParams& P, uint4 raw) {
             t.bad = true;
             return t;
         }
-        const int64_t ctx = ldstep(P.step + (3 * c0 + 2));
-        const int64_t page = ldstep(P.step + (P.ptab + c0 * P.maxp + c1));
+        // (plain loads: the memory core resolves every KV tile, an L2 round trip
+        // each would stall its issue loop; a later resident step only reads
+        // them after the acquire at its token gate)
+        const int64_t ctx = P.step[3 * c0 + 2];
+        const int64_t page = P.step[P.ptab + c0 * P.maxp + c1];
         if (c1 * d.tile_rows >= ctx || page < 0) {
             t.empty = true;
             return t;
@@ -2394,7 +2410,7 @@ __device__ __forceinline__ Tile resolve_load(const RingParams& P, uint4 raw) {
         t.bad = page >= d.grid[0] || c2 >= d.grid[1] || t.run > SLOT;
         return t;
     }
-    if (mode == VDC_LOAD_CTX && c1 * d.tile_rows >= (P.n_step > VDC_STEP_CTX ? ldstep(P.step + (VDC_STEP_CTX)) : 0)) {
+    if (mode == VDC_LOAD_CTX && c1 * d.tile_rows >= (P.n_step > VDC_STEP_CTX ? P.step[VDC_STEP_CTX] : 0)) {
         t.empty = true;  // single-request cache page past the step's context
         return t;
     }
@@ -2441,8 +2457,11 @@ __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
 // barrier (non-blocking test_wait) in one converged loop and issue the bulk
 // copy of their next tile as soon as it is free; optional L2 prefetch of
 // the tile `prefetch` rounds ahead.
-template <bool BATCHED>
-__device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
+// RESIDENT: launches of several decode steps (vdc_set_steps) walk the stream
+// once per step with token-gated KV pages; single-step launches run the
+// instance without that bookkeeping on the issue path
+template <bool BATCHED, bool RESIDENT>
+__device__ __forceinline__ void vmc_loop(const RingParams& P, Shared& S, char* ring) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t core = 2 * blockIdx.x;
     const uint32_t w0 = P.core_off[core], n = P.core_off[core + 1] - w0;
@@ -2459,17 +2478,25 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
     // index (lead pads); a step of odd length would flip that parity for the
     // next step, so resident steps are padded to even length with one
     // data-less tile (the compute core consumes it at the step's end)
-    const uint32_t ept = ntiles + ((BATCHED && P.n_epochs > 1) ? (ntiles & 1u) : 0u);
-    const uint32_t total = ept * P.n_epochs;
-    auto kv_gated = [&](uint4 r, uint32_t gg) {
+    const uint32_t ept = RESIDENT ? ntiles + (BATCHED ? (ntiles & 1u) : 0u) : ntiles;
+    const uint32_t total = RESIDENT ? ept * P.n_epochs : ntiles;
+    // (word index, step) of the lane's tile g, advanced incrementally (no
+    // per-tile division on the issue path)
+    uint32_t wi = lane, ei = 0;
+    while (ept && wi >= ept) {
+        wi -= ept;
+        ++ei;
+    }
+    auto kv_gated = [&](uint4 r) {
+        if constexpr (!RESIDENT) return false;
         const uint32_t mode = (r.y >> 24) & 0xfu;
-        return ntiles && gg >= ept && (mode == VDC_LOAD_CTX || mode == VDC_LOAD_PAGED);
+        return ei > 0 && wi < ntiles && (mode == VDC_LOAD_CTX || mode == VDC_LOAD_PAGED);
     };
-    auto word = [&](uint32_t gg) {  // the LOAD word of tile gg (the step pad: a data-less tile)
-        return gg % ept < ntiles ? __ldg(&P.words[w0 + gg % ept]) : make_uint4(0, 0, 0, 0);
+    auto word = [&]() {  // the LOAD word of the lane's tile (the step pad: a data-less tile)
+        return wi < ntiles ? __ldg(&P.words[w0 + wi]) : make_uint4(0, 0, 0, 0);
     };
-    auto resolve = [&](uint4 r, uint32_t gg) {
-        if (gg % ept >= ntiles) {
+    auto resolve = [&](uint4 r) {
+        if (RESIDENT && wi >= ntiles) {
             Tile t;
             t.empty = true;
             return t;
@@ -2480,12 +2507,12 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
     uint32_t g = lane, m = 0;  // lane s issues tiles s, s + R, s + 2R, ... into slot s
     unsigned long long st_empty = 0, bytes = 0, uops = 0;
     const long long t_start = clock64();
-    uint4 raw = issuer && g < total ? word(g) : make_uint4(0, 0, 0, 0);
+    uint4 raw = issuer && g < total ? word() : make_uint4(0, 0, 0, 0);
     // the lane's next tile is resolved as soon as its word arrives (descriptor,
     // page table and context loads overlap the slot polling), not when the
     // slot frees up
-    bool deferred = issuer && g < total && kv_gated(raw, g);
-    Tile cur = issuer && g < total && !deferred ? resolve(raw, g) : Tile{};
+    bool deferred = issuer && g < total && kv_gated(raw);
+    Tile cur = issuer && g < total && !deferred ? resolve(raw) : Tile{};
     uint32_t pf_g = g + R;  // next tile of this lane to prefetch into L2 (beyond its slot)
     long long idle_since = 0;
     unsigned long long t_idle = 0;
@@ -2498,11 +2525,11 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
         if (pending) {
             slot = lane;
             ready = m == 0 || mbar_test(&S.empty[slot], (m - 1u) & 1u);
-            if (ready && deferred) {  // KV page of a later step: wait for the previous step's token
-                if (int32_t(ld_relaxed(&P.counters[P.fb_ctr]) - (P.epoch + g / ept - 1u)) >= 0) {
+            if (RESIDENT && ready && deferred) {  // KV page of a later step: wait for the previous step's token
+                if (int32_t(ld_relaxed(&P.counters[P.fb_ctr]) - (P.epoch + ei - 1u)) >= 0) {
                     fence_acquire_gpu();
                     fence_proxy_async_global();  // the appends were generic stores; the copy is async-proxy
-                    cur = resolve(raw, g);
+                    cur = resolve(raw);
                     deferred = false;
                 } else {
                     ready = false;
@@ -2534,9 +2561,16 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
             g += R;
             if (pf_g < g + R) pf_g = g + R;
             ++m;
-            raw = g < total ? word(g) : make_uint4(0, 0, 0, 0);
-            deferred = g < total && kv_gated(raw, g);
-            if (g < total && !deferred) cur = resolve(raw, g);
+            wi += R;
+            if constexpr (RESIDENT) {
+                while (ept && wi >= ept) {
+                    wi -= ept;
+                    ++ei;
+                }
+            }
+            raw = g < total ? word() : make_uint4(0, 0, 0, 0);
+            deferred = g < total && kv_gated(raw);
+            if (g < total && !deferred) cur = resolve(raw);
         }
         if (PF && pending && !ready && pf_g < ntiles && pf_g < g + R * (1 + PF)) {
             // slot busy (the compute core is behind or waiting on a dependency):
@@ -2588,6 +2622,14 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
         st.bytes_stored = 0;
         st.tiles_issued = uops;
     }
+}
+
+template <bool BATCHED>
+__device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
+    if (P.n_epochs > 1)
+        vmc_loop<BATCHED, true>(P, S, ring);
+    else
+        vmc_loop<BATCHED, false>(P, S, ring);
 }
 
 template <bool BATCHED, bool QKNORM>
