@@ -80,6 +80,7 @@ struct LayoutConfig {
     // sharing one page allocation (req_pages all equal); one launch appends
     // all their K/V rows and returns every row's logits
     bool prefill = false;
+    int attn_job_cost = -1;  // batched attention load balance: fixed cost per split-KV job in ring tiles (-1: default)
 };
 
 ModelConfig llama3_8b();

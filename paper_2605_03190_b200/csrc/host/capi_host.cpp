@@ -114,6 +114,7 @@ decode::LayoutConfig layout_from(const json& j) {
     l.prefill = j.value("prefill", l.prefill);
     l.req_pages = j.value("req_pages", l.req_pages);
     l.pool_pages = j.value("pool_pages", l.pool_pages);
+    l.attn_job_cost = j.value("attn_job_cost", l.attn_job_cost);
     return l;
 }
 

@@ -410,6 +410,7 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
                                                          {"req_pages", rp}};
         if (l.prefill) attn_attrs["prefill"] = "1";
         if (l.pool_pages > 0) attn_attrs["pool_pages"] = std::to_string(l.pool_pages);
+        if (l.attn_job_cost >= 0) attn_attrs["job_cost"] = std::to_string(l.attn_job_cost);
         if (m.qk_norm) {
             b.norm(L + "q_norm", hd);
             b.norm(L + "k_norm", hd);

@@ -795,12 +795,17 @@ class RingLowering {
         std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t c) {
             return all[size_t(a)].p1 - all[size_t(a)].p0 > all[size_t(c)].p1 - all[size_t(c)].p0;
         });
+        // cost model (in ring tiles): 2 per page plus a fixed per-job cost
+        // (q staging, warp merge, arrival, the last split's combine; measured
+        // ~8 us = ~22 tiles at a 0.35 us tile, tools/attn_cost.py);
+        // layout.attn_job_cost overrides it
+        const int64_t fixed = attr_int(n, "job_cost", 22);
         std::vector<int64_t> load(sms_, 0);
         std::vector<uint32_t> sm_of(all.size());
         for (int64_t i : order) {
             const uint32_t s = uint32_t(std::min_element(load.begin(), load.end()) - load.begin());
             sm_of[size_t(i)] = s;
-            load[s] += 2 * (all[size_t(i)].p1 - all[size_t(i)].p0) + 1;
+            load[s] += 2 * (all[size_t(i)].p1 - all[size_t(i)].p0) + fixed;
         }
         std::map<std::pair<int64_t, int64_t>, int32_t> ctr;
         for (size_t i = 0; i < all.size(); ++i) {
