@@ -174,7 +174,8 @@ int vdc_program_build(const char* request_json, vdc_program** out);
 int vdc_program_parse(const char* streams_json, const char* sidecar, vdc_program** out);
 void vdc_program_free(vdc_program* prog);
 /* JSON: {"streams":{core:text}, "sidecar":..., "words":{core:hex}?, "tilings":..., ...}
- * mode 0: streams + sidecar, 1: also encoded words, 2: summary (descriptors, params, geometry) */
+ * mode 0: streams + sidecar, 1: also encoded words, 2: summary (descriptors, params, geometry),
+ * 3: {"unfolded_words": {core: hex}} every stream with its loops expanded (generator::unfold_stream) */
 int vdc_program_text(const vdc_program* prog, int mode, char** out_json);
 int vdc_program_cores(const vdc_program* prog, uint32_t* n_cores, uint32_t* sm_count, uint32_t* vcc_per_sm);
 /* encoded stream of core i (CoreId order over sm_count x (1 + vcc_per_sm)) */

@@ -174,6 +174,12 @@ class Program:
         check(lib().vdc_program_text(self._h, 1 if with_words else 0, ctypes.byref(out)))
         return json.loads(take_string(out))
 
+    def unfolded_words(self) -> dict:
+        """{core: hex} of every stream with its loops expanded (unfold_stream)."""
+        out = ctypes.c_void_p()
+        check(lib().vdc_program_text(self._h, 3, ctypes.byref(out)))
+        return json.loads(take_string(out))["unfolded_words"]
+
     def info(self) -> dict:
         """Summary (descriptors, params, geometry) without stream text."""
         if self._info is None:

@@ -223,6 +223,24 @@ void ProgramBox::finish() {
 }
 
 std::string ProgramBox::text(int mode) const {
+    if (mode == 3) {  // every core's stream unfolded (LOOP/REPEAT expanded), encoded words as hex
+        static const char* hexd = "0123456789abcdef";
+        json out, hex = json::object();
+        out["ok"] = true;
+        for (const auto& c : cores) {
+            if (!program.streams.count(c)) continue;
+            const auto enc = isa::encode_stream(generator::unfold_stream(program, c));
+            std::string h;
+            h.reserve(enc.size() * 2);
+            for (uint8_t b : enc) {
+                h.push_back(hexd[b >> 4]);
+                h.push_back(hexd[b & 15]);
+            }
+            hex[c.name()] = h;
+        }
+        out["unfolded_words"] = hex;
+        return out.dump();
+    }
     const bool with_words = mode == 1, summary = mode == 2;
     json out;
     out["ok"] = true;

@@ -11,8 +11,10 @@ budget, baseline allocation certificate) must be byte-identical.
 Known reference defect (SURVEY finding 5): nested fold_loops leaves a stale
 LOOP.imm and the reference throws "LOOP body length does not match its
 REPEAT"; our builder folds correctly, so for those cases we require that our
-program unfolds to the same µop sequence as the reference's fold-free build
-of the same request.
+program unfolds (unfold_stream, vdc_program_text mode 3) to the reference's
+fold-free build of the same request — word for word up to the virtual-flow
+ids a folded body shares across iterations and the stream-final `last` flag —
+and that our own fold-free build is byte-identical to it.
 """
 import json
 import subprocess
@@ -40,6 +42,7 @@ def test_builder_matches_reference(name):
         return
     if not ref["ok"]:
         assert NESTED_FOLD_BUG in ref["error"], f"reference error {ref['error']!r} but ours succeeded"
+        check_unfolds_to_reference(case["request"])
         return
     assert ours["tilings"] == ref["tilings"]
     assert ours["streams"] == ref["streams"]
@@ -47,6 +50,38 @@ def test_builder_matches_reference(name):
     assert ours["sidecar"] == ref["sidecar"]
     assert ours["total_uops"] == ref["total_uops"]
     assert ours["certificate_ok"] == ref["certificate_ok"]
+
+
+def _normalised(hex_words: str) -> str:
+    """words with the virtual-flow byte cleared (a folded loop body shares one
+    set of flow ids across its iterations; flows only steer the unit mapping)
+    and the stream-final `last` flag dropped (it marks the final word of the
+    folded or the unfolded form)"""
+    out = []
+    for i in range(0, len(hex_words), 32):
+        w = bytearray.fromhex(hex_words[i:i + 32])
+        w[4] = 0
+        w[1] &= 0xF7
+        out.append(w.hex())
+    return "".join(out)
+
+
+def check_unfolds_to_reference(request: dict):
+    """SURVEY finding 5: the reference cannot build nested folds; ours must
+    unfold (generator::unfold_stream) to the reference's fold-free build."""
+    ours = Program.build(request).unfolded_words()
+    fold_free = json.loads(json.dumps(request))
+    fold_free.setdefault("options", {})["fold"] = False
+    if not harness.REF_CLI.exists():
+        pytest.skip("oracle/_ref not built")
+    r = subprocess.run([str(harness.REF_CLI)], input=json.dumps(fold_free).encode(), capture_output=True)
+    ref = json.loads(r.stdout)
+    assert ref["ok"], ref.get("error")
+    assert set(ours) == set(ref["words"])
+    for core, words in ref["words"].items():
+        assert _normalised(ours[core]) == _normalised(words), core
+    # and our own fold-free build is byte-identical to the reference's
+    assert Program.build(fold_free).text(True)["words"] == ref["words"]
 
 
 def test_corpus_matches_golden_requests():
