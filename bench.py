@@ -191,6 +191,21 @@ def cpu_oracle_tokens_per_s(timeout_s: int = 240) -> dict:
             "cpu": _cpu_name(), "nproc": os.cpu_count()}
 
 
+def dense_cpu_context(ctx: int, timeout_s: int = 120) -> dict:
+    """BASELINE.md §3.2's optional context figure: a dense fp32 Llama-3-8B
+    batch-1 decode step (32 layers + lm_head, ctx rows of KV) on every host
+    core (oracle/_ref/dense_cpu, std::thread). Not the reference path and not
+    the target; reported beside cpu_baseline only."""
+    exe = ROOT / "oracle/_ref/dense_cpu"
+    if not exe.exists():
+        return {"value": None, "unavailable": "oracle/_ref/dense_cpu not built"}
+    r = subprocess.run([str(exe), "32", str(ctx), "2"], capture_output=True, text=True, timeout=timeout_s)
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    return {"value": out["tokens_per_s"], "unit": "tokens/s", "cores": out["threads"],
+            "sample": (f"dense fp32 Llama-3-8B batch-1 decode, 32 layers + lm_head at ctx {ctx}, best of 2 steps, "
+                       "one layer's weights reused for every layer (each step still streams 32 x 0.87 GB)")}
+
+
 def _cpu_name():
     try:
         for line in open("/proc/cpuinfo"):
@@ -690,6 +705,11 @@ def main():
                 result["cpu_baseline"] = cpu_oracle_tokens_per_s()
             except Exception as e:  # the baseline is reported, never the target
                 result["cpu_baseline"] = {"value": None, "unavailable": str(e)[:200]}
+            if args.batch == 1 and args.model == "llama3-8b":
+                try:
+                    result["cpu_baseline"]["dense_fp32_all_cores"] = dense_cpu_context(args.ctx)
+                except Exception as e:
+                    result["cpu_baseline"]["dense_fp32_all_cores"] = {"value": None, "unavailable": str(e)[:200]}
         print(json.dumps(result))
     if world > 1:
         import torch.distributed as dist
