@@ -71,6 +71,9 @@
 #define VDC_JOB_PREFILL 0x4000  /* batched ATTN of a prefill chunk: the batch's rows are consecutive
                                    positions of one sequence sharing its pages; every row appended
                                    in this launch (from request 0's position on) is patched in */
+#define VDC_JOB_KVSWZ 0x8000   /* single-request KV caches with swizzled page rows (VDC_DESC_KPAGE_SWZ):
+                                   the qkv epilogue appends k / v rows swizzled and ATTN_DECODE reads
+                                   them on the tensor cores (batched pools are always swizzled) */
 #define VDC_JOB_TP_ARGMAX 0x10000 /* with ARGMAX under tensor parallelism (vocab-parallel lm_head): the
                                    rank's best (logit, global vocab index) per request is posted to
                                    slot tp_rank of every rank's symmetric exchange buffer and each
@@ -99,7 +102,8 @@
  * bulk copy per ring tile (row-major 128 x 64 boxes would be 128 separate
  * 128-byte DRAM bursts per tile, ~half the HBM rate). */
 #define VDC_DESC_PACKED_SW128 0x80000000u
-/* vdc_desc.tma value of a batched K or V page pool (pages, hkv * 64, hd):
+/* vdc_desc.tma value of a batched K or V page pool (pages, hkv * 64, hd), and
+ * of a single-request bf16 head-dim-128 ring cache (hkv, max_ctx, hd):
  * each page row's 16-byte chunks are stored swizzled, logical chunk c of page
  * row r at chunk (c & 8) | ((c & 7) ^ (r & 7)) (written that way by the qkv
  * epilogue; attention's ldmatrix reads of 8 consecutive rows, K for Q.K^T and

@@ -139,7 +139,11 @@ struct RingParams {
 };
 size_t ring_smem_bytes(uint32_t ring_slots, bool batched = false);
 const void* ring_kernel_entry(bool batched, bool qknorm = false);
-constexpr uint32_t kRingThreads = 32 * (8 + 1);
+// 8 compute warps (two warpgroups) + a third warpgroup whose first warp is
+// the memory core: with 9 warps one SM sub-partition holds 3 warps anyway
+// (168 registers each); with 12, the third warpgroup hands its registers to
+// the compute warpgroups at start (setmaxnreg), which then run at 224
+constexpr uint32_t kRingThreads = 32 * 12;
 
 // A region of `count` slots, not necessarily contiguous (indices packed 8
 // bits each): the allocator prefers a contiguous run but falls back to any

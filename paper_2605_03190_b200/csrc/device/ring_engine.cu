@@ -797,9 +797,12 @@ struct Vcc {
         const bool obf = tdtype(J.o_t) == VDC_DTYPE_BF16;
         const int lr0 = J.r0 - J.out_row0;  // first output row (region-local)
         const int64_t pos = S->sstep[1];
+        const bool swz = J.flags & VDC_JOB_KVSWZ;  // swizzled cache page rows
+        // element d of a cache row at position pos, in storage order
+        auto cache_col = [&](int d) -> int { return swz ? int((kv_swz(uint32_t(d) >> 3, uint32_t(pos & 7)) << 3) | uint32_t(d & 7)) : d; };
         auto out_index = [&](int lr) -> int64_t {
             if (J.flags & VDC_JOB_KV_APPEND)
-                return (int64_t(lr / J.head_dim) * J.cache_rows + pos) * J.head_dim + lr % J.head_dim;
+                return (int64_t(lr / J.head_dim) * J.cache_rows + pos) * J.head_dim + cache_col(lr % J.head_dim);
             return int64_t(J.o_off) + lr;
         };
         if (J.flags & VDC_JOB_QKV) {
@@ -828,7 +831,8 @@ struct Vcc {
                 } else {
                     const bool isk = wr < qrows + kvr;
                     const int lr = isk ? wr - qrows : wr - qrows - kvr;
-                    const int64_t at = (int64_t(lr / hd) * J.cache_rows + pos) * hd + lr % hd;
+                    // (a pair of dims never straddles a 16-byte chunk)
+                    const int64_t at = (int64_t(lr / hd) * J.cache_rows + pos) * hd + cache_col(lr % hd);
                     store_out(isk ? kb : vb, obf, at, a);
                     store_out(isk ? kb : vb, obf, at + 1, b);
                 }
@@ -1621,14 +1625,12 @@ struct Vcc {
             kt += 1;
         }
         const int rows_w = PR / 2;  // rows per warp (<= 32: one per lane)
-        // batched bf16 page pools (K and V page rows swizzled): scores and P.V on
-        // the tensor cores (attn_page_mma). Single-request programs keep the
-        // CUDA-core path: at batch 1 the tensor-core page loop shortens the
-        // attention phase by ~2.9 us per layer, but inside the one persistent
-        // kernel its register demand costs the GEMV operators more
-        // (A/B on one B200: 290.9 vs 293.9 tokens/s)
-        constexpr bool MMA = BATCHED && BF && DPL == 4;
-        if (MMA && !batched) {  // batched kernels only run batched attention jobs
+        // bf16 head-dim-128 caches (K and V page rows swizzled: batched pools and
+        // VDC_JOB_KVSWZ single-request caches): scores and P.V on the tensor
+        // cores (attn_page_mma); the fp32 geometry: CUDA-core path
+        constexpr bool MMA = BF && DPL == 4;
+        const bool swz = batched || (J.flags & VDC_JOB_KVSWZ);
+        if (MMA && !swz) {  // ring bf16 head-dim-128 caches are always swizzled (decode_graph.cpp)
             if (ct == 0) fire(6, 0x2A00u | uint32_t(sm));
             ok = false;
         }
@@ -1763,7 +1765,7 @@ struct Vcc {
                 if constexpr (qkn) {  // QK-norm + rotary of the appended k row, written back to the cache
                     // the lane's 4 stored dims; batched pools hold K rows swizzled
                     const int pc = int(lane >> 1);
-                    const int lc = batched ? ((pc & 8) | ((pc & 7) ^ int(pos & 7))) : pc;
+                    const int lc = swz ? ((pc & 8) | ((pc & 7) ^ int(pos & 7))) : pc;
                     const int dbase = lc * 8 + int(lane & 1u) * 4;
                     const uint2 u = ldcg64(kn + lane * 8);
                     const uint2 wv = *reinterpret_cast<const uint2*>(tptr(J.block) + dbase * 2);
@@ -2632,6 +2634,11 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
         vmc_loop<BATCHED, false>(P, S, ring);
 }
 
+// register split per SM sub-partition (16384 registers = 512 per lane slot,
+// one warp of each warpgroup): 2 x 224 (compute) + 56 (memory warpgroup)
+constexpr uint32_t kVccRegs = 224, kVmcRegs = 56;
+static_assert(2 * kVccRegs + kVmcRegs <= 512 && kRingThreads == 3 * 128 && NCT == 256);
+
 template <bool BATCHED, bool QKNORM>
 __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(const __grid_constant__ RingParams P) {
     extern __shared__ __align__(1024) char smem[];
@@ -2667,6 +2674,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(const __grid_cons
     __syncthreads();
     if (BATCHED) tc_fence_after();
     if (threadIdx.x < NCT) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kVccRegs));
         vcc_role<BATCHED, QKNORM>(P, S, ring);
         if (BATCHED) {
             tc_fence_before();
@@ -2676,7 +2684,8 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(const __grid_cons
                 asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(S.tmem_base), "r"(TMEM_COLS));
         }
     } else {
-        vmc_role<BATCHED>(P, S, ring);
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kVmcRegs));
+        if (threadIdx.x < NCT + 32) vmc_role<BATCHED>(P, S, ring);  // warps 9..11 only donate registers
     }
 }
 

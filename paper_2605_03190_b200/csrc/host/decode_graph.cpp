@@ -209,6 +209,10 @@ OperatorGraph build_decode_graph(const ModelConfig& m, const LayoutConfig& l) {
             TensorRef& t = b.add(L + c, {hkv, l.max_ctx, hd}, l.page_rows, hd,
                                  m.scaled_init ? InitKind::centered : InitKind::random, e);
             t.state = true;
+            // ring programs: bf16 head-dim-128 caches keep their page rows swizzled
+            // for the tensor-core attention (ring_abi.h VDC_DESC_KPAGE_SWZ)
+            if (l.ring && e == ElemType::bf16 && hd == 128 && l.page_rows == 64 && l.max_ctx % 64 == 0)
+                t.tma = VDC_DESC_KPAGE_SWZ;
             b.view(L + c, ".seg", 1, R);
         }
         std::map<std::string, std::string> qkv_attrs = {{"eps", eps}, {"theta", theta}, {"rope", "1"}, {"job_rows", std::to_string(R)}};

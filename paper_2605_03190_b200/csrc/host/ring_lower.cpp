@@ -311,6 +311,7 @@ class RingLowering {
                         j.b_t = storage(idx(n.outputs[1]));
                         j.o2_t = storage(idx(n.outputs[2]));
                         j.cache_rows = int32_t(desc_[idx(n.outputs[1])].shape[1]);
+                        if (desc_[uint16_t(j.b_t)].tma == VDC_DESC_KPAGE_SWZ) j.flags |= VDC_JOB_KVSWZ;
                         if (c0 < qrows) r.publishes.push_back(j.o_t);
                         if (c0 < qrows + kvrows && c1 > qrows) r.publishes.push_back(j.b_t);
                         if (c1 > qrows + kvrows) r.publishes.push_back(j.o2_t);
@@ -401,6 +402,7 @@ class RingLowering {
                 j.split = int32_t(s);
                 j.arrive_ctr = ctr;
                 j.arrive_need = int32_t(splits);
+                if (kd.tma == VDC_DESC_KPAGE_SWZ) j.flags |= VDC_JOB_KVSWZ;
                 qk_norm_fields(n, j);
                 // ctx-bounded: pages past the step's context are not loaded
                 for (int64_t pg = j.r0; pg < j.r1; ++pg) {

@@ -136,8 +136,9 @@ def test_c2_full_llama3_8b_ctx4096_100_steps(cuda):
         nxt = int(tens["next_token"].item())
         assert nxt == int(tens["logits"].view(-1).argmax().item())  # fused argmax = argmax of the device logits
         for l in (0, 15, 31):
-            kc = tens[f"L{l}.kc"].view(hkv, T, hd)[:, pos, :].reshape(-1)
-            vc = tens[f"L{l}.vc"].view(hkv, T, hd)[:, pos, :].reshape(-1)
+            # (bf16 head-dim-128 ring caches store page rows swizzled)
+            kc = tr.unswizzle_k(tens[f"L{l}.kc"].view(hkv, T, hd).contiguous(), hd)[:, pos, :].reshape(-1)
+            vc = tr.unswizzle_k(tens[f"L{l}.vc"].view(hkv, T, hd).contiguous(), hd)[:, pos, :].reshape(-1)
             tally.kv(l, kc, r["k"][l][0], r32["k"][l][0])
             tally.kv(l, vc, r["v"][l][0], r32["v"][l][0])
         assert [int(x) for x in st[:3].tolist()] == [nxt, pos + 1, pos + 2]  # device feedback advanced the step block
