@@ -1,0 +1,16 @@
+set -x
+for r in 1 2; do
+for v in base w12 w12mma; do
+  VDC_LIB=abtest/libvdc_$v.so timeout 300 python bench.py --steps 40 --warmup 5 --no-cpu-baseline > gpurun_out/ab2_c2_${v}_$r.json 2>gpurun_out/ab2_err_$v.txt
+done
+done
+for v in base w12mma; do
+  VDC_LIB=abtest/libvdc_$v.so timeout 300 python bench.py --batch 32 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/ab2_c3_${v}.json 2>>gpurun_out/ab2_err_$v.txt
+done
+python - <<'PY'
+import json,glob
+for f in sorted(glob.glob("gpurun_out/ab2_c*.json")):
+    try:
+        d=json.load(open(f)); print(f, d["value"], d["roofline"]["frac"], d["e2e"]["value"])
+    except Exception as e: print(f, "ERR", e)
+PY
