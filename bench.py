@@ -206,6 +206,13 @@ def dense_cpu_context(ctx: int, timeout_s: int = 120) -> dict:
                        "one layer's weights reused for every layer (each step still streams 32 x 0.87 GB)")}
 
 
+def _stream_stats(eng):
+    try:  # (A/B runs may load an older library without the export)
+        return eng.stream_stats()
+    except Exception:
+        return None
+
+
 def _cpu_name():
     try:
         for line in open("/proc/cpuinfo"):
@@ -400,6 +407,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                    "model": "llama3-8b", "batch": 1, "ctx": args.ctx, "parallelism": parallelism,
                    "l2": "inputs larger than L2 (algorithmic %.2f GB per step vs 126 MB L2)" % (nbytes["total"] / 1e9),
                    "program_uops": info["total_uops"], "virtual_cores": prog.cores()[0], "build_seconds": round(build_s, 2),
+                   "memory_core_streams": _stream_stats(eng),
                    "resident_steps_per_launch": R,
                    **({"ctx_mean_timed": round(ctx_mean, 1)} if R > 1 else {})},
         "e2e": {"value": round(e2e_value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 8 * 8,
@@ -583,7 +591,8 @@ def run_batched(args, rank: int = 0, world: int = 1, local_rank: int = 0):
                    "model": args.model, "batch": B, "contexts": ctxs,
                    "parallelism": f"tp{world} (Megatron split, in-kernel NVLink allreduce)" if tp else "1 GPU",
                    "l2": "inputs larger than L2 (algorithmic %.2f GB per step vs 126 MB L2)" % (nbytes["total"] / 1e9),
-                   "program_uops": info["total_uops"], "build_seconds": round(build_s, 2)},
+                   "program_uops": info["total_uops"], "build_seconds": round(build_s, 2),
+                   "memory_core_streams": _stream_stats(eng)},
         "e2e": {"value": round(B * args.steps / (e2e_ms / 1e3), 2), "unit": "tokens/s", "h2d_bytes_per_step": 3 * B * 8,
                 "d2h_bytes_per_step": B * 8,
                 "sampling": "greedy argmax fused into the lm_head GEMM (device" + (

@@ -168,4 +168,25 @@ typedef struct vdc_job {
                                  the first 128-byte line, the batched ones in the second */
 } vdc_job;  /* 256 bytes */
 
+/* Folded memory-core streams (the loop folding of PAPER.md:773 / fold.cpp on
+ * the ring hot path). A ring program's memory-core stream is one LOAD word per
+ * ring tile. At vdc_load_jobs the engine folds each SM's stream into a
+ * sequence of vdc_run entries, every maximal regular stretch of tiles one
+ * entry (a lone tile is a run of 1); the device expands them tile by tile.
+ * Tile k of a run (k < count):
+ *   a = k % n_alt, j = k / n_alt, i = j % n_in, o = j / n_in;
+ *   tensor = a ? t_alt : the base word's tensor;
+ *   coordinate c = base c + i * d_in[c] + o * d_out[c]   (c = 0, 1, 2);
+ *   every other field is the base word's.
+ * So a GEMV job (row blocks x column tiles, row-major) is one run, and an
+ * attention job (K page, V page, K page, ...) is one run with n_alt = 2.
+ * 32 bytes, self-contained: one load per run on the device. */
+typedef struct vdc_run {
+    uint32_t base[4];         /* the LOAD word of tile 0 */
+    uint32_t count_alt;       /* tiles in the run (bits 0..23) | n_alt (1 or 2) << 24 */
+    uint32_t nin_talt;        /* groups per inner line n_in (bits 0..11) | t_alt << 12 (tensor of odd tiles) */
+    int8_t d_in[3], d_out[3]; /* coordinate steps per inner group / per outer line */
+    uint16_t rsv;
+} vdc_run;  /* 32 bytes */
+
 #endif

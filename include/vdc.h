@@ -154,9 +154,20 @@ int vdc_wait(vdc_ctx* ctx, vdc_report* report);
  * uint64 {core << 32 | pc, t_enter, t_prologue_ready, t_done} in %globaltimer
  * ns, written for each compute µop; dptr = NULL disables tracing */
 int vdc_bind_trace(vdc_ctx* ctx, void* dptr, uint32_t records_per_core);
-/* ring engine: L2 prefetch look-ahead of the memory core, in rounds of 8
- * tiles (default 0 = off, <= 31) */
+/* ring engine: formerly the L2 prefetch look-ahead of the memory core. The
+ * look-ahead measured slower at every depth and was removed: only 0 is
+ * accepted */
 int vdc_set_prefetch(vdc_ctx* ctx, uint32_t tiles);
+/* ring engine: the memory-core streams as loaded (one LOAD word per ring
+ * tile) and as folded on the device (ring_abi.h vdc_run): total LOAD words,
+ * run entries, entries covering more than one tile. Valid after vdc_load_jobs */
+int vdc_ring_stream_stats(vdc_ctx* ctx, uint64_t* load_words, uint64_t* entries, uint64_t* multi_tile_runs);
+/* fold one memory-core stream of LOAD words (16 bytes each, no HALT) the way
+ * vdc_load_jobs does into run entries (`runs`, capacity n); vdc_unfold_stream
+ * expands entries back to LOAD words (the host reference of the device
+ * expansion). Test / tooling entry points */
+int vdc_fold_stream(const uint8_t* words, uint32_t n, vdc_run* runs, uint32_t* n_runs);
+int vdc_unfold_stream(const vdc_run* runs, uint32_t n_runs, uint8_t* words, uint32_t capacity, uint32_t* n_words);
 /* resident decode: every following launch runs `steps`
  * decode steps inside the persistent kernel. Needs a program that samples on
  * the device and feeds the token back (layout.argmax + layout.feedback): step

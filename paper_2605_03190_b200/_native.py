@@ -72,7 +72,8 @@ class vdc_report(ctypes.Structure):
 # every symbol include/vdc.h declares (the CPU suite checks they are exported)
 EXPORTS = [
     "vdc_last_error", "vdc_version", "vdc_create", "vdc_destroy", "vdc_load_program", "vdc_load_jobs", "vdc_set_params",
-    "vdc_bind_tensor", "vdc_bind_symmetric", "vdc_tp_alloc", "vdc_tp_bind", "vdc_bind_step", "vdc_bind_trace", "vdc_launch", "vdc_wait", "vdc_set_watchdog", "vdc_set_prefetch", "vdc_set_steps", "vdc_program_build",
+    "vdc_bind_tensor", "vdc_bind_symmetric", "vdc_tp_alloc", "vdc_tp_bind", "vdc_bind_step", "vdc_bind_trace", "vdc_launch", "vdc_wait", "vdc_set_watchdog", "vdc_set_prefetch", "vdc_set_steps", "vdc_ring_stream_stats",
+    "vdc_fold_stream", "vdc_unfold_stream", "vdc_program_build",
     "vdc_program_parse", "vdc_program_free", "vdc_program_text", "vdc_program_cores", "vdc_program_words",
     "vdc_program_load", "vdc_free_string", "vdc_program_synthesize",
     "vdc_kv_create", "vdc_kv_destroy", "vdc_kv_reserve", "vdc_kv_release", "vdc_kv_stats", "vdc_kv_table",
@@ -110,6 +111,9 @@ def lib() -> ctypes.CDLL:
         "vdc_set_watchdog": ([vp, c.c_uint32], c.c_int),
         "vdc_set_prefetch": ([vp, c.c_uint32], c.c_int),
         "vdc_set_steps": ([vp, c.c_uint32], c.c_int),
+        "vdc_ring_stream_stats": ([vp, c.POINTER(c.c_uint64), c.POINTER(c.c_uint64), c.POINTER(c.c_uint64)], c.c_int),
+        "vdc_fold_stream": ([c.c_char_p, c.c_uint32, vp, c.POINTER(c.c_uint32)], c.c_int),
+        "vdc_unfold_stream": ([vp, c.c_uint32, c.c_char_p, c.c_uint32, c.POINTER(c.c_uint32)], c.c_int),
         "vdc_program_build": ([c.c_char_p, c.POINTER(vp)], c.c_int),
         "vdc_program_parse": ([c.c_char_p, c.c_char_p, c.POINTER(vp)], c.c_int),
         "vdc_program_free": ([vp], None),
@@ -127,6 +131,8 @@ def lib() -> ctypes.CDLL:
         "vdc_kv_table": ([vp, c.POINTER(c.c_int64)], c.c_int),
     }
     for name, (args, res) in sig.items():
+        if "VDC_LIB" in os.environ and not hasattr(L, name):
+            continue  # A/B runs against an older build: symbols it predates stay unbound
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = res

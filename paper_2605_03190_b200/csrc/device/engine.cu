@@ -1862,6 +1862,7 @@ __global__ void __launch_bounds__(32 * (1 + kMaxLdu + kMaxStu + kMaxVcc * kVccWa
 #include <vector>
 
 #include "capi_common.hpp"
+#include "ring_fold.hpp"
 
 using namespace vdc_dev;
 using vdc_impl::fail;
@@ -1886,6 +1887,14 @@ struct vdc_ctx {
     std::vector<DepQueue> dep_init;
     // device buffers
     uint4* d_words = nullptr;
+    // ring programs: host copy of the words (the memory-core streams are
+    // folded at vdc_load_jobs) and the folded streams on the device
+    std::vector<vdc_host::Word> h_words;
+    std::vector<uint32_t> h_off;
+    uint32_t* d_voff = nullptr;
+    uint32_t* d_vtiles = nullptr;
+    vdc_run* d_runs = nullptr;
+    uint64_t n_load_words = 0, n_entries = 0, n_multi = 0;
     uint32_t* d_core_off = nullptr;
     DevDesc* d_descs = nullptr;
     DepQueue* d_deps = nullptr;
@@ -1909,7 +1918,6 @@ struct vdc_ctx {
     char* d_jobs_core = nullptr;
     uint32_t n_jobs = 0;
     uint32_t epoch = 0;
-    uint32_t ring_prefetch = 0;
     size_t n_counters = 0;
     std::vector<char*> sym_host;  // [n_desc][VDC_RING_MAX_TP]
     char** d_sym = nullptr;
@@ -2004,6 +2012,9 @@ int vdc_destroy(vdc_ctx* ctx) {
     dfree(ctx->d_params);
     dfree(ctx->d_jobs);
     dfree(ctx->d_jobs_core);
+    dfree(ctx->d_voff);
+    dfree(ctx->d_vtiles);
+    dfree(ctx->d_runs);
     dfree(ctx->d_sym);
     dfree(ctx->d_tmaps);
     dfree(ctx->d_stats);
@@ -2054,6 +2065,9 @@ int vdc_load_program(vdc_ctx* ctx, const uint8_t* words, const uint32_t* words_p
     if (off[n_cores]) CU(cudaMemcpy(ctx->d_words, words, size_t(off[n_cores]) * 16, cudaMemcpyHostToDevice));
     CU(cudaMalloc(&ctx->d_core_off, off.size() * 4));
     CU(cudaMemcpy(ctx->d_core_off, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
+    ctx->h_words.resize(off[n_cores]);
+    if (off[n_cores]) std::memcpy(ctx->h_words.data(), words, size_t(off[n_cores]) * 16);
+    ctx->h_off = off;
     ctx->n_cores = n_cores;
     ctx->slot_budget = slot_budget;
     ctx->local_depth = local_depth;
@@ -2186,6 +2200,38 @@ int vdc_load_jobs(vdc_ctx* ctx, const vdc_job* jobs, uint32_t n_jobs, uint32_t r
         if (ring_smem_bytes(ring_slots, batched) > size_t(optin))
             return fail(VDC_ERR_INPUT, "ring of " + std::to_string(ring_slots) + " slots needs " +
                                            std::to_string(ring_smem_bytes(ring_slots, batched)) + " B of shared memory");
+    }
+    {
+        // fold every SM's memory-core stream (core 2 sm; LOAD words + HALT)
+        const uint32_t sms = ctx->prof.sm_count;
+        std::vector<vdc_run> runs;
+        std::vector<uint32_t> voff(sms + 1, 0), vtiles(sms, 0);
+        uint64_t loads = 0, multi = 0;
+        for (uint32_t sm = 0; sm < sms; ++sm) {
+            const uint32_t a = ctx->h_off[2 * sm], b = ctx->h_off[2 * sm + 1];
+            uint32_t n = b - a;
+            if (n && (ctx->h_words[b - 1][0] & 0xff) == 0x45) --n;  // HALT
+            for (uint32_t i = a; i < a + n; ++i)
+                if ((ctx->h_words[i][0] & 0xff) != 0x01) return fail(VDC_ERR_INPUT, "ring memory-core streams hold LOAD words only");
+            const vdc_host::FoldedStream f = vdc_host::fold_stream(ctx->h_words.data() + a, n);
+            runs.insert(runs.end(), f.runs.begin(), f.runs.end());
+            voff[sm + 1] = uint32_t(runs.size());
+            vtiles[sm] = uint32_t(f.tiles);
+            loads += n;
+            multi += f.multi;
+        }
+        dfree(ctx->d_voff);
+        dfree(ctx->d_vtiles);
+        dfree(ctx->d_runs);
+        CU(cudaMalloc(&ctx->d_voff, voff.size() * 4));
+        CU(cudaMemcpy(ctx->d_voff, voff.data(), voff.size() * 4, cudaMemcpyHostToDevice));
+        CU(cudaMalloc(&ctx->d_vtiles, vtiles.size() * 4));
+        CU(cudaMemcpy(ctx->d_vtiles, vtiles.data(), vtiles.size() * 4, cudaMemcpyHostToDevice));
+        CU(cudaMalloc(&ctx->d_runs, std::max<size_t>(1, runs.size()) * sizeof(vdc_run)));
+        if (!runs.empty()) CU(cudaMemcpy(ctx->d_runs, runs.data(), runs.size() * sizeof(vdc_run), cudaMemcpyHostToDevice));
+        ctx->n_load_words = loads;
+        ctx->n_entries = runs.size();
+        ctx->n_multi = multi;
     }
     ctx->fb_ctr = -1;  // the counter of the token the device feeds back (resident decode)
     for (uint32_t i = 0; i < n_jobs; ++i)
@@ -2381,8 +2427,15 @@ extern "C" int vdc_debug_tile_trace(vdc_ctx* ctx, void* host, uint32_t n) {
 
 int vdc_set_prefetch(vdc_ctx* ctx, uint32_t tiles) {
     if (!ctx) return fail(VDC_ERR_INPUT, "null ctx");
-    if (tiles > 31) return fail(VDC_ERR_INPUT, "prefetch look-ahead must be <= 31 tiles");
-    ctx->ring_prefetch = tiles;
+    if (tiles) return fail(VDC_ERR_INPUT, "the L2 look-ahead was removed (slower at every depth, DESIGN.md): only 0 is accepted");
+    return VDC_OK;
+}
+
+int vdc_ring_stream_stats(vdc_ctx* ctx, uint64_t* load_words, uint64_t* entries, uint64_t* multi_tile_runs) {
+    if (!ctx || !ctx->ring) return fail(VDC_ERR_INPUT, "load a ring program first");
+    if (load_words) *load_words = ctx->n_load_words;
+    if (entries) *entries = ctx->n_entries;
+    if (multi_tile_runs) *multi_tile_runs = ctx->n_multi;
     return VDC_OK;
 }
 
@@ -2425,7 +2478,9 @@ int vdc_launch(vdc_ctx* ctx, void* stream) {
         R.fb_ctr = ctx->fb_ctr;
         ctx->epoch += ctx->n_epochs;
         R.ring_slots = ctx->ring_slots;
-        R.prefetch = ctx->ring_prefetch;
+        R.voff = ctx->d_voff;
+        R.vtiles = ctx->d_vtiles;
+        R.runs = ctx->d_runs;
         if (ctx->tp_poisoned)
             return fail(VDC_ERR_INPUT, "a tensor-parallel launch aborted: the peers' symmetric headers are stale; "
                                        "zero them on every rank and call vdc_bind_symmetric again before launching");

@@ -117,7 +117,11 @@ struct RingParams {
     int32_t n_step;
     uint32_t epoch;            // 1-based launch ordinal since the counters were zeroed
     uint32_t ring_slots;
-    uint32_t prefetch;         // L2 prefetch look-ahead of the memory core, in tiles (0 = off)
+    // memory-core streams, folded (ring_abi.h vdc_run): run entries of SM s
+    // at runs[voff[s] .. voff[s + 1]), vtiles[s] ring tiles once expanded
+    const uint32_t* voff;
+    const uint32_t* vtiles;
+    const ::vdc_run* runs;
     uint32_t debug;            // bit 0: GEMV tiles are released without computing (bandwidth experiments)
     unsigned long long* tile_trace;  // debug: per ring tile of SM `debug >> 8`: {t_issue, t_full, t_release}
     char* const* sym;          // [n_desc][VDC_RING_MAX_TP] peer buffer bases of symmetric tensors (null: not symmetric)

@@ -2327,9 +2327,7 @@ __device__ __forceinline__ void vcc_role(const RingParams& P, Shared& S, char* r
     }
     if constexpr (BATCHED) {  // resident steps of odd tile count end with the memory core's pad tile
         if (P.n_epochs > 1) {
-            const uint32_t vw0 = P.core_off[core - 1], vn = P.core_off[core] - vw0;
-            const uint32_t vt = vn && ((__ldg(&P.words[vw0 + vn - 1]).x & 0xff) == OP_HALT) ? vn - 1 : vn;
-            if (vt & 1u) {
+            if (P.vtiles[blockIdx.x] & 1u) {
                 const uint32_t s0 = v.kt % v.R;
                 if ((s0 & uint32_t(CW - 1)) == v.w) {
                     if (!v.wait_full(s0, (v.kt / v.R) & 1u)) v.ok = false;
@@ -2436,8 +2434,40 @@ __device__ __forceinline__ Tile resolve_load(const RingParams& P, uint4 raw) {
     return t;
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+// one folded run entry (ring_abi.h vdc_run) as the memory core caches it:
+// the two raw 16-byte halves (fields decoded per tile: the memory warpgroup
+// runs on few registers) and 1 / n_in
+struct Run {
+    uint4 b, m;
+    float rcp;
+};
+__device__ __forceinline__ uint32_t run_count(const Run& r) { return r.m.x & 0xffffffu; }
+__device__ __forceinline__ Run load_run(const RingParams& P, uint32_t i) {
+    const uint4* rp = reinterpret_cast<const uint4*>(P.runs + i);
+    Run r;
+    r.b = __ldg(rp);
+    r.m = __ldg(rp + 1);
+    r.rcp = 1.f / float(r.m.y & 0xfffu);
+    return r;
+}
+// tile k of a run as a LOAD word (the host reference is host/ring_fold.cpp
+// expand_run): the division by n_in is a multiply by its reciprocal with a
+// one-step correction
+__device__ __forceinline__ uint4 expand_run(const Run& r, uint32_t k) {
+    const uint32_t n_alt = r.m.x >> 24, n_in = r.m.y & 0xfffu;
+    const uint32_t a = n_alt == 2u ? (k & 1u) : 0u, j = n_alt == 2u ? (k >> 1) : k;
+    uint32_t o = __float2uint_rz(float(j) * r.rcp);
+    if (o * n_in > j) --o;
+    if ((o + 1u) * n_in <= j) ++o;
+    const int32_t i = int32_t(j - o * n_in), oo = int32_t(o);
+    auto s8 = [](uint32_t v, int q) { return int32_t(int8_t(uint8_t((v >> (8 * q)) & 0xffu))); };
+    const uint64_t pl = uint64_t(r.b.z >> 16) | (uint64_t(r.b.w) << 16);
+    const int32_t c0 = int32_t(pl & 0xfff) + i * s8(r.m.z, 0) + oo * s8(r.m.z, 3);
+    const int32_t c1 = int32_t((pl >> 12) & 0xfff) + i * s8(r.m.z, 1) + oo * s8(r.m.w, 0);
+    const int32_t c2 = int32_t((pl >> 24) & 0xfff) + i * s8(r.m.z, 2) + oo * s8(r.m.w, 1);
+    const uint64_t np = uint64_t(c0 & 0xfff) | (uint64_t(c1 & 0xfff) << 12) | (uint64_t(c2 & 0xfff) << 24) | (pl & ~0xfffffffffull);
+    const uint32_t ti = a ? (r.m.y >> 12) : (r.b.z & 0xffffu);
+    return make_uint4(r.b.x, r.b.y, ti | (uint32_t(np & 0xffffu) << 16), uint32_t(np >> 16));
 }
 
 __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
@@ -2457,8 +2487,9 @@ __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
 // warp) pair is an independent pipeline and a slow tile never blocks the
 // refill of another warp's slot. Lanes poll their own slot's `empty`
 // barrier (non-blocking test_wait) in one converged loop and issue the bulk
-// copy of their next tile as soon as it is free; optional L2 prefetch of
-// the tile `prefetch` rounds ahead.
+// copy of their next tile as soon as it is free.
+// The stream is folded (ring_abi.h vdc_run): each lane keeps a cursor (folded
+// word, offset in it) that it advances by R tiles per issue.
 // RESIDENT: launches of several decode steps (vdc_set_steps) walk the stream
 // once per step with token-gated KV pages; single-step launches run the
 // instance without that bookkeeping on the issue path
@@ -2466,11 +2497,10 @@ template <bool BATCHED, bool RESIDENT>
 __device__ __forceinline__ void vmc_loop(const RingParams& P, Shared& S, char* ring) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t core = 2 * blockIdx.x;
-    const uint32_t w0 = P.core_off[core], n = P.core_off[core + 1] - w0;
     const uint32_t R = P.ring_slots;
-    const uint32_t PF = P.prefetch;
-    // the stream is LOAD words followed by one HALT
-    const uint32_t ntiles = n && ((__ldg(&P.words[w0 + n - 1]).x & 0xff) == OP_HALT) ? n - 1 : n;
+    // the folded stream of this SM and its length in tiles
+    const uint32_t v0 = P.voff[blockIdx.x], fn = P.voff[blockIdx.x + 1] - v0;  // run entries
+    const uint32_t ntiles = P.vtiles[blockIdx.x];
     // resident decode: the stream is walked once per step; tile g is word
     // g % ntiles of step g / ntiles. Weight tiles stream across the step
     // boundary; a KV page of step e > 0 is resolved (context, page table) and
@@ -2494,8 +2524,35 @@ __device__ __forceinline__ void vmc_loop(const RingParams& P, Shared& S, char* r
         const uint32_t mode = (r.y >> 24) & 0xfu;
         return ei > 0 && wi < ntiles && (mode == VDC_LOAD_CTX || mode == VDC_LOAD_PAGED);
     };
+    // cursor: run entry fw (cached in run), tile fk of it; the next entry is
+    // prefetched into L1 whenever the cursor enters one
+    uint32_t fw = 0, fk = 0;
+    Run run{};
+    auto enter = [&](uint32_t i) {
+        fw = i;
+        if (i < fn) {
+            run = load_run(P, v0 + i);
+            if (i + 1 < fn) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.runs + v0 + i + 1));
+        } else {
+            run.m.x = 0xffffffu;  // past the end: a run no cursor leaves
+        }
+    };
+    auto advance = [&](uint32_t d) {
+        fk += d;
+        while (fw < fn && fk >= run_count(run)) {
+            fk -= run_count(run);
+            enter(fw + 1);
+        }
+    };
+    auto seek = [&](uint32_t t) {
+        fk = 0;
+        enter(0);
+        advance(t);
+    };
+    seek(wi);
     auto word = [&]() {  // the LOAD word of the lane's tile (the step pad: a data-less tile)
-        return wi < ntiles ? __ldg(&P.words[w0 + wi]) : make_uint4(0, 0, 0, 0);
+        if (wi >= ntiles) return make_uint4(0, 0, 0, 0);
+        return expand_run(run, fk);
     };
     auto resolve = [&](uint4 r) {
         if (RESIDENT && wi >= ntiles) {
@@ -2515,7 +2572,6 @@ __device__ __forceinline__ void vmc_loop(const RingParams& P, Shared& S, char* r
     // slot frees up
     bool deferred = issuer && g < total && kv_gated(raw);
     Tile cur = issuer && g < total && !deferred ? resolve(raw) : Tile{};
-    uint32_t pf_g = g + R;  // next tile of this lane to prefetch into L2 (beyond its slot)
     long long idle_since = 0;
     unsigned long long t_idle = 0;
     bool real_last = false;  // this lane's last issue was a bulk copy (bytes may still be landing)
@@ -2561,27 +2617,23 @@ __device__ __forceinline__ void vmc_loop(const RingParams& P, Shared& S, char* r
                 ++uops;
             }
             g += R;
-            if (pf_g < g + R) pf_g = g + R;
             ++m;
             wi += R;
+            bool wrapped = false;
             if constexpr (RESIDENT) {
                 while (ept && wi >= ept) {
                     wi -= ept;
                     ++ei;
+                    wrapped = true;
                 }
             }
+            if (wrapped)
+                seek(wi);
+            else
+                advance(R);
             raw = g < total ? word() : make_uint4(0, 0, 0, 0);
             deferred = g < total && kv_gated(raw);
             if (g < total && !deferred) cur = resolve(raw);
-        }
-        if (PF && pending && !ready && pf_g < ntiles && pf_g < g + R * (1 + PF)) {
-            // slot busy (the compute core is behind or waiting on a dependency):
-            // keep DRAM busy by pulling this lane's upcoming tiles into L2
-            const Tile ta = resolve_load<BATCHED>(P, __ldg(&P.words[w0 + pf_g]));
-            if (!ta.bad && !ta.halt)
-                for (uint32_t q = 0; q < ta.copies; ++q) prefetch_l2(ta.src + size_t(q) * ta.pitch, ta.run);
-            pf_g += R;
-            ready = true;  // made progress: skip the back-off
         }
         if (!__any_sync(0xffffffffu, ready)) {
             const long long now = clock64();
@@ -2635,9 +2687,10 @@ __device__ void vmc_role(const RingParams& P, Shared& S, char* ring) {
 }
 
 // register split per SM sub-partition (16384 registers = 512 per lane slot,
-// one warp of each warpgroup): 2 x 224 (compute) + 56 (memory warpgroup)
+// one warp of each warpgroup): 2 x 224 (compute) + 56 (memory warpgroup);
+// (the full 512 is not available: an inc to 2 x 224 + 64 never returns)
 constexpr uint32_t kVccRegs = 224, kVmcRegs = 56;
-static_assert(2 * kVccRegs + kVmcRegs <= 512 && kRingThreads == 3 * 128 && NCT == 256);
+static_assert(2 * kVccRegs + kVmcRegs < 512 && kRingThreads == 3 * 128 && NCT == 256);
 
 template <bool BATCHED, bool QKNORM>
 __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(const __grid_constant__ RingParams P) {

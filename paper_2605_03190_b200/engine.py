@@ -117,6 +117,33 @@ def unpack_sw128(a: np.ndarray, rows: int, cols: int) -> np.ndarray:
     return np.ascontiguousarray(t[:, :, r, c ^ (r & 7), :].transpose(0, 2, 1, 3, 4)).reshape(-1)
 
 
+# ring_abi.h vdc_run: one folded stretch of a memory-core stream
+RUN_DTYPE = np.dtype([("base", "<u4", 4), ("count_alt", "<u4"), ("nin_talt", "<u4"), ("d_in", "i1", 3),
+                      ("d_out", "i1", 3), ("rsv", "<u2")])
+assert RUN_DTYPE.itemsize == 32
+
+
+def fold_stream(words: bytes) -> np.ndarray:
+    """fold a memory-core stream of LOAD words the way vdc_load_jobs does
+    (vdc_fold_stream): the run entries, a RUN_DTYPE array"""
+    import ctypes as c
+    n = len(words) // 16
+    runs = np.zeros(max(1, n), dtype=RUN_DTYPE)
+    nr = c.c_uint32()
+    check(lib().vdc_fold_stream(words, n, runs.ctypes.data, c.byref(nr)))
+    return runs[:nr.value].copy()
+
+
+def unfold_stream(runs: np.ndarray, capacity: int) -> bytes:
+    """host expansion of run entries back to LOAD words (vdc_unfold_stream)"""
+    import ctypes as c
+    out = c.create_string_buffer(max(16, 16 * capacity))
+    n = c.c_uint32()
+    r = np.ascontiguousarray(runs, dtype=RUN_DTYPE)
+    check(lib().vdc_unfold_stream(r.ctypes.data, len(r), out, capacity, c.byref(n)))
+    return out.raw[:16 * n.value]
+
+
 class Engine:
     """One vdc_ctx (one persistent-kernel configuration) with a loaded program."""
 
@@ -142,8 +169,16 @@ class Engine:
         decode steps inside the persistent kernel (feedback programs only)."""
         check(lib().vdc_set_steps(self._h, steps))
 
+    def stream_stats(self) -> dict:
+        """Ring engine: memory-core LOAD words as built and as folded on the
+        device (vdc_ring_stream_stats; ring_abi.h vdc_run)."""
+        import ctypes as c
+        a, b, r = c.c_uint64(), c.c_uint64(), c.c_uint64()
+        check(lib().vdc_ring_stream_stats(self._h, c.byref(a), c.byref(b), c.byref(r)))
+        return {"load_words": a.value, "run_entries": b.value, "multi_tile_runs": r.value}
+
     def set_prefetch(self, tiles: int) -> None:
-        """Ring engine: L2 prefetch look-ahead of the memory core (tiles)."""
+        """Ring engine: the removed L2 look-ahead (only 0 is accepted)."""
         check(lib().vdc_set_prefetch(self._h, tiles))
 
     def storage_names(self):
