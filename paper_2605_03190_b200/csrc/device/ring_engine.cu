@@ -348,22 +348,32 @@ struct Vcc {
         const int K = J.k, nch = K / EPC;
         const int32_t rmsf = J.flags & VDC_JOB_RMS;
         const bool reuse = xk_t == J.x_t && xk_off == J.x_off && xk_flags == rmsf && xk_a == J.a_t;
+        // the norm weight is immutable: its chunks are requested before the
+        // readiness wait (read once per step, it is usually evicted from L2 by
+        // then, and its DRAM latency would otherwise follow the wait)
+        uint4 gr[XPT];
+        if (!reuse && rmsf) {
+            const uint4* ws = reinterpret_cast<const uint4*>(tptr(J.a_t));
+#pragma unroll
+            for (int i = 0; i < XPT; ++i) {
+                const int c = int(ct) + i * NCT;
+                gr[i] = c < nch ? __ldg(ws + c) : make_uint4(0, 0, 0, 0);
+            }
+        }
         if (!wait_ready(reuse ? -1 : J.x_t, J.x_need, (J.flags & VDC_JOB_RESID) ? J.a_t : -1, J.a_need, -1, 0)) {
             ok = false;
             return;
         }
         if (!reuse) {  // stage x (RMS-normalised, rounded to the model dtype) in shared memory
-            // every chunk of x (and of the norm weight) is requested before any
-            // is used: one L2 round trip instead of one per loop iteration
+            // every chunk of x is requested before any is used: one L2 round
+            // trip instead of one per loop iteration
             const uint4* xs = reinterpret_cast<const uint4*>(tptr(J.x_t)) +
                               (J.x_off + (J.flags & VDC_JOB_TOKEN_ROW ? token() * int64_t(K) : 0)) / EPC;
-            const uint4* ws = rmsf ? reinterpret_cast<const uint4*>(tptr(J.a_t)) : nullptr;
-            uint4 xr[XPT], gr[XPT];
+            uint4 xr[XPT];
 #pragma unroll
             for (int i = 0; i < XPT; ++i) {
                 const int c = int(ct) + i * NCT;
                 xr[i] = c < nch ? ldcg128(xs + c) : make_uint4(0, 0, 0, 0);
-                gr[i] = (rmsf && c < nch) ? __ldg(ws + c) : make_uint4(0, 0, 0, 0);
             }
             float inv = 1.f;
             if (rmsf) {
@@ -404,6 +414,7 @@ struct Vcc {
             xk_flags = rmsf;
             xk_a = J.a_t;
             sync();
+            if ((P->debug & 4u) && P->trace && ct == 0) S->t_ready = now_ns();  // debug: trace "ready" = x staged
         }
         if (J.flags & VDC_JOB_RESID) {  // residual element of this thread's output row (hidden behind the sweep)
             const int i = int(ct);
