@@ -286,6 +286,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         req["layout"].update(feedback=True, ctx_pages=pages, max_ctx=pages * 64)
     if tp:
         req["layout"]["tp_world"], req["layout"]["tp_rank"] = world, rank
+        req["layout"]["tp_partials"] = args.tp_partials
     prog = Program.build(req)
     build_s = time.time() - t_build
     eng = Engine(prog, device=local_rank, watchdog_ms=10000)
@@ -478,6 +479,7 @@ def run_batched(args, rank: int = 0, world: int = 1, local_rank: int = 0):
            "profile": {"builtin": "b200"}}
     if tp:
         req["layout"]["tp_world"], req["layout"]["tp_rank"] = world, rank
+        req["layout"]["tp_partials"] = args.tp_partials
     prog = Program.build(req)
     build_s = time.time() - t_build
     eng = Engine(prog, device=local_rank, watchdog_ms=20000)
@@ -638,6 +640,8 @@ def main():
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--ctx", type=int, default=CTX)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tp-partials", default="f32", choices=["f32", "bf16"],
+                    help="TP exchange partials: bf16 halves the NVLink bytes of the in-kernel allreduce")
     ap.add_argument("--engine", default="ring", choices=["ring", "reference"])
     ap.add_argument("--ring-slots", type=int, default=12)
     ap.add_argument("--pages-per-job", type=int, default=None,

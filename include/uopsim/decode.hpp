@@ -57,6 +57,11 @@ struct LayoutConfig {
     // hidden vector, vocab-parallel lm_head, replicated embedding and norms)
     int tp_world = 0;
     int tp_rank = 0;
+    // element type of the TP exchange partials (the W slots each rank stores
+    // its partial sums into), layout.tp_partials "f32" (default) or "bf16":
+    // bf16 halves the NVLink bytes of the in-kernel allreduce at the cost of
+    // one more bf16 rounding of each partial before the residual add
+    bool tp_bf16_partials = false;
     // batched decode (ext): batch >= 1 builds the graph of
     // `batch` concurrent requests: activations (npad, width) with the
     // request index as the row, 128 x 64 weight tiles for the tcgen05 GEMM

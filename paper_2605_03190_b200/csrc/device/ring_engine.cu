@@ -207,12 +207,19 @@ __device__ __forceinline__ uint32_t kv_swz(uint32_t c, uint32_t r7) { return (c 
 
 // TP exchange: this thread's output row rg for requests c0 .. c0 + nh - 1
 // into slot `off` of every rank's buffer (batched BGEMM epilogue)
+// (T = uint16_t: bf16 partials; float: fp32 partials)
+template <typename T>
 __device__ __noinline__ void sym_store_rows(char* const* bases, uint32_t world, int64_t off, int64_t M, int rg, int c0, int nb, int nh,
                                             const float* v) {
     for (uint32_t qr = 0; qr < world; ++qr) {
-        float* dst = reinterpret_cast<float*>(bases[qr] + VDC_SYM_HEADER_BYTES) + off;
-        for (int c = 0; c < nh; ++c)
-            if (c0 + c < nb) dst[int64_t(c0 + c) * M + rg] = v[c];
+        T* dst = reinterpret_cast<T*>(bases[qr] + VDC_SYM_HEADER_BYTES) + off;
+        for (int c = 0; c < nh; ++c) {
+            if (c0 + c >= nb) continue;
+            if constexpr (sizeof(T) == 2)
+                dst[int64_t(c0 + c) * M + rg] = f2bf(v[c]);
+            else
+                dst[int64_t(c0 + c) * M + rg] = v[c];
+        }
     }
 }
 
@@ -351,13 +358,17 @@ struct Vcc {
         // the norm weight is immutable: its chunks are requested before the
         // readiness wait (read once per step, it is usually evicted from L2 by
         // then, and its DRAM latency would otherwise follow the wait)
+        // (single-request kernel only: the batched instance, which runs GEMV
+        // µops rarely, would spill holding them across the wait)
         uint4 gr[XPT];
-        if (!reuse && rmsf) {
-            const uint4* ws = reinterpret_cast<const uint4*>(tptr(J.a_t));
+        const uint4* ws = rmsf ? reinterpret_cast<const uint4*>(tptr(J.a_t)) : nullptr;
+        if constexpr (!BATCHED) {
+            if (!reuse && rmsf) {
 #pragma unroll
-            for (int i = 0; i < XPT; ++i) {
-                const int c = int(ct) + i * NCT;
-                gr[i] = c < nch ? __ldg(ws + c) : make_uint4(0, 0, 0, 0);
+                for (int i = 0; i < XPT; ++i) {
+                    const int c = int(ct) + i * NCT;
+                    gr[i] = c < nch ? __ldg(ws + c) : make_uint4(0, 0, 0, 0);
+                }
             }
         }
         if (!wait_ready(reuse ? -1 : J.x_t, J.x_need, (J.flags & VDC_JOB_RESID) ? J.a_t : -1, J.a_need, -1, 0)) {
@@ -374,6 +385,7 @@ struct Vcc {
             for (int i = 0; i < XPT; ++i) {
                 const int c = int(ct) + i * NCT;
                 xr[i] = c < nch ? ldcg128(xs + c) : make_uint4(0, 0, 0, 0);
+                if constexpr (BATCHED) gr[i] = (rmsf && c < nch) ? __ldg(ws + c) : make_uint4(0, 0, 0, 0);
             }
             float inv = 1.f;
             if (rmsf) {
@@ -873,7 +885,7 @@ struct Vcc {
                 if (res) v += resid;
                 if (symo) {  // TP partial sum -> slot `tp_rank` of every rank's buffer (NVLink peer stores)
                     for (uint32_t q = 0; q < P->tp_world; ++q)
-                        reinterpret_cast<float*>(sym_base(J.o_t, q) + VDC_SYM_HEADER_BYTES)[J.o_off + lr0 + i] = v;
+                        store_out(sym_base(J.o_t, q) + VDC_SYM_HEADER_BYTES, obf, int64_t(J.o_off) + lr0 + i, v);
                 } else {
                     store_out(ob, obf, out_index(lr0 + i), v);
                 }
@@ -1310,7 +1322,10 @@ struct Vcc {
             float vs[NH];
 #pragma unroll
             for (int c = 0; c < NH; ++c) vs[c] = v[c];
-            sym_store_rows(P->sym + size_t(J.o_t) * VDC_RING_MAX_TP, P->tp_world, J.o_off, M, rg, c0, nb, NH, vs);
+            if (tdtype(J.o_t) == VDC_DTYPE_BF16)
+                sym_store_rows<uint16_t>(P->sym + size_t(J.o_t) * VDC_RING_MAX_TP, P->tp_world, J.o_off, M, rg, c0, nb, NH, vs);
+            else
+                sym_store_rows<float>(P->sym + size_t(J.o_t) * VDC_RING_MAX_TP, P->tp_world, J.o_off, M, rg, c0, nb, NH, vs);
         } else {
             const bool obf = tdtype(J.o_t) == VDC_DTYPE_BF16;
 #pragma unroll
@@ -2111,7 +2126,8 @@ struct Vcc {
             ok = false;
             return;
         }
-        const float* part = reinterpret_cast<const float*>(tptr(J.x_t));
+        const char* part = tptr(J.x_t);
+        const bool pbf = tdtype(J.x_t) == VDC_DTYPE_BF16;  // bf16 exchange partials
         const char* ab = tptr(J.a_t);
         const bool abf = tdtype(J.a_t) == VDC_DTYPE_BF16;
         const int64_t aoff = J.a_off + (J.flags & VDC_JOB_TOKEN_AUX ? token() * int64_t(J.cache_rows) : 0);
@@ -2121,7 +2137,9 @@ struct Vcc {
             float acc[VDC_RING_MAX_TP];
 #pragma unroll
             for (int q = 0; q < VDC_RING_MAX_TP; ++q)
-                acc[q] = q < J.group ? ldcg_f32(part + int64_t(q) * J.k + r) : 0.f;
+                acc[q] = q >= J.group ? 0.f
+                         : pbf ? bf_lo(ldcg_u16(reinterpret_cast<const uint16_t*>(part) + int64_t(q) * J.k + r))
+                               : ldcg_f32(reinterpret_cast<const float*>(part) + int64_t(q) * J.k + r);
             float v = 0.f;
 #pragma unroll
             for (int q = 0; q < VDC_RING_MAX_TP; ++q)
@@ -2140,7 +2158,8 @@ struct Vcc {
             ok = false;
             return;
         }
-        const float* part = reinterpret_cast<const float*>(tptr(J.x_t));
+        const char* part = tptr(J.x_t);
+        const bool pbf = tdtype(J.x_t) == VDC_DTYPE_BF16;  // bf16 exchange partials
         const uint16_t* res = u16p(J.a_t);
         const uint16_t* wn = u16p(J.w3_t);
         const int64_t M = J.k, slot = int64_t(J.npad) * M;
@@ -2149,7 +2168,9 @@ struct Vcc {
             const int b = i / rows, r = J.r0 + i % rows;
             const int64_t e = int64_t(b) * M + r;
             float v = 0.f;
-            for (int qr = 0; qr < J.group; ++qr) v += ldcg_f32(part + qr * slot + e);
+            for (int qr = 0; qr < J.group; ++qr)
+                v += pbf ? bf_lo(ldcg_u16(reinterpret_cast<const uint16_t*>(part) + qr * slot + e))
+                         : ldcg_f32(reinterpret_cast<const float*>(part) + qr * slot + e);
             const uint16_t xo = f2bf(v + bf_lo(ldcg_u16(res + e)));
             u16p(J.o_t)[e] = xo;
             u16p(J.o3_t)[e] = f2bf(bf_lo(xo) * bf_lo(wn[r]));

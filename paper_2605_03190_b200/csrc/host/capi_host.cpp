@@ -108,6 +108,11 @@ decode::LayoutConfig layout_from(const json& j) {
     l.ring = j.value("ring", l.ring);
     l.tp_world = j.value("tp_world", l.tp_world);
     l.tp_rank = j.value("tp_rank", l.tp_rank);
+    if (j.contains("tp_partials")) {
+        const std::string tpp = j.at("tp_partials").get<std::string>();
+        if (tpp != "bf16" && tpp != "f32") throw std::invalid_argument("layout.tp_partials must be \"bf16\" or \"f32\"");
+        l.tp_bf16_partials = tpp == "bf16";
+    }
     l.batch = j.value("batch", l.batch);
     l.argmax = j.value("argmax", l.argmax);
     l.feedback = j.value("feedback", l.feedback);

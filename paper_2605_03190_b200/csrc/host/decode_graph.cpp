@@ -187,9 +187,9 @@ OperatorGraph build_decode_graph(const ModelConfig& m, const LayoutConfig& l) {
         a.insert(extra.begin(), extra.end());
         return a;
     };
-    // TP exchange buffer: one (D,1) fp32 slot per rank, peer mapped
+    // TP exchange buffer: one (D,1) slot of partials per rank (bf16 or fp32), peer mapped
     auto sym = [&](const std::string& name) {
-        TensorRef& t = b.add(name, {W * d, 1}, d, 1, InitKind::zeros, ElemType::f32);
+        TensorRef& t = b.add(name, {W * d, 1}, d, 1, InitKind::zeros, l.tp_bf16_partials ? ElemType::bf16 : ElemType::f32);
         t.symmetric = true;
         return name;
     };
@@ -359,8 +359,8 @@ OperatorGraph build_decode_graph_batched(const ModelConfig& m, const LayoutConfi
         pool = l.pool_pages;
     }
     Builder b{{}, m, l};
-    auto sym = [&](const std::string& name) {  // exchange buffer: one (npad, d) fp32 slot per rank
-        TensorRef& t = b.add(name, {W * N * d, 1}, N * d, 1, InitKind::zeros, ElemType::f32);
+    auto sym = [&](const std::string& name) {  // exchange buffer: one (npad, d) slot of partials per rank
+        TensorRef& t = b.add(name, {W * N * d, 1}, N * d, 1, InitKind::zeros, l.tp_bf16_partials ? ElemType::bf16 : ElemType::f32);
         t.symmetric = true;
         return name;
     };
