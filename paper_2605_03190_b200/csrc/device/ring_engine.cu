@@ -2551,10 +2551,13 @@ __device__ __forceinline__ void vmc_loop(const RingParams& P, Shared& S, char* r
         wi -= ept;
         ++ei;
     }
+    uint32_t gate_ep = 0;  // resident: the latest step whose token gate this lane saw open
     auto kv_gated = [&](uint4 r) {
         if constexpr (!RESIDENT) return false;
         const uint32_t mode = (r.y >> 24) & 0xfu;
-        return ei > 0 && wi < ntiles && (mode == VDC_LOAD_CTX || mode == VDC_LOAD_PAGED);
+        // once the lane saw the step's gate open, its later KV tiles of the step
+        // are resolved ahead like any other tile
+        return ei > gate_ep && wi < ntiles && (mode == VDC_LOAD_CTX || mode == VDC_LOAD_PAGED);
     };
     // cursor: run entry fw (cached in run), tile fk of it; the next entry is
     // prefetched into L1 whenever the cursor enters one
@@ -2616,9 +2619,14 @@ __device__ __forceinline__ void vmc_loop(const RingParams& P, Shared& S, char* r
             slot = lane;
             ready = m == 0 || mbar_test(&S.empty[slot], (m - 1u) & 1u);
             if (RESIDENT && ready && deferred) {  // KV page of a later step: wait for the previous step's token
+                // (polled until it opens, once per step and lane: the lane's later
+                // KV tiles of the step follow the acquire in program order and are
+                // resolved ahead like any other tile, see kv_gated; a counter load
+                // per tile stalled the whole issue warp)
                 if (int32_t(ld_relaxed(&P.counters[P.fb_ctr]) - (P.epoch + ei - 1u)) >= 0) {
                     fence_acquire_gpu();
                     fence_proxy_async_global();  // the appends were generic stores; the copy is async-proxy
+                    gate_ep = ei;
                     cur = resolve(raw);
                     deferred = false;
                 } else {
