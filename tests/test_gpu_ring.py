@@ -26,11 +26,11 @@ LLAMA_1L = {"model": {"preset": "llama3-8b", "layers": 1, "vocab": 32000},
             "layout": {"ctx_pages": 16, "max_ctx": 1024, "pages_per_job": 4, "gu_block": 4}}
 
 
-def run(base, sms=None, steps=((17, 40),), seed=0):
+def run(base, sms=None, steps=((17, 40),), seed=0, ring_slots=12):
     from paper_2605_03190_b200.engine import Engine
     import torch
 
-    req = rc.request(base, sms)
+    req = rc.request(base, sms, ring_slots)
     prog = Program.build(req)
     info = prog.info()
     ins = rc.synth_inputs(info, seed)
@@ -72,6 +72,16 @@ def test_tiny_fp32_matches_dense(cuda, sms, token, pos):
 def test_mid_bf16_matches_dense(cuda, token, pos):
     _, _, _, outs = run(rc.MID, None, ((token, pos),))
     assert_close(outs[0][0], fp32=False)
+
+
+@pytest.mark.parametrize("slots", [8, 10, 11])
+def test_mid_bf16_other_ring_depths(cuda, slots):
+    """rings of 8, 10 and 11 slots: the memory core's lanes walk the folded
+    stream (ring_abi.h vdc_run) with stride R, so every run entry is entered
+    at other offsets than with 12 slots; two steps carry the caches"""
+    _, _, _, outs = run(rc.MID, None, ((17, 300), (18, 301)), ring_slots=slots)
+    for res, _ in outs:
+        assert_close(res, fp32=False)
 
 
 def test_fused_argmax_matches_logits(cuda):
