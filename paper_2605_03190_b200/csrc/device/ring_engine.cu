@@ -246,6 +246,12 @@ struct Vcc {
     float rope_theta = 0.f;
     // x held in registers across jobs that share it
     int32_t xk_t = -2, xk_off = 0, xk_flags = 0, xk_a = 0;
+    // RMS jobs stage bf16(x * w) and scale the row sums by 1/rms in the
+    // epilogue (the batched GEMMs' order), so the tile sweep starts without
+    // waiting for the sum-of-squares reduction: xinv of the staged x, taken
+    // from the per-warp partials (S->bc) at the first epilogue
+    float rs_scale = 1.f, xinv = 1.f;
+    bool xinv_pending = false;
 
     __device__ void sync() const { named_bar(BAR_VCC, NCT); }
     __device__ bool aborted() const { return *reinterpret_cast<volatile int32_t*>(&P->status->abort) != 0; }
@@ -387,18 +393,13 @@ struct Vcc {
                 xr[i] = c < nch ? ldcg128(xs + c) : make_uint4(0, 0, 0, 0);
                 if constexpr (BATCHED) gr[i] = (rmsf && c < nch) ? __ldg(ws + c) : make_uint4(0, 0, 0, 0);
             }
-            float inv = 1.f;
-            if (rmsf) {
+            if (rmsf) {  // this warp's sum of squares; 1/rms is formed at the epilogue
                 float ss = 0.f;
 #pragma unroll
                 for (int i = 0; i < XPT; ++i) ss += dot16<BF>(xr[i], xr[i]);
                 ss = warp_sum(ss);
                 if (lane == 0) S->bc[w] = ss;
-                sync();
-                float tot = 0.f;
-#pragma unroll
-                for (int i = 0; i < CW; ++i) tot += S->bc[i];
-                inv = 1.0f / sqrtf(tot / float(K) + J.eps);
+                xinv_pending = true;
             }
 #pragma unroll
             for (int i = 0; i < XPT; ++i) {
@@ -408,15 +409,15 @@ struct Vcc {
                 if (rmsf) {
                     const uint4 g = gr[i];
                     if constexpr (BF) {
-                        v.x = pack2(bf_lo(v.x) * inv * bf_lo(g.x), bf_hi(v.x) * inv * bf_hi(g.x));
-                        v.y = pack2(bf_lo(v.y) * inv * bf_lo(g.y), bf_hi(v.y) * inv * bf_hi(g.y));
-                        v.z = pack2(bf_lo(v.z) * inv * bf_lo(g.z), bf_hi(v.z) * inv * bf_hi(g.z));
-                        v.w = pack2(bf_lo(v.w) * inv * bf_lo(g.w), bf_hi(v.w) * inv * bf_hi(g.w));
+                        v.x = pack2(bf_lo(v.x) * bf_lo(g.x), bf_hi(v.x) * bf_hi(g.x));
+                        v.y = pack2(bf_lo(v.y) * bf_lo(g.y), bf_hi(v.y) * bf_hi(g.y));
+                        v.z = pack2(bf_lo(v.z) * bf_lo(g.z), bf_hi(v.z) * bf_hi(g.z));
+                        v.w = pack2(bf_lo(v.w) * bf_lo(g.w), bf_hi(v.w) * bf_hi(g.w));
                     } else {
-                        v.x = __float_as_uint(__uint_as_float(v.x) * inv * __uint_as_float(g.x));
-                        v.y = __float_as_uint(__uint_as_float(v.y) * inv * __uint_as_float(g.y));
-                        v.z = __float_as_uint(__uint_as_float(v.z) * inv * __uint_as_float(g.z));
-                        v.w = __float_as_uint(__uint_as_float(v.w) * inv * __uint_as_float(g.w));
+                        v.x = __float_as_uint(__uint_as_float(v.x) * __uint_as_float(g.x));
+                        v.y = __float_as_uint(__uint_as_float(v.y) * __uint_as_float(g.y));
+                        v.z = __float_as_uint(__uint_as_float(v.z) * __uint_as_float(g.z));
+                        v.w = __float_as_uint(__uint_as_float(v.w) * __uint_as_float(g.w));
                     }
                 }
                 S->x[c] = v;
@@ -465,6 +466,16 @@ struct Vcc {
             }
         }
         sync();  // (an aborted launch runs on through the epilogue: every warp must reach the same barriers)
+        if (rmsf) {
+            if (xinv_pending) {  // the staging's per-warp sums of squares (S->bc, before the staging barrier)
+                float tot = 0.f;
+#pragma unroll
+                for (int i = 0; i < CW; ++i) tot += S->bc[i];
+                xinv = 1.0f / sqrtf(tot / float(K) + J.eps);
+                xinv_pending = false;
+            }
+            rs_scale = xinv;
+        }
         const long long e0 = clock64();
         gemv_epilogue(J, J.r1 - J.r0);
         if (ct == 0) stat_add(VS_EPI, clock64() - e0);
@@ -485,6 +496,7 @@ struct Vcc {
             if (J.flags & VDC_JOB_ARGMAX) argmax_rows(J, J.r1 - J.r0);
             publish(J.o_t);
         }
+        rs_scale = 1.f;
     }
 
     // TP sampling exchange (one thread): spin at system scope until the
@@ -801,10 +813,11 @@ struct Vcc {
         kt += uint32_t(ntiles);
     }
 
+    // (rs_scale: the RMS jobs' 1/rms, applied to the row sums in the epilogue)
     __device__ float row_sum(int i, int tpr) const {
         float v = S->red[0][i];
         for (int c = 1; c < tpr; ++c) v += S->red[c][i];
-        return v;
+        return v * rs_scale;
     }
 
     __device__ void store_out(char* base, bool bf, int64_t idx, float v) const {

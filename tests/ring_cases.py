@@ -35,7 +35,10 @@ def model_cfg(info: dict, req: dict) -> dict:
     dtype = [x["dtype"] for x in info["descriptors"] if x["name"] == "L0.wqkv"][0]
     return {"hidden": d, "heads": q // hd, "kv_heads": kc[0], "head_dim": hd, "ffn": g["L0.a"]["shape"][0],
             "eps": eps, "theta": theta, "layers": layers, "gu_block": req["layout"]["gu_block"], "dtype": dtype,
-            "qk_norm": "L0.q_norm" in g}
+            "qk_norm": "L0.q_norm" in g,
+            # ring programs stage bf16(x * w) and apply 1/rms to the GEMV output
+            # (reference-form programs normalise before the MATVEC)
+            "norm_scale_after": req.get("engine") == "ring"}
 
 
 def synth_inputs(info: dict, seed: int = 0) -> dict:

@@ -117,7 +117,7 @@ def test_c2_full_llama3_8b_ctx4096_100_steps(cuda):
     info = prog.info()
     eng = Engine(prog, watchdog_ms=20000)
     tens = eng.synthesize(seed=0)
-    cfg = dict(rc.model_cfg(info, req), vocab=128256, norm_scale_after=False)
+    cfg = dict(rc.model_cfg(info, req), vocab=128256)
     assert cfg["layers"] == 32 and cfg["hidden"] == 4096
     W = tr.weights_single(info, tens, cfg)
     ref64, ref32 = _refs(W, cfg, lambda: tr.caches_single(info, tens, cfg))
