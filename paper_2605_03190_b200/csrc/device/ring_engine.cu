@@ -666,9 +666,32 @@ struct Vcc {
             float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
             float d2[4] = {0.f, 0.f, 0.f, 0.f}, d3[4] = {0.f, 0.f, 0.f, 0.f};
             if (!(P->debug & 1u)) {
-                // groups of 4 k-steps: all fragment loads first, then the MMAs
-                // (volatile asm keeps program order, so the order is explicit)
+                // groups of 8 (then 4) k-steps: all fragment loads first, then the
+                // MMAs (volatile asm keeps program order, so the order is
+                // explicit); k-step u of a group accumulates into d[u % 4], the
+                // same per-accumulator order as groups of 4
                 int st = 0;
+                for (; st + 8 <= ksteps; st += 8) {
+                    uint32_t a[8][4], b[8][2];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const uint32_t off = uint32_t((st + u) * 2 * NC) * 16u;
+                        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                                     : "=r"(a[u][0]), "=r"(a[u][1]), "=r"(a[u][2]), "=r"(a[u][3])
+                                     : "r"(abase + off));
+                        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(b[u][0]) : "r"(bbase + off));
+                        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(b[u][1]) : "r"(bbase + off + uint32_t(NC) * 16u));
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        float* d = (u & 3) == 0 ? d0 : (u & 3) == 1 ? d1 : (u & 3) == 2 ? d2 : d3;
+                        asm volatile(
+                            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                            "{%0,%1,%2,%3};"
+                            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                            : "r"(a[u][0]), "r"(a[u][1]), "r"(a[u][2]), "r"(a[u][3]), "r"(b[u][0]), "r"(b[u][1]));
+                    }
+                }
                 for (; st + 4 <= ksteps; st += 4) {
                     uint32_t a[4][4], b[4][2];
 #pragma unroll
